@@ -1,0 +1,178 @@
+/*
+ * hsb200.h — C ABI of the B200-native H/S generator (libhsb200.so).
+ *
+ * This is the drop-in boundary for the reference package `hsgen`
+ * (/root/reference/pkg/src/hsgen).  Every entry point below replaces one
+ * reference interface; the citation next to each declaration names it.
+ * Plain C types only: complex128 matrices are passed as `double*` pointing at
+ * interleaved (re, im) pairs, column-major, leading dimension in complex
+ * elements — the memory layout of a numpy complex128 Fortran-order array
+ * (matcore.py:1-6).  Device pointers are CUDA global-memory pointers; the
+ * `stream` argument is a `cudaStream_t` passed as `void*` (NULL = legacy
+ * default stream).  No function throws across the ABI; every function returns
+ * an hsb_status and stores a message retrievable with hsb_last_error().
+ *
+ * Status codes map onto the reference's exception classes
+ * (matcore.py:16-25): DIMENSION -> DimensionError, INPUT -> InputError,
+ * INVARIANT -> InvariantError.  CUDA/UNSUPPORTED/NOMEM have no reference
+ * counterpart and surface as RuntimeError in the Python host layer.
+ */
+#ifndef HSB200_H
+#define HSB200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define HSB_API __attribute__((visibility("default")))
+#else
+#define HSB_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HSB_OK = 0,
+  HSB_ERR_DIMENSION = 1,   /* matcore.DimensionError */
+  HSB_ERR_INPUT = 2,       /* matcore.InputError */
+  HSB_ERR_INVARIANT = 3,   /* matcore.InvariantError */
+  HSB_ERR_CUDA = 4,        /* CUDA runtime / driver failure */
+  HSB_ERR_UNSUPPORTED = 5, /* request outside what the sm_100a kernels implement */
+  HSB_ERR_NOMEM = 6        /* device or pinned allocation failed */
+} hsb_status;
+
+typedef struct hsb_ctx hsb_ctx;
+
+/* Version of the ABI (bumped on any signature change). */
+HSB_API int32_t hsb_abi_version(void);
+
+/* Context = one CUDA device + cached device workspace + TMA encoder.
+ * Replaces the implicit process-wide state of the reference executor
+ * (executor.py:25-39 ExecPolicy is per call; the context is per device). */
+HSB_API hsb_status hsb_ctx_create(int32_t device, hsb_ctx** out);
+HSB_API void hsb_ctx_destroy(hsb_ctx* ctx);
+/* Message of the last failing call on this context (thread-unsafe, like the
+ * reference's single-entrant build_hs).  ctx may be NULL for
+ * errors raised by hsb_ctx_create. */
+HSB_API const char* hsb_last_error(const hsb_ctx* ctx);
+/* Release cached device workspace (the next call re-allocates). */
+HSB_API hsb_status hsb_ctx_trim(hsb_ctx* ctx);
+
+/* ------------------------------------------------------------------------ */
+/* Kernel level: the five large updates.  Device pointers, caller's stream.  */
+/* These replace run_partitioned(kind, operands, policy) for kind in         */
+/* {HERK, HER2K, GEMM} (executor.py:185-225) and the serial kernels herk     */
+/* (kernels.py:256-264), her2k (kernels.py:267-281), gemm (kernels.py:195).  */
+/* ------------------------------------------------------------------------ */
+
+/* flags */
+#define HSB_LOWER_ONLY   0x1u  /* gemm: write only the lower triangle (GEMMT) */
+#define HSB_MIRROR       0x2u  /* also write the strict upper triangle as the
+                                  conjugate of the lower one and a real
+                                  diagonal (= matcore.hermitian_mirror,
+                                  matcore.py:89-105, fused in the epilogue) */
+
+/* Lower triangle of C <- alpha * A^H A + beta * C, Im(diag C) := 0.
+ * A is k x n (lda >= k), C is n x n (ldc >= n).  kernels.herk / _update_lower
+ * (kernels.py:234-264). */
+HSB_API hsb_status hsb_zherk(hsb_ctx* ctx, void* stream, int64_t n, int64_t k,
+                     double alpha, const double* a, int64_t lda,
+                     double beta, double* c, int64_t ldc, uint32_t flags);
+
+/* Lower triangle of C <- alpha Z^H B + conj(alpha) B^H Z + beta C, Im(diag C) := 0.
+ * Z, B are k x n.  kernels.her2k (kernels.py:267-281). */
+HSB_API hsb_status hsb_zher2k(hsb_ctx* ctx, void* stream, int64_t n, int64_t k,
+                      double alpha_re, double alpha_im,
+                      const double* z, int64_t ldz, const double* b, int64_t ldb,
+                      double beta, double* c, int64_t ldc, uint32_t flags);
+
+/* C <- alpha op(A) op(B) + beta C, op in {'N','T','C'} (kernels.gemm,
+ * kernels.py:195-220).  With HSB_LOWER_ONLY only the lower triangle of the
+ * (square) C is written.  op(A) is m x k, op(B) is k x n. */
+HSB_API hsb_status hsb_zgemm(hsb_ctx* ctx, void* stream, char opa, char opb,
+                     int64_t m, int64_t n, int64_t k,
+                     double alpha_re, double alpha_im,
+                     const double* a, int64_t lda, const double* b, int64_t ldb,
+                     double beta_re, double beta_im, double* c, int64_t ldc,
+                     uint32_t flags);
+
+/* In place: upper triangle := conj(lower), Im(diag) := 0
+ * (matcore.hermitian_mirror, matcore.py:89-105). */
+HSB_API hsb_status hsb_hermitian_mirror(hsb_ctx* ctx, void* stream, int64_t n,
+                                double* c, int64_t ldc);
+
+/* ------------------------------------------------------------------------ */
+/* Pipeline level: builder.build_hs (builder.py:211-224).                   */
+/* ------------------------------------------------------------------------ */
+
+#define HSB_LOC_HOST   0  /* per-atom host blocks (the reference's ProblemInstance
+                             lists, probgen.py:78-92) */
+#define HSB_LOC_DEVICE 1  /* stacked device arrays (see hsb_problem) */
+
+typedef struct {
+  int64_t n_atoms, n_l, n_g;  /* matcore.Dims (matcore.py:28-44) */
+  int32_t location;           /* HSB_LOC_HOST or HSB_LOC_DEVICE */
+  int32_t reserved;
+  /* HSB_LOC_HOST: arrays of n_atoms pointers, one per atom, each to a
+   * column-major complex128 block: a/b n_l x n_g, t_* n_l x n_l; u_norms n_l
+   * float64 values.  (ProblemInstance.a_blocks ... u_norms.) */
+  const double* const* a_blocks;
+  const double* const* b_blocks;
+  const double* const* t_aa;
+  const double* const* t_ab;
+  const double* const* t_bb;
+  const double* const* u_norms;
+  /* HSB_LOC_DEVICE: stacked device arrays.  a_stack/b_stack are
+   * (n_atoms*n_l) x n_g column-major complex128 (ld = n_atoms*n_l), i.e.
+   * matcore.stack(p.a_blocks) (matcore.py:68-86); t_* are n_atoms contiguous
+   * n_l x n_l column-major blocks; u is n_atoms*n_l float64. */
+  const double* a_stack;
+  const double* b_stack;
+  const double* t_aa_dev;
+  const double* t_ab_dev;
+  const double* t_bb_dev;
+  const double* u_dev;
+} hsb_problem;
+
+#define HSB_OPT_FORCE_NONHPD 0x1u  /* builder.build_phase2 force_nonhpd hook
+                                      (builder.py:138,146-147) */
+#define HSB_OPT_UNFUSED      0x2u  /* one launch per reference section
+                                      (S1, U norm, S2, H1, H2, H3 separately,
+                                      mirror last) instead of the fused
+                                      H and S launches */
+
+typedef struct {
+  /* Output location: HSB_LOC_HOST -> h/s are host pointers,
+   * HSB_LOC_DEVICE -> device pointers.  Both n_g x n_g column-major complex128,
+   * leading dimension ld (>= n_g), FULL Hermitian (Fill.FULL). */
+  int32_t location;
+  int32_t reserved;
+  int64_t ld;
+  double* h;
+  double* s;
+} hsb_output;
+
+/* Section timings (seconds, from CUDA events) in the reference's section
+ * vocabulary (kernels.py:38 SECTIONS).  For fused launches the launch time is
+ * split across the sections it covers in proportion to model flops. */
+typedef struct {
+  double loop1, loop2, unorm, s1, s2, h1, h2, h3;
+  double h2d, d2h, total;   /* transfers (host path only) and end-to-end */
+  int32_t n_hpd, n_nonhpd;  /* builder.SplitCounts (builder.py:51-54) */
+  int32_t launches;         /* kernels launched by this call */
+  int32_t reserved;
+} hsb_timings;
+
+/* Build H and S.  `atom_info` (optional, n_atoms int32) receives the
+ * potrf_lower info per atom: 0 = Cholesky succeeded (HPD path), j>0 = first
+ * non-positive leading minor (kernels.py:296-325), -1 = forced non-HPD.
+ * Validation (probgen.validate_instance) is done by the host layer. */
+HSB_API hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p,
+                        uint32_t opts, const hsb_output* out,
+                        hsb_timings* timings, int32_t* atom_info);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HSB200_H */

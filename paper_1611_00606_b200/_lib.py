@@ -1,0 +1,132 @@
+"""ctypes binding of libhsb200.so (the C ABI declared in include/hsb200.h).
+
+There is no fallback: if the shared library is missing or cannot be loaded
+the import of anything that needs it raises ``RuntimeError``.  Build it with
+``python -m paper_1611_00606_b200._build`` (``__graft_entry__.build()``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from pathlib import Path
+
+from .hs_types import DimensionError, InputError, InvariantError
+
+LIB_PATH = Path(__file__).resolve().parent / "libhsb200.so"
+
+HSB_OK, HSB_ERR_DIMENSION, HSB_ERR_INPUT, HSB_ERR_INVARIANT = 0, 1, 2, 3
+HSB_ERR_CUDA, HSB_ERR_UNSUPPORTED, HSB_ERR_NOMEM = 4, 5, 6
+
+HSB_LOWER_ONLY = 0x1
+HSB_MIRROR = 0x2
+HSB_LOC_HOST = 0
+HSB_LOC_DEVICE = 1
+HSB_OPT_FORCE_NONHPD = 0x1
+HSB_OPT_UNFUSED = 0x2
+
+_P = ctypes.c_void_p
+_DPP = ctypes.POINTER(ctypes.c_void_p)
+
+
+class HsbProblem(ctypes.Structure):
+    _fields_ = [
+        ("n_atoms", ctypes.c_int64), ("n_l", ctypes.c_int64), ("n_g", ctypes.c_int64),
+        ("location", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("a_blocks", _DPP), ("b_blocks", _DPP), ("t_aa", _DPP), ("t_ab", _DPP),
+        ("t_bb", _DPP), ("u_norms", _DPP),
+        ("a_stack", _P), ("b_stack", _P), ("t_aa_dev", _P), ("t_ab_dev", _P),
+        ("t_bb_dev", _P), ("u_dev", _P),
+    ]
+
+
+class HsbOutput(ctypes.Structure):
+    _fields_ = [("location", ctypes.c_int32), ("reserved", ctypes.c_int32), ("ld", ctypes.c_int64),
+                ("h", _P), ("s", _P)]
+
+
+class HsbTimings(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in
+                ("loop1", "loop2", "unorm", "s1", "s2", "h1", "h2", "h3", "h2d", "d2h", "total")] + [
+        ("n_hpd", ctypes.c_int32), ("n_nonhpd", ctypes.c_int32), ("launches", ctypes.c_int32),
+        ("reserved", ctypes.c_int32)]
+
+
+_lib = None
+_lock = threading.Lock()
+_ctxs: dict[int, ctypes.c_void_p] = {}
+
+
+def load():
+    """Load libhsb200.so once and declare the prototypes."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: the B200 kernels are not built "
+                "(run `python -m paper_1611_00606_b200._build`); there is no CPU fallback")
+        lib = ctypes.CDLL(os.fspath(LIB_PATH))
+        i32, i64, dbl, u32 = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_uint32
+        ch = ctypes.c_char
+        sig = {
+            "hsb_abi_version": (i32, []),
+            "hsb_ctx_create": (i32, [i32, ctypes.POINTER(ctypes.c_void_p)]),
+            "hsb_ctx_destroy": (None, [_P]),
+            "hsb_last_error": (ctypes.c_char_p, [_P]),
+            "hsb_ctx_trim": (i32, [_P]),
+            "hsb_zherk": (i32, [_P, _P, i64, i64, dbl, _P, i64, dbl, _P, i64, u32]),
+            "hsb_zher2k": (i32, [_P, _P, i64, i64, dbl, dbl, _P, i64, _P, i64, dbl, _P, i64, u32]),
+            "hsb_zgemm": (i32, [_P, _P, ch, ch, i64, i64, i64, dbl, dbl, _P, i64, _P, i64, dbl, dbl,
+                                _P, i64, u32]),
+            "hsb_hermitian_mirror": (i32, [_P, _P, i64, _P, i64]),
+            "hsb_build_hs": (i32, [_P, _P, ctypes.POINTER(HsbProblem), u32, ctypes.POINTER(HsbOutput),
+                                   ctypes.POINTER(HsbTimings), ctypes.POINTER(ctypes.c_int32)]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if lib.hsb_abi_version() != 1:
+            raise RuntimeError("libhsb200.so ABI version mismatch; rebuild it")
+        _lib = lib
+        return lib
+
+
+def check(status: int, ctx) -> None:
+    """Map an hsb_status onto the reference's exception classes."""
+    if status == HSB_OK:
+        return
+    msg = (load().hsb_last_error(ctx) or b"").decode(errors="replace")
+    if status == HSB_ERR_DIMENSION:
+        raise DimensionError(msg)
+    if status == HSB_ERR_INPUT:
+        raise InputError(msg)
+    if status == HSB_ERR_INVARIANT:
+        raise InvariantError(msg)
+    raise RuntimeError(f"libhsb200 error {status}: {msg}")
+
+
+def context(device: int = 0):
+    """Process-wide context for ``device`` (created on first use)."""
+    lib = load()
+    with _lock:
+        ctx = _ctxs.get(device)
+        if ctx is None:
+            out = ctypes.c_void_p()
+            check(lib.hsb_ctx_create(device, ctypes.byref(out)), None)
+            ctx = out
+            _ctxs[device] = ctx
+        return ctx
+
+
+def release_all() -> None:
+    lib = load()
+    with _lock:
+        for ctx in _ctxs.values():
+            lib.hsb_ctx_destroy(ctx)
+        _ctxs.clear()

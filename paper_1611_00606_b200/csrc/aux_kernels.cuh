@@ -1,0 +1,25 @@
+// aux_kernels.cuh — launchers for the small / memory-bound kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "zrk.cuh"
+
+namespace hsb {
+
+constexpr size_t kPotrfSmemMax = 200 * 1024;  // packed lower triangle up to n = 158
+
+cudaError_t launch_zrk(const ZrkParams& p, bool conj, int grid_x, int grid_z, cudaStream_t st);
+cudaError_t launch_potrf_route(const double* t_aa, double* q, int32_t* info, int n_atoms, int n,
+                               bool force_nonhpd, double* gscratch, cudaStream_t st);
+cudaError_t launch_half_mirror(const double* t, double* out, int n, int64_t count, double scale,
+                               cudaStream_t st);
+cudaError_t launch_diag_scale(const double* src, int64_t lds, double* dst, int64_t ldd, const double* u,
+                              int64_t rows, int64_t cols, cudaStream_t st);
+cudaError_t launch_mirror(double* c, int64_t ldc, int n, cudaStream_t st);
+cudaError_t launch_gather_rows(const double* src, int64_t lds, double* dst, int64_t ldd, const int32_t* src_off,
+                               const int32_t* dst_off, int n_blocks, int n_l, int64_t cols, cudaStream_t st);
+cudaError_t launch_transpose(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols,
+                             bool conj, cudaStream_t st);
+
+}  // namespace hsb

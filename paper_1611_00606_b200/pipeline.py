@@ -1,0 +1,239 @@
+"""``build_hs`` — the drop-in for ``hsgen.builder.build_hs`` on one B200.
+
+Reference: /root/reference/pkg/src/hsgen/builder.py:211-224 (and the phases it
+calls, builder.py:73-208).  Same signature, same contracts:
+
+* validates the instance first and raises ``InvariantError`` (probgen.py:140);
+* never mutates the instance's A/B blocks (restore contract);
+* returns FULL Hermitian H and S (``Fill.FULL``);
+* ``SplitCounts(hpd, nonhpd)`` with hpd + nonhpd = n_atoms;
+* one ``FlopRecord`` per reference kernel call, in the reference's order,
+  so ledger totals equal ``section_flops(dims, nonhpd)`` and the first-seen
+  section order is Loop 1, H1, S1, U norm, S2, Loop 2, H2, H3;
+* honours ``force_nonhpd`` (builder.py:138,146-147).
+
+All arithmetic runs in libhsb200.so (hand-written sm_100a kernels, see
+csrc/); this module only marshals pointers and builds the ledger.  Record
+``seconds`` come from CUDA events: batched per-atom launches and fused
+launches are split over their records in proportion to model flops.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .hs_types import Dims, Fill, HermitianResult, InputError, SplitCounts
+from .instances import validate_instance
+from .ledger import FlopLedger, KernelKind, flops_of
+
+
+@dataclass(frozen=True)
+class GpuPolicy:
+    """Device selection and launch strategy for the B200 build.
+
+    A separate type rather than a new ``ExecPolicy.mode`` value, because the
+    reference rejects unknown modes (executor.py:38-39, test_executor.py:18-19).
+    ``fused`` runs H and S as one launch each (mirror fused into the
+    epilogue); ``fused=False`` runs one launch per reference section.
+    """
+
+    device: int = 0
+    fused: bool = True
+
+    def __post_init__(self):
+        if int(self.device) != self.device or self.device < 0:
+            raise InputError(f"device must be a nonnegative integer, got {self.device!r}")
+
+
+@dataclass
+class BuildOutput:
+    h: HermitianResult
+    s: HermitianResult
+    split: SplitCounts
+    ledger: FlopLedger
+    timings: dict | None = None
+
+
+def _policy(policy) -> GpuPolicy:
+    # Accept the reference's ExecPolicy (or None) for signature compatibility.
+    return policy if isinstance(policy, GpuPolicy) else GpuPolicy()
+
+
+def _f_c16(m) -> np.ndarray:
+    a = np.asarray(m)
+    if a.dtype != np.complex128 or not a.flags.f_contiguous:
+        a = np.asfortranarray(a, dtype=np.complex128)
+    return a
+
+
+def _ptr_array(arrays) -> ctypes.Array:
+    return (ctypes.c_void_p * len(arrays))(*[a.ctypes.data for a in arrays])
+
+
+def _timings_dict(t: _lib.HsbTimings) -> dict:
+    return {name: getattr(t, name) for name, _ in _lib.HsbTimings._fields_ if name != "reserved"}
+
+
+def ledger_from_timings(dims: Dims, info, t: dict, force_nonhpd: bool) -> FlopLedger:
+    """Reference-ordered ledger (builder.py:73-208) from section timings."""
+    n_a, n_l, n_g = dims.n_atoms, dims.n_l, dims.n_g
+    k = n_a * n_l
+    hpd = [int(i) == 0 for i in info]
+    led = FlopLedger()
+    loop1 = []
+    for _ in range(n_a):
+        loop1 += [(KernelKind.GEMM, (n_l, n_g, n_l)), (KernelKind.HEMM, (n_l, n_g))]
+    _emit_named(led, t["loop1"], "Loop 1", loop1)
+    _emit_named(led, t["h1"], "H1", [(KernelKind.HER2K, (n_g, k))])
+    _emit_named(led, t["s1"], "S1", [(KernelKind.HERK, (n_g, k))])
+    _emit_named(led, t["unorm"], "U norm", [(KernelKind.DIAG_SCALE, (k, n_g))])
+    _emit_named(led, t["s2"], "S2", [(KernelKind.HERK, (n_g, k))])
+    loop2 = []
+    for ok in hpd:
+        if ok:
+            loop2 += [(KernelKind.POTRF, (n_l,)), (KernelKind.TRMM, (n_l, n_g))]
+        else:
+            loop2 += [(KernelKind.HEMM, (n_l, n_g))]
+    _emit_named(led, t["loop2"], "Loop 2", loop2)
+    n_hpd = sum(hpd)
+    if n_hpd < n_a:
+        _emit_named(led, t["h2"], "H2", [(KernelKind.GEMM, (n_g, n_g, (n_a - n_hpd) * n_l))])
+    if n_hpd:
+        _emit_named(led, t["h3"], "H3", [(KernelKind.HERK, (n_g, n_hpd * n_l))])
+    return led
+
+
+def _emit_named(led: FlopLedger, seconds: float, section: str, records) -> None:
+    total = sum(flops_of(kind, d) for kind, d in records) or 1
+    for kind, d in records:
+        led.add(kind, d, max(0.0, seconds) * flops_of(kind, d) / total, section)
+
+
+def build_hs(p, policy=None, force_nonhpd: bool = False) -> BuildOutput:
+    """Assemble H and S on the GPU from host-resident per-atom blocks."""
+    validate_instance(p)
+    pol = _policy(policy)
+    lib = _lib.load()
+    ctx = _lib.context(pol.device)
+    dims = Dims(p.dims.n_atoms, p.dims.n_l, p.dims.n_g)
+    n_a, n_l, n_g = dims.n_atoms, dims.n_l, dims.n_g
+
+    blocks = {name: [_f_c16(m) for m in getattr(p, name)]
+              for name in ("a_blocks", "b_blocks", "t_aa", "t_ab", "t_bb")}
+    u = [np.ascontiguousarray(np.asarray(v, dtype=np.float64)) for v in p.u_norms]
+    arrays = {name: _ptr_array(v) for name, v in blocks.items()}
+    arrays["u_norms"] = _ptr_array(u)
+
+    prob = _lib.HsbProblem()
+    prob.n_atoms, prob.n_l, prob.n_g = n_a, n_l, n_g
+    prob.location = _lib.HSB_LOC_HOST
+    for name in ("a_blocks", "b_blocks", "t_aa", "t_ab", "t_bb", "u_norms"):
+        setattr(prob, name, ctypes.cast(arrays[name], ctypes.POINTER(ctypes.c_void_p)))
+
+    h = np.empty((n_g, n_g), dtype=np.complex128, order="F")
+    s = np.empty((n_g, n_g), dtype=np.complex128, order="F")
+    out = _lib.HsbOutput()
+    out.location = _lib.HSB_LOC_HOST
+    out.ld = n_g
+    out.h = h.ctypes.data
+    out.s = s.ctypes.data
+
+    opts = (_lib.HSB_OPT_FORCE_NONHPD if force_nonhpd else 0) | (0 if pol.fused else _lib.HSB_OPT_UNFUSED)
+    tim = _lib.HsbTimings()
+    info = (ctypes.c_int32 * n_a)()
+    _lib.check(lib.hsb_build_hs(ctx, None, ctypes.byref(prob), opts, ctypes.byref(out),
+                                ctypes.byref(tim), info), ctx)
+    t = _timings_dict(tim)
+    led = ledger_from_timings(dims, list(info), t, force_nonhpd)
+    return BuildOutput(HermitianResult(h, Fill.FULL), HermitianResult(s, Fill.FULL),
+                       SplitCounts(tim.n_hpd, tim.n_nonhpd), led, t)
+
+
+# ---------------------------------------------------------------- device path
+
+@dataclass
+class DeviceProblem:
+    """Stacked, device-resident instance (torch tensors as plain device memory).
+
+    Column-major K x n_g matrices are stored as row-major (n_g, K) tensors,
+    so ``a_stack`` is exactly ``matcore.stack(p.a_blocks)`` in memory.
+    """
+
+    dims: Dims
+    a_stack: object   # torch.complex128 (n_g, K)
+    b_stack: object
+    t_aa: object      # torch.complex128 (n_atoms, n_l, n_l), [a] = column-major T_a
+    t_ab: object
+    t_bb: object
+    u: object         # torch.float64 (K,)
+
+    @classmethod
+    def from_instance(cls, p, device: int = 0) -> "DeviceProblem":
+        import torch
+
+        validate_instance(p)
+        dims = Dims(p.dims.n_atoms, p.dims.n_l, p.dims.n_g)
+        dev = torch.device("cuda", device)
+
+        def stack_t(blocks):
+            host = np.concatenate([np.asarray(b, dtype=np.complex128).T for b in blocks], axis=1)
+            return torch.from_numpy(np.ascontiguousarray(host)).to(dev)
+
+        def mats(blocks):
+            host = np.stack([np.asarray(b, dtype=np.complex128).T for b in blocks])
+            return torch.from_numpy(np.ascontiguousarray(host)).to(dev)
+
+        u = torch.from_numpy(np.concatenate([np.asarray(x, dtype=np.float64) for x in p.u_norms])).to(dev)
+        return cls(dims, stack_t(p.a_blocks), stack_t(p.b_blocks), mats(p.t_aa), mats(p.t_ab),
+                   mats(p.t_bb), u)
+
+
+def build_hs_device(dp: DeviceProblem, h=None, s=None, policy=None, force_nonhpd: bool = False,
+                    stream=None):
+    """Device-resident build: returns (H, S, SplitCounts, timings, atom_info).
+
+    H and S are torch complex128 (n_g, n_g) tensors holding the column-major
+    matrices (i.e. ``H.T`` is the matrix; for Hermitian H this equals
+    ``H.conj()``).  Inputs are not modified.
+    """
+    import torch
+
+    pol = _policy(policy)
+    lib = _lib.load()
+    ctx = _lib.context(pol.device)
+    n_a, n_l, n_g = dp.dims.n_atoms, dp.dims.n_l, dp.dims.n_g
+    k = n_a * n_l
+    dev = dp.a_stack.device
+    for name, shape, dtype in (("a_stack", (n_g, k), torch.complex128), ("b_stack", (n_g, k), torch.complex128),
+                               ("t_aa", (n_a, n_l, n_l), torch.complex128),
+                               ("t_ab", (n_a, n_l, n_l), torch.complex128),
+                               ("t_bb", (n_a, n_l, n_l), torch.complex128), ("u", (k,), torch.float64)):
+        tns = getattr(dp, name)
+        if tuple(tns.shape) != shape or tns.dtype != dtype or not tns.is_contiguous() or tns.device != dev:
+            raise InputError(f"{name} must be a contiguous {dtype} tensor of shape {shape} on {dev}")
+    if h is None:
+        h = torch.empty((n_g, n_g), dtype=torch.complex128, device=dev)
+    if s is None:
+        s = torch.empty((n_g, n_g), dtype=torch.complex128, device=dev)
+    prob = _lib.HsbProblem()
+    prob.n_atoms, prob.n_l, prob.n_g = n_a, n_l, n_g
+    prob.location = _lib.HSB_LOC_DEVICE
+    prob.a_stack, prob.b_stack = dp.a_stack.data_ptr(), dp.b_stack.data_ptr()
+    prob.t_aa_dev, prob.t_ab_dev, prob.t_bb_dev = dp.t_aa.data_ptr(), dp.t_ab.data_ptr(), dp.t_bb.data_ptr()
+    prob.u_dev = dp.u.data_ptr()
+    out = _lib.HsbOutput()
+    out.location = _lib.HSB_LOC_DEVICE
+    out.ld = n_g
+    out.h, out.s = h.data_ptr(), s.data_ptr()
+    if stream is None:
+        stream = torch.cuda.current_stream(dev)
+    opts = (_lib.HSB_OPT_FORCE_NONHPD if force_nonhpd else 0) | (0 if pol.fused else _lib.HSB_OPT_UNFUSED)
+    tim = _lib.HsbTimings()
+    info = (ctypes.c_int32 * n_a)()
+    _lib.check(lib.hsb_build_hs(ctx, ctypes.c_void_p(stream.cuda_stream), ctypes.byref(prob), opts,
+                                ctypes.byref(out), ctypes.byref(tim), info), ctx)
+    return h, s, SplitCounts(tim.n_hpd, tim.n_nonhpd), _timings_dict(tim), list(info)

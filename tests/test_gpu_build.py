@@ -1,0 +1,130 @@
+"""Pipeline-level parity on the B200: build_hs (the drop-in for
+hsgen.builder.build_hs) against the reference's own outputs
+(tests/golden/, produced by running hsgen) and against the CPU oracle.
+Tolerance: relative Frobenius 1e-10 on H and S (north star)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_cases, load_case
+from oracle import alg1, brute
+from paper_1611_00606_b200 import (
+    CONFIGS, DeviceProblem, Dims, Fill, GpuPolicy, InvariantError, ProblemInstance, ProblemSpec, build_hs,
+    build_hs_device, generate, rel_frob_error, section_flops,
+)
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("name", golden_cases())
+def test_build_matches_reference_golden(name, fused):
+    p, fx, meta = load_case(name)
+    out = build_hs(p, GpuPolicy(fused=fused), force_nonhpd=meta["force_nonhpd"])
+    assert [out.split.hpd, out.split.nonhpd] == fx["split"].tolist()
+    assert rel_frob_error(out.h.matrix, fx["h"]) < TOL
+    assert rel_frob_error(out.s.matrix, fx["s"]) < TOL
+    if "h_ref" in fx:  # the reference's brute-force oracle
+        assert rel_frob_error(out.h.matrix, fx["h_ref"]) < TOL
+        assert rel_frob_error(out.s.matrix, fx["s_ref"]) < TOL
+    assert out.h.fill is Fill.FULL and out.s.fill is Fill.FULL
+    out.h.check()
+    out.s.check()
+    assert [r.kind.value for r in out.ledger] == [str(k) for k in fx["ledger_kind"]]
+    assert [r.section for r in out.ledger] == [str(s) for s in fx["ledger_section"]]
+    assert out.ledger.total_flops() == int(fx["ledger_flops"].sum())
+
+
+def _scalar_instance(a, b, t, u, v, w):
+    inst = ProblemInstance(Dims(1, 1, 1))
+    inst.a_blocks.append(np.array([[a]], dtype=complex, order="F"))
+    inst.b_blocks.append(np.array([[b]], dtype=complex, order="F"))
+    inst.t_aa.append(np.array([[t]], dtype=complex, order="F"))
+    inst.t_ab.append(np.array([[u]], dtype=complex, order="F"))
+    inst.t_bb.append(np.array([[v]], dtype=complex, order="F"))
+    inst.u_norms.append(np.array([w], dtype=float))
+    return inst
+
+
+def test_scalar_closed_form():
+    # pkg/tests/test_builder.py:242-248: H = t + 2 Re(u) + v, S = 1 + w^2
+    t, v, w, u = 0.7, 1.3, 0.6, 0.2 - 0.4j
+    out = build_hs(_scalar_instance(1.0, 1.0, t, u, v, w))
+    np.testing.assert_allclose(out.h.matrix, [[t + 2 * u.real + v]], rtol=1e-14)
+    np.testing.assert_allclose(out.s.matrix, [[1 + w**2]], rtol=1e-14)
+
+
+@pytest.mark.parametrize("dims,frac", [((1, 2, 4), 0.0), ((6, 12, 48), 0.5), ((3, 81, 200), 1.0),
+                                       ((2, 130, 70), 0.5), ((9, 16, 1), 0.0)])
+def test_build_sweep_against_brute_oracle(dims, frac):
+    p = generate(ProblemSpec(Dims(*dims), seed=sum(dims), nonhpd_fraction=frac))
+    out = build_hs(p)
+    assert rel_frob_error(out.h.matrix, brute.h_brute(p)) < TOL
+    assert rel_frob_error(out.s.matrix, brute.s_brute(p)) < TOL
+    assert out.split.hpd + out.split.nonhpd == dims[0]
+
+
+def test_c2_against_alg1_oracle():
+    p = generate(ProblemSpec(CONFIGS["C2"], seed=0, nonhpd_fraction=0.25))
+    out = build_hs(p)
+    ref = alg1.build_hs_cpu(p)
+    assert (out.split.hpd, out.split.nonhpd) == (ref["hpd"], ref["nonhpd"])
+    assert rel_frob_error(out.h.matrix, ref["h"]) < TOL
+    assert rel_frob_error(out.s.matrix, ref["s"]) < TOL
+    tot = out.ledger.section_totals()
+    assert {k: v[0] for k, v in tot.items()} == {k: v for k, v in section_flops(p.dims, ref["nonhpd"]).items() if v}
+
+
+def test_forced_branch_matches_cholesky_path():
+    # acceptance criterion 4 (pkg/tests/test_acceptance.py:72-87)
+    p = generate(ProblemSpec(Dims(4, 24, 150), seed=1000, nonhpd_fraction=0.0))
+    normal = build_hs(p)
+    forced = build_hs(p, force_nonhpd=True)
+    assert normal.split.nonhpd == 0 and forced.split.hpd == 0
+    assert rel_frob_error(forced.h.matrix, normal.h.matrix) < 1e-10
+    assert "H2" in forced.ledger.section_totals() and "H3" not in forced.ledger.section_totals()
+
+
+def test_restore_contract_and_determinism():
+    p = generate(ProblemSpec(Dims(3, 20, 140), seed=17, nonhpd_fraction=0.5))
+    before = [m.tobytes() for m in (*p.a_blocks, *p.b_blocks)]
+    o1 = build_hs(p)
+    o2 = build_hs(p)
+    assert [m.tobytes() for m in (*p.a_blocks, *p.b_blocks)] == before
+    # same kernels, same schedule: bitwise reproducible (cf. criterion 5)
+    assert o1.h.matrix.tobytes() == o2.h.matrix.tobytes()
+    assert o1.s.matrix.tobytes() == o2.s.matrix.tobytes()
+
+
+def test_rejects_invalid_instance_before_work():
+    p = generate(ProblemSpec(Dims(2, 3, 4), seed=20))
+    p.t_aa[0][0, 1] += 1.0
+    with pytest.raises(InvariantError):
+        build_hs(p)
+
+
+def test_psd_and_hermitian():
+    # acceptance criterion 6 (pkg/tests/test_acceptance.py:119-133)
+    for seed, frac in ((0, 0.0), (1, 0.5), (2, 1.0)):
+        out = build_hs(generate(ProblemSpec(Dims(4, 8, 64), seed=seed, nonhpd_fraction=frac)))
+        out.h.check()
+        out.s.check()
+        s = out.s.matrix
+        assert np.linalg.eigvalsh(s)[0] >= -1e-10 * np.linalg.norm(s)
+
+
+def test_device_path_matches_host_path():
+    import torch
+
+    p = generate(ProblemSpec(Dims(5, 49, 333), seed=4, nonhpd_fraction=0.4))
+    host = build_hs(p)
+    dp = DeviceProblem.from_instance(p)
+    h, s, split, t, info = build_hs_device(dp)
+    torch.cuda.synchronize()
+    hm = h.cpu().numpy().T
+    sm = s.cpu().numpy().T
+    assert (split.hpd, split.nonhpd) == (host.split.hpd, host.split.nonhpd)
+    assert rel_frob_error(hm, host.h.matrix) < 1e-14
+    assert rel_frob_error(sm, host.s.matrix) < 1e-14
+    assert t["launches"] >= 5

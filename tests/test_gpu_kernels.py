@@ -1,0 +1,104 @@
+"""Kernel-level parity on the B200: the DMMA contraction kernel through the
+C ABI (via the run_partitioned drop-in) against the reference's own kernel
+outputs (tests/golden/kernels.npz) and the CPU oracle at larger sizes.
+Tolerance: relative Frobenius 1e-12 (north star requires <= 1e-10)."""
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from oracle import kernels as ok
+from paper_1611_00606_b200 import DimensionError, InputError, KernelKind, rel_frob_error, run_partitioned
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def g():
+    with np.load(GOLDEN / "kernels.npz") as z:
+        return {k: z[k] for k in z.files}
+
+
+def _cm(rng, r, c):
+    return np.asfortranarray(rng.standard_normal((r, c)) + 1j * rng.standard_normal((r, c)))
+
+
+def test_herk_matches_reference_kernel(g):
+    i = 0
+    while f"herk{i}_a" in g:
+        alpha, beta = (float(x) for x in g[f"herk{i}_ab"])
+        c = g[f"herk{i}_c"].copy(order="F")
+        res = run_partitioned(KernelKind.HERK, (alpha, g[f"herk{i}_a"], beta, c))
+        assert rel_frob_error(c, g[f"herk{i}_out"]) < TOL, i
+        assert res.seconds >= 0 and res.n_tiles >= 1
+        i += 1
+
+
+def test_her2k_matches_reference_kernel(g):
+    i = 0
+    while f"her2k{i}_z" in g:
+        alpha, beta = g[f"her2k{i}_ab"]
+        c = g[f"her2k{i}_c"].copy(order="F")
+        run_partitioned(KernelKind.HER2K, (complex(alpha), g[f"her2k{i}_z"], g[f"her2k{i}_b"], beta.real, c))
+        assert rel_frob_error(c, g[f"her2k{i}_out"]) < TOL, i
+        assert np.all(np.diagonal(c).imag == 0)
+        i += 1
+
+
+def test_gemm_all_ops_match_reference_kernel(g):
+    i = 0
+    while f"gemm{i}_a" in g:
+        opa, opb = (str(x) for x in g[f"gemm{i}_ops"])
+        alpha, beta = g[f"gemm{i}_ab"]
+        c = g[f"gemm{i}_c"].copy(order="F")
+        run_partitioned(KernelKind.GEMM, (complex(alpha), opa, g[f"gemm{i}_a"], opb, g[f"gemm{i}_b"],
+                                          complex(beta), c))
+        assert rel_frob_error(c, g[f"gemm{i}_out"]) < TOL, (i, opa, opb)
+        i += 1
+
+
+@pytest.mark.parametrize("k,n", [(1, 1), (3, 64), (8, 65), (121, 127), (257, 300), (2000, 700)])
+def test_herk_against_oracle_sizes(k, n):
+    rng = np.random.default_rng(k * 1000 + n)
+    a = _cm(rng, k, n)
+    c = _cm(rng, n, n)
+    want = ok.herk(1.0, a, 0.5, c)
+    run_partitioned(KernelKind.HERK, (1.0, a, 0.5, c))
+    assert rel_frob_error(c, want) < TOL
+
+
+@pytest.mark.parametrize("k,n", [(5, 33), (242, 190), (1000, 513)])
+def test_her2k_against_oracle_sizes(k, n):
+    rng = np.random.default_rng(7 + k + n)
+    z, b = _cm(rng, k, n), _cm(rng, k, n)
+    c = _cm(rng, n, n)
+    want = ok.her2k(1.0, z, b, 0.0, c)
+    run_partitioned(KernelKind.HER2K, (1.0, z, b, 0.0, c))
+    assert rel_frob_error(c, want) < TOL
+
+
+def test_zero_alpha_and_empty_reduction_follow_blas():
+    rng = np.random.default_rng(3)
+    a = _cm(rng, 4, 9)
+    c = _cm(rng, 9, 9)
+    want = ok.herk(0.0, a, 2.0, c)
+    run_partitioned(KernelKind.HERK, (0.0, a, 2.0, c))
+    assert rel_frob_error(c, want) < TOL
+    c2 = _cm(rng, 9, 9)
+    want2 = ok.gemm(1.0, "C", np.zeros((0, 9), complex), "N", np.zeros((0, 9), complex), 0.0, c2)
+    run_partitioned(KernelKind.GEMM, (1.0, "C", np.zeros((0, 9), complex), "N", np.zeros((0, 9), complex), 0.0, c2))
+    assert np.array_equal(c2, want2)
+
+
+def test_errors_match_reference_classes():
+    rng = np.random.default_rng(4)
+    a = _cm(rng, 4, 5)
+    with pytest.raises(DimensionError):
+        run_partitioned(KernelKind.HERK, (1.0, a, 0.0, _cm(rng, 4, 4)))
+    with pytest.raises(InputError):
+        run_partitioned(KernelKind.HERK, (1.0 + 1j, a, 0.0, _cm(rng, 5, 5)))
+    with pytest.raises(InputError):
+        run_partitioned(KernelKind.GEMM, (1.0, "X", a, "N", a, 0.0, _cm(rng, 5, 5)))
+    with pytest.raises(InputError):
+        run_partitioned(KernelKind.POTRF, (a,))

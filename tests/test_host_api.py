@@ -1,0 +1,120 @@
+"""Host-side logic of the drop-in boundary (no GPU): types, generator,
+validation, flop model and the ledger the GPU build reports."""
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import golden_cases, load_case
+from paper_1611_00606_b200 import (
+    CONFIGS, Dims, Fill, GpuPolicy, HermitianResult, InputError, InvariantError, KernelKind, ProblemSpec,
+    generate, heavy_fraction, preset_dims, rel_frob_error, section_flops, total_model_flops, validate_instance,
+)
+from paper_1611_00606_b200.ledger import flops_of
+from paper_1611_00606_b200.pipeline import ledger_from_timings
+
+
+def test_flops_of_frozen_values():
+    # pkg/tests/test_kernels.py:404-413
+    assert flops_of(KernelKind.GEMM, (3, 4, 3)) == 288
+    assert flops_of(KernelKind.HER2K, (9273, 512 * 49)) == 17_258_241_724_416
+    assert flops_of(KernelKind.HERK, (9273, 512 * 49)) == 8_629_120_862_208
+    assert flops_of(KernelKind.DIAG_SCALE, (1, 1)) == 2
+    assert flops_of(KernelKind.POTRF, (49,)) == 156_865
+    assert flops_of(KernelKind.POTRF, (121,)) == 2_362_081
+    assert flops_of(KernelKind.TRMM, (49, 9273)) == 4 * 49 * 49 * 9273
+    assert flops_of(KernelKind.HEMM, (49, 9273)) == 8 * 49 * 49 * 9273
+
+
+def test_config_model_flops_match_survey():
+    # SURVEY.md section 8 table (nonhpd = 0)
+    expected = {"C1": 538_431_730, "C2": 119_798_836_704, "C3": 5_031_259_458_592,
+                "C4": 124_654_541_066_368}
+    for name, flops in expected.items():
+        assert total_model_flops(CONFIGS[name], 0) == flops
+    assert heavy_fraction(preset_dims("NaCl", 4.0), 0) > 0.99
+
+
+def test_section_flops_closed_form():
+    # pkg/tests/test_report.py:106-
+    per = section_flops(Dims(4, 3, 6), 1)
+    assert per["Loop 1"] == 4 * 16 * 9 * 6
+    assert per["U norm"] == 2 * 12 * 6
+    with pytest.raises(InputError):
+        section_flops(Dims(4, 3, 6), 5)
+
+
+def test_dims_and_spec_validation():
+    with pytest.raises(InputError):
+        Dims(0, 1, 1)
+    with pytest.raises(InputError):
+        Dims(1.5, 1, 1)
+    with pytest.raises(InputError):
+        ProblemSpec(Dims(1, 1, 1), nonhpd_fraction=1.5)
+    with pytest.raises(InputError):
+        ProblemSpec(Dims(1, 1, 1), seed=-1)
+    with pytest.raises(InputError):
+        GpuPolicy(device=-1)
+
+
+def test_validate_instance_rejects_broken_inputs():
+    p = generate(ProblemSpec(Dims(2, 3, 4), seed=20))
+    validate_instance(p)
+    p.t_aa[0][0, 1] += 1.0  # pkg/tests/test_builder.py:296-300
+    with pytest.raises(InvariantError):
+        validate_instance(p)
+    p = generate(ProblemSpec(Dims(2, 3, 4), seed=20))
+    p.u_norms[1][0] = 0.0
+    with pytest.raises(InvariantError):
+        validate_instance(p)
+    p = generate(ProblemSpec(Dims(2, 3, 4), seed=20))
+    p.a_blocks[0][0, 0] = np.nan
+    with pytest.raises(InvariantError):
+        validate_instance(p)
+    p = generate(ProblemSpec(Dims(2, 3, 4), seed=20))
+    p.b_blocks.pop()
+    with pytest.raises(InvariantError):
+        validate_instance(p)
+
+
+def test_hermitian_result_check():
+    m = np.array([[1.0, 2 - 1j], [2 + 1j, 3.0]], dtype=complex, order="F")
+    HermitianResult(m, Fill.FULL).check()
+    bad = m.copy()
+    bad[0, 1] = 5
+    with pytest.raises(InvariantError):
+        HermitianResult(bad, Fill.FULL).check()
+    low = np.tril(m)
+    full = HermitianResult(low, Fill.LOWER).mirrored()
+    assert full.fill is Fill.FULL and rel_frob_error(full.matrix, m) == 0.0
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_ledger_matches_reference_ledger(name):
+    """The ledger the GPU build emits has the reference's records, in order."""
+    p, fx, meta = load_case(name)
+    dims = Dims(*meta["dims"])
+    n_hpd = int(fx["split"][0])
+    # routing: reconstruct per-atom info from the reference's Loop 2 records
+    kinds = [str(k) for k in fx["ledger_kind"]]
+    sections = [str(s) for s in fx["ledger_section"]]
+    loop2 = [k for k, s in zip(kinds, sections) if s == "Loop 2"]
+    info, i = [], 0
+    while i < len(loop2):
+        if loop2[i] == "potrf":
+            info.append(0)
+            i += 2
+        else:
+            info.append(-1 if meta["force_nonhpd"] else 1)
+            i += 1
+    assert sum(1 for x in info if x == 0) == n_hpd
+    t = {k: 1.0 for k in ("loop1", "loop2", "unorm", "s1", "s2", "h1", "h2", "h3")}
+    led = ledger_from_timings(dims, info, t, meta["force_nonhpd"])
+    assert [r.kind.value for r in led] == kinds
+    assert [r.section for r in led] == sections
+    assert [list(r.dims) for r in led] == [json.loads(str(d)) for d in fx["ledger_dims"]]
+    assert [r.flops for r in led] == fx["ledger_flops"].tolist()
+    assert led.total_flops() == sum(section_flops(dims, dims.n_atoms - n_hpd).values())
+    first_seen = list(dict.fromkeys(r.section for r in led))
+    assert first_seen == list(dict.fromkeys(sections))
