@@ -1,0 +1,327 @@
+"""Benchmark: H+S build per k-point on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+One step = one full H+S build (Algorithm 1: Loop 1, H1, S1, U norm, S2,
+Loop 2, H2/H3, mirror) for one k-point of the configured synthetic system.
+Under torchrun (N > 1) the atoms are sharded across ranks and each step ends
+with an NCCL reduce-scatter of H and S into 1-D block columns (strong
+scaling: total work fixed).
+
+Reported:
+  value       model FP64 TFLOP/s of the device-resident path (inputs already
+              in HBM; H/S left on device), max-over-ranks CUDA-event time
+  e2e         same metric through the public drop-in API with host numpy
+              inputs and outputs (H2D of every input and D2H of H and S inside
+              the timed region)
+  roofline    the dominant kernel (fused H contraction) against the measured
+              FP64 DMMA peak (profiles/fp64_peak_r01.jsonl)
+  cpu_baseline  the oracle's scipy/OpenBLAS restatement of Algorithm 1 on a
+              bounded sample, timed on this host (rank 0, N = 1 only)
+
+Model flops = sum of report.section_flops (/root/reference/pkg/src/hsgen/
+report.py:79-105), the reference's closed form.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "H+S build time per k-point (s) & FP64 TFLOP/s vs roofline at 1/2/4/8 B200"
+CONFIG_DESC = {
+    "C1": "tiny synthetic FLAPW system: 2 atoms / 1 type, lmax=6 (N_L=49), NG=500",
+    "C2": "NaCl-like cell: 8 atoms / 2 types, lmax=8 (N_L=81), NG=3000",
+    "C3": "paper-scale test: 32 atoms / 4 types, lmax=10 (N_L=121), NG=8000",
+    "C4": "large supercell: 128 atoms / 4 types, lmax=10 (N_L=121), NG=20000",
+}
+NOMINAL_FP64_TFLOPS = 37.2  # 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz
+
+
+def fp64_peak():
+    """Measured FP64 DMMA peak (probes/fp64_peak.cu, committed result)."""
+    path = ROOT / "profiles" / "fp64_peak_r01.jsonl"
+    try:
+        for line in path.read_text().splitlines():
+            rec = json.loads(line)
+            if rec.get("probe") == "dmma_sustained":
+                return rec["tflops"], f"measured FP64 DMMA sustained ({path.relative_to(ROOT)})"
+    except (OSError, ValueError):
+        pass
+    return NOMINAL_FP64_TFLOPS, "nominal FP64 (no measured peak found)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self._t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def shard(n_atoms: int, rank: int, world: int):
+    base, extra = divmod(n_atoms, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def cpu_baseline_run(dims_full, sample_ng: int, seed: int, steps: int = 1):
+    """Time the oracle (scipy/OpenBLAS Algorithm 1) on a bounded sample."""
+    from oracle import alg1
+    from paper_1611_00606_b200 import Dims, ProblemSpec, generate, total_model_flops
+
+    ng = min(sample_ng, dims_full.n_g)
+    d = Dims(dims_full.n_atoms, dims_full.n_l, ng)
+    p = generate(ProblemSpec(d, seed=seed))
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        alg1.build_hs_cpu(p)
+        times.append(time.perf_counter() - t0)
+    flops = total_model_flops(d, 0)
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max((i.get("num_threads", 1) for i in threadpool_info()), default=os.cpu_count())
+    except Exception:  # noqa: BLE001
+        threads = os.cpu_count()
+    sample = (f"{d.n_atoms} atoms x N_L={d.n_l} x NG={d.n_g} (the config's full atom/lm stack, "
+              f"NG cut to {d.n_g}); scipy-OpenBLAS ZHER2K/ZHERK Algorithm 1 (oracle/alg1.py)")
+    return times, flops, threads, sample
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle port of the reference CPU path on this host."""
+    if rank != 0:
+        return
+    from paper_1611_00606_b200 import CONFIGS
+
+    dims = CONFIGS[args.config]
+    times, flops, threads, sample = cpu_baseline_run(dims, args.cpu_sample_ng, args.seed,
+                                                     steps=args.warmup + args.steps)
+    timed = times[args.warmup:] if len(times) > args.warmup else times
+    t = sum(timed) / len(timed)
+    value = flops / t / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
+        "config": {"workload": args.config, "desc": CONFIG_DESC[args.config], "sample_ng": min(args.cpu_sample_ng, dims.n_g)},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIG_DESC))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--nonhpd-fraction", type=float, default=0.0)
+    ap.add_argument("--unfused", action="store_true", help="one launch per reference section")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-ng", type=int, default=4000)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1611_00606_b200 import (CONFIGS, DeviceProblem, Dims, GpuPolicy, ProblemSpec, build_hs,
+                                       build_hs_device, generate, section_flops, total_model_flops)
+    from paper_1611_00606_b200 import distributed as hsdist
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    dims = CONFIGS[args.config]
+    lo, hi = shard(dims.n_atoms, rank, world)
+    local = Dims(hi - lo, dims.n_l, dims.n_g)
+    p = generate(ProblemSpec(local, seed=args.seed * 1000 + rank, nonhpd_fraction=args.nonhpd_fraction))
+    policy = GpuPolicy(device=local_rank, fused=not args.unfused)
+    n_g = dims.n_g
+    ncols = -(-n_g // world) * world
+    flops_full = total_model_flops(dims, round(args.nonhpd_fraction * dims.n_atoms) if world == 1 else 0)
+
+    dp = DeviceProblem.from_instance(p, local_rank)
+    # column-major n_g x ncols outputs (row-major (ncols, n_g)); pad columns stay zero
+    h = torch.zeros((ncols, n_g), dtype=torch.complex128, device=dev)
+    s = torch.zeros((ncols, n_g), dtype=torch.complex128, device=dev)
+    if world > 1:
+        hb = torch.empty((ncols // world, n_g), dtype=torch.complex128, device=dev)
+        sb = torch.empty_like(hb)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        _, _, split, t, _ = build_hs_device(dp, h, s, policy)
+        if world > 1:
+            hsdist.reduce_scatter_block_columns(h, hb)
+            hsdist.reduce_scatter_block_columns(s, sb)
+        return t
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    ts = [step() for _ in range(args.steps)]
+    ev1.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    value = flops_full / (ms * 1e-3) / 1e12
+
+    # dominant kernel: the fused H contraction (H1 + H2 + H3 sections)
+    peak, peak_src = fp64_peak()
+    n_nh_local = int(ts[-1]["n_nonhpd"])
+    sect = section_flops(local, n_nh_local)
+    h_flops = sect["H1"] + sect["H2"] + sect["H3"]
+    h_sec = statistics.mean(t["h1"] + t["h2"] + t["h3"] for t in ts)
+    s_sec = statistics.mean(t["s1"] + t["s2"] for t in ts)
+    achieved = h_flops / h_sec / 1e12
+    launches = sum(int(t["launches"]) for t in ts)
+    traffic = None
+    prof = ROOT / "profiles" / "roofline_traffic.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get(args.config)
+        except ValueError:
+            traffic = None
+
+    # ------------------------------------------------------------ end to end
+    e2e = None
+    if not args.no_e2e:
+        if world == 1:
+            for _ in range(1):
+                build_hs(p, policy)  # warm host path / workspace
+            t0 = time.perf_counter()
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                out = build_hs(p, policy)
+                _ = out.h.matrix[0, 0]
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            wall = (time.perf_counter() - t0) / args.steps
+            e2e_ms = max(e0.elapsed_time(e1) / args.steps, wall * 1e3)
+        else:
+            e2e_ms, wall = hsdist.e2e_sharded_step_ms(p, policy, n_g, ncols, args.steps, dev)
+        h2d = sum(np.asarray(b).nbytes for name in ("a_blocks", "b_blocks", "t_aa", "t_ab", "t_bb", "u_norms")
+                  for b in getattr(p, name))
+        d2h = 2 * n_g * (ncols // world) * 16
+        e2e = {"value": flops_full / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        times, flops, threads, sample = cpu_baseline_run(dims, args.cpu_sample_ng, args.seed, steps=1)
+        cpu = {"value": flops / times[-1] / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "port",
+               "sample": sample, "seconds": times[-1]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic (seeded hsgen-compatible generator)",
+            "config": {"workload": args.config, "desc": CONFIG_DESC[args.config], "n_atoms": dims.n_atoms,
+                       "n_l": dims.n_l, "n_g": dims.n_g, "nonhpd_fraction": args.nonhpd_fraction,
+                       "parallelism": f"atom-shard x{world}" + (" + reduce-scatter" if world > 1 else ""),
+                       "fused": not args.unfused, "model_tflop_per_step": flops_full / 1e12,
+                       "l2_note": "inputs larger than L2 (A/B stacks 496 MB each at C3)"},
+            "gpu_launches": launches,
+            "roofline": {"bound": "tensor", "kernel": "zrk_kernel<conj> fused H = Z^H B + B^H Z + Y^H Y",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "peak_source": peak_src, "traffic": traffic,
+                         "model_flops_per_launch": h_flops, "avg_launch_ms": h_sec * 1e3,
+                         "s_kernel_tflops": (sect["S1"] + sect["S2"]) / s_sec / 1e12},
+            "sections_ms": {k: statistics.mean(t[k] for t in ts) * 1e3
+                            for k in ("loop1", "h1", "s1", "unorm", "s2", "loop2", "h2", "h3", "total")},
+            "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,201 @@
+"""Multi-GPU H/S generation: atom sharding + reduce-scatter, and k-point replicas.
+
+No reference counterpart (the reference is single-process);
+this is the north star's part (3) and SURVEY.md section 8(e):
+
+* H and S are sums over atoms (Eqs. 6-7; linearity is tested in
+  the reference at pkg/tests/test_reference.py:141-152), so each rank builds
+  the partial H/S of its own atoms on its own GPU — the full single-GPU
+  pipeline (Loop 1, Cholesky routing, Loop 2, fused H and S contractions) —
+  and one reduce-scatter per matrix sums the partials and leaves every rank
+  the 1-D block of columns an eigensolver consumes.  Columns are padded to a
+  multiple of the world size so each rank's block is one contiguous chunk of
+  the column-major matrix (a row-major (ncols, n_g) tensor).
+* Independent k-points are replicas: rank r builds k-points r, r+P, ... with
+  no communication.
+
+One process per GPU, ``torch.distributed`` for the plumbing (NCCL on the GPU
+box; gloo in the CPU tests, which inject a CPU partial builder).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from .hs_types import Dims
+from .instances import ProblemInstance
+
+
+def atom_ranges(n_atoms: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous, size-balanced atom ranges (equal-cost atoms for nonhpd = 0)."""
+    base, extra = divmod(n_atoms, world)
+    out, lo = [], 0
+    for r in range(world):
+        hi = lo + base + (1 if r < extra else 0)
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+def balanced_atom_groups(costs, world: int) -> list[list[int]]:
+    """LPT partition of atoms by cost (HPD rows ~12 N_G^2, non-HPD ~16 N_G^2
+    per row in the model of SURVEY.md 8e); groups keep ascending atom order."""
+    bins = [[] for _ in range(world)]
+    load = [0.0] * world
+    for a in sorted(range(len(costs)), key=lambda i: (-costs[i], i)):
+        r = min(range(world), key=lambda j: (load[j], j))
+        bins[r].append(a)
+        load[r] += costs[a]
+    return [sorted(b) for b in bins]
+
+
+def shard_instance(p, atoms) -> ProblemInstance:
+    """View of ``p`` restricted to the given atoms (no copies of the blocks)."""
+    atoms = list(atoms)
+    q = ProblemInstance(Dims(max(1, len(atoms)), p.dims.n_l, p.dims.n_g))
+    for name in ("a_blocks", "b_blocks", "t_aa", "t_ab", "t_bb", "u_norms"):
+        setattr(q, name, [getattr(p, name)[a] for a in atoms])
+    return q
+
+
+def padded_columns(n_g: int, world: int) -> int:
+    return -(-n_g // world) * world
+
+
+def reduce_scatter_block_columns(full, block, group=None) -> None:
+    """block <- this rank's column block of sum_ranks(full).
+
+    ``full`` is a row-major (ncols, n_g) complex128 tensor = column-major
+    n_g x ncols matrix; ``block`` is (ncols / world, n_g).  Complex sums are
+    float64 sums over interleaved (re, im), so the real view is reduced.
+    """
+    import torch
+    import torch.distributed as dist
+
+    dist.reduce_scatter_tensor(torch.view_as_real(block), torch.view_as_real(full), op=dist.ReduceOp.SUM,
+                               group=group)
+
+
+@dataclass
+class ShardedResult:
+    h_block: object      # torch (cols_per_rank, n_g): columns [col0, col0 + cols) of H
+    s_block: object
+    col0: int
+    n_g: int
+    hpd: int             # summed over ranks
+    nonhpd: int
+    timings: dict
+
+    def columns(self, which: str = "h") -> np.ndarray:
+        """Host copy of the block as an n_g x cols column-major numpy array
+        (padding columns beyond n_g removed)."""
+        t = self.h_block if which == "h" else self.s_block
+        cols = max(0, min(t.shape[0], self.n_g - self.col0))
+        return np.asfortranarray(t[:cols].cpu().numpy().T)
+
+
+def build_hs_sharded(p, policy=None, group=None, partial=None) -> ShardedResult:
+    """Atom-sharded H/S build across the ranks of ``group``.
+
+    Every rank passes the same full instance ``p`` (or at least the blocks of
+    its own atoms).  ``partial(shard, h, s)`` fills the rank's partial H/S
+    (row-major (ncols, n_g) tensors, pad columns zero) and returns
+    (SplitCounts, timings); by default it is the GPU pipeline
+    (``pipeline.build_hs_into``).  Returns this rank's block of columns.
+    """
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    n_g = int(p.dims.n_g)
+    ncols = padded_columns(n_g, world)
+    lo, hi = atom_ranges(int(p.dims.n_atoms), world)[rank]
+    if partial is None:
+        from .pipeline import build_hs_into
+
+        dev = torch.device("cuda", torch.cuda.current_device())
+
+        def partial(shard, h, s):
+            split, t, _ = build_hs_into(shard, h, s, policy)
+            return split, t
+    else:
+        dev = torch.device("cpu")
+    h = torch.zeros((ncols, n_g), dtype=torch.complex128, device=dev)
+    s = torch.zeros_like(h)
+    t0 = time.perf_counter()
+    if hi > lo:
+        split, timings = partial(shard_instance(p, range(lo, hi)), h, s)
+        counts = [split.hpd, split.nonhpd]
+    else:  # more ranks than atoms: contribute zeros
+        timings, counts = {}, [0, 0]
+    hb = torch.empty((ncols // world, n_g), dtype=torch.complex128, device=dev)
+    sb = torch.empty_like(hb)
+    reduce_scatter_block_columns(h, hb, group)
+    reduce_scatter_block_columns(s, sb, group)
+    c = torch.tensor(counts, dtype=torch.int64, device=dev)
+    dist.all_reduce(c, group=group)
+    timings = dict(timings)
+    timings["sharded_wall"] = time.perf_counter() - t0
+    return ShardedResult(hb, sb, rank * (ncols // world), n_g, int(c[0]), int(c[1]), timings)
+
+
+def kpoint_assignment(n_kpoints: int, world: int, rank: int) -> list[int]:
+    """k-points handled by ``rank`` (round robin, no communication)."""
+    return list(range(rank, n_kpoints, world))
+
+
+def build_kpoints(instances, policy=None, group=None, builder=None):
+    """Replica-parallel builds of independent k-points: returns
+    {k-index: BuildOutput} for the k-points owned by this rank."""
+    import torch.distributed as dist
+
+    if builder is None:
+        from .pipeline import build_hs as builder
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    return {k: builder(instances[k], policy) for k in kpoint_assignment(len(instances), world, rank)}
+
+
+def e2e_sharded_step_ms(p, policy, n_g: int, ncols: int, steps: int, dev):
+    """End-to-end time per sharded step for bench.py: host blocks in (H2D in
+    the timed region), partial build, reduce-scatter, D2H of this rank's
+    H and S column blocks.  Returns (max-over-ranks ms, local wall s)."""
+    import torch
+    import torch.distributed as dist
+
+    from .pipeline import build_hs_into
+
+    world = dist.get_world_size()
+    h = torch.zeros((ncols, n_g), dtype=torch.complex128, device=dev)
+    s = torch.zeros_like(h)
+    hb = torch.empty((ncols // world, n_g), dtype=torch.complex128, device=dev)
+    sb = torch.empty_like(hb)
+    hh = torch.empty(hb.shape, dtype=hb.dtype, pin_memory=True)
+    sh = torch.empty_like(hh, pin_memory=True)
+
+    def one():
+        build_hs_into(p, h, s, policy)
+        reduce_scatter_block_columns(h, hb)
+        reduce_scatter_block_columns(s, sb)
+        hh.copy_(hb, non_blocking=True)
+        sh.copy_(sb, non_blocking=True)
+
+    one()
+    dist.barrier(device_ids=[dev.index])
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record()
+    for _ in range(steps):
+        one()
+    e1.record()
+    torch.cuda.synchronize(dev)
+    wall = (time.perf_counter() - t0) / steps
+    ms = max(e0.elapsed_time(e1) / steps, wall * 1e3)
+    tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    return float(tt.item()), wall

@@ -113,44 +113,74 @@ def _emit_named(led: FlopLedger, seconds: float, section: str, records) -> None:
         led.add(kind, d, max(0.0, seconds) * flops_of(kind, d) / total, section)
 
 
+def _host_problem(p):
+    """hsb_problem over the instance's own host blocks (no stacking copy)."""
+    n_a, n_l, n_g = int(p.dims.n_atoms), int(p.dims.n_l), int(p.dims.n_g)
+    blocks = {name: [_f_c16(m) for m in getattr(p, name)]
+              for name in ("a_blocks", "b_blocks", "t_aa", "t_ab", "t_bb")}
+    blocks["u_norms"] = [np.ascontiguousarray(np.asarray(v, dtype=np.float64)) for v in p.u_norms]
+    arrays = {name: _ptr_array(v) for name, v in blocks.items()}
+    prob = _lib.HsbProblem()
+    prob.n_atoms, prob.n_l, prob.n_g = n_a, n_l, n_g
+    prob.location = _lib.HSB_LOC_HOST
+    for name, arr in arrays.items():
+        setattr(prob, name, ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p)))
+    return prob, (blocks, arrays)
+
+
+def _call_build(pol, prob, out, stream, force_nonhpd, n_a):
+    lib = _lib.load()
+    ctx = _lib.context(pol.device)
+    opts = (_lib.HSB_OPT_FORCE_NONHPD if force_nonhpd else 0) | (0 if pol.fused else _lib.HSB_OPT_UNFUSED)
+    tim = _lib.HsbTimings()
+    info = (ctypes.c_int32 * n_a)()
+    _lib.check(lib.hsb_build_hs(ctx, stream, ctypes.byref(prob), opts, ctypes.byref(out),
+                                ctypes.byref(tim), info), ctx)
+    return tim, list(info)
+
+
 def build_hs(p, policy=None, force_nonhpd: bool = False) -> BuildOutput:
     """Assemble H and S on the GPU from host-resident per-atom blocks."""
     validate_instance(p)
     pol = _policy(policy)
-    lib = _lib.load()
-    ctx = _lib.context(pol.device)
     dims = Dims(p.dims.n_atoms, p.dims.n_l, p.dims.n_g)
-    n_a, n_l, n_g = dims.n_atoms, dims.n_l, dims.n_g
-
-    blocks = {name: [_f_c16(m) for m in getattr(p, name)]
-              for name in ("a_blocks", "b_blocks", "t_aa", "t_ab", "t_bb")}
-    u = [np.ascontiguousarray(np.asarray(v, dtype=np.float64)) for v in p.u_norms]
-    arrays = {name: _ptr_array(v) for name, v in blocks.items()}
-    arrays["u_norms"] = _ptr_array(u)
-
-    prob = _lib.HsbProblem()
-    prob.n_atoms, prob.n_l, prob.n_g = n_a, n_l, n_g
-    prob.location = _lib.HSB_LOC_HOST
-    for name in ("a_blocks", "b_blocks", "t_aa", "t_ab", "t_bb", "u_norms"):
-        setattr(prob, name, ctypes.cast(arrays[name], ctypes.POINTER(ctypes.c_void_p)))
-
-    h = np.empty((n_g, n_g), dtype=np.complex128, order="F")
-    s = np.empty((n_g, n_g), dtype=np.complex128, order="F")
+    prob, _keep = _host_problem(p)
+    h = np.empty((dims.n_g, dims.n_g), dtype=np.complex128, order="F")
+    s = np.empty((dims.n_g, dims.n_g), dtype=np.complex128, order="F")
     out = _lib.HsbOutput()
     out.location = _lib.HSB_LOC_HOST
-    out.ld = n_g
-    out.h = h.ctypes.data
-    out.s = s.ctypes.data
-
-    opts = (_lib.HSB_OPT_FORCE_NONHPD if force_nonhpd else 0) | (0 if pol.fused else _lib.HSB_OPT_UNFUSED)
-    tim = _lib.HsbTimings()
-    info = (ctypes.c_int32 * n_a)()
-    _lib.check(lib.hsb_build_hs(ctx, None, ctypes.byref(prob), opts, ctypes.byref(out),
-                                ctypes.byref(tim), info), ctx)
+    out.ld = dims.n_g
+    out.h, out.s = h.ctypes.data, s.ctypes.data
+    tim, info = _call_build(pol, prob, out, None, force_nonhpd, dims.n_atoms)
     t = _timings_dict(tim)
-    led = ledger_from_timings(dims, list(info), t, force_nonhpd)
+    led = ledger_from_timings(dims, info, t, force_nonhpd)
     return BuildOutput(HermitianResult(h, Fill.FULL), HermitianResult(s, Fill.FULL),
                        SplitCounts(tim.n_hpd, tim.n_nonhpd), led, t)
+
+
+def build_hs_into(p, h, s, policy=None, force_nonhpd: bool = False, stream=None):
+    """Host per-atom blocks in, device H/S out (torch tensors, row-major
+    (>= n_g, n_g) holding the column-major matrices).  Used by the sharded
+    multi-GPU path, whose partial H/S go straight into a reduce-scatter."""
+    import torch
+
+    validate_instance(p)
+    pol = _policy(policy)
+    n_g = int(p.dims.n_g)
+    for name, t in (("h", h), ("s", s)):
+        if t.dtype != torch.complex128 or t.dim() != 2 or t.shape[1] != n_g or t.shape[0] < n_g \
+                or not t.is_contiguous():
+            raise InputError(f"{name} must be a contiguous complex128 tensor of shape (>= {n_g}, {n_g})")
+    prob, _keep = _host_problem(p)
+    out = _lib.HsbOutput()
+    out.location = _lib.HSB_LOC_DEVICE
+    out.ld = n_g
+    out.h, out.s = h.data_ptr(), s.data_ptr()
+    if stream is None:
+        stream = torch.cuda.current_stream(h.device)
+    tim, info = _call_build(pol, prob, out, ctypes.c_void_p(stream.cuda_stream), force_nonhpd,
+                            int(p.dims.n_atoms))
+    return SplitCounts(tim.n_hpd, tim.n_nonhpd), _timings_dict(tim), info
 
 
 # ---------------------------------------------------------------- device path
@@ -203,8 +233,6 @@ def build_hs_device(dp: DeviceProblem, h=None, s=None, policy=None, force_nonhpd
     import torch
 
     pol = _policy(policy)
-    lib = _lib.load()
-    ctx = _lib.context(pol.device)
     n_a, n_l, n_g = dp.dims.n_atoms, dp.dims.n_l, dp.dims.n_g
     k = n_a * n_l
     dev = dp.a_stack.device
@@ -219,6 +247,10 @@ def build_hs_device(dp: DeviceProblem, h=None, s=None, policy=None, force_nonhpd
         h = torch.empty((n_g, n_g), dtype=torch.complex128, device=dev)
     if s is None:
         s = torch.empty((n_g, n_g), dtype=torch.complex128, device=dev)
+    for name, t in (("h", h), ("s", s)):
+        if t.dtype != torch.complex128 or t.dim() != 2 or t.shape[1] != n_g or t.shape[0] < n_g \
+                or not t.is_contiguous() or t.device != dev:
+            raise InputError(f"{name} must be a contiguous complex128 tensor of shape (>= {n_g}, {n_g})")
     prob = _lib.HsbProblem()
     prob.n_atoms, prob.n_l, prob.n_g = n_a, n_l, n_g
     prob.location = _lib.HSB_LOC_DEVICE
@@ -231,9 +263,5 @@ def build_hs_device(dp: DeviceProblem, h=None, s=None, policy=None, force_nonhpd
     out.h, out.s = h.data_ptr(), s.data_ptr()
     if stream is None:
         stream = torch.cuda.current_stream(dev)
-    opts = (_lib.HSB_OPT_FORCE_NONHPD if force_nonhpd else 0) | (0 if pol.fused else _lib.HSB_OPT_UNFUSED)
-    tim = _lib.HsbTimings()
-    info = (ctypes.c_int32 * n_a)()
-    _lib.check(lib.hsb_build_hs(ctx, ctypes.c_void_p(stream.cuda_stream), ctypes.byref(prob), opts,
-                                ctypes.byref(out), ctypes.byref(tim), info), ctx)
-    return h, s, SplitCounts(tim.n_hpd, tim.n_nonhpd), _timings_dict(tim), list(info)
+    tim, info = _call_build(pol, prob, out, ctypes.c_void_p(stream.cuda_stream), force_nonhpd, n_a)
+    return h, s, SplitCounts(tim.n_hpd, tim.n_nonhpd), _timings_dict(tim), info
