@@ -44,7 +44,7 @@ from .ledger import (
     section_flops,
     total_model_flops,
 )
-from .pipeline import BuildOutput, DeviceProblem, GpuPolicy, build_hs, build_hs_device
+from .pipeline import BuildOutput, DeviceProblem, GpuPolicy, build_hs, build_hs_device, pin_instance
 from .offload import ExecResult, run_partitioned
 
 __version__ = "0.1.0"

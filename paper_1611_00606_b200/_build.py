@@ -18,14 +18,14 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libhsb200.so"
-SOURCES = ["zrk_kernel.cu", "aux_kernels.cu", "hsb_api.cu"]
-HEADERS = ["zrk.cuh", "aux_kernels.cuh"]
+SOURCES = ["zrk_kernel.cu", "aux_kernels.cu", "staging.cu", "hsb_api.cu"]
+HEADERS = ["zrk.cuh", "aux_kernels.cuh", "staging.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-    "-Xptxas", "-warn-spills",
+    "-Xptxas", "-warn-spills", "-Xcompiler", "-fopenmp",
     f"-I{ROOT / 'include'}",
 ]
 
@@ -60,7 +60,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         objs.append(str(obj))
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
-           *objs, "-o", str(tmp)]
+           "-Xcompiler", "-fopenmp", *objs, "-lgomp", "-o", str(tmp)]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)

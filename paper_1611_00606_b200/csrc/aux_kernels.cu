@@ -196,6 +196,33 @@ __global__ void transpose_kernel(const double2* __restrict__ src, int64_t lds, d
   }
 }
 
+// dst (stacked, column g = [atom 0 rows | atom 1 rows | ...], ld = n_atoms*rows)
+//   <- raw (atom-major: n_atoms contiguous rows x cols column-major blocks)
+// i.e. matcore.stack (matcore.py:68-86) on the device, after contiguous DMAs.
+__global__ void stack_blocks_kernel(const double2* __restrict__ raw, double2* __restrict__ dst, int n_atoms,
+                                    int rows, int64_t cols) {
+  const int64_t total = static_cast<int64_t>(n_atoms) * rows * cols;
+  const int64_t K = static_cast<int64_t>(n_atoms) * rows;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t l = idx % rows;
+    const int64_t rest = idx / rows;
+    const int64_t g = rest % cols, a = rest / cols;
+    dst[g * K + a * rows + l] = raw[idx];
+  }
+}
+
+// *flag = min over blocks holding a NaN/Inf of the block index (flag starts at
+// 0x7f7f7f7f).  Device counterpart of the finiteness test in
+// probgen.validate_instance (probgen.py:155-161) for pinned uploads.
+__global__ void first_nonfinite_kernel(const unsigned long long* __restrict__ v, int64_t per_block,
+                                       int64_t total, int* __restrict__ flag) {
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if ((v[idx] & 0x7ff0000000000000ull) == 0x7ff0000000000000ull) atomicMin(flag, static_cast<int>(idx / per_block));
+  }
+}
+
 // ------------------------------------------------------------------ launchers
 static inline int grid_for(int64_t total, int threads, int max_blocks) {
   int64_t b = (total + threads - 1) / threads;
@@ -249,6 +276,25 @@ cudaError_t launch_gather_rows(const double* src, int64_t lds, double* dst, int6
   gather_rows_kernel<<<dim3(gx, n_blocks), 256, 0, st>>>(reinterpret_cast<const double2*>(src), lds,
                                                          reinterpret_cast<double2*>(dst), ldd, src_off, dst_off,
                                                          n_l, cols);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stack_blocks(const double* raw, double* dst, int n_atoms, int rows, int64_t cols,
+                                cudaStream_t st) {
+  const int64_t total = static_cast<int64_t>(n_atoms) * rows * cols;
+  stack_blocks_kernel<<<grid_for(total, 256, 148 * 32), 256, 0, st>>>(reinterpret_cast<const double2*>(raw),
+                                                                       reinterpret_cast<double2*>(dst), n_atoms,
+                                                                       rows, cols);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_first_nonfinite(const double* v, int n_blocks, int64_t doubles_per_block, int* flag,
+                                   cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(flag, 0x7f, sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  const int64_t total = static_cast<int64_t>(n_blocks) * doubles_per_block;
+  first_nonfinite_kernel<<<grid_for(total, 256, 148 * 16), 256, 0, st>>>(
+      reinterpret_cast<const unsigned long long*>(v), doubles_per_block, total, flag);
   return cudaGetLastError();
 }
 

@@ -19,6 +19,10 @@ cudaError_t launch_diag_scale(const double* src, int64_t lds, double* dst, int64
 cudaError_t launch_mirror(double* c, int64_t ldc, int n, cudaStream_t st);
 cudaError_t launch_gather_rows(const double* src, int64_t lds, double* dst, int64_t ldd, const int32_t* src_off,
                                const int32_t* dst_off, int n_blocks, int n_l, int64_t cols, cudaStream_t st);
+cudaError_t launch_stack_blocks(const double* raw, double* dst, int n_atoms, int rows, int64_t cols,
+                                cudaStream_t st);
+cudaError_t launch_first_nonfinite(const double* v, int n_blocks, int64_t doubles_per_block, int* flag,
+                                   cudaStream_t st);
 cudaError_t launch_transpose(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols,
                              bool conj, cudaStream_t st);
 

@@ -21,6 +21,8 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -29,6 +31,7 @@
 
 #include "../../include/hsb200.h"
 #include "aux_kernels.cuh"
+#include "staging.cuh"
 #include "zrk.cuh"
 
 using namespace hsb;
@@ -45,9 +48,28 @@ struct hsb_ctx {
   std::map<std::string, DevBuf> bufs;
   void* pinned = nullptr;  // small pinned host scratch (routing info / offsets)
   size_t pinned_bytes = 0;
+  hsb::Stager stager;                 // pinned-slot host<->device transfers
+  cudaStream_t copy_stream = nullptr;  // overlaps S download with the H contraction
 };
 
 static thread_local std::string g_create_err;
+
+// Host wall-clock phase stamps for diagnosing the host-buffer path.
+struct HostClock {
+  using clk = std::chrono::steady_clock;
+  bool on = std::getenv("HSB_DEBUG_TIMING") != nullptr;
+  clk::time_point t0 = clk::now(), last = t0;
+  std::string log;
+  void mark(const char* what) {
+    if (!on) return;
+    auto now = clk::now();
+    log += std::string(what) + " " + std::to_string(std::chrono::duration<double, std::milli>(now - last).count()) + " ms; ";
+    last = now;
+  }
+  void report() {
+    if (on) std::fprintf(stderr, "[hsb timing] %s\n", log.c_str());
+  }
+};
 
 namespace {
 
@@ -286,6 +308,7 @@ void hsb_ctx_destroy(hsb_ctx* ctx) {
   for (auto& kv : ctx->bufs)
     if (kv.second.ptr) cudaFree(kv.second.ptr);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   delete ctx;
 }
 
@@ -441,6 +464,52 @@ hsb_status hsb_hermitian_mirror(hsb_ctx* ctx, void* stream, int64_t n, double* c
 }
 
 // ----------------------------------------------------------------- pipeline
+namespace {
+
+// Section timeline on the compute stream: each mark closes the interval since
+// the previous mark and charges it to a section tag.
+struct Timeline {
+  std::vector<std::pair<std::string, cudaEvent_t>> marks;
+  ~Timeline() {
+    for (auto& m : marks) cudaEventDestroy(m.second);
+  }
+  cudaError_t mark(cudaStream_t st, const char* tag) {
+    cudaEvent_t e;
+    cudaError_t err = cudaEventCreate(&e);
+    if (err != cudaSuccess) return err;
+    marks.push_back({tag, e});
+    return cudaEventRecord(e, st);
+  }
+  double total(const char* tag) const {
+    double s = 0;
+    for (size_t i = 1; i < marks.size(); ++i)
+      if (marks[i].first == tag) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second);
+        s += ms * 1e-3;
+      }
+    return s;
+  }
+  double span() const {
+    float ms = 0.f;
+    if (marks.size() > 1) cudaEventElapsedTime(&ms, marks.front().second, marks.back().second);
+    return ms * 1e-3;
+  }
+};
+
+ZrkCall tri_call(double* c, int64_t ldc, int64_t n, uint32_t flags, double beta) {
+  ZrkCall z;
+  z.m = z.n = n;
+  z.triangle = true;
+  z.flags = flags;
+  z.beta_re = beta;
+  z.c = c;
+  z.ldc = ldc;
+  return z;
+}
+
+}  // namespace
+
 hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32_t opts, const hsb_output* out,
                         hsb_timings* tm, int32_t* atom_info) {
   if (!ctx) return fail(nullptr, HSB_ERR_INPUT, "ctx is NULL");
@@ -448,59 +517,49 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   const int64_t na = p->n_atoms, nl = p->n_l, ng = p->n_g;
   if (na < 1 || nl < 1 || ng < 1) return fail(ctx, HSB_ERR_INPUT, "dimensions must be positive");
   if (out->ld < ng) return fail(ctx, HSB_ERR_DIMENSION, "output leading dimension < n_g");
+  if (!out->h || !out->s) return fail(ctx, HSB_ERR_INPUT, "output pointers are NULL");
   if (na > 65535) return fail(ctx, HSB_ERR_UNSUPPORTED, "more than 65535 atoms");
   const int64_t K = na * nl;
   if (K > (int64_t{1} << 31)) return fail(ctx, HSB_ERR_UNSUPPORTED, "stack too tall");
+  if (p->location != HSB_LOC_HOST && p->location != HSB_LOC_DEVICE)
+    return fail(ctx, HSB_ERR_INPUT, "unknown problem location");
   cudaSetDevice(ctx->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!ctx->copy_stream) CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  cudaStream_t cs = ctx->copy_stream;
   const bool unfused = opts & HSB_OPT_UNFUSED;
   const bool force_nonhpd = opts & HSB_OPT_FORCE_NONHPD;
+  const bool host_in = p->location == HSB_LOC_HOST;
+  // Host inputs + fused launches: upload B, start U norm and the (UB)^H(UB)
+  // half of S, and stage A on the copy stream meanwhile.
+  const bool overlap_upload = host_in && !unfused;
   int launches = 0;
+  Timeline tl;
+  HostClock hc;  // host-side phase stamps, printed when HSB_DEBUG_TIMING is set
+  CK(tl.mark(st, "start"));
 
-  enum { E_START, E_H2D, E_POTRF, E_LOOP1, E_H1, E_S1, E_UNORM, E_S2, E_SMIR, E_LOOP2, E_H2, E_H3, E_HMIR,
-         E_D2H, E_N };
-  cudaEvent_t ev[E_N];
-  for (int i = 0; i < E_N; ++i) CK(cudaEventCreate(&ev[i]));
-  struct EvGuard {
-    cudaEvent_t* e;
-    ~EvGuard() {
-      for (int i = 0; i < E_N; ++i) cudaEventDestroy(e[i]);
-    }
-  } guard{ev};
-
-  CK(cudaEventRecord(ev[E_START], st));
-
-  // ---------------------------------------------------------------- inputs
-  const double *A, *B, *TAA, *TAB, *TBB, *U;
+  // ------------------------------------------------------------ buffers
   const size_t stack_bytes = static_cast<size_t>(K) * ng * 16;
   const size_t tblk_bytes = static_cast<size_t>(nl) * nl * 16;
-  if (p->location == HSB_LOC_HOST) {
+  const double *A, *B, *TAA, *TAB, *TBB, *U;
+  void *a_in = nullptr, *b_in = nullptr;
+  if (host_in) {
     if (!p->a_blocks || !p->b_blocks || !p->t_aa || !p->t_ab || !p->t_bb || !p->u_norms)
       return fail(ctx, HSB_ERR_INPUT, "host block arrays are NULL");
-    void *a, *b, *taa, *tab, *tbb, *u;
-    CKS(ws(ctx, "in_a", stack_bytes, &a));
-    CKS(ws(ctx, "in_b", stack_bytes, &b));
+    void *taa, *tab, *tbb, *u;
+    CKS(ws(ctx, "in_a", stack_bytes, &a_in));
+    CKS(ws(ctx, "in_b", stack_bytes, &b_in));
     CKS(ws(ctx, "in_taa", tblk_bytes * na, &taa));
     CKS(ws(ctx, "in_tab", tblk_bytes * na, &tab));
     CKS(ws(ctx, "in_tbb", tblk_bytes * na, &tbb));
     CKS(ws(ctx, "in_u", static_cast<size_t>(K) * 8, &u));
-    for (int64_t i = 0; i < na; ++i) {
-      CK(cudaMemcpy2DAsync(static_cast<char*>(a) + i * nl * 16, K * 16, p->a_blocks[i], nl * 16, nl * 16, ng,
-                           cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpy2DAsync(static_cast<char*>(b) + i * nl * 16, K * 16, p->b_blocks[i], nl * 16, nl * 16, ng,
-                           cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(static_cast<char*>(taa) + i * tblk_bytes, p->t_aa[i], tblk_bytes, cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(static_cast<char*>(tab) + i * tblk_bytes, p->t_ab[i], tblk_bytes, cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(static_cast<char*>(tbb) + i * tblk_bytes, p->t_bb[i], tblk_bytes, cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(static_cast<char*>(u) + i * nl * 8, p->u_norms[i], nl * 8, cudaMemcpyHostToDevice, st));
-    }
-    A = static_cast<double*>(a);
-    B = static_cast<double*>(b);
+    A = static_cast<double*>(a_in);
+    B = static_cast<double*>(b_in);
     TAA = static_cast<double*>(taa);
     TAB = static_cast<double*>(tab);
     TBB = static_cast<double*>(tbb);
     U = static_cast<double*>(u);
-  } else if (p->location == HSB_LOC_DEVICE) {
+  } else {
     A = p->a_stack;
     B = p->b_stack;
     TAA = p->t_aa_dev;
@@ -508,11 +567,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     TBB = p->t_bb_dev;
     U = p->u_dev;
     if (!A || !B || !TAA || !TAB || !TBB || !U) return fail(ctx, HSB_ERR_INPUT, "device arrays are NULL");
-  } else {
-    return fail(ctx, HSB_ERR_INPUT, "unknown problem location");
   }
-  CK(cudaEventRecord(ev[E_H2D], st));
-
   double *H, *S;
   int64_t ldo;
   const size_t out_bytes = static_cast<size_t>(ng) * ng * 16;
@@ -528,12 +583,9 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     S = out->s;
     ldo = out->ld;
   }
-  if (!out->h || !out->s) return fail(ctx, HSB_ERR_INPUT, "output pointers are NULL");
-
-  // ------------------------------------------------------ scratch buffers
-  void *q, *info_d, *pbb, *zbuf, *ub, *rbuf, *offs_d, *potrf_scr = nullptr;
+  void *q, *info_d, *pbb, *zbuf, *ub, *rbuf, *offs_d, *potrf_scr = nullptr, *hostbuf;
   CKS(ws(ctx, "q", tblk_bytes * na, &q));
-  CKS(ws(ctx, "info", static_cast<size_t>(na) * 4 * 4, &info_d));
+  CKS(ws(ctx, "info", static_cast<size_t>(na) * 4, &info_d));
   CKS(ws(ctx, "pbb", tblk_bytes * na, &pbb));
   CKS(ws(ctx, "z", stack_bytes, &zbuf));
   CKS(ws(ctx, "ub", stack_bytes, &ub));
@@ -541,108 +593,173 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   CKS(ws(ctx, "offs", static_cast<size_t>(na) * 3 * 4, &offs_d));
   if (static_cast<size_t>(nl) * (nl + 1) / 2 * 16 > kPotrfSmemMax)
     CKS(ws(ctx, "potrf_scr", static_cast<size_t>(na) * nl * (nl + 1) / 2 * 16, &potrf_scr));
-  void* hostbuf;
-  CKS(pinned(ctx, static_cast<size_t>(na) * 4 * 4, &hostbuf));
+  CKS(pinned(ctx, (static_cast<size_t>(na) * 4 + 2) * 4, &hostbuf));
   int32_t* info_h = static_cast<int32_t*>(hostbuf);
-  int32_t* offs_h = info_h + na;  // 3 * na entries: r row offset, anh src, anh dst
+  int32_t* offs_h = info_h + na;  // 3 * na entries: R row offset, A_nh source rows, A_nh dest rows
+  double* Z = static_cast<double*>(zbuf);
+  double* UB = static_cast<double*>(ub);
+  double* R = static_cast<double*>(rbuf);  // [Y_hpd ; X_nh]
+  int32_t* flag_h = offs_h + 3 * na;  // first non-finite atom of A / B (pinned uploads)
+  flag_h[0] = flag_h[1] = -1;
 
-  // --------------------------------------------------- Loop 2, part 1: potrf
+  auto stage_stack = [&](int m, cudaStream_t s) -> hsb_status {
+    // A (m = 0) or B (m = 1) into the stacked layout.  Pinned blocks: one
+    // contiguous DMA per atom into an atom-major buffer, then a device
+    // restack (HBM speed).  Pageable blocks: host threads gather stacked
+    // columns into pinned slots, checking finiteness on the fly
+    // (probgen.validate_instance, probgen.py:155-161).
+    const double* const* blocks = m == 0 ? p->a_blocks : p->b_blocks;
+    double* dst = static_cast<double*>(m == 0 ? a_in : b_in);
+    bool all_pinned = true;
+    for (int64_t i = 0; i < na && all_pinned; ++i) all_pinned = host_is_pinned(blocks[i]);
+    int64_t bad = -1;
+    if (all_pinned) {
+      void* raw;
+      CKS(ws(ctx, m == 0 ? "raw_a" : "raw_b", stack_bytes, &raw));
+      const size_t blk = static_cast<size_t>(nl) * ng * 16;
+      for (int64_t i = 0; i < na; ++i)
+        CK(cudaMemcpyAsync(static_cast<char*>(raw) + i * blk, blocks[i], blk, cudaMemcpyHostToDevice, s));
+      CK(launch_stack_blocks(static_cast<double*>(raw), dst, static_cast<int>(na), static_cast<int>(nl), ng, s));
+      ++launches;
+      void* flag;
+      CKS(ws(ctx, m == 0 ? "bad_a" : "bad_b", 8, &flag));
+      CK(launch_first_nonfinite(static_cast<double*>(raw), static_cast<int>(na), static_cast<int64_t>(nl) * ng * 2,
+                                static_cast<int*>(flag), s));
+      ++launches;
+      CK(cudaMemcpyAsync(flag_h + m, flag, 4, cudaMemcpyDeviceToHost, s));  // checked after the final sync
+      hc.mark(m == 0 ? "h2d A pinned" : "h2d B pinned");
+      return HSB_OK;
+    }
+    CK(ctx->stager.h2d_stack(dst, blocks, na, nl, ng, s, &bad));
+    hc.mark(m == 0 ? "h2d A stack" : "h2d B stack");
+    if (bad >= 0) {
+      cudaStreamSynchronize(st);
+      cudaStreamSynchronize(cs);
+      return fail(ctx, HSB_ERR_INVARIANT, std::string(m == 0 ? "a_blocks" : "b_blocks") + "[" +
+                                              std::to_string(bad) + "] contains non-finite entries");
+    }
+    return HSB_OK;
+  };
+
+  // ------------------------------------------------------------- uploads
+  if (host_in) {
+    std::vector<Copy2D> jobs;  // T blocks and u: the potrf / Loop 1 operands
+    for (int64_t i = 0; i < na; ++i) {
+      jobs.push_back({const_cast<double*>(TAA) + i * nl * nl * 2, tblk_bytes, p->t_aa[i], tblk_bytes, tblk_bytes, 1});
+      jobs.push_back({const_cast<double*>(TAB) + i * nl * nl * 2, tblk_bytes, p->t_ab[i], tblk_bytes, tblk_bytes, 1});
+      jobs.push_back({const_cast<double*>(TBB) + i * nl * nl * 2, tblk_bytes, p->t_bb[i], tblk_bytes, tblk_bytes, 1});
+      jobs.push_back({const_cast<double*>(U) + i * nl, static_cast<size_t>(nl) * 8, p->u_norms[i],
+                      static_cast<size_t>(nl) * 8, static_cast<size_t>(nl) * 8, 1});
+    }
+    CK(ctx->stager.h2d(jobs, st));
+    hc.mark("h2d T,u");
+    CKS(stage_stack(1, st));
+    if (!overlap_upload) CKS(stage_stack(0, st));
+    CK(tl.mark(st, "h2d"));
+  }
+
+  // ------------------------------------------- Loop 2, part 1: Cholesky routing
   CK(launch_potrf_route(TAA, static_cast<double*>(q), static_cast<int32_t*>(info_d), static_cast<int>(na),
                         static_cast<int>(nl), force_nonhpd, static_cast<double*>(potrf_scr), st));
   ++launches;
   CK(cudaMemcpyAsync(info_h, info_d, na * 4, cudaMemcpyDeviceToHost, st));
-  CK(cudaEventRecord(ev[E_POTRF], st));
+  cudaEvent_t ev_info;
+  CK(cudaEventCreateWithFlags(&ev_info, cudaEventDisableTiming));
+  struct EvDel {
+    cudaEvent_t e;
+    ~EvDel() { cudaEventDestroy(e); }
+  } ev_info_del{ev_info};
+  CK(cudaEventRecord(ev_info, st));
+  CK(tl.mark(st, "loop2"));
 
-  // ---------------------------------------------------------------- Loop 1
-  CK(launch_half_mirror(TBB, static_cast<double*>(pbb), static_cast<int>(nl), na, 0.5, st));
-  ++launches;
-  {
+  auto loop1 = [&]() -> hsb_status {  // Z_a = T_AB^H A_a + (1/2 T_BB)^H B_a (builder.py:73-88)
+    CK(launch_half_mirror(TBB, static_cast<double*>(pbb), static_cast<int>(nl), na, 0.5, st));
+    ++launches;
     ZrkCall z;
     z.segs.push_back({atom_mats(TAB, na, nl), atom_rows(A, na, nl, ng, K)});
     z.segs.push_back({atom_mats(static_cast<double*>(pbb), na, nl), atom_rows(B, na, nl, ng, K)});
     z.m = nl;
     z.n = ng;
-    z.c = static_cast<double*>(zbuf);
+    z.c = Z;
     z.ldc = K;
     z.batch = na;
     z.c_bstride = nl;
     CKS(run_zrk(ctx, st, z, &launches));
-  }
-  CK(cudaEventRecord(ev[E_LOOP1], st));
-  double* Z = static_cast<double*>(zbuf);
-  double* UB = static_cast<double*>(ub);
+    CK(tl.mark(st, "loop1"));
+    return HSB_OK;
+  };
+  auto unorm = [&]() -> hsb_status {  // UB = diag(u) B (builder.py:124-127)
+    CK(launch_diag_scale(B, K, UB, K, U, K, ng, st));
+    ++launches;
+    CK(tl.mark(st, "unorm"));
+    return HSB_OK;
+  };
 
-  if (unfused) {
-    // H1: lower(Z^H B + B^H Z), beta = 0 (builder.h_cross, builder.py:91-104)
-    ZrkCall h1;
+  // ------------------------------------------------------ Loop 1, U norm, S
+  if (overlap_upload) {
+    CKS(unorm());
+    ZrkCall s2 = tri_call(S, ldo, ng, kLowerOnly, 0.0);
+    s2.segs.push_back({plain(UB, K, ng, K), plain(UB, K, ng, K)});
+    CKS(run_zrk(ctx, st, s2, &launches));
+    CK(tl.mark(st, "s2"));
+    CKS(stage_stack(0, cs));  // A rides the copy engine while (UB)^H(UB) runs
+    cudaEvent_t ev_a;
+    CK(cudaEventCreateWithFlags(&ev_a, cudaEventDisableTiming));
+    EvDel ev_a_del{ev_a};
+    CK(cudaEventRecord(ev_a, cs));
+    CK(cudaStreamWaitEvent(st, ev_a, 0));
+    CK(tl.mark(st, "h2d"));
+    ZrkCall s1 = tri_call(S, ldo, ng, kLowerOnly | kMirror, 1.0);
+    s1.segs.push_back({plain(A, K, ng, K), plain(A, K, ng, K)});
+    CKS(run_zrk(ctx, st, s1, &launches));
+    CK(tl.mark(st, "s1"));
+    CKS(loop1());
+  } else if (unfused) {
+    CKS(loop1());
+    ZrkCall h1 = tri_call(H, ldo, ng, kLowerOnly | kZeroImagDiag, 0.0);  // builder.h_cross (builder.py:91-104)
     h1.segs.push_back({plain(Z, K, ng, K), plain(B, K, ng, K)});
     h1.segs.push_back({plain(B, K, ng, K), plain(Z, K, ng, K)});
-    h1.m = h1.n = ng;
-    h1.triangle = true;
-    h1.flags = kLowerOnly | kZeroImagDiag;
-    h1.c = H;
-    h1.ldc = ldo;
     CKS(run_zrk(ctx, st, h1, &launches));
-    CK(cudaEventRecord(ev[E_H1], st));
-    // S1 (builder.build_s, builder.py:107-132)
-    ZrkCall s1;
+    CK(tl.mark(st, "h1"));
+    ZrkCall s1 = tri_call(S, ldo, ng, kLowerOnly | kZeroImagDiag, 0.0);  // builder.build_s (builder.py:107-132)
     s1.segs.push_back({plain(A, K, ng, K), plain(A, K, ng, K)});
-    s1.m = s1.n = ng;
-    s1.triangle = true;
-    s1.flags = kLowerOnly | kZeroImagDiag;
-    s1.c = S;
-    s1.ldc = ldo;
     CKS(run_zrk(ctx, st, s1, &launches));
-    CK(cudaEventRecord(ev[E_S1], st));
-  } else {
-    CK(cudaEventRecord(ev[E_H1], st));
-    CK(cudaEventRecord(ev[E_S1], st));
-  }
-  // U norm
-  CK(launch_diag_scale(B, K, UB, K, U, K, ng, st));
-  ++launches;
-  CK(cudaEventRecord(ev[E_UNORM], st));
-  if (unfused) {
-    ZrkCall s2;
+    CK(tl.mark(st, "s1"));
+    CKS(unorm());
+    ZrkCall s2 = tri_call(S, ldo, ng, kLowerOnly | kZeroImagDiag, 1.0);
     s2.segs.push_back({plain(UB, K, ng, K), plain(UB, K, ng, K)});
-    s2.m = s2.n = ng;
-    s2.triangle = true;
-    s2.flags = kLowerOnly | kZeroImagDiag;
-    s2.beta_re = 1.0;
-    s2.c = S;
-    s2.ldc = ldo;
     CKS(run_zrk(ctx, st, s2, &launches));
-    CK(cudaEventRecord(ev[E_S2], st));
     CK(launch_mirror(S, ldo, static_cast<int>(ng), st));
     ++launches;
-    CK(cudaEventRecord(ev[E_SMIR], st));
+    CK(tl.mark(st, "s2"));
   } else {
-    ZrkCall s;
+    CKS(loop1());
+    CKS(unorm());
+    ZrkCall s = tri_call(S, ldo, ng, kLowerOnly | kMirror, 0.0);
     s.segs.push_back({plain(A, K, ng, K), plain(A, K, ng, K)});
     s.segs.push_back({plain(UB, K, ng, K), plain(UB, K, ng, K)});
-    s.m = s.n = ng;
-    s.triangle = true;
-    s.flags = kLowerOnly | kMirror;
-    s.c = S;
-    s.ldc = ldo;
     CKS(run_zrk(ctx, st, s, &launches));
-    CK(cudaEventRecord(ev[E_S2], st));
-    CK(cudaEventRecord(ev[E_SMIR], st));
+    CK(tl.mark(st, "s"));
   }
+  cudaEvent_t ev_s;  // S final
+  CK(cudaEventCreateWithFlags(&ev_s, cudaEventDisableTiming));
+  EvDel ev_s_del{ev_s};
+  CK(cudaEventRecord(ev_s, st));
 
   // ------------------------------------------- routing (host, overlaps S)
-  CK(cudaEventSynchronize(ev[E_POTRF]));
+  hc.mark("enqueue to S");
+  CK(cudaEventSynchronize(ev_info));
+  hc.mark("routing wait");
   int64_t n_hpd = 0, n_nh = 0;
   for (int64_t i = 0; i < na; ++i) (info_h[i] == 0 ? n_hpd : n_nh)++;
   {
     int64_t ih = 0, in = 0;
     for (int64_t i = 0; i < na; ++i) {
       if (info_h[i] == 0) {
-        offs_h[i] = static_cast<int32_t>(ih * nl);
-        ++ih;
+        offs_h[i] = static_cast<int32_t>(ih++ * nl);
       } else {
         offs_h[i] = static_cast<int32_t>((n_hpd + in) * nl);
-        offs_h[na + in] = static_cast<int32_t>(i * nl);    // A_nh source rows
+        offs_h[na + in] = static_cast<int32_t>(i * nl);      // A_nh source rows
         offs_h[2 * na + in] = static_cast<int32_t>(in * nl);  // A_nh dest rows
         ++in;
       }
@@ -652,8 +769,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   CK(cudaMemcpyAsync(offs_d, offs_h, na * 3 * 4, cudaMemcpyHostToDevice, st));
   const int32_t* offs_dev = static_cast<int32_t*>(offs_d);
 
-  // ---------------------------------------------------- Loop 2, part 2
-  double* R = static_cast<double*>(rbuf);  // [Y_hpd ; X_nh]
+  // ------------------------------------------- Loop 2, part 2 (builder.py:162-185)
   double* ANH = nullptr;
   {
     ZrkCall z;
@@ -674,97 +790,84 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
       ++launches;
     }
   }
-  CK(cudaEventRecord(ev[E_LOOP2], st));
+  CK(tl.mark(st, "loop2"));
   const int64_t k_hpd = n_hpd * nl, k_nh = n_nh * nl;
   const double* Y = R;
   const double* XNH = R + 2 * k_hpd;
 
+  // -------------------------------------------------- H (builder.py:91-104, 187-200)
   if (unfused) {
-    if (n_nh > 0) {  // H2: gemm('C','N', beta = 1) (builder.py:187-194), lower tiles
-      ZrkCall h2;
+    if (n_nh > 0) {  // H2: gemm('C','N', beta = 1), lower tiles (the mirror rebuilds the rest)
+      ZrkCall h2 = tri_call(H, ldo, ng, kLowerOnly, 1.0);
       h2.segs.push_back({plain(ANH, k_nh, ng, k_nh), plain(XNH, k_nh, ng, K)});
-      h2.m = h2.n = ng;
-      h2.triangle = true;
-      h2.flags = kLowerOnly;
-      h2.beta_re = 1.0;
-      h2.c = H;
-      h2.ldc = ldo;
       CKS(run_zrk(ctx, st, h2, &launches));
     }
-    CK(cudaEventRecord(ev[E_H2], st));
-    if (n_hpd > 0) {  // H3: herk(beta = 1) (builder.py:195-200)
-      ZrkCall h3;
+    CK(tl.mark(st, "h2"));
+    if (n_hpd > 0) {  // H3: herk(beta = 1)
+      ZrkCall h3 = tri_call(H, ldo, ng, kLowerOnly | kZeroImagDiag, 1.0);
       h3.segs.push_back({plain(Y, k_hpd, ng, K), plain(Y, k_hpd, ng, K)});
-      h3.m = h3.n = ng;
-      h3.triangle = true;
-      h3.flags = kLowerOnly | kZeroImagDiag;
-      h3.beta_re = 1.0;
-      h3.c = H;
-      h3.ldc = ldo;
       CKS(run_zrk(ctx, st, h3, &launches));
     }
-    CK(cudaEventRecord(ev[E_H3], st));
     CK(launch_mirror(H, ldo, static_cast<int>(ng), st));
     ++launches;
-    CK(cudaEventRecord(ev[E_HMIR], st));
+    CK(tl.mark(st, "h3"));
   } else {
-    ZrkCall h;
+    ZrkCall h = tri_call(H, ldo, ng, kLowerOnly | kMirror, 0.0);
     h.segs.push_back({plain(Z, K, ng, K), plain(B, K, ng, K)});
     h.segs.push_back({plain(B, K, ng, K), plain(Z, K, ng, K)});
     if (n_hpd > 0) h.segs.push_back({plain(Y, k_hpd, ng, K), plain(Y, k_hpd, ng, K)});
     if (n_nh > 0) h.segs.push_back({plain(ANH, k_nh, ng, k_nh), plain(XNH, k_nh, ng, K)});
-    h.m = h.n = ng;
-    h.triangle = true;
-    h.flags = kLowerOnly | kMirror;
-    h.c = H;
-    h.ldc = ldo;
     CKS(run_zrk(ctx, st, h, &launches));
-    CK(cudaEventRecord(ev[E_H2], st));
-    CK(cudaEventRecord(ev[E_H3], st));
-    CK(cudaEventRecord(ev[E_HMIR], st));
+    CK(tl.mark(st, "h"));
   }
 
   // --------------------------------------------------------------- outputs
   if (out->location == HSB_LOC_HOST) {
-    CK(cudaMemcpy2DAsync(out->h, out->ld * 16, H, ldo * 16, ng * 16, ng, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpy2DAsync(out->s, out->ld * 16, S, ldo * 16, ng * 16, ng, cudaMemcpyDeviceToHost, st));
+    // S is final at ev_s: its download runs on the copy stream, concurrently
+    // with the H contraction; H follows on the compute stream.
+    CK(cudaStreamWaitEvent(cs, ev_s, 0));
+    const size_t row = static_cast<size_t>(ng) * 16;
+    CK(ctx->stager.d2h({{out->s, static_cast<size_t>(out->ld) * 16, S, static_cast<size_t>(ldo) * 16, row,
+                         static_cast<size_t>(ng)}},
+                       cs));
+    CK(ctx->stager.d2h({{out->h, static_cast<size_t>(out->ld) * 16, H, static_cast<size_t>(ldo) * 16, row,
+                         static_cast<size_t>(ng)}},
+                       st));
   }
-  CK(cudaEventRecord(ev[E_D2H], st));
-  CK(cudaEventSynchronize(ev[E_D2H]));
+  cudaEvent_t ev_cs;
+  CK(cudaEventCreateWithFlags(&ev_cs, cudaEventDisableTiming));
+  EvDel ev_cs_del{ev_cs};
+  CK(cudaEventRecord(ev_cs, cs));
+  CK(cudaStreamWaitEvent(st, ev_cs, 0));
+  CK(tl.mark(st, "d2h"));
+  hc.mark("enqueue H + d2h");
+  CK(cudaEventSynchronize(tl.marks.back().second));
+  hc.mark("final sync");
+  hc.report();
+  for (int m = 0; m < 2; ++m)
+    if (flag_h[m] >= 0 && flag_h[m] < na)  // pinned uploads are scanned on the device; outputs are discarded
+      return fail(ctx, HSB_ERR_INVARIANT, std::string(m == 0 ? "a_blocks" : "b_blocks") + "[" +
+                                              std::to_string(flag_h[m]) + "] contains non-finite entries");
 
   if (tm) {
-    auto el = [&](int a, int b) {
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, ev[a], ev[b]);
-      return ms * 1e-3;
-    };
     std::memset(tm, 0, sizeof(*tm));
-    tm->h2d = el(E_START, E_H2D);
-    const double t_potrf = el(E_H2D, E_POTRF);
-    tm->loop1 = el(E_POTRF, E_LOOP1);
-    tm->unorm = el(E_S1, E_UNORM);
-    tm->loop2 = t_potrf + el(E_SMIR, E_LOOP2);
-    const double fS = 4.0 * K * double(ng) * ng;  // S1 == S2 model flops
+    tm->h2d = tl.total("h2d");
+    tm->loop1 = tl.total("loop1");
+    tm->loop2 = tl.total("loop2");
+    tm->unorm = tl.total("unorm");
+    const double fS = 4.0 * K * double(ng) * ng;
     const double fH1 = 8.0 * K * double(ng) * ng, fH2 = 8.0 * k_nh * double(ng) * ng,
                  fH3 = 4.0 * k_hpd * double(ng) * ng;
-    if (unfused) {
-      tm->h1 = el(E_LOOP1, E_H1);
-      tm->s1 = el(E_H1, E_S1);
-      tm->s2 = el(E_UNORM, E_S2) + el(E_S2, E_SMIR);
-      tm->h2 = el(E_LOOP2, E_H2);
-      tm->h3 = el(E_H2, E_H3) + el(E_H3, E_HMIR);
-    } else {
-      const double ts = el(E_UNORM, E_S2);
-      tm->s1 = ts * 0.5;
-      tm->s2 = ts * 0.5;
-      const double th = el(E_LOOP2, E_H2);
-      const double fh = fH1 + fH2 + fH3;
-      tm->h1 = th * fH1 / fh;
-      tm->h2 = th * fH2 / fh;
-      tm->h3 = th * fH3 / fh;
-    }
-    tm->d2h = el(E_HMIR, E_D2H);
-    tm->total = el(E_START, E_D2H);
+    const double ts = tl.total("s");  // fused S: split S1/S2 by model flops (equal)
+    tm->s1 = tl.total("s1") + ts * 0.5;
+    tm->s2 = tl.total("s2") + ts * 0.5;
+    const double th = tl.total("h"), fh = fH1 + fH2 + fH3;
+    tm->h1 = tl.total("h1") + th * fH1 / fh;
+    tm->h2 = tl.total("h2") + th * fH2 / fh;
+    tm->h3 = tl.total("h3") + th * fH3 / fh;
+    (void)fS;
+    tm->d2h = tl.total("d2h");
+    tm->total = tl.span();
     tm->n_hpd = static_cast<int32_t>(n_hpd);
     tm->n_nonhpd = static_cast<int32_t>(n_nh);
     tm->launches = launches;

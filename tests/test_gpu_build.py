@@ -128,3 +128,42 @@ def test_device_path_matches_host_path():
     assert rel_frob_error(hm, host.h.matrix) < 1e-14
     assert rel_frob_error(sm, host.s.matrix) < 1e-14
     assert t["launches"] >= 5
+
+
+@pytest.mark.parametrize("field", ["a_blocks", "b_blocks"])
+def test_nonfinite_stack_values_raise_invariant_error(field):
+    # probgen.validate_instance (probgen.py:155-161); checked during staging
+    p = generate(ProblemSpec(Dims(3, 5, 40), seed=2))
+    getattr(p, field)[2][1, 7] = np.inf if field == "a_blocks" else np.nan
+    with pytest.raises(InvariantError, match=rf"{field}\[2\]"):
+        build_hs(p)
+    # the context stays usable afterwards
+    q = generate(ProblemSpec(Dims(3, 5, 40), seed=2))
+    out = build_hs(q)
+    assert rel_frob_error(out.s.matrix, brute.s_brute(q)) < TOL
+
+
+def test_pageable_outputs_path():
+    p = generate(ProblemSpec(Dims(2, 9, 77), seed=8, nonhpd_fraction=0.5))
+    a = build_hs(p, GpuPolicy(pinned_outputs=False))
+    b = build_hs(p, GpuPolicy(pinned_outputs=True))
+    assert a.h.matrix.tobytes() == b.h.matrix.tobytes()
+    assert a.s.matrix.tobytes() == b.s.matrix.tobytes()
+
+
+def test_pinned_instance_path_matches_and_checks_values():
+    from paper_1611_00606_b200 import pin_instance
+
+    p = generate(ProblemSpec(Dims(4, 33, 210), seed=12, nonhpd_fraction=0.5))
+    q = pin_instance(p)
+    a, b = build_hs(p), build_hs(q)
+    assert rel_frob_error(b.h.matrix, a.h.matrix) < 1e-15
+    assert rel_frob_error(b.s.matrix, a.s.matrix) < 1e-15
+    assert rel_frob_error(b.h.matrix, brute.h_brute(p)) < TOL
+    q.b_blocks[3][4, 5] = np.nan
+    with pytest.raises(InvariantError, match=r"b_blocks\[3\]"):
+        build_hs(q)
+    q.b_blocks[3][4, 5] = 0
+    q.a_blocks[1][0, 0] = -np.inf
+    with pytest.raises(InvariantError, match=r"a_blocks\[1\]"):
+        build_hs(q)
