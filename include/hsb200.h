@@ -172,6 +172,31 @@ HSB_API hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p
                         uint32_t opts, const hsb_output* out,
                         hsb_timings* timings, int32_t* atom_info);
 
+/* ------------------------------------------------------------------------ */
+/* Matching coefficients (north star part 1; no reference implementation:   */
+/* A, B are random inputs in probgen.py:131-132).  PAPER.md:226-241.        */
+/* ------------------------------------------------------------------------ */
+
+typedef struct {
+  int64_t n_atoms, n_g;
+  int32_t lmax, n_types;
+  const int32_t* gvec;     /* host, n_g x 3 integer G in reciprocal-lattice coordinates */
+  const double* tau;       /* host, n_atoms x 3 Cartesian positions (bohr) */
+  const int32_t* type_of;  /* host, n_atoms, in [0, n_types) */
+  const double* rmt;       /* host, n_types muffin-tin radii (bohr) */
+  const double* radial;    /* host, n_types x (lmax+1) x 4: u_l(R), u_l'(R), udot_l(R), udot_l'(R) */
+  double kpt[3];           /* k in reciprocal-lattice coordinates */
+  double recip[9];         /* reciprocal lattice vectors b1, b2, b3 as rows (1/bohr) */
+  double omega;            /* cell volume (bohr^3) */
+} hsb_phys;
+
+/* Device A, B stacks (n_atoms*(lmax+1)^2) x n_g, column-major complex128,
+ * leading dimension ld (complex elements), rows (atom, L = l^2+l+m):
+ *   A = c [j_l(KR) udot' - K j_l'(KR) udot]/D,  B = c [K j_l'(KR) u - j_l(KR) u']/D,
+ *   c = 4 pi / sqrt(Omega) i^l exp(i K.tau) conj(Y_lm(K^)),  D = u udot' - udot u'. */
+HSB_API hsb_status hsb_match_coeffs(hsb_ctx* ctx, void* stream, const hsb_phys* phys,
+                                    double* a_stack, double* b_stack, int64_t ld);
+
 #ifdef __cplusplus
 }
 #endif

@@ -53,6 +53,13 @@ class HsbTimings(ctypes.Structure):
         ("reserved", ctypes.c_int32)]
 
 
+class HsbPhys(ctypes.Structure):
+    _fields_ = [("n_atoms", ctypes.c_int64), ("n_g", ctypes.c_int64), ("lmax", ctypes.c_int32),
+                ("n_types", ctypes.c_int32), ("gvec", _P), ("tau", _P), ("type_of", _P), ("rmt", _P),
+                ("radial", _P), ("kpt", ctypes.c_double * 3), ("recip", ctypes.c_double * 9),
+                ("omega", ctypes.c_double)]
+
+
 _lib = None
 _lock = threading.Lock()
 _ctxs: dict[int, ctypes.c_void_p] = {}
@@ -84,6 +91,7 @@ def load():
             "hsb_zgemm": (i32, [_P, _P, ch, ch, i64, i64, i64, dbl, dbl, _P, i64, _P, i64, dbl, dbl,
                                 _P, i64, u32]),
             "hsb_hermitian_mirror": (i32, [_P, _P, i64, _P, i64]),
+            "hsb_match_coeffs": (i32, [_P, _P, ctypes.POINTER(HsbPhys), _P, _P, i64]),
             "hsb_build_hs": (i32, [_P, _P, ctypes.POINTER(HsbProblem), u32, ctypes.POINTER(HsbOutput),
                                    ctypes.POINTER(HsbTimings), ctypes.POINTER(ctypes.c_int32)]),
         }

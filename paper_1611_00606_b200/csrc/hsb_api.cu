@@ -24,6 +24,7 @@
 #include <chrono>
 #include <cstdlib>
 #include <cstdio>
+#include <cmath>
 #include <cstring>
 #include <map>
 #include <string>
@@ -31,6 +32,7 @@
 
 #include "../../include/hsb200.h"
 #include "aux_kernels.cuh"
+#include "match.cuh"
 #include "staging.cuh"
 #include "zrk.cuh"
 
@@ -872,6 +874,58 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     tm->n_nonhpd = static_cast<int32_t>(n_nh);
     tm->launches = launches;
   }
+  return HSB_OK;
+}
+
+hsb_status hsb_match_coeffs(hsb_ctx* ctx, void* stream, const hsb_phys* ph, double* a_stack, double* b_stack,
+                            int64_t ld) {
+  if (!ctx) return fail(nullptr, HSB_ERR_INPUT, "ctx is NULL");
+  if (!ph || !a_stack || !b_stack) return fail(ctx, HSB_ERR_INPUT, "NULL argument");
+  if (ph->n_atoms < 1 || ph->n_g < 1 || ph->n_types < 1 || ph->lmax < 0)
+    return fail(ctx, HSB_ERR_INPUT, "dimensions must be positive");
+  if (ph->lmax > kMaxL) return fail(ctx, HSB_ERR_UNSUPPORTED, "lmax above 31");
+  if (ph->n_g > 0x7fffffff) return fail(ctx, HSB_ERR_UNSUPPORTED, "too many G vectors");
+  const int64_t nlm = static_cast<int64_t>(ph->lmax + 1) * (ph->lmax + 1);
+  if (ld < ph->n_atoms * nlm) return fail(ctx, HSB_ERR_DIMENSION, "ld < n_atoms * (lmax+1)^2");
+  if (!(ph->omega > 0.0)) return fail(ctx, HSB_ERR_INPUT, "cell volume must be positive");
+  if (!ph->gvec || !ph->tau || !ph->type_of || !ph->rmt || !ph->radial)
+    return fail(ctx, HSB_ERR_INPUT, "NULL input array");
+  for (int64_t a = 0; a < ph->n_atoms; ++a)
+    if (ph->type_of[a] < 0 || ph->type_of[a] >= ph->n_types) return fail(ctx, HSB_ERR_INPUT, "type index out of range");
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t gb = ph->n_g * 3 * 4, tb = ph->n_atoms * 3 * 8, yb = ph->n_atoms * 4, rb = ph->n_types * 8,
+               db = ph->n_types * (ph->lmax + 1) * 4 * 8;
+  void *g, *t, *y, *r, *d;
+  CKS(ws(ctx, "m_gvec", gb, &g));
+  CKS(ws(ctx, "m_tau", tb, &t));
+  CKS(ws(ctx, "m_type", yb, &y));
+  CKS(ws(ctx, "m_rmt", rb, &r));
+  CKS(ws(ctx, "m_radial", db, &d));
+  CK(cudaMemcpyAsync(g, ph->gvec, gb, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(t, ph->tau, tb, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(y, ph->type_of, yb, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(r, ph->rmt, rb, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d, ph->radial, db, cudaMemcpyHostToDevice, st));
+  MatchParams mp;
+  std::memset(&mp, 0, sizeof(mp));
+  mp.gvec = static_cast<int32_t*>(g);
+  mp.tau = static_cast<double*>(t);
+  mp.type_of = static_cast<int32_t*>(y);
+  mp.rmt = static_cast<double*>(r);
+  mp.radial = static_cast<double*>(d);
+  for (int i = 0; i < 3; ++i) mp.kpt[i] = ph->kpt[i];
+  for (int i = 0; i < 9; ++i) mp.recip[i] = ph->recip[i];
+  mp.pre = 4.0 * 3.14159265358979323846 / std::sqrt(ph->omega);
+  mp.n_g = ph->n_g;
+  mp.ld = ld;
+  mp.n_atoms = static_cast<int32_t>(ph->n_atoms);
+  mp.n_types = ph->n_types;
+  mp.lmax = ph->lmax;
+  if (match_smem_bytes(mp) > 200 * 1024) return fail(ctx, HSB_ERR_UNSUPPORTED, "too many atoms for one column CTA");
+  CK(launch_match_coeffs(mp, a_stack, b_stack, st));
+  // the small uploads above come from caller memory: finish them before returning
+  CK(cudaStreamSynchronize(st));
   return HSB_OK;
 }
 

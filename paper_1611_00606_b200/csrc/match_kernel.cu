@@ -1,0 +1,212 @@
+// match_kernel.cu — FLAPW matching coefficients A^alpha_lm(k+G), B^alpha_lm(k+G).
+//
+// North-star part (1); no reference implementation exists (A, B are random
+// inputs in probgen.py:131-132).  Definition: PAPER.md:226-241 (Rayleigh
+// expansion of exp(i K.r) matched in value and slope at the muffin-tin
+// radius), conventions of SURVEY.md 8(a) row A0, restated on the CPU in
+// oracle/matching.py:
+//
+//   c_lm = (4 pi / sqrt(Omega)) i^l exp(i K.tau_alpha) conj(Y_lm(K^))
+//   A    = c [ j_l(KR) udot'_l - K j_l'(KR) udot_l ] / D_l
+//   B    = c [ K j_l'(KR) u_l  - j_l(KR) u'_l      ] / D_l,   D_l = u udot' - udot u'
+//
+// One CTA per G column.  The per-column special functions are computed once
+// into shared memory (Y_lm by the normalised associated-Legendre recurrence,
+// one lane per m; j_l by upward recurrence for x >= lmax+1, Miller's downward
+// recurrence below that, a 3-term series for x < 1e-3; structure phases by
+// sincos), then all threads stream the n_atoms * N_L rows of the column of A
+// and B with coalesced 16-byte stores: the kernel is HBM-write bound
+// (2 * K * 16 bytes per column).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "match.cuh"
+
+namespace hsb {
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// j_0..j_{nmax} at x >= 0 into j[] (nmax <= kMaxL + 1).
+__device__ void spherical_bessel(double x, int nmax, double* j) {
+  if (x == 0.0) {
+    j[0] = 1.0;
+    for (int l = 1; l <= nmax; ++l) j[l] = 0.0;
+    return;
+  }
+  if (x < 1e-3) {  // j_l = x^l/(2l+1)!! [1 - x^2/(2(2l+3)) + x^4/(8(2l+3)(2l+5)) - ...]
+    double xl = 1.0, df = 1.0;  // x^l, (2l+1)!!
+    const double x2 = x * x;
+    for (int l = 0; l <= nmax; ++l) {
+      if (l > 0) {
+        xl *= x;
+        df *= (2 * l + 1);
+      }
+      const double a3 = 2 * l + 3, a5 = 2 * l + 5, a7 = 2 * l + 7;
+      const double s = 1.0 - x2 / (2.0 * a3) * (1.0 - x2 / (4.0 * a5) * (1.0 - x2 / (6.0 * a7)));
+      j[l] = xl / df * s;
+    }
+    return;
+  }
+  double sn, cs;
+  sincos(x, &sn, &cs);
+  const double j0 = sn / x;
+  const double j1 = sn / (x * x) - cs / x;
+  if (x >= nmax) {  // upward recurrence is stable for l < x
+    j[0] = j0;
+    if (nmax >= 1) j[1] = j1;
+    for (int l = 1; l < nmax; ++l) j[l + 1] = (2 * l + 1) / x * j[l] - j[l - 1];
+    return;
+  }
+  // Miller: downward from well above max(nmax, x), normalised by the larger of j0, j1
+  const int start = nmax + 24 + static_cast<int>(x);
+  double fp1 = 0.0, f = 1e-280;
+  for (int l = start; l > nmax; --l) {  // f = f_l, fp1 = f_{l+1}
+    const double fm1 = (2 * l + 1) / x * f - fp1;
+    fp1 = f;
+    f = fm1;
+    if (fabs(f) > 1e250) {
+      f *= 1e-250;
+      fp1 *= 1e-250;
+    }
+  }
+  // now f = f_nmax, fp1 = f_{nmax+1}
+  j[nmax] = f;
+  double cur = f, nxt = fp1;
+  for (int l = nmax; l > 0; --l) {
+    const double prev = (2 * l + 1) / x * cur - nxt;
+    nxt = cur;
+    cur = prev;
+    j[l - 1] = cur;
+    if (fabs(cur) > 1e250) {
+      for (int q = l - 1; q <= nmax; ++q) j[q] *= 1e-250;
+      cur *= 1e-250;
+      nxt *= 1e-250;
+    }
+  }
+  const double scale = (fabs(j0) >= fabs(j1)) ? j0 / j[0] : j1 / j[1];
+  for (int l = 0; l <= nmax; ++l) j[l] *= scale;
+}
+
+__global__ void match_coeffs_kernel(MatchParams p, double2* __restrict__ A, double2* __restrict__ B) {
+  extern __shared__ double smem_d[];
+  const int lmax = p.lmax, nlm = (lmax + 1) * (lmax + 1), nl1 = lmax + 1;
+  double2* ys = reinterpret_cast<double2*>(smem_d);          // nlm: pre i^l conj(Y_lm)
+  double2* phase = ys + nlm;                                  // n_atoms
+  double* fa = reinterpret_cast<double*>(phase + p.n_atoms);  // n_types * (lmax+1)
+  double* fb = fa + p.n_types * nl1;
+  unsigned char* lidx = reinterpret_cast<unsigned char*>(fb + p.n_types * nl1);  // nlm
+
+  const int g = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int* gv = p.gvec + 3 * g;
+  const double f0 = p.kpt[0] + gv[0], f1 = p.kpt[1] + gv[1], f2 = p.kpt[2] + gv[2];
+  const double kx = f0 * p.recip[0] + f1 * p.recip[3] + f2 * p.recip[6];
+  const double ky = f0 * p.recip[1] + f1 * p.recip[4] + f2 * p.recip[7];
+  const double kz = f0 * p.recip[2] + f1 * p.recip[5] + f2 * p.recip[8];
+  const double rho = sqrt(kx * kx + ky * ky);
+  const double kn = sqrt(kx * kx + ky * ky + kz * kz);
+
+  // ---- radial factors per (type, l)
+  for (int t = tid; t < p.n_types; t += blockDim.x) {
+    double j[kMaxL + 2];
+    const double x = kn * p.rmt[t];
+    spherical_bessel(x, lmax + 1, j);
+    for (int l = 0; l <= lmax; ++l) {
+      const double dj = (l == 0) ? -j[1] : (l * j[l - 1] - (l + 1) * j[l + 1]) / (2 * l + 1);
+      const double* r = p.radial + (t * nl1 + l) * 4;  // u, u', udot, udot'
+      const double d = r[0] * r[3] - r[2] * r[1];
+      fa[t * nl1 + l] = (j[l] * r[3] - kn * dj * r[2]) / d;
+      fb[t * nl1 + l] = (kn * dj * r[0] - j[l] * r[1]) / d;
+    }
+  }
+  // ---- spherical harmonics: lane m of warp 1 runs the l recurrence for m
+  if (tid >= 32 && tid < 64) {
+    const int m = tid - 32;
+    if (m <= lmax) {
+      const double ct = kn > 0.0 ? kz / kn : 1.0;
+      const double st = kn > 0.0 ? rho / kn : 0.0;
+      const double cp = rho > 0.0 ? kx / rho : 1.0, sp = rho > 0.0 ? ky / rho : 0.0;
+      // e^{i m phi}
+      double2 em = make_double2(1.0, 0.0);
+      for (int q = 0; q < m; ++q) em = cmul(em, make_double2(cp, sp));
+      // P_mm (normalised, Condon-Shortley phase)
+      double pmm = 0.28209479177387814;  // 1/sqrt(4 pi)
+      for (int q = 1; q <= m; ++q) pmm *= -sqrt((2.0 * q + 1.0) / (2.0 * q)) * st;
+      double plm2 = 0.0, plm1 = pmm;
+      for (int l = m; l <= lmax; ++l) {
+        double plm;
+        if (l == m) {
+          plm = pmm;
+        } else if (l == m + 1) {
+          plm = sqrt(2.0 * m + 3.0) * ct * pmm;
+        } else {
+          const double a = sqrt((4.0 * l * l - 1.0) / (double(l) * l - double(m) * m));
+          const double b = sqrt((double(l - 1) * (l - 1) - double(m) * m) / (4.0 * (l - 1) * (l - 1) - 1.0));
+          plm = a * (ct * plm1 - b * plm2);
+        }
+        if (l > m) {
+          plm2 = plm1;
+          plm1 = plm;
+        }
+        // Y_lm = plm e^{i m phi};  Y_{l,-m} = (-1)^m conj(Y_lm)
+        const double2 y = make_double2(plm * em.x, plm * em.y);
+        // i^l
+        const int lr = l & 3;
+        const double2 il = lr == 0 ? make_double2(1, 0) : lr == 1 ? make_double2(0, 1)
+                         : lr == 2 ? make_double2(-1, 0) : make_double2(0, -1);
+        const double2 cy = cmul(il, make_double2(y.x, -y.y));  // i^l conj(Y_lm)
+        ys[l * l + l + m] = make_double2(p.pre * cy.x, p.pre * cy.y);
+        if (m > 0) {
+          const double sgn = (m & 1) ? -1.0 : 1.0;  // conj(Y_{l,-m}) = (-1)^m Y_lm
+          const double2 cyn = cmul(il, make_double2(sgn * y.x, sgn * y.y));
+          ys[l * l + l - m] = make_double2(p.pre * cyn.x, p.pre * cyn.y);
+        }
+        lidx[l * l + l + m] = static_cast<unsigned char>(l);
+        lidx[l * l + l - m] = static_cast<unsigned char>(l);
+      }
+    }
+  }
+  // ---- structure phases
+  for (int a = tid; a < p.n_atoms; a += blockDim.x) {
+    const double* tau = p.tau + 3 * a;
+    double s, c;
+    sincos(kx * tau[0] + ky * tau[1] + kz * tau[2], &s, &c);
+    phase[a] = make_double2(c, s);
+  }
+  __syncthreads();
+
+  // ---- stream the column: rows (atom, L)
+  const int64_t K = static_cast<int64_t>(p.n_atoms) * nlm;
+  double2* colA = A + static_cast<int64_t>(g) * p.ld;
+  double2* colB = B + static_cast<int64_t>(g) * p.ld;
+  for (int64_t r = tid; r < K; r += blockDim.x) {
+    const int a = static_cast<int>(r / nlm), L = static_cast<int>(r - static_cast<int64_t>(a) * nlm);
+    const int t = p.type_of[a], l = lidx[L];
+    const double2 base = cmul(ys[L], phase[a]);
+    const double ca = fa[t * nl1 + l], cb = fb[t * nl1 + l];
+    colA[r] = make_double2(base.x * ca, base.y * ca);
+    colB[r] = make_double2(base.x * cb, base.y * cb);
+  }
+}
+
+size_t match_smem_bytes(const MatchParams& p) {
+  const size_t nlm = static_cast<size_t>(p.lmax + 1) * (p.lmax + 1);
+  return nlm * 16 + static_cast<size_t>(p.n_atoms) * 16 + 2 * static_cast<size_t>(p.n_types) * (p.lmax + 1) * 8 +
+         nlm + 16;
+}
+
+cudaError_t launch_match_coeffs(const MatchParams& p, double* A, double* B, cudaStream_t st) {
+  const size_t smem = match_smem_bytes(p);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(match_coeffs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  match_coeffs_kernel<<<static_cast<unsigned>(p.n_g), 256, smem, st>>>(p, reinterpret_cast<double2*>(A),
+                                                                       reinterpret_cast<double2*>(B));
+  return cudaGetLastError();
+}
+
+}  // namespace hsb

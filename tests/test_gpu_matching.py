@@ -1,0 +1,63 @@
+"""Matching-coefficient kernel (csrc/match_kernel.cu) against the scipy-based
+CPU restatement (oracle/matching.py), and the physical entry point
+(atoms/types, lmax, G set, radial data, T -> H, S) against the oracle's
+Algorithm 1 fed with the oracle's coefficients.  Tolerance 1e-12 on the
+coefficients, 1e-10 on H and S (north star)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import alg1
+from oracle import matching as om
+from paper_1611_00606_b200 import Dims, ProblemInstance, rel_frob_error
+from paper_1611_00606_b200.physics import (
+    build_hs_physical, match_coeffs_device, synthetic_system, synthetic_t_matrices,
+)
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle(system, k, g):
+    return om.matching_coeffs(system.lattice.vectors, system.positions, system.types,
+                              [s.rmt for s in system.species], system.radial_table(), system.lmax, k, g)
+
+
+@pytest.mark.parametrize("n_atoms,n_types,lmax,ng,kpt", [
+    (2, 1, 6, 500, (0.0, 0.0, 0.0)),     # C1 shape, Gamma point (K = 0 column present)
+    (8, 2, 8, 3000, (0.25, -0.125, 0.5)),
+    (3, 3, 10, 700, (0.1, 0.2, 0.3)),
+    (1, 1, 0, 50, (0.0, 0.0, 0.0)),
+    (4, 2, 14, 300, (0.5, 0.5, 0.5)),
+])
+def test_match_kernel_against_oracle(n_atoms, n_types, lmax, ng, kpt):
+    system, _, kmax, _ = synthetic_system(n_atoms, n_types, lmax, ng, seed=lmax + n_atoms)
+    from paper_1611_00606_b200.physics import gvector_set
+    g = gvector_set(system.lattice, kpt, kmax)
+    a_d, b_d = match_coeffs_device(system, kpt, g)
+    torch.cuda.synchronize()
+    a = a_d.cpu().numpy().T
+    b = b_d.cpu().numpy().T
+    ra, rb = _oracle(system, kpt, g)
+    assert rel_frob_error(a, ra) < 1e-12
+    assert rel_frob_error(b, rb) < 1e-12
+    # elementwise too (relative to the column scale)
+    assert np.max(np.abs(a - ra)) < 1e-12 * (1 + np.max(np.abs(ra)))
+
+
+def test_physical_build_matches_oracle_pipeline():
+    system, k, kmax, g = synthetic_system(4, 2, 8, 900, seed=3, kpt_frac=(0.0, 0.0, 0.0))
+    t_aa, t_ab, t_bb = synthetic_t_matrices(system, seed=3, nonhpd_fraction=0.25)
+    h, s, split, t, info = build_hs_physical(system, k, g, t_aa, t_ab, t_bb)
+    torch.cuda.synchronize()
+    ra, rb = _oracle(system, k, g)
+    n_l, n_g = system.n_l, len(g)
+    p = ProblemInstance(Dims(system.n_atoms, n_l, n_g))
+    for al in range(system.n_atoms):
+        p.a_blocks.append(np.asfortranarray(ra[al * n_l:(al + 1) * n_l]))
+        p.b_blocks.append(np.asfortranarray(rb[al * n_l:(al + 1) * n_l]))
+    p.t_aa, p.t_ab, p.t_bb, p.u_norms = t_aa, t_ab, t_bb, system.u_norms()
+    ref = alg1.build_hs_cpu(p)
+    assert (split.hpd, split.nonhpd) == (ref["hpd"], ref["nonhpd"])
+    assert rel_frob_error(h.cpu().numpy().T, ref["h"]) < 1e-10
+    assert rel_frob_error(s.cpu().numpy().T, ref["s"]) < 1e-10
