@@ -201,20 +201,26 @@ def main():
                                        total_model_flops)
     from paper_1611_00606_b200 import distributed as hsdist
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    ndev = max(1, torch.cuda.device_count())
+    dev_index = local_rank % ndev
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    backend = os.environ.get("HSB_DIST_BACKEND", "nccl")  # gloo: debugging with ranks sharing a GPU
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     dims = CONFIGS[args.config]
     lo, hi = shard(dims.n_atoms, rank, world)
     local = Dims(hi - lo, dims.n_l, dims.n_g)
     p = generate(ProblemSpec(local, seed=args.seed * 1000 + rank, nonhpd_fraction=args.nonhpd_fraction))
-    policy = GpuPolicy(device=local_rank, fused=not args.unfused)
+    policy = GpuPolicy(device=dev_index, fused=not args.unfused)
     n_g = dims.n_g
     ncols = -(-n_g // world) * world
     flops_full = total_model_flops(dims, round(args.nonhpd_fraction * dims.n_atoms) if world == 1 else 0)
 
-    dp = DeviceProblem.from_instance(p, local_rank)
+    dp = DeviceProblem.from_instance(p, dev_index)
     # column-major n_g x ncols outputs (row-major (ncols, n_g)); pad columns stay zero
     h = torch.zeros((ncols, n_g), dtype=torch.complex128, device=dev)
     s = torch.zeros((ncols, n_g), dtype=torch.complex128, device=dev)
@@ -231,14 +237,12 @@ def main():
         return t
 
     def barrier():
-        if world > 1:
-            dist.barrier(device_ids=[local_rank])
-        torch.cuda.synchronize(dev)
+        hsdist.barrier(dev)
 
     for _ in range(args.warmup):
         step()
     barrier()
-    sampler = ClockSampler(local_rank)
+    sampler = ClockSampler(dev_index)
     sampler.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
@@ -247,10 +251,7 @@ def main():
     barrier()
     clocks = sampler.stop()
     ms = ev0.elapsed_time(ev1) / args.steps
-    if world > 1:
-        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+    ms = hsdist.max_over_ranks(ms, dev)
     value = flops_full / (ms * 1e-3) / 1e12
 
     # dominant kernel: the fused H contraction (H1 + H2 + H3 sections)

@@ -75,6 +75,13 @@ def reduce_scatter_block_columns(full, block, group=None) -> None:
     import torch
     import torch.distributed as dist
 
+    if full.is_cuda and dist.get_backend(group) == "gloo":
+        # debugging path (several ranks sharing one GPU): gloo reduces host copies
+        host = torch.empty_like(block, device="cpu")
+        dist.reduce_scatter_tensor(torch.view_as_real(host), torch.view_as_real(full.cpu()), op=dist.ReduceOp.SUM,
+                                   group=group)
+        block.copy_(host)
+        return
     dist.reduce_scatter_tensor(torch.view_as_real(block), torch.view_as_real(full), op=dist.ReduceOp.SUM,
                                group=group)
 
@@ -136,7 +143,8 @@ def build_hs_sharded(p, policy=None, group=None, partial=None) -> ShardedResult:
     sb = torch.empty_like(hb)
     reduce_scatter_block_columns(h, hb, group)
     reduce_scatter_block_columns(s, sb, group)
-    c = torch.tensor(counts, dtype=torch.int64, device=dev)
+    c = torch.tensor(counts, dtype=torch.int64,
+                     device=dev if dist.get_backend(group) == "nccl" else torch.device("cpu"))
     dist.all_reduce(c, group=group)
     timings = dict(timings)
     timings["sharded_wall"] = time.perf_counter() - t0
@@ -185,8 +193,7 @@ def e2e_sharded_step_ms(p, policy, n_g: int, ncols: int, steps: int, dev):
         sh.copy_(sb, non_blocking=True)
 
     one()
-    dist.barrier(device_ids=[dev.index])
-    torch.cuda.synchronize(dev)
+    barrier(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
     e0.record()
@@ -196,6 +203,29 @@ def e2e_sharded_step_ms(p, policy, n_g: int, ncols: int, steps: int, dev):
     torch.cuda.synchronize(dev)
     wall = (time.perf_counter() - t0) / steps
     ms = max(e0.elapsed_time(e1) / steps, wall * 1e3)
-    tt = torch.tensor([ms], dtype=torch.float64, device=dev)
-    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    return float(tt.item()), wall
+    return max_over_ranks(ms, dev), wall
+
+
+def barrier(dev) -> None:
+    """Barrier + device synchronize (NCCL barrier bound to the rank's device)."""
+    import torch
+    import torch.distributed as dist
+
+    if dist.is_initialized() and dist.get_world_size() > 1:
+        if dist.get_backend() == "nccl":
+            dist.barrier(device_ids=[dev.index])
+        else:
+            dist.barrier()
+    torch.cuda.synchronize(dev)
+
+
+def max_over_ranks(value: float, dev) -> float:
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_initialized() and dist.get_world_size() > 1):
+        return value
+    on = dev if dist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.tensor([value], dtype=torch.float64, device=on)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
