@@ -118,3 +118,21 @@ def test_ledger_matches_reference_ledger(name):
     assert led.total_flops() == sum(section_flops(dims, dims.n_atoms - n_hpd).values())
     first_seen = list(dict.fromkeys(r.section for r in led))
     assert first_seen == list(dict.fromkeys(sections))
+
+
+def test_report_summarize_and_table5():
+    from paper_1611_00606_b200 import FlopLedger
+    from paper_1611_00606_b200.report import TABLE5, compare_with_table5, format_table, summarize
+
+    led = FlopLedger()
+    led.add(KernelKind.HER2K, (100, 50), 0.002, "H1")
+    led.add(KernelKind.HERK, (100, 50), 0.001, "S1")
+    led.add(KernelKind.DIAG_SCALE, (50, 100), 0.0, "U norm")
+    reps = summarize(led, peak_gflops=10.0)
+    assert [r.section for r in reps] == ["U norm", "S1", "H1"]  # Table-5 order
+    assert reps[0].gflops_per_s is None and reps[0].efficiency is None  # zero time -> absent
+    assert reps[1].gflops_per_s == pytest.approx(4 * 50 * 100 * 100 / 0.001 / 1e9)
+    assert "-" in format_table(reps) and "H1" in compare_with_table5(reps)
+    assert [r.section for r in TABLE5] == ["Loop 1", "Loop 2", "U norm", "S1", "S2", "H1", "H2", "H3"]
+    with pytest.raises(InputError):
+        summarize(FlopLedger())
