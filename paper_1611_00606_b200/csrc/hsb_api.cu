@@ -21,6 +21,8 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <chrono>
 #include <cstdlib>
 #include <cstdio>
@@ -51,6 +53,8 @@ struct hsb_ctx {
   void* pinned = nullptr;  // small pinned host scratch (routing info / offsets)
   size_t pinned_bytes = 0;
   hsb::Stager stager;                 // pinned-slot host<->device transfers
+  int* done_cnt = nullptr;            // mapped pinned per-column-block tile counters
+  size_t done_cnt_len = 0;
   cudaStream_t copy_stream = nullptr;  // overlaps S download with the H contraction
 };
 
@@ -180,6 +184,7 @@ struct ZrkCall {
   int64_t batch = 1;
   int64_t c_bstride = 0;
   const int32_t* c_rowoff = nullptr;
+  int* done_cnt = nullptr;
 };
 
 hsb_status run_zrk(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launches) {
@@ -220,6 +225,7 @@ hsb_status run_zrk(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launche
   p.ldc = z.ldc;
   p.c_bstride = z.c_bstride;
   p.c_rowoff = z.c_rowoff;
+  p.done_cnt = z.triangle ? z.done_cnt : nullptr;
   int64_t grid_x = z.triangle ? static_cast<int64_t>(p.tiles_m) * (p.tiles_m + 1) / 2
                               : static_cast<int64_t>(p.tiles_m) * p.tiles_n;
   if (grid_x > 0x7fffffff || z.batch > 65535) return fail(ctx, HSB_ERR_UNSUPPORTED, "grid too large");
@@ -311,6 +317,7 @@ void hsb_ctx_destroy(hsb_ctx* ctx) {
     if (kv.second.ptr) cudaFree(kv.second.ptr);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  if (ctx->done_cnt) cudaFreeHost(ctx->done_cnt);
   delete ctx;
 }
 
@@ -644,6 +651,12 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   };
 
   // ------------------------------------------------------------- uploads
+  cudaEvent_t ev_b_up;  // B stack uploaded
+  CK(cudaEventCreateWithFlags(&ev_b_up, cudaEventDisableTiming));
+  struct EvDel0 {
+    cudaEvent_t e;
+    ~EvDel0() { cudaEventDestroy(e); }
+  } ev_b_up_del{ev_b_up};
   if (host_in) {
     std::vector<Copy2D> jobs;  // T blocks and u: the potrf / Loop 1 operands
     for (int64_t i = 0; i < na; ++i) {
@@ -656,6 +669,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     CK(ctx->stager.h2d(jobs, st));
     hc.mark("h2d T,u");
     CKS(stage_stack(1, st));
+    CK(cudaEventRecord(ev_b_up, st));
     if (!overlap_upload) CKS(stage_stack(0, st));
     CK(tl.mark(st, "h2d"));
   }
@@ -704,7 +718,10 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     s2.segs.push_back({plain(UB, K, ng, K), plain(UB, K, ng, K)});
     CKS(run_zrk(ctx, st, s2, &launches));
     CK(tl.mark(st, "s2"));
-    CKS(stage_stack(0, cs));  // A rides the copy engine while (UB)^H(UB) runs
+    // A rides the copy engine while (UB)^H(UB) runs -- after B's DMAs, so the
+    // two uploads do not split the PCIe bandwidth B is waited on
+    CK(cudaStreamWaitEvent(cs, ev_b_up, 0));
+    CKS(stage_stack(0, cs));
     cudaEvent_t ev_a;
     CK(cudaEventCreateWithFlags(&ev_a, cudaEventDisableTiming));
     EvDel ev_a_del{ev_a};
@@ -796,6 +813,9 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   const int64_t k_hpd = n_hpd * nl, k_nh = n_nh * nl;
   const double* Y = R;
   const double* XNH = R + 2 * k_hpd;
+  // Stream H to pinned host memory while the H contraction runs (fused path)
+  const int64_t ntiles = (ng + kBN - 1) / kBN;
+  const bool stream_h = !unfused && out->location == HSB_LOC_HOST && host_is_pinned(out->h);
 
   // -------------------------------------------------- H (builder.py:91-104, 187-200)
   if (unfused) {
@@ -819,6 +839,20 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     h.segs.push_back({plain(B, K, ng, K), plain(Z, K, ng, K)});
     if (n_hpd > 0) h.segs.push_back({plain(Y, k_hpd, ng, K), plain(Y, k_hpd, ng, K)});
     if (n_nh > 0) h.segs.push_back({plain(ANH, k_nh, ng, k_nh), plain(XNH, k_nh, ng, K)});
+    if (stream_h) {  // per-column-block completion counters in mapped host memory
+      const size_t nb = static_cast<size_t>(ntiles);
+      if (ctx->done_cnt_len < nb) {
+        if (ctx->done_cnt) cudaFreeHost(ctx->done_cnt);
+        ctx->done_cnt = nullptr;
+        ctx->done_cnt_len = 0;
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&ctx->done_cnt), nb * sizeof(int), cudaHostAllocMapped));
+        ctx->done_cnt_len = nb;
+      }
+      std::memset(ctx->done_cnt, 0, nb * sizeof(int));
+      int* dptr = nullptr;
+      CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dptr), ctx->done_cnt, 0));
+      h.done_cnt = dptr;
+    }
     CKS(run_zrk(ctx, st, h, &launches));
     CK(tl.mark(st, "h"));
   }
@@ -832,9 +866,39 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     CK(ctx->stager.d2h({{out->s, static_cast<size_t>(out->ld) * 16, S, static_cast<size_t>(ldo) * 16, row,
                          static_cast<size_t>(ng)}},
                        cs));
-    CK(ctx->stager.d2h({{out->h, static_cast<size_t>(out->ld) * 16, H, static_cast<size_t>(ldo) * 16, row,
-                         static_cast<size_t>(ng)}},
-                       st));
+    if (stream_h) {
+      // poll the tile counters; a column block is final when all T tiles that
+      // write into it are done (column-major tile order makes this a prefix)
+      cudaEvent_t ev_h;
+      CK(cudaEventCreateWithFlags(&ev_h, cudaEventDisableTiming));
+      EvDel ev_h_del{ev_h};
+      CK(cudaEventRecord(ev_h, st));
+      volatile int* cnt = ctx->done_cnt;
+      const int64_t T = ntiles;
+      const int64_t batch = std::max<int64_t>(1, T / 16);
+      int64_t sent = 0;
+      while (sent < T) {
+        int64_t c = sent;
+        while (c < T && cnt[c] >= T) ++c;
+        const bool kernel_done = cudaEventQuery(ev_h) == cudaSuccess;
+        if (kernel_done) c = T;  // everything is final (also guards a counter mismatch)
+        if (c - sent >= batch || (c == T && c > sent)) {
+          std::atomic_thread_fence(std::memory_order_acquire);
+          const int64_t c0 = sent * kBN, c1 = std::min<int64_t>(c * kBN, ng);
+          CK(cudaMemcpy2DAsync(reinterpret_cast<char*>(out->h) + c0 * out->ld * 16, out->ld * 16,
+                               reinterpret_cast<const char*>(H) + c0 * ldo * 16, ldo * 16, row, c1 - c0,
+                               cudaMemcpyDeviceToHost, cs));
+          sent = c;
+        } else {
+          std::this_thread::sleep_for(std::chrono::microseconds(50));
+        }
+      }
+      hc.mark("stream H");
+    } else {
+      CK(ctx->stager.d2h({{out->h, static_cast<size_t>(out->ld) * 16, H, static_cast<size_t>(ldo) * 16, row,
+                           static_cast<size_t>(ng)}},
+                         st));
+    }
   }
   cudaEvent_t ev_cs;
   CK(cudaEventCreateWithFlags(&ev_cs, cudaEventDisableTiming));

@@ -70,6 +70,9 @@ struct ZrkParams {
   int64_t ldc;              // complex elements
   int64_t c_bstride;        // complex elements between batch outputs
   const int32_t* c_rowoff;  // optional per-batch row offset (complex), overrides c_bstride
+  int* done_cnt;            // optional (triangle mode): per 64-column block, tiles finished
+                            // writing into it; host-visible (mapped pinned memory).  A block
+                            // is final when its count reaches tiles_m.
 };
 
 // Host-side description of one operand (complex view).

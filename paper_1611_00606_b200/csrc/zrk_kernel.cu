@@ -49,13 +49,19 @@ __device__ __forceinline__ double flip_sign(double x, unsigned long long mask) {
   return __longlong_as_double(__double_as_longlong(x) ^ mask);
 }
 
-// Decode blockIdx into (tile row, tile col) for the lower-triangle schedule.
-__device__ __forceinline__ void tri_tile(int t, int& bi, int& bj) {
-  int i = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-  while (i * (i + 1) / 2 > t) --i;
-  while ((i + 1) * (i + 2) / 2 <= t) ++i;
-  bi = i;
-  bj = t - i * (i + 1) / 2;
+// Decode blockIdx into (tile row, tile col) for the lower-triangle schedule,
+// column-major: column block j holds tiles (j..T-1, j).  With the mirrored
+// epilogue, column block c of the output is final once tile columns 0..c
+// are done, so completed columns stream out in order (done_cnt).
+__device__ __forceinline__ void tri_tile(int t, int T, int& bi, int& bj) {
+  // tiles before column j: S(j) = j*T - j*(j-1)/2
+  const double b = 2.0 * T + 1.0;
+  int j = static_cast<int>((b - sqrt(b * b - 8.0 * t)) * 0.5);
+  if (j < 0) j = 0;
+  while (j > 0 && j * T - (j * (j - 1)) / 2 > t) --j;
+  while ((j + 1) * T - ((j + 1) * j) / 2 <= t) ++j;
+  bj = j;
+  bi = j + (t - (j * T - (j * (j - 1)) / 2));
 }
 
 // Offset (in doubles) of element (row, k) in a 64 x 16 double tile written by
@@ -81,7 +87,7 @@ __global__ void __launch_bounds__(kThreads, 2) zrk_kernel(const __grid_constant_
 
   int tm, tn;
   if (p.triangle) {
-    tri_tile(blockIdx.x, tm, tn);
+    tri_tile(blockIdx.x, p.tiles_m, tm, tn);
   } else {
     tm = blockIdx.x % p.tiles_m;
     tn = blockIdx.x / p.tiles_m;
@@ -238,6 +244,16 @@ __global__ void __launch_bounds__(kThreads, 2) zrk_kernel(const __grid_constant_
           reinterpret_cast<double2*>(C)[col + row * ldc] = make_double2(vr, -vi);
         }
       }
+    }
+  }
+  if (p.done_cnt) {
+    // all consumer stores of this tile precede the count (bar.sync orders them
+    // CTA-wide; the system-scope fence makes them visible to the host/DMA)
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      atomicAdd_system(p.done_cnt + tn, 1);
+      if (tm != tn) atomicAdd_system(p.done_cnt + tm, 1);
     }
   }
 }
