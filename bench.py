@@ -179,6 +179,8 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--nonhpd-fraction", type=float, default=0.0)
     ap.add_argument("--unfused", action="store_true", help="one launch per reference section")
+    ap.add_argument("--complex-mult", default="3m", choices=["3m", "4m"],
+                    help="real-product form of the complex contractions (3 or 4 DMMA products)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-ng", type=int, default=4000)
@@ -215,7 +217,7 @@ def main():
     lo, hi = shard(dims.n_atoms, rank, world)
     local = Dims(hi - lo, dims.n_l, dims.n_g)
     p = generate(ProblemSpec(local, seed=args.seed * 1000 + rank, nonhpd_fraction=args.nonhpd_fraction))
-    policy = GpuPolicy(device=dev_index, fused=not args.unfused)
+    policy = GpuPolicy(device=dev_index, fused=not args.unfused, complex_mult=args.complex_mult)
     n_g = dims.n_g
     ncols = -(-n_g // world) * world
     flops_full = total_model_flops(dims, round(args.nonhpd_fraction * dims.n_atoms) if world == 1 else 0)
@@ -314,7 +316,7 @@ def main():
             "config": {"workload": args.config, "desc": CONFIG_DESC[args.config], "n_atoms": dims.n_atoms,
                        "n_l": dims.n_l, "n_g": dims.n_g, "nonhpd_fraction": args.nonhpd_fraction,
                        "parallelism": f"atom-shard x{world}" + (" + reduce-scatter" if world > 1 else ""),
-                       "fused": not args.unfused, "model_tflop_per_step": flops_full / 1e12,
+                       "fused": not args.unfused, "complex_mult": args.complex_mult, "model_tflop_per_step": flops_full / 1e12,
                        "l2_note": "inputs larger than L2 (A/B stacks 496 MB each at C3)"},
             "gpu_launches": launches,
             "roofline": {"bound": "tensor", "kernel": "zrk_kernel<conj> fused H = Z^H B + B^H Z + Y^H Y",

@@ -59,6 +59,17 @@ HSB_API const char* hsb_last_error(const hsb_ctx* ctx);
 /* Release cached device workspace (the next call re-allocates). */
 HSB_API hsb_status hsb_ctx_trim(hsb_ctx* ctx);
 
+/* Real-arithmetic form of the complex products in every dense contraction.
+ * HSB_CPLX_3M (default): Gauss/Karatsuba, 3 real DMMA products per complex
+ *   product (P = Lr^T Rr, Q = Li^T Ri, W = (Lr -/+ Li)^T (Rr + Ri)), 25 % fewer
+ *   tensor-core cycles than the reference's 8-flop complex MAC
+ *   (kernels.py:66-85); results agree to ~1e-15 relative Frobenius.
+ * HSB_CPLX_4M: 4 real products per complex product (the conventional form).
+ * The ledger always charges the reference's model flops. */
+#define HSB_CPLX_4M 0
+#define HSB_CPLX_3M 1
+HSB_API hsb_status hsb_ctx_set_complex_mult(hsb_ctx* ctx, int32_t algo);
+
 /* ------------------------------------------------------------------------ */
 /* Kernel level: the five large updates.  Device pointers, caller's stream.  */
 /* These replace run_partitioned(kind, operands, policy) for kind in         */

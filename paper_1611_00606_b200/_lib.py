@@ -25,6 +25,9 @@ HSB_LOC_HOST = 0
 HSB_LOC_DEVICE = 1
 HSB_OPT_FORCE_NONHPD = 0x1
 HSB_OPT_UNFUSED = 0x2
+HSB_CPLX_4M = 0
+HSB_CPLX_3M = 1
+COMPLEX_MULT = {"4m": HSB_CPLX_4M, "3m": HSB_CPLX_3M}
 
 _P = ctypes.c_void_p
 _DPP = ctypes.POINTER(ctypes.c_void_p)
@@ -86,6 +89,7 @@ def load():
             "hsb_ctx_destroy": (None, [_P]),
             "hsb_last_error": (ctypes.c_char_p, [_P]),
             "hsb_ctx_trim": (i32, [_P]),
+            "hsb_ctx_set_complex_mult": (i32, [_P, i32]),
             "hsb_zherk": (i32, [_P, _P, i64, i64, dbl, _P, i64, dbl, _P, i64, u32]),
             "hsb_zher2k": (i32, [_P, _P, i64, i64, dbl, dbl, _P, i64, _P, i64, dbl, _P, i64, u32]),
             "hsb_zgemm": (i32, [_P, _P, ch, ch, i64, i64, i64, dbl, dbl, _P, i64, _P, i64, dbl, dbl,
@@ -119,9 +123,15 @@ def check(status: int, ctx) -> None:
     raise RuntimeError(f"libhsb200 error {status}: {msg}")
 
 
-def context(device: int = 0):
-    """Process-wide context for ``device`` (created on first use)."""
+def context(device: int = 0, complex_mult: str | None = None):
+    """Process-wide context for ``device`` (created on first use).
+
+    ``complex_mult`` ("3m" | "4m") selects the real-product form of the
+    complex contractions for the calls that follow (hsb_ctx_set_complex_mult).
+    """
     lib = load()
+    if complex_mult is not None and complex_mult not in COMPLEX_MULT:
+        raise InputError(f"complex_mult must be one of {sorted(COMPLEX_MULT)}, got {complex_mult!r}")
     with _lock:
         ctx = _ctxs.get(device)
         if ctx is None:
@@ -129,6 +139,8 @@ def context(device: int = 0):
             check(lib.hsb_ctx_create(device, ctypes.byref(out)), None)
             ctx = out
             _ctxs[device] = ctx
+        if complex_mult is not None:
+            check(lib.hsb_ctx_set_complex_mult(ctx, COMPLEX_MULT[complex_mult]), ctx)
         return ctx
 
 

@@ -10,6 +10,8 @@ namespace hsb {
 constexpr size_t kPotrfSmemMax = 200 * 1024;  // packed lower triangle up to n = 158
 
 cudaError_t launch_zrk(const ZrkParams& p, bool conj, int grid_x, int grid_z, cudaStream_t st);
+// 3M (Gauss) variant, persistent: ntiles tiles per batch x nbatch batches
+cudaError_t launch_zrk3m(const ZrkParams& p, bool conj, int ntiles, int nbatch, cudaStream_t st);
 cudaError_t launch_potrf_route(const double* t_aa, double* q, int32_t* info, int n_atoms, int n,
                                bool force_nonhpd, double* gscratch, cudaStream_t st);
 cudaError_t launch_half_mirror(const double* t, double* out, int n, int64_t count, double scale,

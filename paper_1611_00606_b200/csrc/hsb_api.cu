@@ -56,6 +56,7 @@ struct hsb_ctx {
   int* done_cnt = nullptr;            // mapped pinned per-column-block tile counters
   size_t done_cnt_len = 0;
   cudaStream_t copy_stream = nullptr;  // overlaps S download with the H contraction
+  int32_t cplx = HSB_CPLX_3M;          // complex product form of the zrk kernels
 };
 
 static thread_local std::string g_create_err;
@@ -229,7 +230,12 @@ hsb_status run_zrk(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launche
   int64_t grid_x = z.triangle ? static_cast<int64_t>(p.tiles_m) * (p.tiles_m + 1) / 2
                               : static_cast<int64_t>(p.tiles_m) * p.tiles_n;
   if (grid_x > 0x7fffffff || z.batch > 65535) return fail(ctx, HSB_ERR_UNSUPPORTED, "grid too large");
-  CK(launch_zrk(p, z.conj, static_cast<int>(grid_x), static_cast<int>(z.batch), st));
+  if (ctx->cplx == HSB_CPLX_3M) {
+    if (grid_x * z.batch > 0x7fffffff) return fail(ctx, HSB_ERR_UNSUPPORTED, "grid too large");
+    CK(launch_zrk3m(p, z.conj, static_cast<int>(grid_x), static_cast<int>(z.batch), st));
+  } else {
+    CK(launch_zrk(p, z.conj, static_cast<int>(grid_x), static_cast<int>(z.batch), st));
+  }
   if (launches) ++*launches;
   return HSB_OK;
 }
@@ -322,6 +328,13 @@ void hsb_ctx_destroy(hsb_ctx* ctx) {
 }
 
 const char* hsb_last_error(const hsb_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+
+hsb_status hsb_ctx_set_complex_mult(hsb_ctx* ctx, int32_t algo) {
+  if (!ctx) return fail(nullptr, HSB_ERR_INPUT, "ctx is NULL");
+  if (algo != HSB_CPLX_4M && algo != HSB_CPLX_3M) return fail(ctx, HSB_ERR_INPUT, "unknown complex product form");
+  ctx->cplx = algo;
+  return HSB_OK;
+}
 
 hsb_status hsb_ctx_trim(hsb_ctx* ctx) {
   if (!ctx) return fail(nullptr, HSB_ERR_INPUT, "ctx is NULL");

@@ -8,7 +8,8 @@ import pytest
 
 from conftest import GOLDEN
 from oracle import kernels as ok
-from paper_1611_00606_b200 import DimensionError, InputError, KernelKind, rel_frob_error, run_partitioned
+from paper_1611_00606_b200 import (DimensionError, GpuPolicy, InputError, KernelKind, rel_frob_error,
+                                   run_partitioned)
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-12
@@ -24,57 +25,62 @@ def _cm(rng, r, c):
     return np.asfortranarray(rng.standard_normal((r, c)) + 1j * rng.standard_normal((r, c)))
 
 
-def test_herk_matches_reference_kernel(g):
+@pytest.fixture(params=["3m", "4m"])
+def pol(request):
+    return GpuPolicy(complex_mult=request.param)
+
+
+def test_herk_matches_reference_kernel(g, pol):
     i = 0
     while f"herk{i}_a" in g:
         alpha, beta = (float(x) for x in g[f"herk{i}_ab"])
         c = g[f"herk{i}_c"].copy(order="F")
-        res = run_partitioned(KernelKind.HERK, (alpha, g[f"herk{i}_a"], beta, c))
+        res = run_partitioned(KernelKind.HERK, (alpha, g[f"herk{i}_a"], beta, c), pol)
         assert rel_frob_error(c, g[f"herk{i}_out"]) < TOL, i
         assert res.seconds >= 0 and res.n_tiles >= 1
         i += 1
 
 
-def test_her2k_matches_reference_kernel(g):
+def test_her2k_matches_reference_kernel(g, pol):
     i = 0
     while f"her2k{i}_z" in g:
         alpha, beta = g[f"her2k{i}_ab"]
         c = g[f"her2k{i}_c"].copy(order="F")
-        run_partitioned(KernelKind.HER2K, (complex(alpha), g[f"her2k{i}_z"], g[f"her2k{i}_b"], beta.real, c))
+        run_partitioned(KernelKind.HER2K, (complex(alpha), g[f"her2k{i}_z"], g[f"her2k{i}_b"], beta.real, c), pol)
         assert rel_frob_error(c, g[f"her2k{i}_out"]) < TOL, i
         assert np.all(np.diagonal(c).imag == 0)
         i += 1
 
 
-def test_gemm_all_ops_match_reference_kernel(g):
+def test_gemm_all_ops_match_reference_kernel(g, pol):
     i = 0
     while f"gemm{i}_a" in g:
         opa, opb = (str(x) for x in g[f"gemm{i}_ops"])
         alpha, beta = g[f"gemm{i}_ab"]
         c = g[f"gemm{i}_c"].copy(order="F")
         run_partitioned(KernelKind.GEMM, (complex(alpha), opa, g[f"gemm{i}_a"], opb, g[f"gemm{i}_b"],
-                                          complex(beta), c))
+                                          complex(beta), c), pol)
         assert rel_frob_error(c, g[f"gemm{i}_out"]) < TOL, (i, opa, opb)
         i += 1
 
 
 @pytest.mark.parametrize("k,n", [(1, 1), (3, 64), (8, 65), (121, 127), (257, 300), (2000, 700)])
-def test_herk_against_oracle_sizes(k, n):
+def test_herk_against_oracle_sizes(k, n, pol):
     rng = np.random.default_rng(k * 1000 + n)
     a = _cm(rng, k, n)
     c = _cm(rng, n, n)
     want = ok.herk(1.0, a, 0.5, c)
-    run_partitioned(KernelKind.HERK, (1.0, a, 0.5, c))
+    run_partitioned(KernelKind.HERK, (1.0, a, 0.5, c), pol)
     assert rel_frob_error(c, want) < TOL
 
 
 @pytest.mark.parametrize("k,n", [(5, 33), (242, 190), (1000, 513)])
-def test_her2k_against_oracle_sizes(k, n):
+def test_her2k_against_oracle_sizes(k, n, pol):
     rng = np.random.default_rng(7 + k + n)
     z, b = _cm(rng, k, n), _cm(rng, k, n)
     c = _cm(rng, n, n)
     want = ok.her2k(1.0, z, b, 0.0, c)
-    run_partitioned(KernelKind.HER2K, (1.0, z, b, 0.0, c))
+    run_partitioned(KernelKind.HER2K, (1.0, z, b, 0.0, c), pol)
     assert rel_frob_error(c, want) < TOL
 
 
