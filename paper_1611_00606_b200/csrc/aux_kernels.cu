@@ -127,6 +127,23 @@ __global__ void diag_scale_kernel(const double2* __restrict__ src, int64_t lds,
   }
 }
 
+// Sum planes for the 3M contraction (zrk3m_kernel.cu): for a complex k x n
+// operand X, minus = Re X - Im X (its role as the conjugated left factor) and
+// plus = Re X + Im X (right factor), both k x n real, leading dimension ldp.
+// Computed once per operand here instead of once per output tile inside the
+// contraction, where the adds would share the FP64 pipe with DMMA.
+__global__ void sum_planes_kernel(const double2* __restrict__ x, int64_t ldx, int64_t rows, int64_t cols,
+                                  double* __restrict__ minus, double* __restrict__ plus, int64_t ldp) {
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = idx % rows, c = idx / rows;
+    const double2 v = x[r + c * ldx];
+    minus[r + c * ldp] = v.x - v.y;
+    plus[r + c * ldp] = v.x + v.y;
+  }
+}
+
 // In-place Hermitian mirror (matcore.hermitian_mirror, matcore.py:89-105):
 // 32 x 32 tile pairs staged through shared memory so both the lower-tile read
 // and the upper-tile write are coalesced.
@@ -259,6 +276,14 @@ cudaError_t launch_diag_scale(const double* src, int64_t lds, double* dst, int64
                               int64_t rows, int64_t cols, cudaStream_t st) {
   diag_scale_kernel<<<grid_for(rows * cols, 256, 148 * 32), 256, 0, st>>>(
       reinterpret_cast<const double2*>(src), lds, reinterpret_cast<double2*>(dst), ldd, u, rows, cols);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sum_planes(const double* x, int64_t ldx, int64_t rows, int64_t cols, double* minus,
+                              double* plus, int64_t ldp, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  sum_planes_kernel<<<grid_for(rows * cols, 256, 148 * 32), 256, 0, st>>>(reinterpret_cast<const double2*>(x), ldx,
+                                                                          rows, cols, minus, plus, ldp);
   return cudaGetLastError();
 }
 

@@ -11,7 +11,7 @@ constexpr size_t kPotrfSmemMax = 200 * 1024;  // packed lower triangle up to n =
 
 cudaError_t launch_zrk(const ZrkParams& p, bool conj, int grid_x, int grid_z, cudaStream_t st);
 // 3M (Gauss) variant, persistent: ntiles tiles per batch x nbatch batches
-cudaError_t launch_zrk3m(const ZrkParams& p, bool conj, int ntiles, int nbatch, cudaStream_t st);
+cudaError_t launch_zrk3m(const ZrkParams& p, bool conj, bool planes, int ntiles, int nbatch, cudaStream_t st);
 cudaError_t launch_potrf_route(const double* t_aa, double* q, int32_t* info, int n_atoms, int n,
                                bool force_nonhpd, double* gscratch, cudaStream_t st);
 cudaError_t launch_half_mirror(const double* t, double* out, int n, int64_t count, double scale,
@@ -19,6 +19,8 @@ cudaError_t launch_half_mirror(const double* t, double* out, int n, int64_t coun
 cudaError_t launch_diag_scale(const double* src, int64_t lds, double* dst, int64_t ldd, const double* u,
                               int64_t rows, int64_t cols, cudaStream_t st);
 cudaError_t launch_mirror(double* c, int64_t ldc, int n, cudaStream_t st);
+cudaError_t launch_sum_planes(const double* x, int64_t ldx, int64_t rows, int64_t cols, double* minus,
+                              double* plus, int64_t ldp, cudaStream_t st);
 cudaError_t launch_gather_rows(const double* src, int64_t lds, double* dst, int64_t ldd, const int32_t* src_off,
                                const int32_t* dst_off, int n_blocks, int n_l, int64_t cols, cudaStream_t st);
 cudaError_t launch_stack_blocks(const double* raw, double* dst, int n_atoms, int rows, int64_t cols,

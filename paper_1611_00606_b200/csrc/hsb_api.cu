@@ -169,6 +169,21 @@ hsb_status encode_operand(hsb_ctx* ctx, CUtensorMap* map, const OperandView& v) 
   return HSB_OK;
 }
 
+// 2-D TMA map over one real sum plane (k x cols, leading dimension ldp doubles),
+// box {8 complex k, 64 cols}, no swizzle (zrk3m_kernel.cu, PLANES).
+hsb_status encode_plane(hsb_ctx* ctx, CUtensorMap* map, const double* base, int64_t k, int64_t cols, int64_t ldp) {
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(cols)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldp) * 8};
+  cuuint32_t box[2] = {8, static_cast<cuuint32_t>(kBM)}, estr[2] = {1, 1};
+  CUresult r = ctx->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(ctx, HSB_ERR_CUDA, "cuTensorMapEncodeTiled failed for a sum plane (code " +
+                                       std::to_string(static_cast<int>(r)) + ")");
+  return HSB_OK;
+}
+
 struct Seg {
   OperandView l, r;
 };
@@ -196,12 +211,53 @@ hsb_status run_zrk(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launche
     return fail(ctx, HSB_ERR_UNSUPPORTED, "output dimension too large");
   ZrkParams p;
   std::memset(&p, 0, sizeof(p));
+  // 3M on plain (unbatched) operands: Re-Im / Re+Im planes of each distinct
+  // operand, computed once here and fed to the kernel by TMA
+  const bool g3 = ctx->cplx == HSB_CPLX_3M;
+  bool planes = g3 && z.batch == 1;
+  for (const Seg& s : z.segs)
+    if (s.l.batch != 1 || s.r.batch != 1) planes = false;
+  struct PlaneSrc {
+    const double* base;
+    int64_t k, cols, ld, ldp;
+    double* minus;
+    double* plus;
+  };
+  std::vector<PlaneSrc> srcs;
+  auto plane_of = [&](const OperandView& v, bool minus, const double** out, int64_t* ldp) -> hsb_status {
+    for (const PlaneSrc& q : srcs)
+      if (q.base == v.base && q.k == v.k && q.cols == v.cols && q.ld == v.ld) {
+        *out = minus ? q.minus : q.plus;
+        *ldp = q.ldp;
+        return HSB_OK;
+      }
+    PlaneSrc q{v.base, v.k, v.cols, v.ld, v.k + (v.k & 1), nullptr, nullptr};
+    const std::string name = "zplane" + std::to_string(srcs.size());
+    void* buf;
+    CKS(ws(ctx, name.c_str(), static_cast<size_t>(2 * q.ldp) * q.cols * 8, &buf));
+    q.minus = static_cast<double*>(buf);
+    q.plus = q.minus + q.ldp * q.cols;
+    CK(launch_sum_planes(q.base, q.ld, q.k, q.cols, q.minus, q.plus, q.ldp, st));
+    srcs.push_back(q);
+    *out = minus ? q.minus : q.plus;
+    *ldp = q.ldp;
+    return HSB_OK;
+  };
   int nseg = 0, total = 0;
   for (const Seg& s : z.segs) {
     if (s.l.k <= 0) continue;
     if (s.l.k != s.r.k) return fail(ctx, HSB_ERR_DIMENSION, "segment operands disagree in reduction length");
     CKS(encode_operand(ctx, &p.lmap[nseg], s.l));
     CKS(encode_operand(ctx, &p.rmap[nseg], s.r));
+    if (planes) {
+      const double *lp, *rp;
+      int64_t ldl, ldr;
+      // left factor: Re-Im for L^H R (conj), Re+Im for L^T R
+      CKS(plane_of(s.l, z.conj, &lp, &ldl));
+      CKS(plane_of(s.r, false, &rp, &ldr));
+      CKS(encode_plane(ctx, &p.lsum[nseg], lp, s.l.k, s.l.cols, ldl));
+      CKS(encode_plane(ctx, &p.rsum[nseg], rp, s.r.k, s.r.cols, ldr));
+    }
     const int64_t chunks = (2 * s.l.k + kBK - 1) / kBK;
     if (chunks > (int64_t{1} << 30)) return fail(ctx, HSB_ERR_UNSUPPORTED, "reduction too long");
     p.seg[nseg].kchunks = static_cast<int32_t>(chunks);
@@ -230,9 +286,10 @@ hsb_status run_zrk(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launche
   int64_t grid_x = z.triangle ? static_cast<int64_t>(p.tiles_m) * (p.tiles_m + 1) / 2
                               : static_cast<int64_t>(p.tiles_m) * p.tiles_n;
   if (grid_x > 0x7fffffff || z.batch > 65535) return fail(ctx, HSB_ERR_UNSUPPORTED, "grid too large");
-  if (ctx->cplx == HSB_CPLX_3M) {
+  if (g3) {
     if (grid_x * z.batch > 0x7fffffff) return fail(ctx, HSB_ERR_UNSUPPORTED, "grid too large");
-    CK(launch_zrk3m(p, z.conj, static_cast<int>(grid_x), static_cast<int>(z.batch), st));
+    CK(launch_zrk3m(p, z.conj, planes, static_cast<int>(grid_x), static_cast<int>(z.batch), st));
+    if (launches) *launches += static_cast<int>(srcs.size());
   } else {
     CK(launch_zrk(p, z.conj, static_cast<int>(grid_x), static_cast<int>(z.batch), st));
   }

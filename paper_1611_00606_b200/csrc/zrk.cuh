@@ -58,6 +58,8 @@ struct SegDesc {
 struct ZrkParams {
   CUtensorMap lmap[kMaxSeg];  // 3-D maps over the real view, box {16, 64|1, 1|64}
   CUtensorMap rmap[kMaxSeg];
+  CUtensorMap lsum[kMaxSeg];  // 3M with planes: 2-D maps over Re-Im of L / Re+Im of R,
+  CUtensorMap rsum[kMaxSeg];  // box {8 complex k, 64 cols}, no swizzle (zrk3m_kernel.cu)
   SegDesc seg[kMaxSeg];
   int32_t nseg;
   int32_t total_chunks;

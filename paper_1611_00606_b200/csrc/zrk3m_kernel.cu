@@ -26,6 +26,13 @@
 //     (rows g, g+1; chunks {s, 2+s, 4+s, 6+s} ^ g) hit 8 distinct 16-byte
 //     chunks: conflict-free LDS.128;
 //   * 12 pipeline stages x 16 KB.
+//
+// PLANES: the host precomputes Re-Im of every left operand and Re+Im of every
+// right operand (sum_planes_kernel), loaded by TMA beside the complex tiles
+// (+8 KB per stage, 8 stages), so the main loop is LDS + DMMA only.  Without
+// planes (batched per-atom views, whose odd row strides TMA cannot address
+// as real planes) the sums are formed in registers with DADD, which shares
+// the FP64 pipe with DMMA (ncu: 90 % vs 96 % DMMA-active on the H launch).
 #include <algorithm>
 
 #include "aux_kernels.cuh"
@@ -36,13 +43,26 @@ namespace hsb {
 
 constexpr int k3ConsumerWarps = 8;  // 2 (rows) x 4 (cols) warps of 32 x 16
 constexpr int k3Threads = (k3ConsumerWarps + 1) * 32;
-constexpr int k3Stages = 12;
-constexpr int k3SmemBytes = k3Stages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kPlaneTileBytes = kBM * 8 * 8;  // 64 rows x 8 complex k, one double each
+template <bool PLANES>
+struct Cfg3 {
+  static constexpr int stage_bytes = kStageBytes + (PLANES ? 2 * kPlaneTileBytes : 0);
+  static constexpr int stages = PLANES ? 8 : 12;
+  static constexpr int smem = stages * stage_bytes + 1024 /*align*/ + 256 /*barriers*/;
+};
 
 __device__ __forceinline__ void dmma_nv(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
       : "+d"(d0), "+d"(d1)
       : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
 }
 
 __device__ __forceinline__ void work_tile(const ZrkParams& p, int w, int ntiles, int& tm, int& tn, int& z) {
@@ -56,22 +76,25 @@ __device__ __forceinline__ void work_tile(const ZrkParams& p, int w, int ntiles,
   }
 }
 
-template <bool CONJ>
+template <bool CONJ, bool PLANES>
 __global__ void __launch_bounds__(k3Threads, 1) zrk3m_kernel(const __grid_constant__ ZrkParams p, int ntiles,
                                                               int nwork) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;  // 128B swizzle atom = 1024 B
   const double2* tiles = reinterpret_cast<const double2*>(smem_raw + (base - raw));
-  const uint32_t bar_base = base + k3Stages * kStageBytes;  // full[s] then empty[s]
+  using C3 = Cfg3<PLANES>;
+  constexpr int kSt = C3::stages;
+  constexpr int kSB = C3::stage_bytes;
+  const uint32_t bar_base = base + kSt * kSB;  // full[s] then empty[s]
   auto full_bar = [&](int s) { return bar_base + 8u * s; };
-  auto empty_bar = [&](int s) { return bar_base + 8u * (k3Stages + s); };
+  auto empty_bar = [&](int s) { return bar_base + 8u * (kSt + s); };
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < k3Stages; ++s) {
+    for (int s = 0; s < kSt; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), k3ConsumerWarps);
     }
@@ -85,6 +108,10 @@ __global__ void __launch_bounds__(k3Threads, 1) zrk3m_kernel(const __grid_consta
       for (int s = 0; s < p.nseg; ++s) {
         prefetch_tmap(&p.lmap[s]);
         prefetch_tmap(&p.rmap[s]);
+        if (PLANES) {
+          prefetch_tmap(&p.lsum[s]);
+          prefetch_tmap(&p.rsum[s]);
+        }
       }
       int stage = 0;
       uint32_t phase = 1;  // fresh empty barriers read as "released"
@@ -97,8 +124,8 @@ __global__ void __launch_bounds__(k3Threads, 1) zrk3m_kernel(const __grid_consta
           for (int kc = 0; kc < sd.kchunks; ++kc) {
             mbar_wait(empty_bar(stage), phase);
             const uint32_t fb = full_bar(stage);
-            mbar_expect_tx(fb, kStageBytes);
-            const uint32_t dst = base + stage * kStageBytes;
+            mbar_expect_tx(fb, kSB);
+            const uint32_t dst = base + stage * kSB;
             const int k0 = kc * kBK;
             if (sd.lbpos == 1)
               tma_load_3d(dst, &p.lmap[s], k0, z, row0, fb);
@@ -108,7 +135,11 @@ __global__ void __launch_bounds__(k3Threads, 1) zrk3m_kernel(const __grid_consta
               tma_load_3d(dst + kTileBytes, &p.rmap[s], k0, z, col0, fb);
             else
               tma_load_3d(dst + kTileBytes, &p.rmap[s], k0, col0, z, fb);
-            if (++stage == k3Stages) {
+            if (PLANES) {  // plain operands only (z == 0): 2-D planes, k in complex units
+              tma_load_2d(dst + kStageBytes, &p.lsum[s], kc * 8, row0, fb);
+              tma_load_2d(dst + kStageBytes + kPlaneTileBytes, &p.rsum[s], kc * 8, col0, fb);
+            }
+            if (++stage == kSt) {
               stage = 0;
               phase ^= 1u;
             }
@@ -152,8 +183,18 @@ __global__ void __launch_bounds__(k3Threads, 1) zrk3m_kernel(const __grid_consta
 
     for (int it = 0; it < p.total_chunks; ++it) {
       mbar_wait(full_bar(stage), phase);
-      const double2* As = tiles + stage * (kStageBytes / 16);
+      const double2* As = tiles + stage * (kSB / 16);
       const double2* Bs = As + kTile2;
+      // plane tiles: 64 rows x 4 double2 (complex k = 2t, 2t+1 of this lane)
+      double2 sa[4], sb[2];
+      if (PLANES) {
+        const double2* Ps = Bs + kTile2;
+        const double2* Qs = Ps + kPlaneTileBytes / 16;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) sa[i] = Ps[(wm * 32 + i * 8 + g) * 4 + t];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) sb[j] = Qs[(wn * 16 + j * 8 + g) * 4 + t];
+      }
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         const int oa = s ? offa1 : offa0;
@@ -164,10 +205,17 @@ __global__ void __launch_bounds__(k3Threads, 1) zrk3m_kernel(const __grid_consta
         for (int i = 0; i < 4; ++i) a[i] = As[oa + i * 64];
 #pragma unroll
         for (int j = 0; j < 2; ++j) b[j] = Bs[ob + j * 64];
+        if (PLANES) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) as[i] = CONJ ? a[i].x - a[i].y : a[i].x + a[i].y;
+          for (int i = 0; i < 4; ++i) as[i] = s ? sa[i].y : sa[i].x;
 #pragma unroll
-        for (int j = 0; j < 2; ++j) bs[j] = b[j].x + b[j].y;
+          for (int j = 0; j < 2; ++j) bs[j] = s ? sb[j].y : sb[j].x;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) as[i] = CONJ ? a[i].x - a[i].y : a[i].x + a[i].y;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) bs[j] = b[j].x + b[j].y;
+        }
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -179,7 +227,7 @@ __global__ void __launch_bounds__(k3Threads, 1) zrk3m_kernel(const __grid_consta
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty_bar(stage));
-      if (++stage == k3Stages) {
+      if (++stage == kSt) {
         stage = 0;
         phase ^= 1u;
       }
@@ -228,15 +276,22 @@ __global__ void __launch_bounds__(k3Threads, 1) zrk3m_kernel(const __grid_consta
 }
 
 // ------------------------------------------------------------------ launcher
-cudaError_t launch_zrk3m(const ZrkParams& p, bool conj, int ntiles, int nbatch, cudaStream_t st) {
-  static bool attr_done[2] = {false, false};
-  static int n_sm = 0;
-  auto kern = conj ? zrk3m_kernel<true> : zrk3m_kernel<false>;
-  if (!attr_done[conj]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, k3SmemBytes);
+template <bool CONJ, bool PLANES>
+static cudaError_t launch3(const ZrkParams& p, int ntiles, int nwork, int n_sm, cudaStream_t st) {
+  static bool attr_done = false;
+  auto kern = zrk3m_kernel<CONJ, PLANES>;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg3<PLANES>::smem);
     if (e != cudaSuccess) return e;
-    attr_done[conj] = true;
+    attr_done = true;
   }
+  const int grid = std::min(nwork, n_sm);
+  kern<<<dim3(grid), dim3(k3Threads), Cfg3<PLANES>::smem, st>>>(p, ntiles, nwork);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_zrk3m(const ZrkParams& p, bool conj, bool planes, int ntiles, int nbatch, cudaStream_t st) {
+  static int n_sm = 0;
   if (n_sm == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -245,9 +300,10 @@ cudaError_t launch_zrk3m(const ZrkParams& p, bool conj, int ntiles, int nbatch, 
   }
   const int64_t nwork = static_cast<int64_t>(ntiles) * nbatch;
   if (nwork > 0x7fffffff) return cudaErrorInvalidConfiguration;
-  const int grid = static_cast<int>(std::min<int64_t>(nwork, n_sm));
-  kern<<<dim3(grid), dim3(k3Threads), k3SmemBytes, st>>>(p, ntiles, static_cast<int>(nwork));
-  return cudaGetLastError();
+  if (planes && nbatch != 1) return cudaErrorInvalidValue;
+  const int nw = static_cast<int>(nwork);
+  if (conj) return planes ? launch3<true, true>(p, ntiles, nw, n_sm, st) : launch3<true, false>(p, ntiles, nw, n_sm, st);
+  return planes ? launch3<false, true>(p, ntiles, nw, n_sm, st) : launch3<false, false>(p, ntiles, nw, n_sm, st);
 }
 
 }  // namespace hsb
