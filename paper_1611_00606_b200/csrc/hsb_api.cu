@@ -56,6 +56,8 @@ struct hsb_ctx {
   int* done_cnt = nullptr;            // mapped pinned per-column-block tile counters
   size_t done_cnt_len = 0;
   cudaStream_t copy_stream = nullptr;  // overlaps S download with the H contraction
+  int64_t tile_list_T = 0;             // tile rows of the cached grouped triangle order
+  std::vector<int2> tile_list_host;    // its host copy (source of an async upload)
   int32_t cplx = HSB_CPLX_3M;          // complex product form of the zrk kernels
 };
 
@@ -203,6 +205,34 @@ struct ZrkCall {
   int* done_cnt = nullptr;
 };
 
+// Lower-triangle tile order for the persistent 3M kernel.  The 148 CTAs run
+// consecutive list entries concurrently and advance through k in near
+// lockstep, so the operand panels they share stay in L2.  Column-major tile
+// order puts ~148 distinct row panels in flight at once (each streamed from
+// HBM: 117 GB per C3 H launch); kTileGroup x kTileGroup blocks of tiles
+// (column groups left to right, row groups top to bottom, i >= j) put 2 x 12.
+// Column groups still complete left to right, which the H download stream
+// relies on (done_cnt prefix).
+constexpr int kTileGroup = 12;
+hsb_status tile_order(hsb_ctx* ctx, int64_t T, cudaStream_t st, const int2** out) {
+  void* buf;
+  CKS(ws(ctx, "tile_list", static_cast<size_t>(T * (T + 1) / 2) * sizeof(int2), &buf));
+  if (ctx->tile_list_T != T) {
+    std::vector<int2>& v = ctx->tile_list_host;
+    v.clear();
+    v.reserve(static_cast<size_t>(T * (T + 1) / 2));
+    for (int64_t j0 = 0; j0 < T; j0 += kTileGroup)
+      for (int64_t i0 = j0; i0 < T; i0 += kTileGroup)
+        for (int64_t j = j0; j < std::min<int64_t>(j0 + kTileGroup, T); ++j)
+          for (int64_t i = std::max(i0, j); i < std::min<int64_t>(i0 + kTileGroup, T); ++i)
+            v.push_back(make_int2(static_cast<int>(i), static_cast<int>(j)));
+    CK(cudaMemcpyAsync(buf, v.data(), v.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+    ctx->tile_list_T = T;
+  }
+  *out = static_cast<const int2*>(buf);
+  return HSB_OK;
+}
+
 hsb_status run_zrk(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launches) {
   if (z.m <= 0 || z.n <= 0 || z.batch <= 0) return HSB_OK;
   if (z.segs.size() > static_cast<size_t>(kMaxSeg)) return fail(ctx, HSB_ERR_UNSUPPORTED, "too many segments");
@@ -286,6 +316,7 @@ hsb_status run_zrk(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launche
   int64_t grid_x = z.triangle ? static_cast<int64_t>(p.tiles_m) * (p.tiles_m + 1) / 2
                               : static_cast<int64_t>(p.tiles_m) * p.tiles_n;
   if (grid_x > 0x7fffffff || z.batch > 65535) return fail(ctx, HSB_ERR_UNSUPPORTED, "grid too large");
+  if (g3 && z.triangle && z.batch == 1 && p.tiles_m > kTileGroup) CKS(tile_order(ctx, p.tiles_m, st, &p.tile_list));
   if (g3) {
     if (grid_x * z.batch > 0x7fffffff) return fail(ctx, HSB_ERR_UNSUPPORTED, "grid too large");
     CK(launch_zrk3m(p, z.conj, planes, static_cast<int>(grid_x), static_cast<int>(z.batch), st));
@@ -400,6 +431,7 @@ hsb_status hsb_ctx_trim(hsb_ctx* ctx) {
   for (auto& kv : ctx->bufs)
     if (kv.second.ptr) cudaFree(kv.second.ptr);
   ctx->bufs.clear();
+  ctx->tile_list_T = 0;
   return HSB_OK;
 }
 

@@ -72,6 +72,8 @@ struct ZrkParams {
   int64_t ldc;              // complex elements
   int64_t c_bstride;        // complex elements between batch outputs
   const int32_t* c_rowoff;  // optional per-batch row offset (complex), overrides c_bstride
+  const int2* tile_list;    // optional (triangle mode, 3M kernel): work order as (tile row,
+                            // tile col), grouped for L2 reuse of the operand panels
   int* done_cnt;            // optional (triangle mode): per 64-column block, tiles finished
                             // writing into it; host-visible (mapped pinned memory).  A block
                             // is final when its count reaches tiles_m.

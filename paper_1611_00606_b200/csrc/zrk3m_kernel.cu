@@ -68,7 +68,11 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
 __device__ __forceinline__ void work_tile(const ZrkParams& p, int w, int ntiles, int& tm, int& tn, int& z) {
   z = w / ntiles;
   const int t = w - z * ntiles;
-  if (p.triangle) {
+  if (p.tile_list) {
+    const int2 tt = p.tile_list[t];
+    tm = tt.x;
+    tn = tt.y;
+  } else if (p.triangle) {
     tri_tile(t, p.tiles_m, tm, tn);
   } else {
     tm = t % p.tiles_m;
