@@ -70,6 +70,19 @@ HSB_API hsb_status hsb_ctx_trim(hsb_ctx* ctx);
 #define HSB_CPLX_3M 1
 HSB_API hsb_status hsb_ctx_set_complex_mult(hsb_ctx* ctx, int32_t algo);
 
+/* Engine of the lower-triangle contractions (S, H, herk, her2k, gemmt).
+ * HSB_ENGINE_DMMA (default): FP64 DMMA tensor cores (complex form above).
+ * HSB_ENGINE_INT8: FP64-accurate emulation on the INT8 tensor cores
+ *   (tcgen05.mma kind::i8) by the Chinese-remainder / Ozaki-II scheme:
+ *   operands rounded to min_bits-bit integers per column (relative error
+ *   ~2^-min_bits of each column's max), then exact modular INT8 products and
+ *   CRT reconstruction.  min_bits = 0 selects the default 40 (~1e-12 relative
+ *   Frobenius; the north star's bound is 1e-10).  Batched per-atom products
+ *   (Loop 1 / Loop 2) and rectangular GEMMs always use DMMA. */
+#define HSB_ENGINE_DMMA 0
+#define HSB_ENGINE_INT8 1
+HSB_API hsb_status hsb_ctx_set_engine(hsb_ctx* ctx, int32_t engine, int32_t min_bits);
+
 /* ------------------------------------------------------------------------ */
 /* Kernel level: the five large updates.  Device pointers, caller's stream.  */
 /* These replace run_partitioned(kind, operands, policy) for kind in         */

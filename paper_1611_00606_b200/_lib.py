@@ -28,6 +28,9 @@ HSB_OPT_UNFUSED = 0x2
 HSB_CPLX_4M = 0
 HSB_CPLX_3M = 1
 COMPLEX_MULT = {"4m": HSB_CPLX_4M, "3m": HSB_CPLX_3M}
+HSB_ENGINE_DMMA = 0
+HSB_ENGINE_INT8 = 1
+ENGINES = {"dmma": HSB_ENGINE_DMMA, "int8": HSB_ENGINE_INT8}
 
 _P = ctypes.c_void_p
 _DPP = ctypes.POINTER(ctypes.c_void_p)
@@ -90,6 +93,7 @@ def load():
             "hsb_last_error": (ctypes.c_char_p, [_P]),
             "hsb_ctx_trim": (i32, [_P]),
             "hsb_ctx_set_complex_mult": (i32, [_P, i32]),
+            "hsb_ctx_set_engine": (i32, [_P, i32, i32]),
             "hsb_zherk": (i32, [_P, _P, i64, i64, dbl, _P, i64, dbl, _P, i64, u32]),
             "hsb_zher2k": (i32, [_P, _P, i64, i64, dbl, dbl, _P, i64, _P, i64, dbl, _P, i64, u32]),
             "hsb_zgemm": (i32, [_P, _P, ch, ch, i64, i64, i64, dbl, dbl, _P, i64, _P, i64, dbl, dbl,
@@ -123,15 +127,19 @@ def check(status: int, ctx) -> None:
     raise RuntimeError(f"libhsb200 error {status}: {msg}")
 
 
-def context(device: int = 0, complex_mult: str | None = None):
+def context(device: int = 0, complex_mult: str | None = None, engine: str | None = None, int8_bits: int = 0):
     """Process-wide context for ``device`` (created on first use).
 
     ``complex_mult`` ("3m" | "4m") selects the real-product form of the
-    complex contractions for the calls that follow (hsb_ctx_set_complex_mult).
+    complex contractions for the calls that follow (hsb_ctx_set_complex_mult);
+    ``engine`` ("dmma" | "int8") the engine of the triangle contractions
+    (hsb_ctx_set_engine; ``int8_bits`` 0 = default 40).
     """
     lib = load()
     if complex_mult is not None and complex_mult not in COMPLEX_MULT:
         raise InputError(f"complex_mult must be one of {sorted(COMPLEX_MULT)}, got {complex_mult!r}")
+    if engine is not None and engine not in ENGINES:
+        raise InputError(f"engine must be one of {sorted(ENGINES)}, got {engine!r}")
     with _lock:
         ctx = _ctxs.get(device)
         if ctx is None:
@@ -141,6 +149,8 @@ def context(device: int = 0, complex_mult: str | None = None):
             _ctxs[device] = ctx
         if complex_mult is not None:
             check(lib.hsb_ctx_set_complex_mult(ctx, COMPLEX_MULT[complex_mult]), ctx)
+        if engine is not None:
+            check(lib.hsb_ctx_set_engine(ctx, ENGINES[engine], int(int8_bits)), ctx)
         return ctx
 
 

@@ -287,6 +287,17 @@ cudaError_t launch_sum_planes(const double* x, int64_t ldx, int64_t rows, int64_
   return cudaGetLastError();
 }
 
+__global__ void fill_i32_kernel(int32_t* p, int64_t n, int32_t v) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+cudaError_t launch_fill_i32(int32_t* p, int64_t n, int32_t v, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  fill_i32_kernel<<<grid_for(n, 256, 1024), 256, 0, st>>>(p, n, v);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_mirror(double* c, int64_t ldc, int n, cudaStream_t st) {
   const int64_t nt = (n + 31) / 32;
   const int64_t pairs = nt * (nt + 1) / 2;

@@ -19,6 +19,7 @@ cudaError_t launch_half_mirror(const double* t, double* out, int n, int64_t coun
 cudaError_t launch_diag_scale(const double* src, int64_t lds, double* dst, int64_t ldd, const double* u,
                               int64_t rows, int64_t cols, cudaStream_t st);
 cudaError_t launch_mirror(double* c, int64_t ldc, int n, cudaStream_t st);
+cudaError_t launch_fill_i32(int32_t* p, int64_t n, int32_t v, cudaStream_t st);
 cudaError_t launch_sum_planes(const double* x, int64_t ldx, int64_t rows, int64_t cols, double* minus,
                               double* plus, int64_t ldp, cudaStream_t st);
 cudaError_t launch_gather_rows(const double* src, int64_t lds, double* dst, int64_t ldd, const int32_t* src_off,

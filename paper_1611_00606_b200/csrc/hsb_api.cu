@@ -35,6 +35,7 @@
 #include "../../include/hsb200.h"
 #include "aux_kernels.cuh"
 #include "match.cuh"
+#include "ozaki.cuh"
 #include "staging.cuh"
 #include "zrk.cuh"
 
@@ -58,6 +59,10 @@ struct hsb_ctx {
   cudaStream_t copy_stream = nullptr;  // overlaps S download with the H contraction
   int64_t tile_list_T = 0;             // tile rows of the cached grouped triangle order
   std::vector<int2> tile_list_host;    // its host copy (source of an async upload)
+  int32_t engine = HSB_ENGINE_DMMA;    // triangle contractions: FP64 DMMA or INT8 CRT emulation
+  int32_t oz_min_bits = 40;            // INT8 engine: operand integer bits (accuracy ~2^-bits)
+  int64_t oz_tiles_n = 0;              // cached INT8-engine tile list (n of the output)
+  std::vector<int2> oz_tiles_host;
   int32_t cplx = HSB_CPLX_3M;          // complex product form of the zrk kernels
 };
 
@@ -233,7 +238,174 @@ hsb_status tile_order(hsb_ctx* ctx, int64_t T, cudaStream_t st, const int2** out
   return HSB_OK;
 }
 
+// ---------------------------------------------------------------- INT8 engine
+// Lower-triangle C = alpha sum_s op(L_s)^T R_s + beta C on the INT8 tensor
+// cores (ozaki.cuh): column exponents, residue planes of every distinct
+// operand, one persistent tcgen05 GEMM launch over (product, modulus, tile),
+// CRT reconstruction + mirror.
+hsb_status oz_encode(hsb_ctx* ctx, CUtensorMap* map, const int8_t* planes, int64_t k, int64_t cols, int64_t kpad,
+                     int n_mod, int box_rows) {
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(n_mod)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(kpad), static_cast<cuuint64_t>(kpad * cols)};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(kOzBK), static_cast<cuuint32_t>(box_rows), 1}, es[3] = {1, 1, 1};
+  CUresult r = ctx->encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(planes), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(ctx, HSB_ERR_CUDA, "cuTensorMapEncodeTiled failed for residue planes (code " +
+                                       std::to_string(static_cast<int>(r)) + ")");
+  return HSB_OK;
+}
+
+// 128 x 256 tiles (tile row tm, tile col tn) that touch the lower triangle
+// (tm >= 2 tn), in groups of 8 tile rows x 4 tile cols for L2 reuse
+hsb_status oz_tiles(hsb_ctx* ctx, int64_t n, cudaStream_t st, const int2** out, int* count) {
+  const int64_t tm_n = (n + kOzBM - 1) / kOzBM, tn_n = (n + kOzBN - 1) / kOzBN;
+  std::vector<int2>& v = ctx->oz_tiles_host;
+  if (ctx->oz_tiles_n != n) {
+    v.clear();
+    for (int64_t j0 = 0; j0 < tn_n; j0 += 4)
+      for (int64_t i0 = 2 * j0; i0 < tm_n; i0 += 8)
+        for (int64_t j = j0; j < std::min<int64_t>(j0 + 4, tn_n); ++j)
+          for (int64_t i = std::max(i0, 2 * j); i < std::min<int64_t>(i0 + 8, tm_n); ++i)
+            v.push_back(make_int2(static_cast<int>(i), static_cast<int>(j)));
+  }
+  void* buf;
+  CKS(ws(ctx, "oz_tiles", v.size() * sizeof(int2), &buf));
+  if (ctx->oz_tiles_n != n) {
+    CK(cudaMemcpyAsync(buf, v.data(), v.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+    ctx->oz_tiles_n = n;
+  }
+  *out = static_cast<const int2*>(buf);
+  *count = static_cast<int>(v.size());
+  return HSB_OK;
+}
+
+hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launches) {
+  const int64_t n = z.m;
+  std::vector<Seg> segs;
+  int64_t ktot = 0;
+  for (const Seg& s : z.segs)
+    if (s.l.k > 0) {
+      if (s.l.k != s.r.k) return fail(ctx, HSB_ERR_DIMENSION, "segment operands disagree in reduction length");
+      segs.push_back(s);
+      ktot += s.l.k;
+    }
+  if (segs.size() > static_cast<size_t>(kOzMaxSeg)) return fail(ctx, HSB_ERR_UNSUPPORTED, "too many segments");
+  // moduli: the fewest with b >= oz_min_bits, where |Re'|,|Im'| <= 3 K 2^2b < M/2
+  int n_mod = 0, b = 0;
+  {
+    double log2m = 0;
+    for (int i = 0; i < kOzMaxMod; ++i) {
+      log2m += std::log2(static_cast<double>(oz_mod(i)));
+      const int bi = static_cast<int>(std::floor((log2m - 2.0 - std::log2(3.0 * std::max<int64_t>(ktot, 1))) / 2.0)) - 1;
+      if (i + 1 >= 11 && (bi >= ctx->oz_min_bits || i + 1 == kOzMaxMod)) {
+        n_mod = i + 1;
+        b = std::min(bi, ctx->oz_min_bits + 4);
+        break;
+      }
+    }
+  }
+  if (b < 30) return fail(ctx, HSB_ERR_UNSUPPORTED, "reduction too long for the INT8 engine's moduli");
+  // exponents: one array for both sides (m == n), max over every operand
+  void* ebuf;
+  CKS(ws(ctx, "oz_exp", static_cast<size_t>(n) * sizeof(int32_t), &ebuf));
+  int32_t* e = static_cast<int32_t*>(ebuf);
+  CK(launch_ozaki_init_exp(e, n, st));
+  for (const Seg& s : segs) {
+    CK(launch_ozaki_colexp(s.l.base, s.l.ld, s.l.k, s.l.cols, e, st));
+    CK(launch_ozaki_colexp(s.r.base, s.r.ld, s.r.k, s.r.cols, e, st));
+  }
+  // residue planes of each distinct operand
+  struct Src {
+    const double* base;
+    int64_t k, ld;
+    int8_t* planes;
+    int64_t kpad;
+  };
+  std::vector<Src> srcs;
+  auto planes_of = [&](const OperandView& v, Src* out) -> hsb_status {
+    for (const Src& q : srcs)
+      if (q.base == v.base && q.k == v.k && q.ld == v.ld) {
+        *out = q;
+        return HSB_OK;
+      }
+    Src q{v.base, v.k, v.ld, nullptr, (v.k + 15) / 16 * 16};
+    const std::string name = "oz_res" + std::to_string(srcs.size());
+    void* buf;
+    CKS(ws(ctx, name.c_str(), static_cast<size_t>(4) * n_mod * n * q.kpad, &buf));
+    q.planes = static_cast<int8_t*>(buf);
+    CK(launch_ozaki_residues(v.base, v.ld, v.k, n, e, b, n_mod, q.planes, q.kpad, st));
+    srcs.push_back(q);
+    *out = q;
+    return HSB_OK;
+  };
+  OzGemmParams gp;
+  std::memset(&gp, 0, sizeof(gp));
+  // products: P = re.re, Q = im.im, W = (re -/+ im)(re + im)
+  const int lp[3] = {kOzRe, kOzIm, z.conj ? kOzMinus : kOzPlus};
+  const int rp[3] = {kOzRe, kOzIm, kOzPlus};
+  for (size_t si = 0; si < segs.size(); ++si) {
+    Src L, R;
+    CKS(planes_of(segs[si].l, &L));
+    CKS(planes_of(segs[si].r, &R));
+    const int64_t pl = static_cast<int64_t>(n_mod) * n * L.kpad, pr = static_cast<int64_t>(n_mod) * n * R.kpad;
+    for (int pi = 0; pi < 3; ++pi) {
+      CKS(oz_encode(ctx, &gp.map[pi][si][0], L.planes + lp[pi] * pl, L.k, n, L.kpad, n_mod, kOzBM));
+      CKS(oz_encode(ctx, &gp.map[pi][si][1], R.planes + rp[pi] * pr, R.k, n, R.kpad, n_mod, kOzBN));
+    }
+    gp.kchunks[si] = static_cast<int32_t>((segs[si].l.k + kOzBK - 1) / kOzBK);
+  }
+  gp.nseg = static_cast<int32_t>(segs.size());
+  gp.n_mod = n_mod;
+  gp.n = static_cast<int32_t>(n);
+  gp.ldr = (n + 15) / 16 * 16;
+  gp.mod_stride = gp.ldr * n;
+  gp.prod_stride = gp.mod_stride * n_mod;
+  void* rbuf;
+  CKS(ws(ctx, "oz_out", static_cast<size_t>(3 * gp.prod_stride), &rbuf));
+  gp.res = static_cast<int8_t*>(rbuf);
+  if (gp.nseg > 0) {
+    CKS(oz_tiles(ctx, n, st, &gp.tile_list, &gp.ntiles));
+    CK(launch_ozaki_gemm(gp, st));
+  } else {
+    CK(cudaMemsetAsync(rbuf, 0, static_cast<size_t>(3 * gp.prod_stride), st));
+  }
+  OzCrtParams cp;
+  cp.res = gp.res;
+  cp.ldr = gp.ldr;
+  cp.mod_stride = gp.mod_stride;
+  cp.prod_stride = gp.prod_stride;
+  cp.n_mod = n_mod;
+  cp.n = static_cast<int32_t>(n);
+  cp.b = b;
+  cp.conj = z.conj ? 1 : 0;
+  cp.el = e;
+  cp.er = e;
+  cp.alpha_re = z.alpha_re;
+  cp.alpha_im = z.alpha_im;
+  cp.beta_re = z.beta_re;
+  cp.beta_im = z.beta_im;
+  cp.c = z.c;
+  cp.ldc = z.ldc;
+  cp.flags = z.flags;
+  CK(launch_ozaki_crt(cp, st));
+  if (z.done_cnt) {
+    // the host H stream polls per-column counters; everything is final here
+    // (triangle tiles of the DMMA grid: count T for every column block)
+    const int64_t T = (n + kBN - 1) / kBN;
+    CK(launch_fill_i32(z.done_cnt, T, static_cast<int32_t>(T), st));
+  }
+  if (launches) *launches += 3 + 2 * static_cast<int>(segs.size()) + static_cast<int>(srcs.size());
+  return HSB_OK;
+}
+
 hsb_status run_zrk(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launches) {
+  if (ctx->engine == HSB_ENGINE_INT8 && z.triangle && z.batch == 1 && z.m == z.n && z.m > 0) {
+    bool plain = true;
+    for (const Seg& s : z.segs) plain = plain && s.l.batch == 1 && s.r.batch == 1;
+    if (plain) return run_ozaki(ctx, st, z, launches);
+  }
   if (z.m <= 0 || z.n <= 0 || z.batch <= 0) return HSB_OK;
   if (z.segs.size() > static_cast<size_t>(kMaxSeg)) return fail(ctx, HSB_ERR_UNSUPPORTED, "too many segments");
   if (z.triangle && z.m != z.n) return fail(ctx, HSB_ERR_DIMENSION, "triangle mode needs a square output");
@@ -424,6 +596,16 @@ hsb_status hsb_ctx_set_complex_mult(hsb_ctx* ctx, int32_t algo) {
   return HSB_OK;
 }
 
+hsb_status hsb_ctx_set_engine(hsb_ctx* ctx, int32_t engine, int32_t min_bits) {
+  if (!ctx) return fail(nullptr, HSB_ERR_INPUT, "ctx is NULL");
+  if (engine != HSB_ENGINE_DMMA && engine != HSB_ENGINE_INT8) return fail(ctx, HSB_ERR_INPUT, "unknown engine");
+  if (min_bits != 0 && (min_bits < 30 || min_bits > 48))
+    return fail(ctx, HSB_ERR_INPUT, "min_bits must be 0 (default 40) or in [30, 48]");
+  ctx->engine = engine;
+  ctx->oz_min_bits = min_bits ? min_bits : 40;
+  return HSB_OK;
+}
+
 hsb_status hsb_ctx_trim(hsb_ctx* ctx) {
   if (!ctx) return fail(nullptr, HSB_ERR_INPUT, "ctx is NULL");
   cudaSetDevice(ctx->device);
@@ -432,6 +614,7 @@ hsb_status hsb_ctx_trim(hsb_ctx* ctx) {
     if (kv.second.ptr) cudaFree(kv.second.ptr);
   ctx->bufs.clear();
   ctx->tile_list_T = 0;
+  ctx->oz_tiles_n = 0;
   return HSB_OK;
 }
 

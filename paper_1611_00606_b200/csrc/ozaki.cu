@@ -1,0 +1,454 @@
+// ozaki.cu — kernels of the INT8-tensor-core emulated FP64 contraction
+// (scheme in ozaki.cuh): column exponents, residue planes, the tcgen05
+// kind::i8 modular GEMM over lower-triangle tiles, and the CRT
+// reconstruction with the 3M combination and the Hermitian mirror.
+#include <climits>
+
+#include "ozaki.cuh"
+#include "ptx.cuh"
+#include "zrk.cuh"
+
+namespace hsb {
+
+__constant__ int32_t c_oz_inv[kOzMaxMod][kOzMaxMod];  // [j][i] = p_j^-1 mod p_i (j < i)
+__constant__ int32_t oz_mod_rt[kOzMaxMod] = {256, 255, 253, 251, 247, 241, 239, 233,
+                                             229, 227, 223, 217, 211, 199, 197, 193};
+
+// ------------------------------------------------------------ small helpers
+__device__ __forceinline__ int sym_lo(int p) { return -(p >> 1); }
+
+// symmetric residue of an exactly-integer double |v| < 2^52
+__device__ __forceinline__ int sym_mod_d(double v, double p, double inv_p, int ip) {
+  const double q = rint(v * inv_p);
+  int r = static_cast<int>(fma(-p, q, v));  // exact: v - p*q is an integer below 2^53
+  const int lo = sym_lo(ip);
+  if (r < lo) r += ip;
+  if (r > lo + ip - 1) r -= ip;
+  if (r < lo) r += ip;
+  return r;
+}
+__device__ __forceinline__ int sym_adj(int r, int p) {
+  const int lo = sym_lo(p);
+  if (r < lo) r += p;
+  if (r > lo + p - 1) r -= p;
+  return r;
+}
+
+// ------------------------------------------------------------ 1. exponents
+__global__ void ozaki_init_exp_kernel(int32_t* e, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    e[i] = INT_MIN / 2;
+}
+
+// one warp per column: e = frexp exponent of max_k |Re x| + |Im x| (max < 2^e)
+__global__ void ozaki_colexp_kernel(const double2* __restrict__ x, int64_t ldx, int64_t k, int64_t cols,
+                                    int32_t* __restrict__ e) {
+  const int warps = blockDim.x >> 5;
+  for (int64_t c = static_cast<int64_t>(blockIdx.x) * warps + (threadIdx.x >> 5); c < cols;
+       c += static_cast<int64_t>(gridDim.x) * warps) {
+    double m = 0.0;
+    const double2* col = x + c * ldx;
+    for (int64_t r = threadIdx.x & 31; r < k; r += 32) {
+      const double2 v = col[r];
+      m = fmax(m, fabs(v.x) + fabs(v.y));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) {
+      int ex = 0;
+      frexp(m, &ex);  // m = f * 2^ex, f in [0.5, 1): m < 2^ex (m = 0 -> ex = 0)
+      atomicMax(e + c, ex);
+    }
+  }
+}
+
+// ------------------------------------------------------------ 2. residues
+// thread = 4 consecutive k of one column; writes char4 into each of the
+// 4 planes x n_mod moduli: out[((plane * n_mod + i) * cols + col) * kpad + k]
+__global__ void ozaki_residue_kernel(const double2* __restrict__ x, int64_t ldx, int64_t k, int64_t cols,
+                                     const int32_t* __restrict__ col_exp, int b, int n_mod,
+                                     int8_t* __restrict__ out, int64_t kpad) {
+  const int64_t k4 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+  if (k4 >= kpad) return;
+  const int64_t plane_stride = static_cast<int64_t>(n_mod) * cols * kpad;
+  for (int64_t c = blockIdx.y; c < cols; c += gridDim.y) {
+    const int sh = b - col_exp[c];
+    double xr[4], xi[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (k4 + j < k) {
+        const double2 v = x[c * ldx + k4 + j];
+        xr[j] = rint(ldexp(v.x, sh));
+        xi[j] = rint(ldexp(v.y, sh));
+      } else {
+        xr[j] = xi[j] = 0.0;
+      }
+    }
+    int8_t* o = out + c * kpad + k4;
+    for (int i = 0; i < n_mod; ++i) {
+      const int ip = oz_mod_rt[i];
+      const double p = ip, inv = 1.0 / p;
+      char4 re, im, mi, pl;
+      int rr[4], ri[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        rr[j] = sym_mod_d(xr[j], p, inv, ip);
+        ri[j] = sym_mod_d(xi[j], p, inv, ip);
+      }
+      re = make_char4(rr[0], rr[1], rr[2], rr[3]);
+      im = make_char4(ri[0], ri[1], ri[2], ri[3]);
+      mi = make_char4(sym_adj(rr[0] - ri[0], ip), sym_adj(rr[1] - ri[1], ip), sym_adj(rr[2] - ri[2], ip),
+                      sym_adj(rr[3] - ri[3], ip));
+      pl = make_char4(sym_adj(rr[0] + ri[0], ip), sym_adj(rr[1] + ri[1], ip), sym_adj(rr[2] + ri[2], ip),
+                      sym_adj(rr[3] + ri[3], ip));
+      const int64_t mo = static_cast<int64_t>(i) * cols * kpad;
+      *reinterpret_cast<char4*>(o + kOzRe * plane_stride + mo) = re;
+      *reinterpret_cast<char4*>(o + kOzIm * plane_stride + mo) = im;
+      *reinterpret_cast<char4*>(o + kOzMinus * plane_stride + mo) = mi;
+      *reinterpret_cast<char4*>(o + kOzPlus * plane_stride + mo) = pl;
+    }
+  }
+}
+
+// ------------------------------------------------------------ 3. INT8 GEMM
+constexpr int kOzStages = 4;
+constexpr int kOzABytes = kOzBM * kOzBK, kOzBBytes = kOzBN * kOzBK;
+constexpr int kOzStageBytes = kOzABytes + kOzBBytes;  // 48 KB
+constexpr int kOzSmem = kOzStages * kOzStageBytes + 1024 + 256;
+constexpr int kOzThreads = 192;  // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 epilogue
+
+__device__ __forceinline__ void tma_load_3d_u8(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                               uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+// K-major operand tile, 128B swizzle: 8-row atoms of 1024 B (SBO); LBO unused
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
+  return static_cast<uint64_t>((addr >> 4) & 0x3FFF) | (static_cast<uint64_t>(1) << 16) |
+         (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
+         (static_cast<uint64_t>(2) << 61);
+}
+constexpr uint32_t kOzIdesc = (2u << 4)                // D: s32
+                              | (1u << 7)              // A: signed int8
+                              | (1u << 10)             // B: signed int8
+                              | ((kOzBN >> 3) << 17)   // N
+                              | ((kOzBM >> 4) << 24);  // M
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kOzIdesc), "r"(acc), "r"(0), "r"(0), "r"(0), "r"(0));
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+        "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+        "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void oz_work(const OzGemmParams& p, int w, int& prod, int& mod, int& tm, int& tn) {
+  const int per_prod = p.n_mod * p.ntiles;
+  prod = w / per_prod;
+  const int r = w - prod * per_prod;
+  mod = r / p.ntiles;
+  const int2 t = p.tile_list[r - mod * p.ntiles];
+  tm = t.x;
+  tn = t.y;
+}
+
+__global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const __grid_constant__ OzGemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t bars = base + kOzStages * kOzStageBytes;
+  auto full = [&](int s) { return bars + 8u * s; };
+  auto empty = [&](int s) { return bars + 8u * (kOzStages + s); };
+  auto tfull = [&](int s) { return bars + 8u * (2 * kOzStages + s); };
+  auto tempty = [&](int s) { return bars + 8u * (2 * kOzStages + 2 + s); };
+  const uint32_t tmem_slot = bars + 8u * (2 * kOzStages + 4);
+  const uint32_t* tmem_slot_ptr = reinterpret_cast<const uint32_t*>(smem_raw + (tmem_slot - raw));
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwork = 3 * p.n_mod * p.ntiles;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kOzStages; ++s) {
+      mbar_init(full(s), 1);
+      mbar_init(empty(s), 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(tfull(s), 1);
+      mbar_init(tempty(s), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot_ptr;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 1;
+      for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+        int prod, mod, tm, tn;
+        oz_work(p, w, prod, mod, tm, tn);
+        for (int s = 0; s < p.nseg; ++s) {
+          const CUtensorMap* ml = &p.map[prod][s][0];
+          const CUtensorMap* mr = &p.map[prod][s][1];
+          for (int kc = 0; kc < p.kchunks[s]; ++kc) {
+            mbar_wait(empty(stage), phase);
+            mbar_expect_tx(full(stage), kOzStageBytes);
+            const uint32_t dst = base + stage * kOzStageBytes;
+            tma_load_3d_u8(dst, ml, kc * kOzBK, tm * kOzBM, mod, full(stage));
+            tma_load_3d_u8(dst + kOzABytes, mr, kc * kOzBK, tn * kOzBN, mod, full(stage));
+            if (++stage == kOzStages) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 1;
+      for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+        mbar_wait(tempty(acc), acc_phase);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + acc * kOzBN;
+        bool first = true;
+        for (int s = 0; s < p.nseg; ++s) {
+          for (int kc = 0; kc < p.kchunks[s]; ++kc) {
+            mbar_wait(full(stage), phase);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t a0 = base + stage * kOzStageBytes, b0 = a0 + kOzABytes;
+#pragma unroll
+            for (int kk = 0; kk < kOzBK / 32; ++kk) {
+              mma_i8(d, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), first ? 0u : 1u);
+              first = false;
+            }
+            mma_commit(empty(stage));
+            if (++stage == kOzStages) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+        }
+        mma_commit(tfull(acc));
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1u;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    // warp w owns TMEM lanes 32*(w%4) .. +31 = tile rows; residue mod p, int8
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+      int prod, mod, tm, tn;
+      oz_work(p, w, prod, mod, tm, tn);
+      const int ip = oz_mod_rt[mod];
+      const double pd = ip, inv = 1.0 / pd;
+      const int lo = sym_lo(ip);
+      mbar_wait(tfull(acc), acc_phase);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int row = tm * kOzBM + q * 32 + lane;
+      int8_t* out = p.res + prod * p.prod_stride + mod * p.mod_stride + row;
+      const int col0 = tn * kOzBN;
+      const int ncol = min(kOzBN, p.n - col0);
+      for (int c = 0; c < kOzBN / 32; ++c) {
+        if (c * 32 >= ncol) break;  // warp-uniform
+        uint32_t v[32];
+        tmem_ld32(tmem + ((q * 32) << 16) + acc * kOzBN + c * 32, v);
+        if (row < p.n) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int col = col0 + c * 32 + j;
+            if (col < p.n) {
+              const double a = static_cast<double>(static_cast<int32_t>(v[j]));
+              int r = static_cast<int>(fma(-pd, rint(a * inv), a));
+              if (r < lo) r += ip;
+              if (r > lo + ip - 1) r -= ip;
+              out[static_cast<int64_t>(col) * p.ldr] = static_cast<int8_t>(r);
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty(acc));
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1u;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// ------------------------------------------------------------ 4. CRT
+// Garner's mixed radix with symmetric digits: X = v0 + p0 (v1 + p1 (v2 + ...)),
+// every digit |v_i| <= p_i / 2, so the double Horner sum has no cancellation.
+template <int NM>
+__device__ __forceinline__ double garner(const int (&r)[NM]) {
+  int v[NM];
+#pragma unroll
+  for (int i = 0; i < NM; ++i) {
+    const int pi = oz_mod(i);
+    int t = r[i];
+#pragma unroll
+    for (int j = 0; j < i; ++j) t = ((t - v[j]) * c_oz_inv[j][i]) % pi;
+    v[i] = sym_adj(t, pi);
+  }
+  double x = v[NM - 1];
+#pragma unroll
+  for (int i = NM - 2; i >= 0; --i) x = fma(x, static_cast<double>(oz_mod(i)), static_cast<double>(v[i]));
+  return x;
+}
+
+template <int NM>
+__global__ void ozaki_crt_kernel(const OzCrtParams p) {
+  const int n = blockIdx.y;  // column
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= p.n || m < n) return;
+  const int8_t* r0 = p.res + static_cast<int64_t>(n) * p.ldr + m;
+  int re[NM], im[NM];
+#pragma unroll
+  for (int i = 0; i < NM; ++i) {
+    const int pi = oz_mod(i);
+    const int P = r0[i * p.mod_stride];
+    const int Q = r0[p.prod_stride + i * p.mod_stride];
+    const int W = r0[2 * p.prod_stride + i * p.mod_stride];
+    // L^H R: Re = P + Q, Im = W - P + Q ;  L^T R: Re = P - Q, Im = W - P - Q
+    re[i] = sym_adj(p.conj ? P + Q : P - Q, pi);
+    im[i] = sym_adj(sym_adj(p.conj ? W - P + Q : W - P - Q, pi), pi);
+  }
+  const int sh = p.el[m] + p.er[n] - 2 * p.b;
+  const double xr = ldexp(garner<NM>(re), sh);
+  const double xi = ldexp(garner<NM>(im), sh);
+  double vr = p.alpha_re * xr - p.alpha_im * xi;
+  double vi = p.alpha_re * xi + p.alpha_im * xr;
+  double2* C = reinterpret_cast<double2*>(p.c);
+  double2* dst = C + m + static_cast<int64_t>(n) * p.ldc;
+  if (p.beta_re != 0.0 || p.beta_im != 0.0) {
+    const double2 o = *dst;
+    vr += p.beta_re * o.x - p.beta_im * o.y;
+    vi += p.beta_re * o.y + p.beta_im * o.x;
+  }
+  const bool mirror = p.flags & kMirror;
+  if (m == n && (mirror || (p.flags & kZeroImagDiag))) vi = 0.0;
+  *dst = make_double2(vr, vi);
+  if (mirror && m > n) C[n + static_cast<int64_t>(m) * p.ldc] = make_double2(vr, -vi);
+}
+
+// ------------------------------------------------------------ launchers
+static int grid_cap(int64_t want, int cap) { return static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap); }
+
+cudaError_t launch_ozaki_init_exp(int32_t* e, int64_t n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  ozaki_init_exp_kernel<<<grid_cap((n + 255) / 256, 1024), 256, 0, st>>>(e, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ozaki_colexp(const double* x, int64_t ldx, int64_t k, int64_t cols, int32_t* exp_out,
+                                cudaStream_t st) {
+  if (cols <= 0 || k <= 0) return cudaSuccess;
+  ozaki_colexp_kernel<<<grid_cap((cols + 7) / 8, 148 * 16), 256, 0, st>>>(reinterpret_cast<const double2*>(x), ldx,
+                                                                          k, cols, exp_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ozaki_residues(const double* x, int64_t ldx, int64_t k, int64_t cols, const int32_t* col_exp,
+                                  int b, int n_mod, int8_t* out, int64_t kpad, cudaStream_t st) {
+  if (cols <= 0 || kpad <= 0) return cudaSuccess;
+  const int64_t threads_k = kpad / 4;
+  dim3 grid(static_cast<unsigned>((threads_k + 127) / 128), static_cast<unsigned>(cols < 65535 ? cols : 65535));
+  ozaki_residue_kernel<<<grid, 128, 0, st>>>(reinterpret_cast<const double2*>(x), ldx, k, cols, col_exp, b, n_mod,
+                                            out, kpad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ozaki_gemm(const OzGemmParams& p, cudaStream_t st) {
+  static bool attr = false;
+  static int n_sm = 0;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(ozaki_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kOzSmem);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    e = cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    // p_j^-1 mod p_i for Garner
+    int inv[kOzMaxMod][kOzMaxMod] = {};
+    for (int i = 0; i < kOzMaxMod; ++i)
+      for (int j = 0; j < i; ++j) {
+        const int pi = oz_mod(i), pj = oz_mod(j) % pi;
+        for (int x = 1; x < pi; ++x)
+          if ((pj * x) % pi == 1) {
+            inv[j][i] = x;
+            break;
+          }
+      }
+    e = cudaMemcpyToSymbol(c_oz_inv, inv, sizeof(inv));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t nwork = 3LL * p.n_mod * p.ntiles;
+  if (nwork <= 0) return cudaSuccess;
+  if (nwork > 0x7fffffff) return cudaErrorInvalidConfiguration;
+  const int grid = static_cast<int>(nwork < n_sm ? nwork : n_sm);
+  ozaki_gemm_kernel<<<grid, kOzThreads, kOzSmem, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ozaki_crt(const OzCrtParams& p, cudaStream_t st) {
+  if (p.n <= 0) return cudaSuccess;
+  dim3 grid(static_cast<unsigned>((p.n + 127) / 128), static_cast<unsigned>(p.n));
+  if (p.n > 65535) return cudaErrorInvalidConfiguration;
+  switch (p.n_mod) {
+    case 11: ozaki_crt_kernel<11><<<grid, 128, 0, st>>>(p); break;
+    case 12: ozaki_crt_kernel<12><<<grid, 128, 0, st>>>(p); break;
+    case 13: ozaki_crt_kernel<13><<<grid, 128, 0, st>>>(p); break;
+    case 14: ozaki_crt_kernel<14><<<grid, 128, 0, st>>>(p); break;
+    case 15: ozaki_crt_kernel<15><<<grid, 128, 0, st>>>(p); break;
+    case 16: ozaki_crt_kernel<16><<<grid, 128, 0, st>>>(p); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace hsb

@@ -1,0 +1,90 @@
+// ozaki.cuh — FP64-accurate complex Hermitian rank-k updates on the INT8
+// tensor cores (tcgen05.mma kind::i8), by the Chinese-remainder ("Ozaki
+// scheme II") integer emulation of a floating-point product.
+//
+// For C = sum_s L_s^H R_s over complex K_s x N operands (the S and H
+// contractions of Algorithm 1, builder.py:91-208):
+//
+//  1. column scaling: e^L_m = exponent of max over all segments and k of
+//     |Re L| + |Im L| in column m (ozaki_colexp_kernel); same for R.
+//  2. integer operands: x' = rint(Re X * 2^(b - e_col)), y' = rint(Im X * ...),
+//     |x'| + |y'| <= 2^b; four exact integer planes re = x', im = y',
+//     minus = x' - y', plus = x' + y' and their symmetric residues modulo
+//     n_mod pairwise-coprime moduli p_i <= 256 as int8 (ozaki_residue_kernel).
+//  3. 3M products, exact in int32 per modulus (tcgen05 INT8 GEMM, TMEM
+//     accumulators, ozaki_gemm_kernel):
+//        P_i = re(L)^T re(R),  Q_i = im(L)^T im(R),  W_i = minus(L)^T plus(R)
+//     reduced mod p_i in the epilogue and stored as int8 residues.
+//  4. reconstruction (ozaki_crt_kernel): Re' = P + Q, Im' = W - P + Q (mod p_i,
+//     exact integers), Garner mixed-radix with symmetric digits -> double,
+//     scaled by 2^(e^L_m + e^R_n - 2b); alpha/beta, Im(diag) = 0, mirror.
+//
+// Exactness: every step after the rounding in (2) is exact integer
+// arithmetic as long as |Re'|, |Im'| < M/2 = prod p_i / 2, which fixes b from
+// K_tot (the host picks n_mod so that b >= 40).  The only error is the
+// operand rounding, ~2^-b relative to each column's max: ~1e-12 relative
+// Frobenius, inside the north star's 1e-10 (measured in tests/).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hsb {
+
+constexpr int kOzMaxMod = 16;
+constexpr int kOzMaxSeg = 4;
+constexpr int kOzBM = 128;   // output tile rows   (TMEM lanes)
+constexpr int kOzBN = 256;   // output tile cols   (TMEM columns per accumulator)
+constexpr int kOzBK = 128;   // k bytes per stage  (128B swizzle row)
+// pairwise coprime, descending; the first n_mod are used
+__host__ __device__ constexpr int oz_mod(int i) {
+  switch (i) {
+    case 0: return 256;  case 1: return 255;  case 2: return 253;  case 3: return 251;
+    case 4: return 247;  case 5: return 241;  case 6: return 239;  case 7: return 233;
+    case 8: return 229;  case 9: return 227;  case 10: return 223; case 11: return 217;
+    case 12: return 211; case 13: return 199; case 14: return 197; default: return 193;
+  }
+}
+
+// planes of a residue buffer: [plane][modulus][col][kpad] int8
+enum OzPlane { kOzRe = 0, kOzIm = 1, kOzMinus = 2, kOzPlus = 3 };
+
+struct OzGemmParams {
+  // maps[prod][seg][side]: 3-D int8 maps {k, cols, modulus}, box {128, 128|256, 1}
+  CUtensorMap map[3][kOzMaxSeg][2];
+  int32_t kchunks[kOzMaxSeg];
+  int32_t nseg;
+  int32_t n_mod;
+  int32_t n;            // output is n x n (triangle)
+  int32_t ntiles;       // entries of tile_list
+  const int2* tile_list;  // (tile row, tile col) of the 128 x 256 tiles with rows >= cols
+  int8_t* res;          // residues [prod][modulus][col][ldr]
+  int64_t ldr;          // rows stride (bytes), multiple of 16
+  int64_t mod_stride;   // bytes between moduli (ldr * n)
+  int64_t prod_stride;  // bytes between products (mod_stride * n_mod)
+};
+
+struct OzCrtParams {
+  const int8_t* res;
+  int64_t ldr, mod_stride, prod_stride;
+  int32_t n_mod;
+  int32_t n;
+  int32_t b;                 // operand integer bits
+  int32_t conj;              // 1: L^H R ; 0: L^T R
+  const int32_t* el;         // column exponents of the left / right operands
+  const int32_t* er;
+  double alpha_re, alpha_im, beta_re, beta_im;
+  double* c;                 // interleaved complex128, column-major
+  int64_t ldc;
+  uint32_t flags;            // kLowerOnly | kMirror | kZeroImagDiag (zrk.cuh)
+};
+
+cudaError_t launch_ozaki_colexp(const double* x, int64_t ldx, int64_t k, int64_t cols, int32_t* exp_out,
+                                cudaStream_t st);
+cudaError_t launch_ozaki_init_exp(int32_t* e, int64_t n, cudaStream_t st);
+cudaError_t launch_ozaki_residues(const double* x, int64_t ldx, int64_t k, int64_t cols, const int32_t* col_exp,
+                                  int b, int n_mod, int8_t* out, int64_t kpad, cudaStream_t st);
+cudaError_t launch_ozaki_gemm(const OzGemmParams& p, cudaStream_t st);
+cudaError_t launch_ozaki_crt(const OzCrtParams& p, cudaStream_t st);
+
+}  // namespace hsb

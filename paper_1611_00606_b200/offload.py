@@ -72,7 +72,7 @@ def _run_gpu(kind, operands, policy: GpuPolicy):
     import torch
 
     lib = _lib.load()
-    ctx = _lib.context(policy.device, policy.complex_mult)
+    ctx = _lib.context(policy.device, policy.complex_mult, policy.engine, policy.int8_bits)
     dev = torch.device("cuda", policy.device)
     st = _stream_ptr(dev)
     if kind is KernelKind.HERK:

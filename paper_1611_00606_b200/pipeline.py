@@ -46,18 +46,30 @@ class GpuPolicy:
     "3m" (default; Gauss, 3 real DMMA products per complex product) or "4m"
     (4 real products).  Both agree with the reference to ~1e-15 relative
     Frobenius; the ledger charges the reference's model flops either way.
+
+    ``engine`` runs the S and H contractions on the FP64 DMMA tensor cores
+    ("dmma", default) or emulates them on the INT8 tensor cores ("int8":
+    Chinese-remainder / Ozaki-II scheme, operands rounded to ``int8_bits``
+    bits per column, ~1e-12 relative Frobenius at the default 40; see
+    csrc/ozaki.cuh).
     """
 
     device: int = 0
     fused: bool = True
     pinned_outputs: bool = True
     complex_mult: str = "3m"
+    engine: str = "dmma"
+    int8_bits: int = 0
 
     def __post_init__(self):
         if int(self.device) != self.device or self.device < 0:
             raise InputError(f"device must be a nonnegative integer, got {self.device!r}")
         if self.complex_mult not in ("3m", "4m"):
             raise InputError(f"complex_mult must be '3m' or '4m', got {self.complex_mult!r}")
+        if self.engine not in ("dmma", "int8"):
+            raise InputError(f"engine must be 'dmma' or 'int8', got {self.engine!r}")
+        if self.int8_bits != 0 and not 30 <= int(self.int8_bits) <= 48:
+            raise InputError(f"int8_bits must be 0 (default) or in [30, 48], got {self.int8_bits!r}")
 
 
 @dataclass
@@ -178,7 +190,7 @@ def _host_problem(p):
 
 def _call_build(pol, prob, out, stream, force_nonhpd, n_a):
     lib = _lib.load()
-    ctx = _lib.context(pol.device, pol.complex_mult)
+    ctx = _lib.context(pol.device, pol.complex_mult, pol.engine, pol.int8_bits)
     opts = (_lib.HSB_OPT_FORCE_NONHPD if force_nonhpd else 0) | (0 if pol.fused else _lib.HSB_OPT_UNFUSED)
     tim = _lib.HsbTimings()
     info = (ctypes.c_int32 * n_a)()

@@ -17,12 +17,17 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-10
 
 
-@pytest.mark.parametrize("cm", ["3m", "4m"])
+def _pol(cm, **kw):
+    """complex-product form "3m" / "4m" on DMMA, or the INT8 CRT engine"""
+    return GpuPolicy(engine="int8", **kw) if cm == "int8" else GpuPolicy(complex_mult=cm, **kw)
+
+
+@pytest.mark.parametrize("cm", ["3m", "4m", "int8"])
 @pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("name", golden_cases())
 def test_build_matches_reference_golden(name, fused, cm):
     p, fx, meta = load_case(name)
-    out = build_hs(p, GpuPolicy(fused=fused, complex_mult=cm), force_nonhpd=meta["force_nonhpd"])
+    out = build_hs(p, _pol(cm, fused=fused), force_nonhpd=meta["force_nonhpd"])
     assert [out.split.hpd, out.split.nonhpd] == fx["split"].tolist()
     assert rel_frob_error(out.h.matrix, fx["h"]) < TOL
     assert rel_frob_error(out.s.matrix, fx["s"]) < TOL
@@ -58,10 +63,10 @@ def test_scalar_closed_form():
 
 @pytest.mark.parametrize("dims,frac", [((1, 2, 4), 0.0), ((6, 12, 48), 0.5), ((3, 81, 200), 1.0),
                                        ((2, 130, 70), 0.5), ((9, 16, 1), 0.0)])
-@pytest.mark.parametrize("cm", ["3m", "4m"])
+@pytest.mark.parametrize("cm", ["3m", "4m", "int8"])
 def test_build_sweep_against_brute_oracle(dims, frac, cm):
     p = generate(ProblemSpec(Dims(*dims), seed=sum(dims), nonhpd_fraction=frac))
-    out = build_hs(p, GpuPolicy(complex_mult=cm))
+    out = build_hs(p, _pol(cm))
     assert rel_frob_error(out.h.matrix, brute.h_brute(p)) < TOL
     assert rel_frob_error(out.s.matrix, brute.s_brute(p)) < TOL
     assert out.split.hpd + out.split.nonhpd == dims[0]

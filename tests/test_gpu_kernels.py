@@ -13,6 +13,11 @@ from paper_1611_00606_b200 import (DimensionError, GpuPolicy, InputError, Kernel
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-12
+TOL_INT8 = 1e-10  # north star bound; the INT8 engine's operand rounding gives ~1e-12
+
+
+def _tol(pol):
+    return TOL_INT8 if pol.engine == "int8" else TOL
 
 
 @pytest.fixture(scope="module")
@@ -25,8 +30,10 @@ def _cm(rng, r, c):
     return np.asfortranarray(rng.standard_normal((r, c)) + 1j * rng.standard_normal((r, c)))
 
 
-@pytest.fixture(params=["3m", "4m"])
+@pytest.fixture(params=["3m", "4m", "int8"])
 def pol(request):
+    if request.param == "int8":  # INT8 tensor-core CRT emulation of the triangle updates
+        return GpuPolicy(engine="int8")
     return GpuPolicy(complex_mult=request.param)
 
 
@@ -36,7 +43,7 @@ def test_herk_matches_reference_kernel(g, pol):
         alpha, beta = (float(x) for x in g[f"herk{i}_ab"])
         c = g[f"herk{i}_c"].copy(order="F")
         res = run_partitioned(KernelKind.HERK, (alpha, g[f"herk{i}_a"], beta, c), pol)
-        assert rel_frob_error(c, g[f"herk{i}_out"]) < TOL, i
+        assert rel_frob_error(c, g[f"herk{i}_out"]) < _tol(pol), i
         assert res.seconds >= 0 and res.n_tiles >= 1
         i += 1
 
@@ -47,7 +54,7 @@ def test_her2k_matches_reference_kernel(g, pol):
         alpha, beta = g[f"her2k{i}_ab"]
         c = g[f"her2k{i}_c"].copy(order="F")
         run_partitioned(KernelKind.HER2K, (complex(alpha), g[f"her2k{i}_z"], g[f"her2k{i}_b"], beta.real, c), pol)
-        assert rel_frob_error(c, g[f"her2k{i}_out"]) < TOL, i
+        assert rel_frob_error(c, g[f"her2k{i}_out"]) < _tol(pol), i
         assert np.all(np.diagonal(c).imag == 0)
         i += 1
 
@@ -60,7 +67,7 @@ def test_gemm_all_ops_match_reference_kernel(g, pol):
         c = g[f"gemm{i}_c"].copy(order="F")
         run_partitioned(KernelKind.GEMM, (complex(alpha), opa, g[f"gemm{i}_a"], opb, g[f"gemm{i}_b"],
                                           complex(beta), c), pol)
-        assert rel_frob_error(c, g[f"gemm{i}_out"]) < TOL, (i, opa, opb)
+        assert rel_frob_error(c, g[f"gemm{i}_out"]) < _tol(pol), (i, opa, opb)
         i += 1
 
 
@@ -71,7 +78,7 @@ def test_herk_against_oracle_sizes(k, n, pol):
     c = _cm(rng, n, n)
     want = ok.herk(1.0, a, 0.5, c)
     run_partitioned(KernelKind.HERK, (1.0, a, 0.5, c), pol)
-    assert rel_frob_error(c, want) < TOL
+    assert rel_frob_error(c, want) < _tol(pol)
 
 
 @pytest.mark.parametrize("k,n", [(5, 33), (242, 190), (1000, 513)])
@@ -81,7 +88,7 @@ def test_her2k_against_oracle_sizes(k, n, pol):
     c = _cm(rng, n, n)
     want = ok.her2k(1.0, z, b, 0.0, c)
     run_partitioned(KernelKind.HER2K, (1.0, z, b, 0.0, c), pol)
-    assert rel_frob_error(c, want) < TOL
+    assert rel_frob_error(c, want) < _tol(pol)
 
 
 def test_zero_alpha_and_empty_reduction_follow_blas():
