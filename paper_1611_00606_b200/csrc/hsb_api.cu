@@ -312,9 +312,19 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
   CKS(ws(ctx, "oz_exp", static_cast<size_t>(n) * sizeof(int32_t), &ebuf));
   int32_t* e = static_cast<int32_t*>(ebuf);
   CK(launch_ozaki_init_exp(e, n, st));
-  for (const Seg& s : segs) {
-    CK(launch_ozaki_colexp(s.l.base, s.l.ld, s.l.k, s.l.cols, e, st));
-    CK(launch_ozaki_colexp(s.r.base, s.r.ld, s.r.k, s.r.cols, e, st));
+  {
+    std::vector<const OperandView*> seen;
+    auto colexp = [&](const OperandView& v) -> hsb_status {
+      for (const OperandView* q : seen)
+        if (q->base == v.base && q->k == v.k && q->ld == v.ld) return HSB_OK;
+      seen.push_back(&v);
+      CK(launch_ozaki_colexp(v.base, v.ld, v.k, v.cols, e, st));
+      return HSB_OK;
+    };
+    for (const Seg& s : segs) {
+      CKS(colexp(s.l));
+      CKS(colexp(s.r));
+    }
   }
   // residue planes of each distinct operand
   struct Src {

@@ -3,6 +3,7 @@
 // kind::i8 modular GEMM over lower-triangle tiles, and the CRT
 // reconstruction with the 3M combination and the Hermitian mirror.
 #include <climits>
+#include <cstring>
 
 #include "ozaki.cuh"
 #include "ptx.cuh"
@@ -10,22 +11,21 @@
 
 namespace hsb {
 
-__constant__ int32_t c_oz_inv[kOzMaxMod][kOzMaxMod];  // [j][i] = p_j^-1 mod p_i (j < i)
 __constant__ int32_t oz_mod_rt[kOzMaxMod] = {256, 255, 253, 251, 247, 241, 239, 233,
                                              229, 227, 223, 217, 211, 199, 197, 193};
 
 // ------------------------------------------------------------ small helpers
 __device__ __forceinline__ int sym_lo(int p) { return -(p >> 1); }
 
-// symmetric residue of an exactly-integer double |v| < 2^52
-__device__ __forceinline__ int sym_mod_d(double v, double p, double inv_p, int ip) {
-  const double q = rint(v * inv_p);
-  int r = static_cast<int>(fma(-p, q, v));  // exact: v - p*q is an integer below 2^53
-  const int lo = sym_lo(ip);
-  if (r < lo) r += ip;
-  if (r > lo + ip - 1) r -= ip;
-  if (r < lo) r += ip;
-  return r;
+// symmetric residue of an exactly-integer double |v| < 2^46: r = v - p*floor(v/p + 1/2)
+// lies in [-p/2, p/2) ([-(p-1)/2, (p-1)/2] for odd p) with no correction:
+// for p = 2^8 the quotient is exact; for odd p, v/p is never within
+// 1/(2p) = 2^-9 of a half-integer while the product's error is ~2^-15.
+// The integer is read from the mantissa (magic 1.5 * 2^52) instead of F2I.
+__device__ __forceinline__ int sym_mod_d(double v, double p, double inv_p) {
+  const double q = floor(fma(v, inv_p, 0.5));
+  const double r = fma(-p, q, v) + 6755399441055744.0;
+  return static_cast<int>(__double2loint(r));
 }
 __device__ __forceinline__ int sym_adj(int r, int p) {
   const int lo = sym_lo(p);
@@ -93,8 +93,8 @@ __global__ void ozaki_residue_kernel(const double2* __restrict__ x, int64_t ldx,
       int rr[4], ri[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        rr[j] = sym_mod_d(xr[j], p, inv, ip);
-        ri[j] = sym_mod_d(xi[j], p, inv, ip);
+        rr[j] = sym_mod_d(xr[j], p, inv);
+        ri[j] = sym_mod_d(xi[j], p, inv);
       }
       re = make_char4(rr[0], rr[1], rr[2], rr[3]);
       im = make_char4(ri[0], ri[1], ri[2], ri[3]);
@@ -278,7 +278,6 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const __grid_
       oz_work(p, w, prod, mod, tm, tn);
       const int ip = oz_mod_rt[mod];
       const double pd = ip, inv = 1.0 / pd;
-      const int lo = sym_lo(ip);
       mbar_wait(tfull(acc), acc_phase);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int row = tm * kOzBM + q * 32 + lane;
@@ -294,10 +293,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const __grid_
           for (int j = 0; j < 32; ++j) {
             const int col = col0 + c * 32 + j;
             if (col < p.n) {
-              const double a = static_cast<double>(static_cast<int32_t>(v[j]));
-              int r = static_cast<int>(fma(-pd, rint(a * inv), a));
-              if (r < lo) r += ip;
-              if (r > lo + ip - 1) r -= ip;
+              const int r = sym_mod_d(static_cast<double>(static_cast<int32_t>(v[j])), pd, inv);
               out[static_cast<int64_t>(col) * p.ldr] = static_cast<int8_t>(r);
             }
           }
@@ -321,23 +317,37 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const __grid_
 }
 
 // ------------------------------------------------------------ 4. CRT
-// Garner's mixed radix with symmetric digits: X = v0 + p0 (v1 + p1 (v2 + ...)),
-// every digit |v_i| <= p_i / 2, so the double Horner sum has no cancellation.
+// Explicit CRT in exact double limbs.  With M = prod p_i, y_i = (M/p_i) *
+// ((M/p_i)^-1 mod p_i) and any representatives r_i (|r_i| <= 384):
+//     X = sum_i r_i y_i - k M,   k = rint(sum_i r_i (y_i / M)),
+// exact for |X| < M/4 (the host's choice of b leaves >= 4 bits of margin).
+// y_i and M are split into 4 limbs of 32 bits; every limb sum
+// S_j = sum_i r_i y_ij (< 2^45) and T_j = S_j - k M_j is an exact double, so
+// X = ((T3 2^32 + T2) 2^32 + T1) 2^32 + T0 is rounded once, at the end.
+struct OzCrtConst {
+  double y[kOzMaxMod][4];   // limbs of y_i, least significant first
+  double f[kOzMaxMod];      // y_i / M
+  double m[4];              // limbs of M
+};
+__constant__ OzCrtConst c_oz_crt;
+
 template <int NM>
-__device__ __forceinline__ double garner(const int (&r)[NM]) {
-  int v[NM];
+__device__ __forceinline__ double crt_value(const int (&r)[NM]) {
+  double fk = 0.0, s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
-    const int pi = oz_mod(i);
-    int t = r[i];
-#pragma unroll
-    for (int j = 0; j < i; ++j) t = ((t - v[j]) * c_oz_inv[j][i]) % pi;
-    v[i] = sym_adj(t, pi);
+    const double ri = static_cast<double>(r[i]);
+    fk = fma(ri, c_oz_crt.f[i], fk);
+    s0 = fma(ri, c_oz_crt.y[i][0], s0);
+    s1 = fma(ri, c_oz_crt.y[i][1], s1);
+    s2 = fma(ri, c_oz_crt.y[i][2], s2);
+    s3 = fma(ri, c_oz_crt.y[i][3], s3);
   }
-  double x = v[NM - 1];
-#pragma unroll
-  for (int i = NM - 2; i >= 0; --i) x = fma(x, static_cast<double>(oz_mod(i)), static_cast<double>(v[i]));
-  return x;
+  const double k = rint(fk);
+  const double t0 = fma(-k, c_oz_crt.m[0], s0), t1 = fma(-k, c_oz_crt.m[1], s1);
+  const double t2 = fma(-k, c_oz_crt.m[2], s2), t3 = fma(-k, c_oz_crt.m[3], s3);
+  constexpr double kL = 4294967296.0;  // 2^32
+  return fma(fma(fma(t3, kL, t2), kL, t1), kL, t0);
 }
 
 template <int NM>
@@ -349,17 +359,16 @@ __global__ void ozaki_crt_kernel(const OzCrtParams p) {
   int re[NM], im[NM];
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
-    const int pi = oz_mod(i);
     const int P = r0[i * p.mod_stride];
     const int Q = r0[p.prod_stride + i * p.mod_stride];
     const int W = r0[2 * p.prod_stride + i * p.mod_stride];
     // L^H R: Re = P + Q, Im = W - P + Q ;  L^T R: Re = P - Q, Im = W - P - Q
-    re[i] = sym_adj(p.conj ? P + Q : P - Q, pi);
-    im[i] = sym_adj(sym_adj(p.conj ? W - P + Q : W - P - Q, pi), pi);
+    re[i] = p.conj ? P + Q : P - Q;
+    im[i] = p.conj ? W - P + Q : W - P - Q;
   }
   const int sh = p.el[m] + p.er[n] - 2 * p.b;
-  const double xr = ldexp(garner<NM>(re), sh);
-  const double xi = ldexp(garner<NM>(im), sh);
+  const double xr = ldexp(crt_value<NM>(re), sh);
+  const double xi = ldexp(crt_value<NM>(im), sh);
   double vr = p.alpha_re * xr - p.alpha_im * xi;
   double vi = p.alpha_re * xi + p.alpha_im * xr;
   double2* C = reinterpret_cast<double2*>(p.c);
@@ -373,6 +382,41 @@ __global__ void ozaki_crt_kernel(const OzCrtParams p) {
   if (m == n && (mirror || (p.flags & kZeroImagDiag))) vi = 0.0;
   *dst = make_double2(vr, vi);
   if (mirror && m > n) C[n + static_cast<int64_t>(m) * p.ldc] = make_double2(vr, -vi);
+}
+
+static cudaError_t oz_crt_constants(int n_mod) {
+  static int done_for = 0;
+  if (done_for == n_mod) return cudaSuccess;
+  using u128 = unsigned __int128;
+  u128 M = 1;
+  for (int i = 0; i < n_mod; ++i) M *= static_cast<u128>(oz_mod(i));
+  OzCrtConst c;
+  std::memset(&c, 0, sizeof(c));
+  auto limbs = [](u128 v, double* out) {
+    for (int j = 0; j < 4; ++j) {
+      out[j] = static_cast<double>(static_cast<uint32_t>(v & 0xffffffffu));
+      v >>= 32;
+    }
+  };
+  const double Md = static_cast<double>(M);
+  for (int i = 0; i < n_mod; ++i) {
+    const int pi = oz_mod(i);
+    const u128 Mi = M / static_cast<u128>(pi);
+    const int mi_mod = static_cast<int>(Mi % static_cast<u128>(pi));
+    int inv = 0;
+    for (int x = 1; x < pi; ++x)
+      if ((mi_mod * x) % pi == 1) {
+        inv = x;
+        break;
+      }
+    const u128 y = Mi * static_cast<u128>(inv);  // < M
+    limbs(y, c.y[i]);
+    c.f[i] = static_cast<double>(y) / Md;
+  }
+  limbs(M, c.m);
+  cudaError_t e = cudaMemcpyToSymbol(c_oz_crt, &c, sizeof(c));
+  if (e == cudaSuccess) done_for = n_mod;
+  return e;
 }
 
 // ------------------------------------------------------------ launchers
@@ -412,19 +456,6 @@ cudaError_t launch_ozaki_gemm(const OzGemmParams& p, cudaStream_t st) {
     cudaGetDevice(&dev);
     e = cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
-    // p_j^-1 mod p_i for Garner
-    int inv[kOzMaxMod][kOzMaxMod] = {};
-    for (int i = 0; i < kOzMaxMod; ++i)
-      for (int j = 0; j < i; ++j) {
-        const int pi = oz_mod(i), pj = oz_mod(j) % pi;
-        for (int x = 1; x < pi; ++x)
-          if ((pj * x) % pi == 1) {
-            inv[j][i] = x;
-            break;
-          }
-      }
-    e = cudaMemcpyToSymbol(c_oz_inv, inv, sizeof(inv));
-    if (e != cudaSuccess) return e;
     attr = true;
   }
   const int64_t nwork = 3LL * p.n_mod * p.ntiles;
@@ -437,6 +468,8 @@ cudaError_t launch_ozaki_gemm(const OzGemmParams& p, cudaStream_t st) {
 
 cudaError_t launch_ozaki_crt(const OzCrtParams& p, cudaStream_t st) {
   if (p.n <= 0) return cudaSuccess;
+  cudaError_t ce = oz_crt_constants(p.n_mod);
+  if (ce != cudaSuccess) return ce;
   dim3 grid(static_cast<unsigned>((p.n + 127) / 128), static_cast<unsigned>(p.n));
   if (p.n > 65535) return cudaErrorInvalidConfiguration;
   switch (p.n_mod) {
