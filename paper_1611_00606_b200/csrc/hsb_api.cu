@@ -257,17 +257,17 @@ hsb_status oz_encode(hsb_ctx* ctx, CUtensorMap* map, const int8_t* planes, int64
   return HSB_OK;
 }
 
-// 128 x 256 tiles (tile row tm, tile col tn) that touch the lower triangle
-// (tm >= 2 tn), in groups of 8 tile rows x 4 tile cols for L2 reuse
+// 256 x 256 tiles (tile row tm >= tile col tn) of the lower triangle, in
+// groups of 6 x 6 tiles for L2 reuse
 hsb_status oz_tiles(hsb_ctx* ctx, int64_t n, cudaStream_t st, const int2** out, int* count) {
-  const int64_t tm_n = (n + kOzBM - 1) / kOzBM, tn_n = (n + kOzBN - 1) / kOzBN;
+  const int64_t T = (n + kOzBN - 1) / kOzBN;
   std::vector<int2>& v = ctx->oz_tiles_host;
   if (ctx->oz_tiles_n != n) {
     v.clear();
-    for (int64_t j0 = 0; j0 < tn_n; j0 += 4)
-      for (int64_t i0 = 2 * j0; i0 < tm_n; i0 += 8)
-        for (int64_t j = j0; j < std::min<int64_t>(j0 + 4, tn_n); ++j)
-          for (int64_t i = std::max(i0, 2 * j); i < std::min<int64_t>(i0 + 8, tm_n); ++i)
+    for (int64_t j0 = 0; j0 < T; j0 += 6)
+      for (int64_t i0 = j0; i0 < T; i0 += 6)
+        for (int64_t j = j0; j < std::min<int64_t>(j0 + 6, T); ++j)
+          for (int64_t i = std::max(i0, j); i < std::min<int64_t>(i0 + 6, T); ++i)
             v.push_back(make_int2(static_cast<int>(i), static_cast<int>(j)));
   }
   void* buf;
@@ -361,8 +361,8 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
     CKS(planes_of(segs[si].r, &R));
     const int64_t pl = static_cast<int64_t>(n_mod) * n * L.kpad, pr = static_cast<int64_t>(n_mod) * n * R.kpad;
     for (int pi = 0; pi < 3; ++pi) {
-      CKS(oz_encode(ctx, &gp.map[pi][si][0], L.planes + lp[pi] * pl, L.k, n, L.kpad, n_mod, kOzBM));
-      CKS(oz_encode(ctx, &gp.map[pi][si][1], R.planes + rp[pi] * pr, R.k, n, R.kpad, n_mod, kOzBN));
+      CKS(oz_encode(ctx, &gp.map[pi][si][0], L.planes + lp[pi] * pl, L.k, n, L.kpad, n_mod, 128));
+      CKS(oz_encode(ctx, &gp.map[pi][si][1], R.planes + rp[pi] * pr, R.k, n, R.kpad, n_mod, 128));
     }
     gp.kchunks[si] = static_cast<int32_t>((segs[si].l.k + kOzBK - 1) / kOzBK);
   }

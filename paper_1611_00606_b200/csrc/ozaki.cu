@@ -112,18 +112,27 @@ __global__ void ozaki_residue_kernel(const double2* __restrict__ x, int64_t ldx,
 }
 
 // ------------------------------------------------------------ 3. INT8 GEMM
-constexpr int kOzStages = 4;
-constexpr int kOzABytes = kOzBM * kOzBK, kOzBBytes = kOzBN * kOzBK;
-constexpr int kOzStageBytes = kOzABytes + kOzBBytes;  // 48 KB
+// CTA pairs (cluster of 2, tcgen05 cta_group::2): the pair owns a 256 x 256
+// output tile; CTA r holds rows 128 r .. 128 r + 127 of the A tile and of the
+// B tile in its own shared memory, the leader (rank 0) issues one
+// M = 256, N = 256, K = 32 MMA per 32-byte k step and each CTA's TMEM receives
+// its 128 rows x 256 int32 columns.  Per SM and 128-byte k chunk that is
+// 32 KB of TMA traffic for 4M MACs (half of a 1-CTA 128 x 256 tile's), so six
+// 32 KB stages fit in shared memory.
+constexpr int kOzStages = 6;
+constexpr int kOzHalf = 128;                      // rows of A and of B per CTA
+constexpr int kOzABytes = kOzHalf * kOzBK;        // 16 KB
+constexpr int kOzStageBytes = 2 * kOzABytes;      // 32 KB
 constexpr int kOzSmem = kOzStages * kOzStageBytes + 1024 + 256;
-constexpr int kOzThreads = 192;  // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 epilogue
+constexpr int kOzThreads = 192;  // warp 0 TMA, warp 1 MMA (leader) + TMEM owner, warps 2-5 epilogue
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;       // shared::cluster address of the leader's copy
 
-__device__ __forceinline__ void tma_load_3d_u8(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
-                                               uint32_t bar) {
+__device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                 uint32_t leader_bar) {
   asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(leader_bar)
       : "memory");
 }
 // K-major operand tile, 128B swizzle: 8-row atoms of 1024 B (SBO); LBO unused
@@ -135,18 +144,34 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
 constexpr uint32_t kOzIdesc = (2u << 4)                // D: s32
                               | (1u << 7)              // A: signed int8
                               | (1u << 10)             // B: signed int8
-                              | ((kOzBN >> 3) << 17)   // N
-                              | ((kOzBM >> 4) << 24);  // M
-__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+                              | ((kOzBN >> 3) << 17)   // N = 256
+                              | ((256 >> 4) << 24);    // M = 256 (pair)
+__device__ __forceinline__ void mma_i8_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(kOzIdesc), "r"(acc), "r"(0), "r"(0), "r"(0), "r"(0));
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8, %9, %10, %11, %12}, p;\n\t}\n" ::"r"(
+          tmem_d),
+      "l"(da), "l"(db), "r"(kOzIdesc), "r"(acc), "r"(0), "r"(0), "r"(0), "r"(0), "r"(0), "r"(0), "r"(0), "r"(0));
 }
-__device__ __forceinline__ void mma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-               : "memory");
+// arrive on the barrier at this offset in both CTAs of the pair
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          bar),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
@@ -171,7 +196,8 @@ __device__ __forceinline__ void oz_work(const OzGemmParams& p, int w, int& prod,
   tn = t.y;
 }
 
-__global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const __grid_constant__ OzGemmParams p) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
+    ozaki_gemm_kernel(const __grid_constant__ OzGemmParams p) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -184,45 +210,51 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const __grid_
   const uint32_t* tmem_slot_ptr = reinterpret_cast<const uint32_t*>(smem_raw + (tmem_slot - raw));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const int nwork = 3 * p.n_mod * p.ntiles;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kOzStages; ++s) {
-      mbar_init(full(s), 1);
-      mbar_init(empty(s), 1);
+      mbar_init(full(s), 1);   // leader: its expect_tx covers both CTAs' bytes
+      mbar_init(empty(s), 1);  // one multicast MMA commit per use
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(tfull(s), 1);
-      mbar_init(tempty(s), 4);
+      mbar_init(tempty(s), 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot), "r"(512));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  cluster_sync();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot_ptr;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 1;
-      for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+      for (int w = pair; w < nwork; w += npairs) {
         int prod, mod, tm, tn;
         oz_work(p, w, prod, mod, tm, tn);
+        const int row0 = tm * 256 + static_cast<int>(rank) * kOzHalf;
+        const int col0 = tn * 256 + static_cast<int>(rank) * kOzHalf;
         for (int s = 0; s < p.nseg; ++s) {
           const CUtensorMap* ml = &p.map[prod][s][0];
           const CUtensorMap* mr = &p.map[prod][s][1];
           for (int kc = 0; kc < p.kchunks[s]; ++kc) {
             mbar_wait(empty(stage), phase);
-            mbar_expect_tx(full(stage), kOzStageBytes);
+            if (leader) mbar_expect_tx(full(stage), 2 * kOzStageBytes);
             const uint32_t dst = base + stage * kOzStageBytes;
-            tma_load_3d_u8(dst, ml, kc * kOzBK, tm * kOzBM, mod, full(stage));
-            tma_load_3d_u8(dst + kOzABytes, mr, kc * kOzBK, tn * kOzBN, mod, full(stage));
+            const uint32_t fb = full(stage) & kPeerMask;
+            tma_load_3d_pair(dst, ml, kc * kOzBK, row0, mod, fb);
+            tma_load_3d_pair(dst + kOzABytes, mr, kc * kOzBK, col0, mod, fb);
             if (++stage == kOzStages) {
               stage = 0;
               phase ^= 1u;
@@ -232,13 +264,13 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const __grid_
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // ------------------------------------------------------------ MMA issuer (leader only)
+    if (leader && lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 1;
-      for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+      for (int w = pair; w < nwork; w += npairs) {
         mbar_wait(tempty(acc), acc_phase);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + acc * kOzBN;
@@ -250,17 +282,17 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const __grid_
             const uint32_t a0 = base + stage * kOzStageBytes, b0 = a0 + kOzABytes;
 #pragma unroll
             for (int kk = 0; kk < kOzBK / 32; ++kk) {
-              mma_i8(d, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), first ? 0u : 1u);
+              mma_i8_pair(d, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), first ? 0u : 1u);
               first = false;
             }
-            mma_commit(empty(stage));
+            mma_commit_pair(empty(stage));
             if (++stage == kOzStages) {
               stage = 0;
               phase ^= 1u;
             }
           }
         }
-        mma_commit(tfull(acc));
+        mma_commit_pair(tfull(acc));
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1u;
@@ -268,21 +300,21 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const __grid_
       }
     }
   } else {
-    // ------------------------------------------------------------ epilogue
-    // warp w owns TMEM lanes 32*(w%4) .. +31 = tile rows; residue mod p, int8
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    // warp w owns TMEM lanes 32*(w%4) .. +31 = rows of this CTA's half; residue mod p, int8
     const int q = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+    for (int w = pair; w < nwork; w += npairs) {
       int prod, mod, tm, tn;
       oz_work(p, w, prod, mod, tm, tn);
       const int ip = oz_mod_rt[mod];
       const double pd = ip, inv = 1.0 / pd;
       mbar_wait(tfull(acc), acc_phase);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int row = tm * kOzBM + q * 32 + lane;
+      const int row = tm * 256 + static_cast<int>(rank) * kOzHalf + q * 32 + lane;
       int8_t* out = p.res + prod * p.prod_stride + mod * p.mod_stride + row;
-      const int col0 = tn * kOzBN;
+      const int col0 = tn * 256;
       const int ncol = min(kOzBN, p.n - col0);
       for (int c = 0; c < kOzBN / 32; ++c) {
         if (c * 32 >= ncol) break;  // warp-uniform
@@ -301,7 +333,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const __grid_
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty(acc));
+      if (lane == 0) mbar_arrive_cluster(tempty(acc) & kPeerMask);
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1u;
@@ -309,10 +341,10 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const __grid_
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  cluster_sync();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
 }
 
@@ -461,7 +493,8 @@ cudaError_t launch_ozaki_gemm(const OzGemmParams& p, cudaStream_t st) {
   const int64_t nwork = 3LL * p.n_mod * p.ntiles;
   if (nwork <= 0) return cudaSuccess;
   if (nwork > 0x7fffffff) return cudaErrorInvalidConfiguration;
-  const int grid = static_cast<int>(nwork < n_sm ? nwork : n_sm);
+  const int pairs = static_cast<int>(nwork < n_sm / 2 ? nwork : n_sm / 2);
+  const int grid = 2 * pairs;
   ozaki_gemm_kernel<<<grid, kOzThreads, kOzSmem, st>>>(p);
   return cudaGetLastError();
 }

@@ -33,7 +33,7 @@ namespace hsb {
 
 constexpr int kOzMaxMod = 16;
 constexpr int kOzMaxSeg = 4;
-constexpr int kOzBM = 128;   // output tile rows   (TMEM lanes)
+constexpr int kOzBM = 256;   // output tile rows   (CTA pair: 128 TMEM lanes each)
 constexpr int kOzBN = 256;   // output tile cols   (TMEM columns per accumulator)
 constexpr int kOzBK = 128;   // k bytes per stage  (128B swizzle row)
 // pairwise coprime, descending; the first n_mod are used
@@ -50,14 +50,14 @@ __host__ __device__ constexpr int oz_mod(int i) {
 enum OzPlane { kOzRe = 0, kOzIm = 1, kOzMinus = 2, kOzPlus = 3 };
 
 struct OzGemmParams {
-  // maps[prod][seg][side]: 3-D int8 maps {k, cols, modulus}, box {128, 128|256, 1}
+  // maps[prod][seg][side]: 3-D int8 maps {k, cols, modulus}, box {128, 128, 1}
   CUtensorMap map[3][kOzMaxSeg][2];
   int32_t kchunks[kOzMaxSeg];
   int32_t nseg;
   int32_t n_mod;
   int32_t n;            // output is n x n (triangle)
   int32_t ntiles;       // entries of tile_list
-  const int2* tile_list;  // (tile row, tile col) of the 128 x 256 tiles with rows >= cols
+  const int2* tile_list;  // (tile row, tile col) of the 256 x 256 tiles on or below the diagonal
   int8_t* res;          // residues [prod][modulus][col][ldr]
   int64_t ldr;          // rows stride (bytes), multiple of 16
   int64_t mod_stride;   // bytes between moduli (ldr * n)
