@@ -50,6 +50,13 @@ CONFIG_DESC = {
 NOMINAL_FP64_TFLOPS = 37.2  # 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz
 
 
+def measured_peaks() -> dict:
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except (OSError, ValueError):
+        return {}
+
+
 def fp64_peak():
     """Measured FP64 DMMA peak (probes/fp64_peak.cu, committed result)."""
     path = ROOT / "profiles" / "fp64_peak_r01.jsonl"
@@ -181,6 +188,9 @@ def main():
     ap.add_argument("--unfused", action="store_true", help="one launch per reference section")
     ap.add_argument("--complex-mult", default="3m", choices=["3m", "4m"],
                     help="real-product form of the complex contractions (3 or 4 DMMA products)")
+    ap.add_argument("--engine", default="int8", choices=["int8", "dmma"],
+                    help="S/H contractions on the INT8 tensor cores (CRT emulation, ~1e-12) or FP64 DMMA")
+    ap.add_argument("--no-compare", action="store_true", help="skip the second-engine measurement")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-ng", type=int, default=4000)
@@ -217,7 +227,7 @@ def main():
     lo, hi = shard(dims.n_atoms, rank, world)
     local = Dims(hi - lo, dims.n_l, dims.n_g)
     p = generate(ProblemSpec(local, seed=args.seed * 1000 + rank, nonhpd_fraction=args.nonhpd_fraction))
-    policy = GpuPolicy(device=dev_index, fused=not args.unfused, complex_mult=args.complex_mult)
+    policy = GpuPolicy(device=dev_index, fused=not args.unfused, complex_mult=args.complex_mult, engine=args.engine)
     n_g = dims.n_g
     ncols = -(-n_g // world) * world
     flops_full = total_model_flops(dims, round(args.nonhpd_fraction * dims.n_atoms) if world == 1 else 0)
@@ -231,8 +241,8 @@ def main():
         sb = torch.empty_like(hb)
     stream = torch.cuda.current_stream(dev)
 
-    def step():
-        _, _, split, t, _ = build_hs_device(dp, h, s, policy)
+    def step(pol=policy):
+        _, _, split, t, _ = build_hs_device(dp, h, s, pol)
         if world > 1:
             hsdist.reduce_scatter_block_columns(h, hb)
             hsdist.reduce_scatter_block_columns(s, sb)
@@ -256,26 +266,77 @@ def main():
     ms = hsdist.max_over_ranks(ms, dev)
     value = flops_full / (ms * 1e-3) / 1e12
 
-    # dominant kernel: the fused H contraction (H1 + H2 + H3 sections)
-    peak, peak_src = fp64_peak()
+    # dominant kernel: the fused H contraction (H1 + H2 + H3 sections), timed
+    # alone by CUDA events on the launching stream (timings["h_core"])
     n_nh_local = int(ts[-1]["n_nonhpd"])
     sect = section_flops(local, n_nh_local)
     h_flops = sect["H1"] + sect["H2"] + sect["H3"]
     h_sec = statistics.mean(t["h1"] + t["h2"] + t["h3"] for t in ts)
     s_sec = statistics.mean(t["s1"] + t["s2"] for t in ts)
-    # algorithmic flops of the form that runs: 3M spends 3 real MACs per complex
-    # MAC (6 flops) where the reference's model charges 8 (kernels.py:66-85)
-    alg_factor = 0.75 if args.complex_mult == "3m" else 1.0
-    achieved = h_flops * alg_factor / h_sec / 1e12
+    h_core = statistics.mean(t["h_core"] for t in ts)
+    k_l = local.n_atoms * local.n_l
+    k_tot_h = 2 * k_l + k_l  # Z^H B + B^H Z + [Y; X_nh]-segment(s): N_A N_L rows in total
+    if args.engine == "int8":
+        from paper_1611_00606_b200 import int8_gemm_ops, int8_moduli
+
+        n_mod, bits = int8_moduli(k_tot_h)
+        alg = int8_gemm_ops(n_g, k_tot_h)
+        peak_tops = 2.0 * measured_peaks().get("bf16_tflops_sustained", 1394.7)
+        roof = {"bound": "tensor",
+                "kernel": "ozaki_gemm_kernel (tcgen05.mma.cta_group::2.kind::i8, TMA, TMEM) of the fused H "
+                          "= Z^H B + B^H Z + Y^H Y, INT8 CRT emulation",
+                "achieved": alg / h_core / 1e12, "peak": peak_tops, "unit": "TOPS (int8)",
+                "frac": alg / h_core / 1e12 / peak_tops,
+                "peak_source": "2 x bf16_tflops_sustained of MEASURED_PEAKS.json (B200 dense INT8 = 2x dense BF16; "
+                               "no INT8 entry is measured)",
+                "algorithmic_ops_per_launch": alg,
+                "op_form": f"3 real products x {n_mod} moduli x K_tot {k_tot_h} x N(N+1)/2, 2 ops per MAC "
+                           f"(operands rounded to {bits} bits)",
+                "model_flops_per_launch": h_flops, "model_tflops": h_flops / h_core / 1e12,
+                "avg_launch_ms": h_core * 1e3}
+    else:
+        peak, peak_src = fp64_peak()
+        # algorithmic flops of the form that runs: 3M spends 3 real MACs per complex
+        # MAC (6 flops) where the reference's model charges 8 (kernels.py:66-85)
+        alg_factor = 0.75 if args.complex_mult == "3m" else 1.0
+        achieved = h_flops * alg_factor / h_core / 1e12
+        roof = {"bound": "tensor",
+                "kernel": ("zrk3m_kernel<conj,planes>" if args.complex_mult == "3m" else "zrk_kernel<conj>")
+                + " fused H = Z^H B + B^H Z + Y^H Y",
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "peak_source": peak_src,
+                "algorithmic_flops_per_launch": h_flops * alg_factor,
+                "flop_form": ("3M: 6 real flops per complex MAC = 3/4 of the model"
+                              if args.complex_mult == "3m" else "4M: 8 flops per complex MAC = the model"),
+                "model_flops_per_launch": h_flops, "model_tflops": h_flops / h_core / 1e12,
+                "avg_launch_ms": h_core * 1e3}
     launches = sum(int(t["launches"]) for t in ts)
     traffic = None
     prof = ROOT / "profiles" / "roofline_traffic.json"
     if prof.exists():
         try:
-            rec = json.loads(prof.read_text()).get(f"{args.config}/{args.complex_mult}")
+            key = f"{args.config}/int8" if args.engine == "int8" else f"{args.config}/{args.complex_mult}"
+            rec = json.loads(prof.read_text()).get(key)
             traffic = rec["bytes"] if rec else None
         except ValueError:
             traffic = None
+
+    # ---------------------------------------------- the other engine, same run
+    other = None
+    if not args.no_compare:
+        alt = "dmma" if args.engine == "int8" else "int8"
+        pol2 = GpuPolicy(device=dev_index, fused=not args.unfused, complex_mult=args.complex_mult, engine=alt)
+        for _ in range(args.warmup):
+            step(pol2)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step(pol2)
+        e1.record(stream)
+        barrier()
+        ms2 = hsdist.max_over_ranks(e0.elapsed_time(e1) / args.steps, dev)
+        other = {"engine": alt, "ms_per_step": ms2, "value": flops_full / (ms2 * 1e-3) / 1e12, "unit": "TFLOP/s"}
 
     # ------------------------------------------------------------ end to end
     e2e = None
@@ -316,27 +377,21 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic (seeded hsgen-compatible generator)",
+            "vs_baseline": None,
+            "dtype": ("c128 in/out; S/H products as exact int8 residue GEMMs (CRT), f64 reconstruction"
+                      if args.engine == "int8" else "c128 (f64 DMMA)"),
+            "data": "synthetic (seeded hsgen-compatible generator)",
             "config": {"workload": args.config, "desc": CONFIG_DESC[args.config], "n_atoms": dims.n_atoms,
                        "n_l": dims.n_l, "n_g": dims.n_g, "nonhpd_fraction": args.nonhpd_fraction,
                        "parallelism": f"atom-shard x{world}" + (" + reduce-scatter" if world > 1 else ""),
-                       "fused": not args.unfused, "complex_mult": args.complex_mult, "model_tflop_per_step": flops_full / 1e12,
+                       "fused": not args.unfused, "engine": args.engine, "complex_mult": args.complex_mult, "model_tflop_per_step": flops_full / 1e12,
                        "l2_note": "inputs larger than L2 (A/B stacks 496 MB each at C3)"},
             "gpu_launches": launches,
-            "roofline": {"bound": "tensor",
-                         "kernel": ("zrk3m_kernel<conj,planes>" if args.complex_mult == "3m" else "zrk_kernel<conj>")
-                         + " fused H = Z^H B + B^H Z + Y^H Y (incl. its sum-plane pass)",
-                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                         "peak_source": peak_src, "traffic": traffic,
-                         "algorithmic_flops_per_launch": h_flops * alg_factor,
-                         "flop_form": ("3M: 6 real flops per complex MAC = 3/4 of the model"
-                                       if args.complex_mult == "3m" else "4M: 8 flops per complex MAC = the model"),
-                         "model_flops_per_launch": h_flops, "model_tflops": h_flops / h_sec / 1e12,
-                         "avg_launch_ms": h_sec * 1e3,
-                         "s_kernel_tflops": (sect["S1"] + sect["S2"]) / s_sec / 1e12},
+            "roofline": dict(roof, traffic=traffic, h_section_ms=h_sec * 1e3,
+                             s_section_model_tflops=(sect["S1"] + sect["S2"]) / s_sec / 1e12),
             "sections_ms": {k: statistics.mean(t[k] for t in ts) * 1e3
                             for k in ("loop1", "h1", "s1", "unorm", "s2", "loop2", "h2", "h3", "total")},
-            "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
+            "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks, "other_engine": other,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

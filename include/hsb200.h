@@ -183,6 +183,8 @@ typedef struct {
 typedef struct {
   double loop1, loop2, unorm, s1, s2, h1, h2, h3;
   double h2d, d2h, total;   /* transfers (host path only) and end-to-end */
+  double s_core, h_core;    /* the fused S / H contraction kernel alone (DMMA zrk
+                               or INT8 modular GEMM), included in the sections */
   int32_t n_hpd, n_nonhpd;  /* builder.SplitCounts (builder.py:51-54) */
   int32_t launches;         /* kernels launched by this call */
   int32_t reserved;

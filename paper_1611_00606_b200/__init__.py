@@ -46,5 +46,6 @@ from .ledger import (
 )
 from .pipeline import BuildOutput, DeviceProblem, GpuPolicy, build_hs, build_hs_device, pin_instance
 from .offload import ExecResult, run_partitioned
+from .engine import int8_gemm_ops, int8_moduli
 
 __version__ = "0.1.0"

@@ -54,7 +54,8 @@ class HsbOutput(ctypes.Structure):
 
 class HsbTimings(ctypes.Structure):
     _fields_ = [(n, ctypes.c_double) for n in
-                ("loop1", "loop2", "unorm", "s1", "s2", "h1", "h2", "h3", "h2d", "d2h", "total")] + [
+                ("loop1", "loop2", "unorm", "s1", "s2", "h1", "h2", "h3", "h2d", "d2h", "total",
+                 "s_core", "h_core")] + [
         ("n_hpd", ctypes.c_int32), ("n_nonhpd", ctypes.c_int32), ("launches", ctypes.c_int32),
         ("reserved", ctypes.c_int32)]
 
@@ -107,7 +108,7 @@ def load():
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.hsb_abi_version() != 1:
+        if lib.hsb_abi_version() != 2:
             raise RuntimeError("libhsb200.so ABI version mismatch; rebuild it")
         _lib = lib
         return lib

@@ -195,6 +195,39 @@ struct Seg {
   OperandView l, r;
 };
 
+// Section timeline on the compute stream: each mark closes the interval since
+// the previous mark and charges it to a section tag.
+struct Timeline {
+  std::vector<std::pair<std::string, cudaEvent_t>> marks;
+  ~Timeline() {
+    for (auto& m : marks) cudaEventDestroy(m.second);
+  }
+  cudaError_t mark(cudaStream_t st, const char* tag) {
+    cudaEvent_t e;
+    cudaError_t err = cudaEventCreate(&e);
+    if (err != cudaSuccess) return err;
+    marks.push_back({tag, e});
+    return cudaEventRecord(e, st);
+  }
+  double total(const char* tag) const {
+    double s = 0;
+    for (size_t i = 1; i < marks.size(); ++i)
+      if (marks[i].first == tag) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second);
+        s += ms * 1e-3;
+      }
+    return s;
+  }
+  double span() const {
+    float ms = 0.f;
+    if (marks.size() > 1) cudaEventElapsedTime(&ms, marks.front().second, marks.back().second);
+    return ms * 1e-3;
+  }
+};
+
+cudaError_t timeline_mark(Timeline* tl, cudaStream_t st, const char* tag) { return tl->mark(st, tag); }
+
 struct ZrkCall {
   std::vector<Seg> segs;
   int64_t m = 0, n = 0;
@@ -208,6 +241,11 @@ struct ZrkCall {
   int64_t c_bstride = 0;
   const int32_t* c_rowoff = nullptr;
   int* done_cnt = nullptr;
+  // optional: mark the contraction kernel alone on this timeline, charging the
+  // work before it to `sect` and the kernel itself to `core`
+  Timeline* tl = nullptr;
+  const char* sect = nullptr;
+  const char* core = nullptr;
 };
 
 // Lower-triangle tile order for the persistent 3M kernel.  The 148 CTAs run
@@ -377,7 +415,9 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
   gp.res = static_cast<int8_t*>(rbuf);
   if (gp.nseg > 0) {
     CKS(oz_tiles(ctx, n, st, &gp.tile_list, &gp.ntiles));
+    if (z.tl) CK(timeline_mark(z.tl, st, z.sect));
     CK(launch_ozaki_gemm(gp, st));
+    if (z.tl) CK(timeline_mark(z.tl, st, z.core));
   } else {
     CK(cudaMemsetAsync(rbuf, 0, static_cast<size_t>(3 * gp.prod_stride), st));
   }
@@ -499,6 +539,7 @@ hsb_status run_zrk(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launche
                               : static_cast<int64_t>(p.tiles_m) * p.tiles_n;
   if (grid_x > 0x7fffffff || z.batch > 65535) return fail(ctx, HSB_ERR_UNSUPPORTED, "grid too large");
   if (g3 && z.triangle && z.batch == 1 && p.tiles_m > kTileGroup) CKS(tile_order(ctx, p.tiles_m, st, &p.tile_list));
+  if (z.tl) CK(timeline_mark(z.tl, st, z.sect));
   if (g3) {
     if (grid_x * z.batch > 0x7fffffff) return fail(ctx, HSB_ERR_UNSUPPORTED, "grid too large");
     CK(launch_zrk3m(p, z.conj, planes, static_cast<int>(grid_x), static_cast<int>(z.batch), st));
@@ -506,6 +547,7 @@ hsb_status run_zrk(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launche
   } else {
     CK(launch_zrk(p, z.conj, static_cast<int>(grid_x), static_cast<int>(z.batch), st));
   }
+  if (z.tl) CK(timeline_mark(z.tl, st, z.core));
   if (launches) ++*launches;
   return HSB_OK;
 }
@@ -552,7 +594,7 @@ OperandView atom_mats(const double* base, int64_t n_atoms, int64_t n_l) {
 // =============================================================================
 extern "C" {
 
-int32_t hsb_abi_version(void) { return 1; }
+int32_t hsb_abi_version(void) { return 2; }
 
 hsb_status hsb_ctx_create(int32_t device, hsb_ctx** out) {
   hsb_ctx* ctx = nullptr;
@@ -770,37 +812,6 @@ hsb_status hsb_hermitian_mirror(hsb_ctx* ctx, void* stream, int64_t n, double* c
 // ----------------------------------------------------------------- pipeline
 namespace {
 
-// Section timeline on the compute stream: each mark closes the interval since
-// the previous mark and charges it to a section tag.
-struct Timeline {
-  std::vector<std::pair<std::string, cudaEvent_t>> marks;
-  ~Timeline() {
-    for (auto& m : marks) cudaEventDestroy(m.second);
-  }
-  cudaError_t mark(cudaStream_t st, const char* tag) {
-    cudaEvent_t e;
-    cudaError_t err = cudaEventCreate(&e);
-    if (err != cudaSuccess) return err;
-    marks.push_back({tag, e});
-    return cudaEventRecord(e, st);
-  }
-  double total(const char* tag) const {
-    double s = 0;
-    for (size_t i = 1; i < marks.size(); ++i)
-      if (marks[i].first == tag) {
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second);
-        s += ms * 1e-3;
-      }
-    return s;
-  }
-  double span() const {
-    float ms = 0.f;
-    if (marks.size() > 1) cudaEventElapsedTime(&ms, marks.front().second, marks.back().second);
-    return ms * 1e-3;
-  }
-};
-
 ZrkCall tri_call(double* c, int64_t ldc, int64_t n, uint32_t flags, double beta) {
   ZrkCall z;
   z.m = z.n = n;
@@ -1011,6 +1022,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     CKS(unorm());
     ZrkCall s2 = tri_call(S, ldo, ng, kLowerOnly, 0.0);
     s2.segs.push_back({plain(UB, K, ng, K), plain(UB, K, ng, K)});
+    s2.tl = &tl, s2.sect = "s2", s2.core = "s2_core";
     CKS(run_zrk(ctx, st, s2, &launches));
     CK(tl.mark(st, "s2"));
     // A rides the copy engine while (UB)^H(UB) runs -- after B's DMAs, so the
@@ -1025,6 +1037,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     CK(tl.mark(st, "h2d"));
     ZrkCall s1 = tri_call(S, ldo, ng, kLowerOnly | kMirror, 1.0);
     s1.segs.push_back({plain(A, K, ng, K), plain(A, K, ng, K)});
+    s1.tl = &tl, s1.sect = "s1", s1.core = "s1_core";
     CKS(run_zrk(ctx, st, s1, &launches));
     CK(tl.mark(st, "s1"));
     CKS(loop1());
@@ -1052,6 +1065,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     ZrkCall s = tri_call(S, ldo, ng, kLowerOnly | kMirror, 0.0);
     s.segs.push_back({plain(A, K, ng, K), plain(A, K, ng, K)});
     s.segs.push_back({plain(UB, K, ng, K), plain(UB, K, ng, K)});
+    s.tl = &tl, s.sect = "s", s.core = "s_core";
     CKS(run_zrk(ctx, st, s, &launches));
     CK(tl.mark(st, "s"));
   }
@@ -1134,6 +1148,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     h.segs.push_back({plain(B, K, ng, K), plain(Z, K, ng, K)});
     if (n_hpd > 0) h.segs.push_back({plain(Y, k_hpd, ng, K), plain(Y, k_hpd, ng, K)});
     if (n_nh > 0) h.segs.push_back({plain(ANH, k_nh, ng, k_nh), plain(XNH, k_nh, ng, K)});
+    h.tl = &tl, h.sect = "h", h.core = "h_core";
     if (stream_h) {  // per-column-block completion counters in mapped host memory
       const size_t nb = static_cast<size_t>(ntiles);
       if (ctx->done_cnt_len < nb) {
@@ -1219,10 +1234,12 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     const double fS = 4.0 * K * double(ng) * ng;
     const double fH1 = 8.0 * K * double(ng) * ng, fH2 = 8.0 * k_nh * double(ng) * ng,
                  fH3 = 4.0 * k_hpd * double(ng) * ng;
-    const double ts = tl.total("s");  // fused S: split S1/S2 by model flops (equal)
-    tm->s1 = tl.total("s1") + ts * 0.5;
-    tm->s2 = tl.total("s2") + ts * 0.5;
-    const double th = tl.total("h"), fh = fH1 + fH2 + fH3;
+    const double ts = tl.total("s") + tl.total("s_core");  // fused S: split S1/S2 by model flops (equal)
+    tm->s1 = tl.total("s1") + tl.total("s1_core") + ts * 0.5;
+    tm->s2 = tl.total("s2") + tl.total("s2_core") + ts * 0.5;
+    tm->s_core = tl.total("s_core") + tl.total("s1_core") + tl.total("s2_core");
+    tm->h_core = tl.total("h_core");
+    const double th = tl.total("h") + tl.total("h_core"), fh = fH1 + fH2 + fH3;
     tm->h1 = tl.total("h1") + th * fH1 / fh;
     tm->h2 = tl.total("h2") + th * fH2 / fh;
     tm->h3 = tl.total("h3") + th * fH3 / fh;

@@ -119,7 +119,7 @@ __global__ void ozaki_residue_kernel(const double2* __restrict__ x, int64_t ldx,
 // its 128 rows x 256 int32 columns.  Per SM and 128-byte k chunk that is
 // 32 KB of TMA traffic for 4M MACs (half of a 1-CTA 128 x 256 tile's), so six
 // 32 KB stages fit in shared memory.
-constexpr int kOzStages = 6;
+constexpr int kOzStages = 7;
 constexpr int kOzHalf = 128;                      // rows of A and of B per CTA
 constexpr int kOzABytes = kOzHalf * kOzBK;        // 16 KB
 constexpr int kOzStageBytes = 2 * kOzABytes;      // 32 KB
@@ -161,6 +161,15 @@ __device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
           bar),
       "h"(static_cast<uint16_t>(3))
       : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
 }
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
@@ -237,62 +246,72 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 1;
-      for (int w = pair; w < nwork; w += npairs) {
-        int prod, mod, tm, tn;
-        oz_work(p, w, prod, mod, tm, tn);
-        const int row0 = tm * 256 + static_cast<int>(rank) * kOzHalf;
-        const int col0 = tn * 256 + static_cast<int>(rank) * kOzHalf;
-        for (int s = 0; s < p.nseg; ++s) {
-          const CUtensorMap* ml = &p.map[prod][s][0];
-          const CUtensorMap* mr = &p.map[prod][s][1];
-          for (int kc = 0; kc < p.kchunks[s]; ++kc) {
-            mbar_wait(empty(stage), phase);
+    // the whole warp runs the loop (uniform control flow keeps the TMA
+    // operands in uniform registers); one elected lane issues
+    int stage = 0;
+    uint32_t phase = 1;
+    for (int w = pair; w < nwork; w += npairs) {
+      int prod, mod, tm, tn;
+      oz_work(p, w, prod, mod, tm, tn);
+      const int row0 = tm * 256 + static_cast<int>(rank) * kOzHalf;
+      const int col0 = tn * 256 + static_cast<int>(rank) * kOzHalf;
+      for (int s = 0; s < p.nseg; ++s) {
+        const CUtensorMap* ml = &p.map[prod][s][0];
+        const CUtensorMap* mr = &p.map[prod][s][1];
+        for (int kc = 0; kc < p.kchunks[s]; ++kc) {
+          mbar_wait(empty(stage), phase);
+          if (elect_one()) {
             if (leader) mbar_expect_tx(full(stage), 2 * kOzStageBytes);
             const uint32_t dst = base + stage * kOzStageBytes;
             const uint32_t fb = full(stage) & kPeerMask;
             tma_load_3d_pair(dst, ml, kc * kOzBK, row0, mod, fb);
             tma_load_3d_pair(dst + kOzABytes, mr, kc * kOzBK, col0, mod, fb);
-            if (++stage == kOzStages) {
-              stage = 0;
-              phase ^= 1u;
-            }
+          }
+          __syncwarp();
+          if (++stage == kOzStages) {
+            stage = 0;
+            phase ^= 1u;
           }
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader only)
-    if (leader && lane == 0) {
+    if (leader) {
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 1;
+      // descriptors of stage 0; a stage is kOzStageBytes further, a 32-byte k step +2
+      const uint64_t da0 = sw128_desc(base), db0 = sw128_desc(base + kOzABytes);
       for (int w = pair; w < nwork; w += npairs) {
         mbar_wait(tempty(acc), acc_phase);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + acc * kOzBN;
-        bool first = true;
+        uint32_t accum = 0;
         for (int s = 0; s < p.nseg; ++s) {
           for (int kc = 0; kc < p.kchunks[s]; ++kc) {
             mbar_wait(full(stage), phase);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t a0 = base + stage * kOzStageBytes, b0 = a0 + kOzABytes;
+            if (elect_one()) {
+              const uint64_t so = static_cast<uint64_t>((stage * kOzStageBytes) >> 4);
 #pragma unroll
-            for (int kk = 0; kk < kOzBK / 32; ++kk) {
-              mma_i8_pair(d, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), first ? 0u : 1u);
-              first = false;
+#pragma unroll
+              for (int kk = 0; kk < kOzBK / 32; ++kk) {
+                mma_i8_pair(d, da0 + so + 2 * kk, db0 + so + 2 * kk, accum | kk);
+              }
+              mma_commit_pair(empty(stage));
             }
-            mma_commit_pair(empty(stage));
+            __syncwarp();
+            accum = 1;
             if (++stage == kOzStages) {
               stage = 0;
               phase ^= 1u;
             }
           }
         }
-        mma_commit_pair(tfull(acc));
+        if (elect_one()) mma_commit_pair(tfull(acc));
+        __syncwarp();
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1u;

@@ -47,18 +47,18 @@ class GpuPolicy:
     (4 real products).  Both agree with the reference to ~1e-15 relative
     Frobenius; the ledger charges the reference's model flops either way.
 
-    ``engine`` runs the S and H contractions on the FP64 DMMA tensor cores
-    ("dmma", default) or emulates them on the INT8 tensor cores ("int8":
-    Chinese-remainder / Ozaki-II scheme, operands rounded to ``int8_bits``
-    bits per column, ~1e-12 relative Frobenius at the default 40; see
-    csrc/ozaki.cuh).
+    ``engine`` emulates the S and H contractions on the INT8 tensor cores
+    ("int8", default: Chinese-remainder / Ozaki-II scheme, operands rounded
+    to ``int8_bits`` bits per column, ~1e-12 relative Frobenius at the
+    default 40, 3.4x faster at C3; see csrc/ozaki.cuh) or runs them on the
+    FP64 DMMA tensor cores ("dmma": ~1e-15).
     """
 
     device: int = 0
     fused: bool = True
     pinned_outputs: bool = True
     complex_mult: str = "3m"
-    engine: str = "dmma"
+    engine: str = "int8"
     int8_bits: int = 0
 
     def __post_init__(self):
