@@ -34,7 +34,7 @@ def _cm(rng, r, c):
 def pol(request):
     if request.param == "int8":  # INT8 tensor-core CRT emulation of the triangle updates
         return GpuPolicy(engine="int8")
-    return GpuPolicy(complex_mult=request.param)
+    return GpuPolicy(engine="dmma", complex_mult=request.param)
 
 
 def test_herk_matches_reference_kernel(g, pol):

@@ -45,10 +45,17 @@ def test_match_kernel_against_oracle(n_atoms, n_types, lmax, ng, kpt):
     assert np.max(np.abs(a - ra)) < 1e-12 * (1 + np.max(np.abs(ra)))
 
 
-def test_physical_build_matches_oracle_pipeline():
-    system, k, kmax, g = synthetic_system(4, 2, 8, 900, seed=3, kpt_frac=(0.0, 0.0, 0.0))
+@pytest.mark.parametrize("engine", ["int8", "dmma"])
+@pytest.mark.parametrize("lmax,kpt", [(8, (0.0, 0.0, 0.0)), (10, (0.1, 0.2, 0.3))])
+def test_physical_build_matches_oracle_pipeline(engine, lmax, kpt):
+    # physical coefficients span many orders of magnitude within a G column
+    # (j_l(KR) ~ (KR)^l / (2l+1)!!): the INT8 engine's per-column scaling
+    # must still meet the north star's 1e-10
+    from paper_1611_00606_b200 import GpuPolicy
+
+    system, k, kmax, g = synthetic_system(4, 2, lmax, 900, seed=3, kpt_frac=kpt)
     t_aa, t_ab, t_bb = synthetic_t_matrices(system, seed=3, nonhpd_fraction=0.25)
-    h, s, split, t, info = build_hs_physical(system, k, g, t_aa, t_ab, t_bb)
+    h, s, split, t, info = build_hs_physical(system, k, g, t_aa, t_ab, t_bb, policy=GpuPolicy(engine=engine))
     torch.cuda.synchronize()
     ra, rb = _oracle(system, k, g)
     n_l, n_g = system.n_l, len(g)

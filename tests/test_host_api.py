@@ -136,3 +136,24 @@ def test_report_summarize_and_table5():
     assert [r.section for r in TABLE5] == ["Loop 1", "Loop 2", "U norm", "S1", "S2", "H1", "H2", "H3"]
     with pytest.raises(InputError):
         summarize(FlopLedger())
+
+
+def test_int8_engine_moduli_choice():
+    # engine.int8_moduli restates hsb_api.cu run_ozaki: the fewest moduli with
+    # b >= 40 bits and 3 K 2^(2b) below M/16
+    import math
+
+    from paper_1611_00606_b200 import int8_gemm_ops, int8_moduli
+    from paper_1611_00606_b200.engine import MODULI
+
+    for k in (1, 98, 7744, 11616, 46464):
+        n_mod, b = int8_moduli(k)
+        log2m = sum(math.log2(p) for p in MODULI[:n_mod])
+        assert b >= 40 and 3 * k * 2.0 ** (2 * b) < 2.0 ** log2m / 16
+        if n_mod > 11:
+            prev = sum(math.log2(p) for p in MODULI[:n_mod - 1])
+            assert math.floor((prev - 2 - math.log2(3 * k)) / 2) - 1 < 40
+    assert all(math.gcd(a, b) == 1 for i, a in enumerate(MODULI) for b in MODULI[i + 1:])
+    assert int8_gemm_ops(8000, 11616) == 2 * 3 * 13 * 11616 * 8000 * 8001 // 2
+    with pytest.raises(InputError):
+        GpuPolicy(engine="fp16")
