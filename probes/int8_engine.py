@@ -17,7 +17,7 @@ bits = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 p = generate(ProblemSpec(CONFIGS[cfg], seed=0))
 dp = DeviceProblem.from_instance(p)
 res = {}
-for name, pol in (("dmma", GpuPolicy()), ("int8", GpuPolicy(engine="int8", int8_bits=bits))):
+for name, pol in (("dmma", GpuPolicy(engine="dmma")), ("int8", GpuPolicy(engine="int8", int8_bits=bits))):
     for _ in range(2):
         h, s, split, t, info = build_hs_device(dp, policy=pol)
     torch.cuda.synchronize()
