@@ -63,6 +63,7 @@ struct hsb_ctx {
   int32_t oz_min_bits = 40;            // INT8 engine: operand integer bits (accuracy ~2^-bits)
   int64_t oz_tiles_n = 0;              // cached INT8-engine tile list (n of the output)
   std::vector<int2> oz_tiles_host;
+  std::vector<int32_t> oz_tile_index_host;
   int32_t cplx = HSB_CPLX_3M;          // complex product form of the zrk kernels
 };
 
@@ -297,9 +298,11 @@ hsb_status oz_encode(hsb_ctx* ctx, CUtensorMap* map, const int8_t* planes, int64
 
 // 256 x 256 tiles (tile row tm >= tile col tn) of the lower triangle, in
 // groups of 6 x 6 tiles for L2 reuse
-hsb_status oz_tiles(hsb_ctx* ctx, int64_t n, cudaStream_t st, const int2** out, int* count) {
+hsb_status oz_tiles(hsb_ctx* ctx, int64_t n, cudaStream_t st, const int2** out, int* count,
+                    const int32_t** index) {
   const int64_t T = (n + kOzBN - 1) / kOzBN;
   std::vector<int2>& v = ctx->oz_tiles_host;
+  std::vector<int32_t>& ix = ctx->oz_tile_index_host;
   if (ctx->oz_tiles_n != n) {
     v.clear();
     for (int64_t j0 = 0; j0 < T; j0 += 6)
@@ -307,15 +310,20 @@ hsb_status oz_tiles(hsb_ctx* ctx, int64_t n, cudaStream_t st, const int2** out, 
         for (int64_t j = j0; j < std::min<int64_t>(j0 + 6, T); ++j)
           for (int64_t i = std::max(i0, j); i < std::min<int64_t>(i0 + 6, T); ++i)
             v.push_back(make_int2(static_cast<int>(i), static_cast<int>(j)));
+    ix.assign(static_cast<size_t>(T * T), -1);
+    for (size_t t = 0; t < v.size(); ++t) ix[static_cast<size_t>(v[t].x * T + v[t].y)] = static_cast<int32_t>(t);
   }
-  void* buf;
+  void *buf, *ibuf;
   CKS(ws(ctx, "oz_tiles", v.size() * sizeof(int2), &buf));
+  CKS(ws(ctx, "oz_tile_index", ix.size() * sizeof(int32_t), &ibuf));
   if (ctx->oz_tiles_n != n) {
     CK(cudaMemcpyAsync(buf, v.data(), v.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ibuf, ix.data(), ix.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
     ctx->oz_tiles_n = n;
   }
   *out = static_cast<const int2*>(buf);
   *count = static_cast<int>(v.size());
+  *index = static_cast<const int32_t*>(ibuf);
   return HSB_OK;
 }
 
@@ -402,19 +410,26 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
       CKS(oz_encode(ctx, &gp.map[pi][si][0], L.planes + lp[pi] * pl, L.k, n, L.kpad, n_mod, 128));
       CKS(oz_encode(ctx, &gp.map[pi][si][1], R.planes + rp[pi] * pr, R.k, n, R.kpad, n_mod, 128));
     }
-    gp.kchunks[si] = static_cast<int32_t>((segs[si].l.k + kOzBK - 1) / kOzBK);
+    gp.seg_chunk0[si + 1] = gp.seg_chunk0[si] + static_cast<int32_t>((segs[si].l.k + kOzBK - 1) / kOzBK);
   }
   gp.nseg = static_cast<int32_t>(segs.size());
+  // slabs of ~16 KB of k (see ozaki.cuh), balanced
+  const int32_t total_chunks = gp.seg_chunk0[gp.nseg];
+  constexpr int32_t kSlabChunks = 16384 / kOzBK;
+  gp.nslab = std::max(1, std::min<int32_t>(kOzMaxSlab, (total_chunks + kSlabChunks - 1) / kSlabChunks));
+  for (int sl = 0; sl <= gp.nslab; ++sl)
+    gp.slab_chunk0[sl] = static_cast<int32_t>(static_cast<int64_t>(total_chunks) * sl / gp.nslab);
   gp.n_mod = n_mod;
   gp.n = static_cast<int32_t>(n);
-  gp.ldr = (n + 15) / 16 * 16;
-  gp.mod_stride = gp.ldr * n;
-  gp.prod_stride = gp.mod_stride * n_mod;
+  const int32_t* tile_index = nullptr;
+  CKS(oz_tiles(ctx, n, st, &gp.tile_list, &gp.ntiles, &tile_index));
+  gp.mod_stride = static_cast<int64_t>(gp.ntiles) * kOzTileBytes;
+  gp.slab_stride = gp.mod_stride * n_mod;
+  gp.prod_stride = gp.slab_stride * gp.nslab;
   void* rbuf;
   CKS(ws(ctx, "oz_out", static_cast<size_t>(3 * gp.prod_stride), &rbuf));
   gp.res = static_cast<int8_t*>(rbuf);
   if (gp.nseg > 0) {
-    CKS(oz_tiles(ctx, n, st, &gp.tile_list, &gp.ntiles));
     if (z.tl) CK(timeline_mark(z.tl, st, z.sect));
     CK(launch_ozaki_gemm(gp, st));
     if (z.tl) CK(timeline_mark(z.tl, st, z.core));
@@ -423,9 +438,12 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
   }
   OzCrtParams cp;
   cp.res = gp.res;
-  cp.ldr = gp.ldr;
   cp.mod_stride = gp.mod_stride;
+  cp.slab_stride = gp.slab_stride;
   cp.prod_stride = gp.prod_stride;
+  cp.tile_index = tile_index;
+  cp.T = static_cast<int32_t>((n + kOzBN - 1) / kOzBN);
+  cp.nslab = gp.nslab;
   cp.n_mod = n_mod;
   cp.n = static_cast<int32_t>(n);
   cp.b = b;

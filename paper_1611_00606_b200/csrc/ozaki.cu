@@ -195,14 +195,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__device__ __forceinline__ void oz_work(const OzGemmParams& p, int w, int& prod, int& mod, int& tm, int& tn) {
-  const int per_prod = p.n_mod * p.ntiles;
-  prod = w / per_prod;
-  const int r = w - prod * per_prod;
-  mod = r / p.ntiles;
-  const int2 t = p.tile_list[r - mod * p.ntiles];
-  tm = t.x;
-  tn = t.y;
+__device__ __forceinline__ void oz_work(const OzGemmParams& p, int w, int& prod, int& slab, int& mod, int& t,
+                                        int& tm, int& tn) {
+  t = w % p.ntiles;
+  int r = w / p.ntiles;
+  mod = r % p.n_mod;
+  r /= p.n_mod;
+  slab = r % p.nslab;
+  prod = r / p.nslab;
+  const int2 tt = p.tile_list[t];
+  tm = tt.x;
+  tn = tt.y;
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
@@ -222,7 +225,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const int nwork = 3 * p.n_mod * p.ntiles;
+  const int nwork = 3 * p.nslab * p.n_mod * p.ntiles;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kOzStages; ++s) {
@@ -251,27 +254,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
     int stage = 0;
     uint32_t phase = 1;
     for (int w = pair; w < nwork; w += npairs) {
-      int prod, mod, tm, tn;
-      oz_work(p, w, prod, mod, tm, tn);
+      int prod, slab, mod, t, tm, tn;
+      oz_work(p, w, prod, slab, mod, t, tm, tn);
       const int row0 = tm * 256 + static_cast<int>(rank) * kOzHalf;
       const int col0 = tn * 256 + static_cast<int>(rank) * kOzHalf;
-      for (int s = 0; s < p.nseg; ++s) {
-        const CUtensorMap* ml = &p.map[prod][s][0];
-        const CUtensorMap* mr = &p.map[prod][s][1];
-        for (int kc = 0; kc < p.kchunks[s]; ++kc) {
-          mbar_wait(empty(stage), phase);
-          if (elect_one()) {
-            if (leader) mbar_expect_tx(full(stage), 2 * kOzStageBytes);
-            const uint32_t dst = base + stage * kOzStageBytes;
-            const uint32_t fb = full(stage) & kPeerMask;
-            tma_load_3d_pair(dst, ml, kc * kOzBK, row0, mod, fb);
-            tma_load_3d_pair(dst + kOzABytes, mr, kc * kOzBK, col0, mod, fb);
-          }
-          __syncwarp();
-          if (++stage == kOzStages) {
-            stage = 0;
-            phase ^= 1u;
-          }
+      int seg = 0;
+      for (int c = p.slab_chunk0[slab]; c < p.slab_chunk0[slab + 1]; ++c) {
+        while (c >= p.seg_chunk0[seg + 1]) ++seg;
+        const int kc = c - p.seg_chunk0[seg];
+        mbar_wait(empty(stage), phase);
+        if (elect_one()) {
+          if (leader) mbar_expect_tx(full(stage), 2 * kOzStageBytes);
+          const uint32_t dst = base + stage * kOzStageBytes;
+          const uint32_t fb = full(stage) & kPeerMask;
+          tma_load_3d_pair(dst, &p.map[prod][seg][0], kc * kOzBK, row0, mod, fb);
+          tma_load_3d_pair(dst + kOzABytes, &p.map[prod][seg][1], kc * kOzBK, col0, mod, fb);
+        }
+        __syncwarp();
+        if (++stage == kOzStages) {
+          stage = 0;
+          phase ^= 1u;
         }
       }
     }
@@ -289,25 +291,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + acc * kOzBN;
         uint32_t accum = 0;
-        for (int s = 0; s < p.nseg; ++s) {
-          for (int kc = 0; kc < p.kchunks[s]; ++kc) {
-            mbar_wait(full(stage), phase);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            if (elect_one()) {
-              const uint64_t so = static_cast<uint64_t>((stage * kOzStageBytes) >> 4);
+        const int slab = (w / p.ntiles / p.n_mod) % p.nslab;
+        for (int c = p.slab_chunk0[slab]; c < p.slab_chunk0[slab + 1]; ++c) {
+          mbar_wait(full(stage), phase);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          if (elect_one()) {
+            const uint64_t so = static_cast<uint64_t>((stage * kOzStageBytes) >> 4);
 #pragma unroll
-#pragma unroll
-              for (int kk = 0; kk < kOzBK / 32; ++kk) {
-                mma_i8_pair(d, da0 + so + 2 * kk, db0 + so + 2 * kk, accum | kk);
-              }
-              mma_commit_pair(empty(stage));
+            for (int kk = 0; kk < kOzBK / 32; ++kk) {
+              mma_i8_pair(d, da0 + so + 2 * kk, db0 + so + 2 * kk, accum | kk);
             }
-            __syncwarp();
-            accum = 1;
-            if (++stage == kOzStages) {
-              stage = 0;
-              phase ^= 1u;
-            }
+            mma_commit_pair(empty(stage));
+          }
+          __syncwarp();
+          accum = 1;
+          if (++stage == kOzStages) {
+            stage = 0;
+            phase ^= 1u;
           }
         }
         if (elect_one()) mma_commit_pair(tfull(acc));
@@ -325,14 +325,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int w = pair; w < nwork; w += npairs) {
-      int prod, mod, tm, tn;
-      oz_work(p, w, prod, mod, tm, tn);
+      int prod, slab, mod, t, tm, tn;
+      oz_work(p, w, prod, slab, mod, t, tm, tn);
       const int ip = oz_mod_rt[mod];
       const double pd = ip, inv = 1.0 / pd;
       mbar_wait(tfull(acc), acc_phase);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int row = tm * 256 + static_cast<int>(rank) * kOzHalf + q * 32 + lane;
-      int8_t* out = p.res + prod * p.prod_stride + mod * p.mod_stride + row;
+      const int rloc = static_cast<int>(rank) * kOzHalf + q * 32 + lane;  // row within the tile
+      const int row = tm * 256 + rloc;
+      int8_t* out = p.res + prod * p.prod_stride + slab * p.slab_stride + mod * p.mod_stride +
+                    static_cast<int64_t>(t) * kOzTileBytes + rloc;
       const int col0 = tn * 256;
       const int ncol = min(kOzBN, p.n - col0);
       for (int c = 0; c < kOzBN / 32; ++c) {
@@ -342,11 +344,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
         if (row < p.n) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            const int col = col0 + c * 32 + j;
-            if (col < p.n) {
-              const int r = sym_mod_d(static_cast<double>(static_cast<int32_t>(v[j])), pd, inv);
-              out[static_cast<int64_t>(col) * p.ldr] = static_cast<int8_t>(r);
-            }
+            const int r = sym_mod_d(static_cast<double>(static_cast<int32_t>(v[j])), pd, inv);
+            out[(c * 32 + j) * 256] = static_cast<int8_t>(r);
           }
         }
       }
@@ -369,7 +368,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
 
 // ------------------------------------------------------------ 4. CRT
 // Explicit CRT in exact double limbs.  With M = prod p_i, y_i = (M/p_i) *
-// ((M/p_i)^-1 mod p_i) and any representatives r_i (|r_i| <= 384):
+// ((M/p_i)^-1 mod p_i) and any representatives r_i (|r_i| <= 384 per slab, <= 16 slabs):
 //     X = sum_i r_i y_i - k M,   k = rint(sum_i r_i (y_i / M)),
 // exact for |X| < M/4 (the host's choice of b leaves >= 4 bits of margin).
 // y_i and M are split into 4 limbs of 32 bits; every limb sum
@@ -406,13 +405,18 @@ __global__ void ozaki_crt_kernel(const OzCrtParams p) {
   const int n = blockIdx.y;  // column
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= p.n || m < n) return;
-  const int8_t* r0 = p.res + static_cast<int64_t>(n) * p.ldr + m;
+  const int t = p.tile_index[(m >> 8) * p.T + (n >> 8)];
+  const int8_t* r0 = p.res + static_cast<int64_t>(t) * kOzTileBytes + (n & 255) * 256 + (m & 255);
   int re[NM], im[NM];
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
-    const int P = r0[i * p.mod_stride];
-    const int Q = r0[p.prod_stride + i * p.mod_stride];
-    const int W = r0[2 * p.prod_stride + i * p.mod_stride];
+    int P = 0, Q = 0, W = 0;
+    for (int sl = 0; sl < p.nslab; ++sl) {  // the residue of a sum is the sum of the slabs' residues
+      const int8_t* q = r0 + sl * p.slab_stride + i * p.mod_stride;
+      P += q[0];
+      Q += q[p.prod_stride];
+      W += q[2 * p.prod_stride];
+    }
     // L^H R: Re = P + Q, Im = W - P + Q ;  L^T R: Re = P - Q, Im = W - P - Q
     re[i] = p.conj ? P + Q : P - Q;
     im[i] = p.conj ? W - P + Q : W - P - Q;
@@ -509,7 +513,7 @@ cudaError_t launch_ozaki_gemm(const OzGemmParams& p, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int64_t nwork = 3LL * p.n_mod * p.ntiles;
+  const int64_t nwork = 3LL * p.nslab * p.n_mod * p.ntiles;
   if (nwork <= 0) return cudaSuccess;
   if (nwork > 0x7fffffff) return cudaErrorInvalidConfiguration;
   const int pairs = static_cast<int>(nwork < n_sm / 2 ? nwork : n_sm / 2);

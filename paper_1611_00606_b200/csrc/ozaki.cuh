@@ -49,24 +49,36 @@ __host__ __device__ constexpr int oz_mod(int i) {
 // planes of a residue buffer: [plane][modulus][col][kpad] int8
 enum OzPlane { kOzRe = 0, kOzIm = 1, kOzMinus = 2, kOzPlus = 3 };
 
+constexpr int kOzMaxSlab = 16;
+constexpr int kOzTileBytes = 256 * 256;  // one tile of int8 residues, column-major
+
+// The reduction (the concatenated segments, in 128-byte k chunks) is split into
+// slabs of ~16 KB of k: each work item covers one slab of one tile, so the
+// operand panels a wave of tiles streams (256 rows x slab) stay L2-resident
+// even for long reductions (C4: 46464 bytes of k), and the per-slab residues
+// are summed in the CRT (the product is linear).
 struct OzGemmParams {
   // maps[prod][seg][side]: 3-D int8 maps {k, cols, modulus}, box {128, 128, 1}
   CUtensorMap map[3][kOzMaxSeg][2];
-  int32_t kchunks[kOzMaxSeg];
-  int32_t nseg;
+  int32_t seg_chunk0[kOzMaxSeg + 1];    // first global k chunk of each segment (+ total)
+  int32_t slab_chunk0[kOzMaxSlab + 1];  // first global k chunk of each slab (+ total)
+  int32_t nseg, nslab;
   int32_t n_mod;
   int32_t n;            // output is n x n (triangle)
   int32_t ntiles;       // entries of tile_list
   const int2* tile_list;  // (tile row, tile col) of the 256 x 256 tiles on or below the diagonal
-  int8_t* res;          // residues [prod][modulus][col][ldr]
-  int64_t ldr;          // rows stride (bytes), multiple of 16
-  int64_t mod_stride;   // bytes between moduli (ldr * n)
-  int64_t prod_stride;  // bytes between products (mod_stride * n_mod)
+  int8_t* res;          // residues [prod][slab][modulus][tile][256 x 256 col-major]
+  int64_t mod_stride;   // bytes between moduli (ntiles * kOzTileBytes)
+  int64_t slab_stride;  // bytes between slabs (mod_stride * n_mod)
+  int64_t prod_stride;  // bytes between products (slab_stride * nslab)
 };
 
 struct OzCrtParams {
   const int8_t* res;
-  int64_t ldr, mod_stride, prod_stride;
+  int64_t mod_stride, slab_stride, prod_stride;
+  const int32_t* tile_index;  // T x T: tile_list position of tile (tm, tn), tm >= tn
+  int32_t T;                  // tiles per side
+  int32_t nslab;
   int32_t n_mod;
   int32_t n;
   int32_t b;                 // operand integer bits
