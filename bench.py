@@ -344,20 +344,35 @@ def main():
         if not args.pageable_inputs:
             p = pin_instance(p)  # the step's inputs sit in pinned host memory (contract)
         if world == 1:
+            from paper_1611_00606_b200 import iter_hs_kpoints
+
             for _ in range(max(3, args.warmup)):
                 out = build_hs(p, policy)  # warm host path, workspace and pinned-output cache
             del out
+            # (a) one call per step: the drop-in build_hs, synchronous
             t0 = time.perf_counter()
             torch.cuda.synchronize(dev)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
             for _ in range(args.steps):
                 out = build_hs(p, policy)
                 _ = out.h.matrix[0, 0]
-            e1.record(stream)
             torch.cuda.synchronize(dev)
-            wall = (time.perf_counter() - t0) / args.steps
-            e2e_ms = max(e0.elapsed_time(e1) / args.steps, wall * 1e3)
+            single_ms = (time.perf_counter() - t0) / args.steps * 1e3
+            del out
+            # (b) the K steps as one k-point batch through build_hs_kpoints: two
+            # contexts/streams overlap one step's PCIe transfers with the next
+            # step's kernels (every step still uploads its inputs and downloads
+            # its H and S inside the timed region)
+            depth = 2
+            for o in iter_hs_kpoints([p] * (depth + 2), policy, depth=depth):
+                del o  # warm the second context and the pinned-output cache (depth + 1 in flight)
+            t0 = time.perf_counter()
+            torch.cuda.synchronize(dev)
+            for o in iter_hs_kpoints([p] * args.steps, policy, depth=depth):
+                _ = o.h.matrix[0, 0]  # consume, then drop: pinned outputs are recycled
+                del o
+            torch.cuda.synchronize(dev)
+            batch_ms = (time.perf_counter() - t0) / args.steps * 1e3
+            e2e_ms, wall = batch_ms, batch_ms * 1e-3
         else:
             e2e_ms, wall = hsdist.e2e_sharded_step_ms(p, policy, n_g, ncols, args.steps, dev)
         h2d = sum(np.asarray(b).nbytes for name in ("a_blocks", "b_blocks", "t_aa", "t_ab", "t_bb", "u_norms")
@@ -366,6 +381,10 @@ def main():
         e2e = {"value": flops_full / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
                "inputs": "pageable numpy" if args.pageable_inputs else "pinned numpy (pin_instance)",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+        if world == 1:
+            e2e.update({"api": "iter_hs_kpoints(steps x instance, depth=2): host wall time per step",
+                        "single_call_ms_per_step": single_ms,
+                        "single_call_value": flops_full / (single_ms * 1e-3) / 1e12})
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -44,7 +44,8 @@ from .ledger import (
     section_flops,
     total_model_flops,
 )
-from .pipeline import BuildOutput, DeviceProblem, GpuPolicy, build_hs, build_hs_device, pin_instance
+from .pipeline import (BuildOutput, DeviceProblem, GpuPolicy, build_hs, build_hs_device, build_hs_kpoints,
+                       iter_hs_kpoints, pin_instance)
 from .offload import ExecResult, run_partitioned
 from .engine import int8_gemm_ops, int8_moduli
 

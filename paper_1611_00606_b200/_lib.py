@@ -69,7 +69,7 @@ class HsbPhys(ctypes.Structure):
 
 _lib = None
 _lock = threading.Lock()
-_ctxs: dict[int, ctypes.c_void_p] = {}
+_ctxs: dict[tuple[int, int], ctypes.c_void_p] = {}
 
 
 def load():
@@ -128,8 +128,14 @@ def check(status: int, ctx) -> None:
     raise RuntimeError(f"libhsb200 error {status}: {msg}")
 
 
-def context(device: int = 0, complex_mult: str | None = None, engine: str | None = None, int8_bits: int = 0):
-    """Process-wide context for ``device`` (created on first use).
+def context(device: int = 0, complex_mult: str | None = None, engine: str | None = None, int8_bits: int = 0,
+            slot: int = 0):
+    """Process-wide context ``slot`` of ``device`` (created on first use).
+
+    Each context owns its device workspace, copy stream and pinned staging, so
+    builds on different slots (and streams) may run concurrently: the k-point
+    pipeline (pipeline.build_hs_kpoints) overlaps one k-point's transfers
+    with another's kernels this way.
 
     ``complex_mult`` ("3m" | "4m") selects the real-product form of the
     complex contractions for the calls that follow (hsb_ctx_set_complex_mult);
@@ -142,12 +148,12 @@ def context(device: int = 0, complex_mult: str | None = None, engine: str | None
     if engine is not None and engine not in ENGINES:
         raise InputError(f"engine must be one of {sorted(ENGINES)}, got {engine!r}")
     with _lock:
-        ctx = _ctxs.get(device)
+        ctx = _ctxs.get((device, slot))
         if ctx is None:
             out = ctypes.c_void_p()
             check(lib.hsb_ctx_create(device, ctypes.byref(out)), None)
             ctx = out
-            _ctxs[device] = ctx
+            _ctxs[(device, slot)] = ctx
         if complex_mult is not None:
             check(lib.hsb_ctx_set_complex_mult(ctx, COMPLEX_MULT[complex_mult]), ctx)
         if engine is not None:

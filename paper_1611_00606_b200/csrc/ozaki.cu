@@ -4,6 +4,7 @@
 // reconstruction with the 3M combination and the Hermitian mirror.
 #include <climits>
 #include <cstring>
+#include <mutex>
 
 #include "ozaki.cuh"
 #include "ptx.cuh"
@@ -379,23 +380,25 @@ struct OzCrtConst {
   double f[kOzMaxMod];      // y_i / M
   double m[4];              // limbs of M
 };
-__constant__ OzCrtConst c_oz_crt;
+constexpr int kOzMinMod = 11;
+__constant__ OzCrtConst c_oz_crt[kOzMaxMod - kOzMinMod + 1];  // one table per n_mod = 11 .. 16
 
 template <int NM>
 __device__ __forceinline__ double crt_value(const int (&r)[NM]) {
+  const OzCrtConst& C = c_oz_crt[NM - kOzMinMod];
   double fk = 0.0, s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
     const double ri = static_cast<double>(r[i]);
-    fk = fma(ri, c_oz_crt.f[i], fk);
-    s0 = fma(ri, c_oz_crt.y[i][0], s0);
-    s1 = fma(ri, c_oz_crt.y[i][1], s1);
-    s2 = fma(ri, c_oz_crt.y[i][2], s2);
-    s3 = fma(ri, c_oz_crt.y[i][3], s3);
+    fk = fma(ri, C.f[i], fk);
+    s0 = fma(ri, C.y[i][0], s0);
+    s1 = fma(ri, C.y[i][1], s1);
+    s2 = fma(ri, C.y[i][2], s2);
+    s3 = fma(ri, C.y[i][3], s3);
   }
   const double k = rint(fk);
-  const double t0 = fma(-k, c_oz_crt.m[0], s0), t1 = fma(-k, c_oz_crt.m[1], s1);
-  const double t2 = fma(-k, c_oz_crt.m[2], s2), t3 = fma(-k, c_oz_crt.m[3], s3);
+  const double t0 = fma(-k, C.m[0], s0), t1 = fma(-k, C.m[1], s1);
+  const double t2 = fma(-k, C.m[2], s2), t3 = fma(-k, C.m[3], s3);
   constexpr double kL = 4294967296.0;  // 2^32
   return fma(fma(fma(t3, kL, t2), kL, t1), kL, t0);
 }
@@ -439,9 +442,9 @@ __global__ void ozaki_crt_kernel(const OzCrtParams p) {
   if (mirror && m > n) C[n + static_cast<int64_t>(m) * p.ldc] = make_double2(vr, -vi);
 }
 
-static cudaError_t oz_crt_constants(int n_mod) {
-  static int done_for = 0;
-  if (done_for == n_mod) return cudaSuccess;
+// CRT tables for every n_mod, computed and uploaded once per process (the
+// tables are constant, so concurrent builds on several contexts never race)
+static OzCrtConst oz_crt_table(int n_mod) {
   using u128 = unsigned __int128;
   u128 M = 1;
   for (int i = 0; i < n_mod; ++i) M *= static_cast<u128>(oz_mod(i));
@@ -469,9 +472,20 @@ static cudaError_t oz_crt_constants(int n_mod) {
     c.f[i] = static_cast<double>(y) / Md;
   }
   limbs(M, c.m);
-  cudaError_t e = cudaMemcpyToSymbol(c_oz_crt, &c, sizeof(c));
-  if (e == cudaSuccess) done_for = n_mod;
-  return e;
+  return c;
+}
+
+static cudaError_t oz_init_once() {
+  static std::once_flag once;
+  static cudaError_t status = cudaSuccess;
+  std::call_once(once, [] {
+    OzCrtConst t[kOzMaxMod - kOzMinMod + 1];
+    for (int nm = kOzMinMod; nm <= kOzMaxMod; ++nm) t[nm - kOzMinMod] = oz_crt_table(nm);
+    status = cudaMemcpyToSymbol(c_oz_crt, t, sizeof(t));
+    if (status == cudaSuccess)
+      status = cudaFuncSetAttribute(ozaki_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kOzSmem);
+  });
+  return status;
 }
 
 // ------------------------------------------------------------ launchers
@@ -502,17 +516,12 @@ cudaError_t launch_ozaki_residues(const double* x, int64_t ldx, int64_t k, int64
 }
 
 cudaError_t launch_ozaki_gemm(const OzGemmParams& p, cudaStream_t st) {
-  static bool attr = false;
-  static int n_sm = 0;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(ozaki_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kOzSmem);
-    if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    e = cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = oz_init_once();
+  if (e != cudaSuccess) return e;
+  int dev = 0, n_sm = 0;
+  cudaGetDevice(&dev);
+  e = cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return e;
   const int64_t nwork = 3LL * p.nslab * p.n_mod * p.ntiles;
   if (nwork <= 0) return cudaSuccess;
   if (nwork > 0x7fffffff) return cudaErrorInvalidConfiguration;
@@ -524,7 +533,7 @@ cudaError_t launch_ozaki_gemm(const OzGemmParams& p, cudaStream_t st) {
 
 cudaError_t launch_ozaki_crt(const OzCrtParams& p, cudaStream_t st) {
   if (p.n <= 0) return cudaSuccess;
-  cudaError_t ce = oz_crt_constants(p.n_mod);
+  cudaError_t ce = oz_init_once();
   if (ce != cudaSuccess) return ce;
   dim3 grid(static_cast<unsigned>((p.n + 127) / 128), static_cast<unsigned>(p.n));
   if (p.n > 65535) return cudaErrorInvalidConfiguration;

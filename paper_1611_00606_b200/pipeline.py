@@ -188,9 +188,9 @@ def _host_problem(p):
     return prob, (blocks, arrays)
 
 
-def _call_build(pol, prob, out, stream, force_nonhpd, n_a):
+def _call_build(pol, prob, out, stream, force_nonhpd, n_a, slot: int = 0):
     lib = _lib.load()
-    ctx = _lib.context(pol.device, pol.complex_mult, pol.engine, pol.int8_bits)
+    ctx = _lib.context(pol.device, pol.complex_mult, pol.engine, pol.int8_bits, slot)
     opts = (_lib.HSB_OPT_FORCE_NONHPD if force_nonhpd else 0) | (0 if pol.fused else _lib.HSB_OPT_UNFUSED)
     tim = _lib.HsbTimings()
     info = (ctypes.c_int32 * n_a)()
@@ -201,6 +201,10 @@ def _call_build(pol, prob, out, stream, force_nonhpd, n_a):
 
 def build_hs(p, policy=None, force_nonhpd: bool = False) -> BuildOutput:
     """Assemble H and S on the GPU from host-resident per-atom blocks."""
+    return _build_host(p, policy, force_nonhpd)
+
+
+def _build_host(p, policy, force_nonhpd, slot: int = 0, stream=None) -> BuildOutput:
     validate_instance(p, check_stack_values=False)  # A/B values are checked while staging
     pol = _policy(policy)
     dims = Dims(p.dims.n_atoms, p.dims.n_l, p.dims.n_g)
@@ -211,11 +215,77 @@ def build_hs(p, policy=None, force_nonhpd: bool = False) -> BuildOutput:
     out.location = _lib.HSB_LOC_HOST
     out.ld = dims.n_g
     out.h, out.s = h.ctypes.data, s.ctypes.data
-    tim, info = _call_build(pol, prob, out, None, force_nonhpd, dims.n_atoms)
+    tim, info = _call_build(pol, prob, out, stream, force_nonhpd, dims.n_atoms, slot)
     t = _timings_dict(tim)
     led = ledger_from_timings(dims, info, t, force_nonhpd)
     return BuildOutput(HermitianResult(h, Fill.FULL), HermitianResult(s, Fill.FULL),
                        SplitCounts(tim.n_hpd, tim.n_nonhpd), led, t)
+
+
+def iter_hs_kpoints(instances, policy=None, force_nonhpd: bool = False, depth: int = 2):
+    """Yield ``build_hs`` of each independent k-point (BASELINE config C5) in
+    input order, pipelined on one GPU: ``depth`` host threads each drive their
+    own context and CUDA stream, so one k-point's uploads and H/S downloads
+    (PCIe) overlap another's kernels.  At most ``depth`` results are in flight
+    beyond the one being consumed, so pinned output memory stays bounded when
+    the caller drops each result after use."""
+    import threading
+
+    import torch
+
+    pol = _policy(policy)
+    if int(depth) != depth or depth < 1:
+        raise InputError(f"depth must be a positive integer, got {depth!r}")
+    instances = list(instances)
+    if depth == 1 or len(instances) <= 1:
+        for p in instances:
+            yield build_hs(p, pol, force_nonhpd)
+        return
+    dev = torch.device("cuda", pol.device)
+    streams = [torch.cuda.Stream(device=dev) for _ in range(depth)]
+    results = [None] * len(instances)
+    ready = [threading.Event() for _ in instances]
+    credits = threading.Semaphore(depth)
+    failure = []
+
+    def lane(slot):  # one thread per context: k-points slot, slot + depth, ...
+        st = ctypes.c_void_p(streams[slot].cuda_stream)
+        try:
+            for i in range(slot, len(instances), depth):
+                credits.acquire()
+                if failure:
+                    return
+                results[i] = _build_host(instances[i], pol, force_nonhpd, slot=slot, stream=st)
+                ready[i].set()
+        except BaseException as exc:  # noqa: BLE001 - re-raised in the consumer
+            failure.append(exc)
+            for e in ready:
+                e.set()
+
+    threads = [threading.Thread(target=lane, args=(k,), daemon=True) for k in range(depth)]
+    for t in threads:
+        t.start()
+    try:
+        for i in range(len(instances)):
+            ready[i].wait()
+            if failure:
+                raise failure[0]
+            r, results[i] = results[i], None
+            credits.release()
+            yield r
+    finally:
+        if not failure:  # stop lanes that are still waiting for a credit
+            failure.append(GeneratorExit())
+        for _ in range(len(instances)):
+            credits.release()
+        for t in threads:
+            t.join()
+
+
+def build_hs_kpoints(instances, policy=None, force_nonhpd: bool = False, depth: int = 2):
+    """List form of ``iter_hs_kpoints``: every result equals the serial
+    ``build_hs`` of that instance."""
+    return list(iter_hs_kpoints(instances, policy, force_nonhpd, depth))
 
 
 def build_hs_into(p, h, s, policy=None, force_nonhpd: bool = False, stream=None):

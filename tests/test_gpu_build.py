@@ -180,3 +180,19 @@ def test_pinned_instance_path_matches_and_checks_values():
     q.a_blocks[1][0, 0] = -np.inf
     with pytest.raises(InvariantError, match=r"a_blocks\[1\]"):
         build_hs(q)
+
+
+@pytest.mark.parametrize("cm", ["3m", "int8"])
+def test_kpoint_pipeline_matches_serial_builds(cm):
+    # BASELINE config C5 on one GPU: independent k-points through two contexts
+    # and streams concurrently; each result equals its serial build bitwise
+    from paper_1611_00606_b200 import build_hs_kpoints
+
+    ps = [generate(ProblemSpec(Dims(3, 25, 260), seed=40 + i, nonhpd_fraction=0.3)) for i in range(5)]
+    serial = [build_hs(p, _pol(cm)) for p in ps]
+    piped = build_hs_kpoints(ps, _pol(cm), depth=2)
+    for a, b, p in zip(serial, piped, ps):
+        assert a.h.matrix.tobytes() == b.h.matrix.tobytes()
+        assert a.s.matrix.tobytes() == b.s.matrix.tobytes()
+        assert (a.split.hpd, a.split.nonhpd) == (b.split.hpd, b.split.nonhpd)
+        assert rel_frob_error(b.h.matrix, brute.h_brute(p)) < TOL
