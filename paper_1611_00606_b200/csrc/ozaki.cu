@@ -404,10 +404,7 @@ __device__ __forceinline__ double crt_value(const int (&r)[NM]) {
 }
 
 template <int NM>
-__global__ void ozaki_crt_kernel(const OzCrtParams p) {
-  const int n = blockIdx.y;  // column
-  const int m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= p.n || m < n) return;
+__device__ __forceinline__ double2 crt_element(const OzCrtParams& p, int m, int n) {
   const int t = p.tile_index[(m >> 8) * p.T + (n >> 8)];
   const int8_t* r0 = p.res + static_cast<int64_t>(t) * kOzTileBytes + (n & 255) * 256 + (m & 255);
   int re[NM], im[NM];
@@ -429,17 +426,46 @@ __global__ void ozaki_crt_kernel(const OzCrtParams p) {
   const double xi = ldexp(crt_value<NM>(im), sh);
   double vr = p.alpha_re * xr - p.alpha_im * xi;
   double vi = p.alpha_re * xi + p.alpha_im * xr;
-  double2* C = reinterpret_cast<double2*>(p.c);
-  double2* dst = C + m + static_cast<int64_t>(n) * p.ldc;
   if (p.beta_re != 0.0 || p.beta_im != 0.0) {
-    const double2 o = *dst;
+    const double2 o = reinterpret_cast<const double2*>(p.c)[m + static_cast<int64_t>(n) * p.ldc];
     vr += p.beta_re * o.x - p.beta_im * o.y;
     vi += p.beta_re * o.y + p.beta_im * o.x;
   }
-  const bool mirror = p.flags & kMirror;
-  if (m == n && (mirror || (p.flags & kZeroImagDiag))) vi = 0.0;
-  *dst = make_double2(vr, vi);
-  if (mirror && m > n) C[n + static_cast<int64_t>(m) * p.ldc] = make_double2(vr, -vi);
+  if (m == n && ((p.flags & kMirror) || (p.flags & kZeroImagDiag))) vi = 0.0;
+  return make_double2(vr, vi);
+}
+
+// One CTA per 32 x 32 block pair (bi >= bj) of the lower triangle: threads
+// along m read the residues and write C[m, n] coalesced; the mirrored block
+// C[n, m] = conj(C[m, n]) is transposed through shared memory so its stores
+// are coalesced too (matcore.hermitian_mirror, matcore.py:89-105).
+template <int NM>
+__global__ void __launch_bounds__(256) ozaki_crt_kernel(const OzCrtParams p) {
+  __shared__ double2 tile[32][33];
+  const int64_t t = blockIdx.x;
+  int bi = static_cast<int>((sqrt(8.0 * static_cast<double>(t) + 1.0) - 1.0) * 0.5);
+  while (static_cast<int64_t>(bi) * (bi + 1) / 2 > t) --bi;
+  while (static_cast<int64_t>(bi + 1) * (bi + 2) / 2 <= t) ++bi;
+  const int bj = static_cast<int>(t - static_cast<int64_t>(bi) * (bi + 1) / 2);
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  double2* C = reinterpret_cast<double2*>(p.c);
+  for (int k = ty; k < 32; k += 8) {
+    const int m = bi * 32 + tx, n = bj * 32 + k;
+    if (m < p.n && n < p.n && m >= n) {
+      const double2 v = crt_element<NM>(p, m, n);
+      C[m + static_cast<int64_t>(n) * p.ldc] = v;
+      tile[k][tx] = v;
+    }
+  }
+  if (!(p.flags & kMirror)) return;
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    const int m = bi * 32 + k, n = bj * 32 + tx;  // mirror element (n, m) = conj of (m, n)
+    if (m < p.n && n < p.n && m > n) {
+      const double2 v = tile[tx][k];
+      C[n + static_cast<int64_t>(m) * p.ldc] = make_double2(v.x, -v.y);
+    }
+  }
 }
 
 // CRT tables for every n_mod, computed and uploaded once per process (the
@@ -535,15 +561,17 @@ cudaError_t launch_ozaki_crt(const OzCrtParams& p, cudaStream_t st) {
   if (p.n <= 0) return cudaSuccess;
   cudaError_t ce = oz_init_once();
   if (ce != cudaSuccess) return ce;
-  dim3 grid(static_cast<unsigned>((p.n + 127) / 128), static_cast<unsigned>(p.n));
-  if (p.n > 65535) return cudaErrorInvalidConfiguration;
+  const int64_t tb = (p.n + 31) / 32;
+  const int64_t blocks = tb * (tb + 1) / 2;
+  if (blocks > 0x7fffffff) return cudaErrorInvalidConfiguration;
+  const dim3 grid(static_cast<unsigned>(blocks)), block(32, 8);
   switch (p.n_mod) {
-    case 11: ozaki_crt_kernel<11><<<grid, 128, 0, st>>>(p); break;
-    case 12: ozaki_crt_kernel<12><<<grid, 128, 0, st>>>(p); break;
-    case 13: ozaki_crt_kernel<13><<<grid, 128, 0, st>>>(p); break;
-    case 14: ozaki_crt_kernel<14><<<grid, 128, 0, st>>>(p); break;
-    case 15: ozaki_crt_kernel<15><<<grid, 128, 0, st>>>(p); break;
-    case 16: ozaki_crt_kernel<16><<<grid, 128, 0, st>>>(p); break;
+    case 11: ozaki_crt_kernel<11><<<grid, block, 0, st>>>(p); break;
+    case 12: ozaki_crt_kernel<12><<<grid, block, 0, st>>>(p); break;
+    case 13: ozaki_crt_kernel<13><<<grid, block, 0, st>>>(p); break;
+    case 14: ozaki_crt_kernel<14><<<grid, block, 0, st>>>(p); break;
+    case 15: ozaki_crt_kernel<15><<<grid, block, 0, st>>>(p); break;
+    case 16: ozaki_crt_kernel<16><<<grid, block, 0, st>>>(p); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
