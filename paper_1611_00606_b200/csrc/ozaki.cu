@@ -403,23 +403,16 @@ __device__ __forceinline__ double crt_value(const int (&r)[NM]) {
   return fma(fma(fma(t3, kL, t2), kL, t1), kL, t0);
 }
 
+// Finish one element from its per-modulus P, Q, W residue sums.
 template <int NM>
-__device__ __forceinline__ double2 crt_element(const OzCrtParams& p, int m, int n) {
-  const int t = p.tile_index[(m >> 8) * p.T + (n >> 8)];
-  const int8_t* r0 = p.res + static_cast<int64_t>(t) * kOzTileBytes + (n & 255) * 256 + (m & 255);
+__device__ __forceinline__ double2 crt_finish(const OzCrtParams& p, const int (&P)[NM], const int (&Q)[NM],
+                                              const int (&W)[NM], int m, int n) {
   int re[NM], im[NM];
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
-    int P = 0, Q = 0, W = 0;
-    for (int sl = 0; sl < p.nslab; ++sl) {  // the residue of a sum is the sum of the slabs' residues
-      const int8_t* q = r0 + sl * p.slab_stride + i * p.mod_stride;
-      P += q[0];
-      Q += q[p.prod_stride];
-      W += q[2 * p.prod_stride];
-    }
     // L^H R: Re = P + Q, Im = W - P + Q ;  L^T R: Re = P - Q, Im = W - P - Q
-    re[i] = p.conj ? P + Q : P - Q;
-    im[i] = p.conj ? W - P + Q : W - P - Q;
+    re[i] = p.conj ? P[i] + Q[i] : P[i] - Q[i];
+    im[i] = p.conj ? W[i] - P[i] + Q[i] : W[i] - P[i] - Q[i];
   }
   const int sh = p.el[m] + p.er[n] - 2 * p.b;
   const double xr = ldexp(crt_value<NM>(re), sh);
@@ -435,37 +428,44 @@ __device__ __forceinline__ double2 crt_element(const OzCrtParams& p, int m, int 
   return make_double2(vr, vi);
 }
 
-// One CTA per 32 x 32 block pair (bi >= bj) of the lower triangle: threads
-// along m read the residues and write C[m, n] coalesced; the mirrored block
-// C[n, m] = conj(C[m, n]) is transposed through shared memory so its stores
-// are coalesced too (matcore.hermitian_mirror, matcore.py:89-105).
-template <int NM>
-__global__ void __launch_bounds__(256) ozaki_crt_kernel(const OzCrtParams p) {
-  __shared__ double2 tile[32][33];
-  const int64_t t = blockIdx.x;
-  int bi = static_cast<int>((sqrt(8.0 * static_cast<double>(t) + 1.0) - 1.0) * 0.5);
-  while (static_cast<int64_t>(bi) * (bi + 1) / 2 > t) --bi;
-  while (static_cast<int64_t>(bi + 1) * (bi + 2) / 2 <= t) ++bi;
-  const int bj = static_cast<int>(t - static_cast<int64_t>(bi) * (bi + 1) / 2);
-  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+// One thread per lower-triangle element (m >= n), threads along m: residue
+// loads and the C[m, n] store are coalesced; the mirror C[n, m] = conj(C[m, n])
+// is a strided store (matcore.hermitian_mirror, matcore.py:89-105).  Measured
+// faster than shared-memory-transposed variants, which run fewer threads per
+// SM.  ONE_SLAB: straight-line code, all 3 x NM loads in flight at once.
+template <int NM, bool ONE_SLAB>
+__global__ void __launch_bounds__(128) ozaki_crt_kernel(const OzCrtParams p) {
+  const int n = blockIdx.y;  // column
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= p.n || m < n) return;
+  const int t = p.tile_index[(m >> 8) * p.T + (n >> 8)];
+  const int8_t* r0 = p.res + static_cast<int64_t>(t) * kOzTileBytes + (n & 255) * 256 + (m & 255);
+  int P[NM], Q[NM], W[NM];
+  if (ONE_SLAB) {
+#pragma unroll
+    for (int i = 0; i < NM; ++i) {
+      P[i] = r0[i * p.mod_stride];
+      Q[i] = r0[p.prod_stride + i * p.mod_stride];
+      W[i] = r0[2 * p.prod_stride + i * p.mod_stride];
+    }
+  } else {
+    // the residue of a sum is the sum of the k slabs' residues
+#pragma unroll
+    for (int i = 0; i < NM; ++i) P[i] = Q[i] = W[i] = 0;
+    for (int sl = 0; sl < p.nslab; ++sl) {
+      const int8_t* q = r0 + sl * p.slab_stride;
+#pragma unroll
+      for (int i = 0; i < NM; ++i) {
+        P[i] += q[i * p.mod_stride];
+        Q[i] += q[p.prod_stride + i * p.mod_stride];
+        W[i] += q[2 * p.prod_stride + i * p.mod_stride];
+      }
+    }
+  }
+  const double2 v = crt_finish<NM>(p, P, Q, W, m, n);
   double2* C = reinterpret_cast<double2*>(p.c);
-  for (int k = ty; k < 32; k += 8) {
-    const int m = bi * 32 + tx, n = bj * 32 + k;
-    if (m < p.n && n < p.n && m >= n) {
-      const double2 v = crt_element<NM>(p, m, n);
-      C[m + static_cast<int64_t>(n) * p.ldc] = v;
-      tile[k][tx] = v;
-    }
-  }
-  if (!(p.flags & kMirror)) return;
-  __syncthreads();
-  for (int k = ty; k < 32; k += 8) {
-    const int m = bi * 32 + k, n = bj * 32 + tx;  // mirror element (n, m) = conj of (m, n)
-    if (m < p.n && n < p.n && m > n) {
-      const double2 v = tile[tx][k];
-      C[n + static_cast<int64_t>(m) * p.ldc] = make_double2(v.x, -v.y);
-    }
-  }
+  C[m + static_cast<int64_t>(n) * p.ldc] = v;
+  if ((p.flags & kMirror) && m > n) C[n + static_cast<int64_t>(m) * p.ldc] = make_double2(v.x, -v.y);
 }
 
 // CRT tables for every n_mod, computed and uploaded once per process (the
@@ -561,19 +561,26 @@ cudaError_t launch_ozaki_crt(const OzCrtParams& p, cudaStream_t st) {
   if (p.n <= 0) return cudaSuccess;
   cudaError_t ce = oz_init_once();
   if (ce != cudaSuccess) return ce;
-  const int64_t tb = (p.n + 31) / 32;
-  const int64_t blocks = tb * (tb + 1) / 2;
-  if (blocks > 0x7fffffff) return cudaErrorInvalidConfiguration;
-  const dim3 grid(static_cast<unsigned>(blocks)), block(32, 8);
+  if (p.n > 65535) return cudaErrorInvalidConfiguration;
+  const dim3 grid(static_cast<unsigned>((p.n + 127) / 128), static_cast<unsigned>(p.n)), block(128);
+  const bool one = p.nslab == 1;
+#define HSB_OZ_CRT(NMV)                                                        \
+  case NMV:                                                                  \
+    if (one)                                                                 \
+      ozaki_crt_kernel<NMV, true><<<grid, block, 0, st>>>(p);                \
+    else                                                                     \
+      ozaki_crt_kernel<NMV, false><<<grid, block, 0, st>>>(p);               \
+    break;
   switch (p.n_mod) {
-    case 11: ozaki_crt_kernel<11><<<grid, block, 0, st>>>(p); break;
-    case 12: ozaki_crt_kernel<12><<<grid, block, 0, st>>>(p); break;
-    case 13: ozaki_crt_kernel<13><<<grid, block, 0, st>>>(p); break;
-    case 14: ozaki_crt_kernel<14><<<grid, block, 0, st>>>(p); break;
-    case 15: ozaki_crt_kernel<15><<<grid, block, 0, st>>>(p); break;
-    case 16: ozaki_crt_kernel<16><<<grid, block, 0, st>>>(p); break;
+    HSB_OZ_CRT(11)
+    HSB_OZ_CRT(12)
+    HSB_OZ_CRT(13)
+    HSB_OZ_CRT(14)
+    HSB_OZ_CRT(15)
+    HSB_OZ_CRT(16)
     default: return cudaErrorInvalidValue;
   }
+#undef HSB_OZ_CRT
   return cudaGetLastError();
 }
 
