@@ -14,7 +14,7 @@ from pathlib import Path
 
 from .hs_types import DimensionError, InputError, InvariantError
 
-LIB_PATH = Path(__file__).resolve().parent / "libhsb200.so"
+LIB_PATH = Path(os.environ.get("HSB200_LIB", Path(__file__).resolve().parent / "libhsb200.so"))
 
 HSB_OK, HSB_ERR_DIMENSION, HSB_ERR_INPUT, HSB_ERR_INVARIANT = 0, 1, 2, 3
 HSB_ERR_CUDA, HSB_ERR_UNSUPPORTED, HSB_ERR_NOMEM = 4, 5, 6

@@ -429,6 +429,9 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
   void* rbuf;
   CKS(ws(ctx, "oz_out", static_cast<size_t>(3 * gp.prod_stride), &rbuf));
   gp.res = static_cast<int8_t*>(rbuf);
+  void* cbuf;
+  CKS(ws(ctx, "oz_counter", 16, &cbuf));
+  gp.counter = static_cast<int32_t*>(cbuf);
   if (gp.nseg > 0) {
     if (z.tl) CK(timeline_mark(z.tl, st, z.sect));
     CK(launch_ozaki_gemm(gp, st));

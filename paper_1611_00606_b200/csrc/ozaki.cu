@@ -175,6 +175,28 @@ __device__ __forceinline__ bool elect_one() {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t mapa_peer(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_shared_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -221,12 +243,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
   auto tempty = [&](int s) { return bars + 8u * (2 * kOzStages + 2 + s); };
   const uint32_t tmem_slot = bars + 8u * (2 * kOzStages + 4);
   const uint32_t* tmem_slot_ptr = reinterpret_cast<const uint32_t*>(smem_raw + (tmem_slot - raw));
+  // work queue: the leader's producer steals work items from a global counter
+  // and hands each to every role of both CTAs through kOzQ smem slots
+  constexpr int kOzQ = 4;
+  auto wfull = [&](int j) { return bars + 8u * (2 * kOzStages + 5 + j); };
+  auto wempty = [&](int j) { return bars + 8u * (2 * kOzStages + 5 + kOzQ + j); };
+  auto wslot = [&](int j) { return bars + 8u * (2 * kOzStages + 5 + 2 * kOzQ) + 4u * j; };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
-  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const int nwork = 3 * p.nslab * p.n_mod * p.ntiles;
+  // consumer side of the queue (every role except the leader's producer)
+  auto take = [&](int seq) -> int {
+    const int j = seq & (kOzQ - 1);
+    mbar_wait_cluster(wfull(j), static_cast<uint32_t>((seq / kOzQ) & 1));
+    const int w = static_cast<int>(ld_shared_u32(wslot(j)));
+    __syncwarp();
+    if (lane == 0) mbar_arrive_cluster(wempty(j) & kPeerMask);  // the leader's copy
+    return w;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kOzStages; ++s) {
@@ -236,6 +272,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(tfull(s), 1);
       mbar_init(tempty(s), 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    }
+    for (int j = 0; j < kOzQ; ++j) {
+      mbar_init(wfull(j), 1);
+      mbar_init(wempty(j), 10);  // leader: MMA + 4 epilogue warps; peer: producer + 4 epilogue warps
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -254,7 +294,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
     // operands in uniform registers); one elected lane issues
     int stage = 0;
     uint32_t phase = 1;
-    for (int w = pair; w < nwork; w += npairs) {
+    for (int seq = 0;; ++seq) {
+      int w;
+      if (leader) {
+        const int j = seq & (kOzQ - 1);
+        w = 0;
+        const bool me = elect_one();
+        if (me) {
+          mbar_wait(wempty(j), static_cast<uint32_t>(((seq / kOzQ) & 1) ^ 1));
+          w = atomicAdd(p.counter, 1);
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(wslot(j)), "r"(static_cast<uint32_t>(w)) : "memory");
+          st_cluster_u32(mapa_peer(wslot(j), 1), static_cast<uint32_t>(w));
+          mbar_arrive(wfull(j));
+          mbar_arrive_cluster(mapa_peer(wfull(j), 1));
+        }
+        w = __shfl_sync(0xffffffffu, w, __ffs(__ballot_sync(0xffffffffu, me)) - 1);
+      } else {
+        w = take(seq);
+      }
+      if (w >= nwork) break;
       int prod, slab, mod, t, tm, tn;
       oz_work(p, w, prod, slab, mod, t, tm, tn);
       const int row0 = tm * 256 + static_cast<int>(rank) * kOzHalf;
@@ -287,7 +345,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
       uint32_t acc_phase = 1;
       // descriptors of stage 0; a stage is kOzStageBytes further, a 32-byte k step +2
       const uint64_t da0 = sw128_desc(base), db0 = sw128_desc(base + kOzABytes);
-      for (int w = pair; w < nwork; w += npairs) {
+      for (int seq = 0;; ++seq) {
+        const int w = take(seq);
+        if (w >= nwork) break;
         mbar_wait(tempty(acc), acc_phase);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + acc * kOzBN;
@@ -325,7 +385,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
     const int q = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int w = pair; w < nwork; w += npairs) {
+    for (int seq = 0;; ++seq) {
+      const int w = take(seq);
+      if (w >= nwork) break;
       int prod, slab, mod, t, tm, tn;
       oz_work(p, w, prod, slab, mod, t, tm, tn);
       const int ip = oz_mod_rt[mod];
@@ -553,6 +615,8 @@ cudaError_t launch_ozaki_gemm(const OzGemmParams& p, cudaStream_t st) {
   if (nwork > 0x7fffffff) return cudaErrorInvalidConfiguration;
   const int pairs = static_cast<int>(nwork < n_sm / 2 ? nwork : n_sm / 2);
   const int grid = 2 * pairs;
+  e = cudaMemsetAsync(p.counter, 0, sizeof(int32_t), st);
+  if (e != cudaSuccess) return e;
   ozaki_gemm_kernel<<<grid, kOzThreads, kOzSmem, st>>>(p);
   return cudaGetLastError();
 }

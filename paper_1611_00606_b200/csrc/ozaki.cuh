@@ -71,6 +71,7 @@ struct OzGemmParams {
   int64_t mod_stride;   // bytes between moduli (ntiles * kOzTileBytes)
   int64_t slab_stride;  // bytes between slabs (mod_stride * n_mod)
   int64_t prod_stride;  // bytes between products (slab_stride * nslab)
+  int32_t* counter;     // work-stealing counter (zeroed by the launcher)
 };
 
 struct OzCrtParams {
