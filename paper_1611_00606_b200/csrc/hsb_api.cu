@@ -247,6 +247,9 @@ struct ZrkCall {
   Timeline* tl = nullptr;
   const char* sect = nullptr;
   const char* core = nullptr;
+  // optional (INT8 engine): run in column groups and record, after each, an
+  // event and the end column of the columns that are final
+  std::vector<std::pair<cudaEvent_t, int64_t>>* chunk_events = nullptr;
 };
 
 // Lower-triangle tile order for the persistent 3M kernel.  The 148 CTAs run
@@ -422,8 +425,9 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
   gp.n_mod = n_mod;
   gp.n = static_cast<int32_t>(n);
   const int32_t* tile_index = nullptr;
-  CKS(oz_tiles(ctx, n, st, &gp.tile_list, &gp.ntiles, &tile_index));
-  gp.mod_stride = static_cast<int64_t>(gp.ntiles) * kOzTileBytes;
+  int total_tiles = 0;
+  CKS(oz_tiles(ctx, n, st, &gp.tile_list, &total_tiles, &tile_index));
+  gp.mod_stride = static_cast<int64_t>(total_tiles) * kOzTileBytes;
   gp.slab_stride = gp.mod_stride * n_mod;
   gp.prod_stride = gp.slab_stride * gp.nslab;
   void* rbuf;
@@ -432,13 +436,8 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
   void* cbuf;
   CKS(ws(ctx, "oz_counter", 16, &cbuf));
   gp.counter = static_cast<int32_t*>(cbuf);
-  if (gp.nseg > 0) {
-    if (z.tl) CK(timeline_mark(z.tl, st, z.sect));
-    CK(launch_ozaki_gemm(gp, st));
-    if (z.tl) CK(timeline_mark(z.tl, st, z.core));
-  } else {
-    CK(cudaMemsetAsync(rbuf, 0, static_cast<size_t>(3 * gp.prod_stride), st));
-  }
+  if (gp.nseg == 0) CK(cudaMemsetAsync(rbuf, 0, static_cast<size_t>(3 * gp.prod_stride), st));
+
   OzCrtParams cp;
   cp.res = gp.res;
   cp.mod_stride = gp.mod_stride;
@@ -460,12 +459,42 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
   cp.c = z.c;
   cp.ldc = z.ldc;
   cp.flags = z.flags;
-  CK(launch_ozaki_crt(cp, st));
-  if (z.done_cnt) {
-    // the host H stream polls per-column counters; everything is final here
-    // (triangle tiles of the DMMA grid: count T for every column block)
-    const int64_t T = (n + kBN - 1) / kBN;
-    CK(launch_fill_i32(z.done_cnt, T, static_cast<int32_t>(T), st));
+
+  // With a host download waiting on per-column counters (done_cnt), the
+  // product runs in column groups of 6 tiles (contiguous in the tile list):
+  // once groups 0..g are done their columns are final (the mirror of an
+  // entry of an earlier group lands in a later column), so their download
+  // overlaps the remaining groups.  Otherwise one GEMM + one CRT launch.
+  const int64_t T = (n + kOzBN - 1) / kOzBN;
+  const int64_t T64 = (n + kBN - 1) / kBN;  // the host's 64-column blocks
+  const std::vector<int2>& tl_host = ctx->oz_tiles_host;
+  const int64_t group = (z.done_cnt || z.chunk_events) ? 6 : T;
+  int t0 = 0;
+  for (int64_t j0 = 0; j0 < T; j0 += group) {
+    const int64_t j1 = std::min<int64_t>(j0 + group, T);
+    int t1 = t0;
+    while (t1 < total_tiles && tl_host[static_cast<size_t>(t1)].y < j1) ++t1;
+    if (gp.nseg > 0 && t1 > t0) {
+      gp.tile0 = t0;
+      gp.ntiles = t1 - t0;
+      if (z.tl) CK(timeline_mark(z.tl, st, z.sect));
+      CK(launch_ozaki_gemm(gp, st));
+      if (z.tl) CK(timeline_mark(z.tl, st, z.core));
+    }
+    const int64_t c0 = j0 * kOzBN, c1 = std::min<int64_t>(j1 * kOzBN, n);
+    cp.n0 = static_cast<int32_t>(c0);
+    CK(launch_ozaki_crt_cols(cp, c1 - c0, st));
+    if (z.done_cnt) {
+      const int64_t b0 = c0 / kBN, b1 = (j1 == T) ? T64 : c1 / kBN;
+      CK(launch_fill_i32(z.done_cnt + b0, b1 - b0, static_cast<int32_t>(T64), st));
+    }
+    if (z.chunk_events) {
+      cudaEvent_t ev;
+      CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      z.chunk_events->push_back({ev, c1});
+      CK(cudaEventRecord(ev, st));
+    }
+    t0 = t1;
   }
   if (launches) *launches += 3 + 2 * static_cast<int>(segs.size()) + static_cast<int>(srcs.size());
   return HSB_OK;
@@ -869,6 +898,17 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   // Host inputs + fused launches: upload B, start U norm and the (UB)^H(UB)
   // half of S, and stage A on the copy stream meanwhile.
   const bool overlap_upload = host_in && !unfused;
+  // INT8 engine + pinned host S: S runs in column groups whose downloads
+  // start as each group is final (events), overlapping the rest of S and H
+  std::vector<std::pair<cudaEvent_t, int64_t>> s_chunks;
+  struct ChunkDel {
+    std::vector<std::pair<cudaEvent_t, int64_t>>& v;
+    ~ChunkDel() {
+      for (auto& c : v) cudaEventDestroy(c.first);
+    }
+  } s_chunks_del{s_chunks};
+  const bool chunk_s = !unfused && ctx->engine == HSB_ENGINE_INT8 && out->location == HSB_LOC_HOST &&
+                       host_is_pinned(out->s);
   int launches = 0;
   Timeline tl;
   HostClock hc;  // host-side phase stamps, printed when HSB_DEBUG_TIMING is set
@@ -1059,6 +1099,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     ZrkCall s1 = tri_call(S, ldo, ng, kLowerOnly | kMirror, 1.0);
     s1.segs.push_back({plain(A, K, ng, K), plain(A, K, ng, K)});
     s1.tl = &tl, s1.sect = "s1", s1.core = "s1_core";
+    if (chunk_s) s1.chunk_events = &s_chunks;
     CKS(run_zrk(ctx, st, s1, &launches));
     CK(tl.mark(st, "s1"));
     CKS(loop1());
@@ -1087,6 +1128,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     s.segs.push_back({plain(A, K, ng, K), plain(A, K, ng, K)});
     s.segs.push_back({plain(UB, K, ng, K), plain(UB, K, ng, K)});
     s.tl = &tl, s.sect = "s", s.core = "s_core";
+    if (chunk_s) s.chunk_events = &s_chunks;
     CKS(run_zrk(ctx, st, s, &launches));
     CK(tl.mark(st, "s"));
   }
@@ -1192,11 +1234,24 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   if (out->location == HSB_LOC_HOST) {
     // S is final at ev_s: its download runs on the copy stream, concurrently
     // with the H contraction; H follows on the compute stream.
-    CK(cudaStreamWaitEvent(cs, ev_s, 0));
     const size_t row = static_cast<size_t>(ng) * 16;
-    CK(ctx->stager.d2h({{out->s, static_cast<size_t>(out->ld) * 16, S, static_cast<size_t>(ldo) * 16, row,
-                         static_cast<size_t>(ng)}},
-                       cs));
+    if (!s_chunks.empty()) {
+      // column groups of S download as soon as each is final
+      int64_t c0 = 0;
+      for (const auto& c : s_chunks) {
+        CK(cudaStreamWaitEvent(cs, c.first, 0));
+        if (c.second > c0)
+          CK(cudaMemcpy2DAsync(reinterpret_cast<char*>(out->s) + c0 * out->ld * 16, out->ld * 16,
+                               reinterpret_cast<const char*>(S) + c0 * ldo * 16, ldo * 16, row, c.second - c0,
+                               cudaMemcpyDeviceToHost, cs));
+        c0 = c.second;
+      }
+    } else {
+      CK(cudaStreamWaitEvent(cs, ev_s, 0));
+      CK(ctx->stager.d2h({{out->s, static_cast<size_t>(out->ld) * 16, S, static_cast<size_t>(ldo) * 16, row,
+                           static_cast<size_t>(ng)}},
+                         cs));
+    }
     if (stream_h) {
       // poll the tile counters; a column block is final when all T tiles that
       // write into it are done (column-major tile order makes this a prefix)

@@ -220,7 +220,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 
 __device__ __forceinline__ void oz_work(const OzGemmParams& p, int w, int& prod, int& slab, int& mod, int& t,
                                         int& tm, int& tn) {
-  t = w % p.ntiles;
+  t = p.tile0 + w % p.ntiles;
   int r = w / p.ntiles;
   mod = r % p.n_mod;
   r /= p.n_mod;
@@ -497,8 +497,8 @@ __device__ __forceinline__ double2 crt_finish(const OzCrtParams& p, const int (&
 // SM.  ONE_SLAB: straight-line code, all 3 x NM loads in flight at once.
 template <int NM, bool ONE_SLAB>
 __global__ void __launch_bounds__(128) ozaki_crt_kernel(const OzCrtParams p) {
-  const int n = blockIdx.y;  // column
-  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = p.n0 + blockIdx.y;  // column
+  const int m = (p.n0 & ~127) + blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= p.n || m < n) return;
   const int t = p.tile_index[(m >> 8) * p.T + (n >> 8)];
   const int8_t* r0 = p.res + static_cast<int64_t>(t) * kOzTileBytes + (n & 255) * 256 + (m & 255);
@@ -625,8 +625,17 @@ cudaError_t launch_ozaki_crt(const OzCrtParams& p, cudaStream_t st) {
   if (p.n <= 0) return cudaSuccess;
   cudaError_t ce = oz_init_once();
   if (ce != cudaSuccess) return ce;
-  if (p.n > 65535) return cudaErrorInvalidConfiguration;
-  const dim3 grid(static_cast<unsigned>((p.n + 127) / 128), static_cast<unsigned>(p.n)), block(128);
+  const int64_t ncols = p.n - p.n0;  // columns n0 .. n-1 unless the caller shrinks gridDim.y
+  return launch_ozaki_crt_cols(p, ncols, st);
+}
+
+cudaError_t launch_ozaki_crt_cols(const OzCrtParams& p, int64_t ncols, cudaStream_t st) {
+  if (ncols <= 0) return cudaSuccess;
+  cudaError_t ce = oz_init_once();
+  if (ce != cudaSuccess) return ce;
+  if (ncols > 65535) return cudaErrorInvalidConfiguration;
+  // rows m >= n0 only: the first row block starts at n0
+  const dim3 grid(static_cast<unsigned>((p.n - (p.n0 & ~127) + 127) / 128), static_cast<unsigned>(ncols)), block(128);
   const bool one = p.nslab == 1;
 #define HSB_OZ_CRT(NMV)                                                        \
   case NMV:                                                                  \

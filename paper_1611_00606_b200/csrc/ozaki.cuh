@@ -65,10 +65,11 @@ struct OzGemmParams {
   int32_t nseg, nslab;
   int32_t n_mod;
   int32_t n;            // output is n x n (triangle)
-  int32_t ntiles;       // entries of tile_list
+  int32_t ntiles;       // tiles of this launch: tile_list[tile0 .. tile0 + ntiles)
+  int32_t tile0;
   const int2* tile_list;  // (tile row, tile col) of the 256 x 256 tiles on or below the diagonal
   int8_t* res;          // residues [prod][slab][modulus][tile][256 x 256 col-major]
-  int64_t mod_stride;   // bytes between moduli (ntiles * kOzTileBytes)
+  int64_t mod_stride;   // bytes between moduli (all tiles of the triangle * kOzTileBytes)
   int64_t slab_stride;  // bytes between slabs (mod_stride * n_mod)
   int64_t prod_stride;  // bytes between products (slab_stride * nslab)
   int32_t* counter;     // work-stealing counter (zeroed by the launcher)
@@ -79,6 +80,7 @@ struct OzCrtParams {
   int64_t mod_stride, slab_stride, prod_stride;
   const int32_t* tile_index;  // T x T: tile_list position of tile (tm, tn), tm >= tn
   int32_t T;                  // tiles per side
+  int32_t n0;                 // first output column of this launch (grid.y columns follow)
   int32_t nslab;
   int32_t n_mod;
   int32_t n;
@@ -99,5 +101,6 @@ cudaError_t launch_ozaki_residues(const double* x, int64_t ldx, int64_t k, int64
                                   int b, int n_mod, int8_t* out, int64_t kpad, cudaStream_t st);
 cudaError_t launch_ozaki_gemm(const OzGemmParams& p, cudaStream_t st);
 cudaError_t launch_ozaki_crt(const OzCrtParams& p, cudaStream_t st);
+cudaError_t launch_ozaki_crt_cols(const OzCrtParams& p, int64_t ncols, cudaStream_t st);
 
 }  // namespace hsb
