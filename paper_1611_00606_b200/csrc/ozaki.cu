@@ -74,14 +74,16 @@ __global__ void ozaki_residue_kernel(const double2* __restrict__ x, int64_t ldx,
   if (k4 >= kpad) return;
   const int64_t plane_stride = static_cast<int64_t>(n_mod) * cols * kpad;
   for (int64_t c = blockIdx.y; c < cols; c += gridDim.y) {
+    // x * 2^(b - e) in two exact power-of-two steps (each factor stays finite)
     const int sh = b - col_exp[c];
+    const double s1 = ldexp(1.0, sh / 2), s2 = ldexp(1.0, sh - sh / 2);
     double xr[4], xi[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       if (k4 + j < k) {
         const double2 v = x[c * ldx + k4 + j];
-        xr[j] = rint(ldexp(v.x, sh));
-        xi[j] = rint(ldexp(v.y, sh));
+        xr[j] = rint((v.x * s1) * s2);
+        xi[j] = rint((v.y * s1) * s2);
       } else {
         xr[j] = xi[j] = 0.0;
       }
