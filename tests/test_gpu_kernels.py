@@ -115,3 +115,20 @@ def test_errors_match_reference_classes():
         run_partitioned(KernelKind.GEMM, (1.0, "X", a, "N", a, 0.0, _cm(rng, 5, 5)))
     with pytest.raises(InputError):
         run_partitioned(KernelKind.POTRF, (a,))
+
+
+@pytest.mark.parametrize("k,n", [(17000, 260), (40000, 130), (9000, 513)])
+def test_int8_engine_long_reductions_use_several_slabs(k, n):
+    # k > 16384 bytes of reduction: the INT8 GEMM splits k into slabs whose
+    # residues are summed in the CRT (C4's H call has three)
+    rng = np.random.default_rng(k + n)
+    z, b = _cm(rng, k, n), _cm(rng, k, n)
+    c = _cm(rng, n, n)
+    want = ok.her2k(1.0, z, b, 0.0, c)
+    run_partitioned(KernelKind.HER2K, (1.0, z, b, 0.0, c), GpuPolicy(engine="int8"))
+    assert rel_frob_error(c, want) < TOL_INT8
+    a = _cm(rng, k, n)
+    c2 = _cm(rng, n, n)
+    want2 = ok.herk(0.5, a, 2.0, c2)
+    run_partitioned(KernelKind.HERK, (0.5, a, 2.0, c2), GpuPolicy(engine="int8"))
+    assert rel_frob_error(c2, want2) < TOL_INT8
