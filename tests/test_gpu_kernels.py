@@ -132,3 +132,25 @@ def test_int8_engine_long_reductions_use_several_slabs(k, n):
     want2 = ok.herk(0.5, a, 2.0, c2)
     run_partitioned(KernelKind.HERK, (0.5, a, 2.0, c2), GpuPolicy(engine="int8"))
     assert rel_frob_error(c2, want2) < TOL_INT8
+
+
+def test_int8_engine_is_column_scale_invariant():
+    # the INT8 engine scales every column to its own exponent, so columns whose
+    # magnitudes differ by 300 orders (and an all-zero column) keep ~2^-40
+    # accuracy relative to sqrt(C_mm C_nn) element by element
+    rng = np.random.default_rng(5)
+    k, n = 700, 300
+    a = _cm(rng, k, n)
+    scale = 10.0 ** rng.uniform(-150, 150, n)
+    a *= scale[None, :]
+    a[:, 7] = 0
+    c = np.zeros((n, n), complex, order="F")
+    want = ok.herk(1.0, a, 0.0, c.copy(order="F"))
+    run_partitioned(KernelKind.HERK, (1.0, a, 0.0, c), GpuPolicy(engine="int8"))
+    want = np.tril(want)
+    got = np.tril(c)
+    d = np.sqrt(np.abs(np.diag(want)))
+    norm = np.outer(d, d)
+    norm[norm == 0] = 1.0
+    assert np.all(got[:, 7] == 0) and np.all(got[7, :] == 0)
+    assert np.max(np.abs(got - want) / norm) < 1e-10
