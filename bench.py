@@ -241,11 +241,14 @@ def main():
         sb = torch.empty_like(hb)
     stream = torch.cuda.current_stream(dev)
 
+    comm_stream = torch.cuda.Stream(device=dev) if world > 1 else None
+
     def step(pol=policy):
-        _, _, split, t, _ = build_hs_device(dp, h, s, pol)
         if world > 1:
-            hsdist.reduce_scatter_block_columns(h, hb)
-            hsdist.reduce_scatter_block_columns(s, sb)
+            # S's reduce-scatter overlaps the H contraction (s_ready event)
+            hsdist.build_hs_sharded_device(dp, h, s, hb, sb, pol, comm_stream=comm_stream)
+            return None
+        _, _, split, t, _ = build_hs_device(dp, h, s, pol)
         return t
 
     def barrier():
@@ -266,6 +269,8 @@ def main():
     ms = hsdist.max_over_ranks(ms, dev)
     value = flops_full / (ms * 1e-3) / 1e12
 
+    if world > 1:  # section timings of this rank's partial build (one synchronous build, untimed)
+        ts = [build_hs_device(dp, h, s, policy)[3]]
     # dominant kernel: the fused H contraction (H1 + H2 + H3 sections), timed
     # alone by CUDA events on the launching stream (timings["h_core"])
     n_nh_local = int(ts[-1]["n_nonhpd"])
@@ -310,7 +315,7 @@ def main():
                               if args.complex_mult == "3m" else "4M: 8 flops per complex MAC = the model"),
                 "model_flops_per_launch": h_flops, "model_tflops": h_flops / h_core / 1e12,
                 "avg_launch_ms": h_core * 1e3}
-    launches = sum(int(t["launches"]) for t in ts)
+    launches = sum(int(t["launches"]) for t in ts) * (args.steps if world > 1 else 1)
     traffic = None
     prof = ROOT / "profiles" / "roofline_traffic.json"
     if prof.exists():

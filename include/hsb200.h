@@ -175,6 +175,12 @@ typedef struct {
   int64_t ld;
   double* h;
   double* s;
+  /* Optional cudaEvent_t, recorded on the stream as soon as S is final (before
+   * the H contraction), so a caller can start consuming S -- e.g. its
+   * reduce-scatter -- while H computes.  With device inputs, device outputs
+   * and timings == NULL, hsb_build_hs returns without waiting for the device
+   * (the work completes in stream order). */
+  void* s_ready;
 } hsb_output;
 
 /* Section timings (seconds, from CUDA events) in the reference's section

@@ -49,7 +49,7 @@ class HsbProblem(ctypes.Structure):
 
 class HsbOutput(ctypes.Structure):
     _fields_ = [("location", ctypes.c_int32), ("reserved", ctypes.c_int32), ("ld", ctypes.c_int64),
-                ("h", _P), ("s", _P)]
+                ("h", _P), ("s", _P), ("s_ready", _P)]
 
 
 class HsbTimings(ctypes.Structure):
@@ -108,7 +108,7 @@ def load():
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.hsb_abi_version() != 2:
+        if lib.hsb_abi_version() != 3:
             raise RuntimeError("libhsb200.so ABI version mismatch; rebuild it")
         _lib = lib
         return lib

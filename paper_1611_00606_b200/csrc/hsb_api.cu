@@ -644,7 +644,7 @@ OperandView atom_mats(const double* base, int64_t n_atoms, int64_t n_l) {
 // =============================================================================
 extern "C" {
 
-int32_t hsb_abi_version(void) { return 2; }
+int32_t hsb_abi_version(void) { return 3; }
 
 hsb_status hsb_ctx_create(int32_t device, hsb_ctx** out) {
   hsb_ctx* ctx = nullptr;
@@ -1136,6 +1136,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   CK(cudaEventCreateWithFlags(&ev_s, cudaEventDisableTiming));
   EvDel ev_s_del{ev_s};
   CK(cudaEventRecord(ev_s, st));
+  if (out->s_ready) CK(cudaEventRecord(static_cast<cudaEvent_t>(out->s_ready), st));
 
   // ------------------------------------------- routing (host, overlaps S)
   hc.mark("enqueue to S");
@@ -1293,6 +1294,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   CK(cudaStreamWaitEvent(st, ev_cs, 0));
   CK(tl.mark(st, "d2h"));
   hc.mark("enqueue H + d2h");
+  if (!tm && !host_in && out->location == HSB_LOC_DEVICE) return HSB_OK;  // asynchronous: stream order
   CK(cudaEventSynchronize(tl.marks.back().second));
   hc.mark("final sync");
   hc.report();

@@ -151,6 +151,30 @@ def build_hs_sharded(p, policy=None, group=None, partial=None) -> ShardedResult:
     return ShardedResult(hb, sb, rank * (ncols // world), n_g, int(c[0]), int(c[1]), timings)
 
 
+def build_hs_sharded_device(dp, h, s, hb, sb, policy=None, group=None, comm_stream=None):
+    """One atom-sharded step on device-resident inputs with S's reduce-scatter
+    overlapping the H contraction: the library records an event when S is
+    final, a communication stream waits on it and reduce-scatters S while the
+    compute stream runs Loop 2 and H; H's reduce-scatter follows on the
+    compute stream.  ``dp`` holds this rank's atoms; h, s are (ncols, n_g)
+    partial buffers, hb, sb this rank's (ncols / world, n_g) column blocks."""
+    import torch
+
+    from .pipeline import build_hs_device
+
+    dev = h.device
+    compute = torch.cuda.current_stream(dev)
+    comm = comm_stream if comm_stream is not None else torch.cuda.Stream(device=dev)
+    s_ready = torch.cuda.Event()
+    build_hs_device(dp, h, s, policy, s_ready=s_ready, wait=False)
+    with torch.cuda.stream(comm):
+        comm.wait_event(s_ready)
+        reduce_scatter_block_columns(s, sb, group)
+    reduce_scatter_block_columns(h, hb, group)
+    compute.wait_stream(comm)
+    return hb, sb
+
+
 def kpoint_assignment(n_kpoints: int, world: int, rank: int) -> list[int]:
     """k-points handled by ``rank`` (round robin, no communication)."""
     return list(range(rank, n_kpoints, world))

@@ -188,15 +188,16 @@ def _host_problem(p):
     return prob, (blocks, arrays)
 
 
-def _call_build(pol, prob, out, stream, force_nonhpd, n_a, slot: int = 0):
+def _call_build(pol, prob, out, stream, force_nonhpd, n_a, slot: int = 0, wait: bool = True):
     lib = _lib.load()
     ctx = _lib.context(pol.device, pol.complex_mult, pol.engine, pol.int8_bits, slot)
     opts = (_lib.HSB_OPT_FORCE_NONHPD if force_nonhpd else 0) | (0 if pol.fused else _lib.HSB_OPT_UNFUSED)
     tim = _lib.HsbTimings()
     info = (ctypes.c_int32 * n_a)()
+    # no timings -> the library returns without waiting (device in/out only)
     _lib.check(lib.hsb_build_hs(ctx, stream, ctypes.byref(prob), opts, ctypes.byref(out),
-                                ctypes.byref(tim), info), ctx)
-    return tim, list(info)
+                                ctypes.byref(tim) if wait else None, info if wait else None), ctx)
+    return (tim, list(info)) if wait else (None, None)
 
 
 def build_hs(p, policy=None, force_nonhpd: bool = False) -> BuildOutput:
@@ -353,12 +354,15 @@ class DeviceProblem:
 
 
 def build_hs_device(dp: DeviceProblem, h=None, s=None, policy=None, force_nonhpd: bool = False,
-                    stream=None):
+                    stream=None, s_ready=None, wait: bool = True):
     """Device-resident build: returns (H, S, SplitCounts, timings, atom_info).
 
     H and S are torch complex128 (n_g, n_g) tensors holding the column-major
     matrices (i.e. ``H.T`` is the matrix; for Hermitian H this equals
-    ``H.conj()``).  Inputs are not modified.
+    ``H.conj()``).  Inputs are not modified.  ``s_ready`` (a torch.cuda.Event)
+    is recorded on the stream as soon as S is final.  With ``wait=False`` the
+    call returns once the work is enqueued (split counts, timings and atom
+    info are then None); the results are ready in stream order.
     """
     import torch
 
@@ -391,7 +395,12 @@ def build_hs_device(dp: DeviceProblem, h=None, s=None, policy=None, force_nonhpd
     out.location = _lib.HSB_LOC_DEVICE
     out.ld = n_g
     out.h, out.s = h.data_ptr(), s.data_ptr()
+    if s_ready is not None:
+        s_ready.record(torch.cuda.current_stream(dev))  # materialise the CUDA event
+        out.s_ready = s_ready.cuda_event
     if stream is None:
         stream = torch.cuda.current_stream(dev)
-    tim, info = _call_build(pol, prob, out, ctypes.c_void_p(stream.cuda_stream), force_nonhpd, n_a)
+    tim, info = _call_build(pol, prob, out, ctypes.c_void_p(stream.cuda_stream), force_nonhpd, n_a, wait=wait)
+    if not wait:
+        return h, s, None, None, None
     return h, s, SplitCounts(tim.n_hpd, tim.n_nonhpd), _timings_dict(tim), info
