@@ -367,7 +367,9 @@ def main():
             # contexts/streams overlap one step's PCIe transfers with the next
             # step's kernels (every step still uploads its inputs and downloads
             # its H and S inside the timed region)
-            depth = 2
+            # a second context doubles the device workspace: pipeline only when it fits
+            free, _total = torch.cuda.mem_get_info(dev)
+            depth = 2 if free > 1.2 * torch.cuda.memory_reserved(dev) + 0.5 * _total else 1
             for o in iter_hs_kpoints([p] * (depth + 2), policy, depth=depth):
                 del o  # warm the second context and the pinned-output cache (depth + 1 in flight)
             t0 = time.perf_counter()
@@ -387,7 +389,7 @@ def main():
                "inputs": "pageable numpy" if args.pageable_inputs else "pinned numpy (pin_instance)",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
         if world == 1:
-            e2e.update({"api": "iter_hs_kpoints(steps x instance, depth=2): host wall time per step",
+            e2e.update({"api": f"iter_hs_kpoints(steps x instance, depth={depth}): host wall time per step",
                         "single_call_ms_per_step": single_ms,
                         "single_call_value": flops_full / (single_ms * 1e-3) / 1e12})
 
