@@ -191,6 +191,9 @@ def main():
     ap.add_argument("--engine", default="int8", choices=["int8", "dmma"],
                     help="S/H contractions on the INT8 tensor cores (CRT emulation, ~1e-12) or FP64 DMMA")
     ap.add_argument("--no-compare", action="store_true", help="skip the second-engine measurement")
+    ap.add_argument("--rs", default="nccl", choices=["nccl", "fused"],
+                    help="N > 1: NCCL reduce-scatter (S overlapped with H) or the fused scatter from the "
+                         "reconstruction epilogue into CUDA-IPC peer slots (INT8 engine)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-ng", type=int, default=4000)
@@ -242,8 +245,12 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     comm_stream = torch.cuda.Stream(device=dev) if world > 1 else None
+    slots = hsdist.PeerSlots.group(n_g, dev) if world > 1 and args.rs == "fused" else None
 
     def step(pol=policy):
+        if world > 1 and slots is not None and pol.engine == "int8":
+            hsdist.build_hs_sharded_fused(dp, slots, pol)
+            return None
         if world > 1:
             # S's reduce-scatter overlaps the H contraction (s_ready event)
             hsdist.build_hs_sharded_device(dp, h, s, hb, sb, pol, comm_stream=comm_stream)
@@ -409,7 +416,8 @@ def main():
             "data": "synthetic (seeded hsgen-compatible generator)",
             "config": {"workload": args.config, "desc": CONFIG_DESC[args.config], "n_atoms": dims.n_atoms,
                        "n_l": dims.n_l, "n_g": dims.n_g, "nonhpd_fraction": args.nonhpd_fraction,
-                       "parallelism": f"atom-shard x{world}" + (" + reduce-scatter" if world > 1 else ""),
+                       "parallelism": f"atom-shard x{world}" + ((" + fused peer scatter" if args.rs == "fused" else
+                                                                      " + NCCL reduce-scatter") if world > 1 else ""),
                        "fused": not args.unfused, "engine": args.engine, "complex_mult": args.complex_mult, "model_tflop_per_step": flops_full / 1e12,
                        "l2_note": "inputs larger than L2 (A/B stacks 496 MB each at C3)"},
             "gpu_launches": launches,

@@ -166,6 +166,28 @@ typedef struct {
                                       mirror last) instead of the fused
                                       H and S launches */
 
+/* Receive slots of an atom-sharded build across n_ranks GPUs (north star (3);
+ * SURVEY 8f row 2).  Rank q owns columns [q * cols_per_rank, (q + 1) *
+ * cols_per_rank) of H and S and a receive buffer of n_ranks slots, each
+ * cols_per_rank columns x ld rows of complex128 (column-major): slot r holds
+ * rank r's partial sum for q's columns.  h_slots / s_slots are DEVICE arrays
+ * of n_ranks device pointers (peer pointers from hsb_ipc_open, or local ones
+ * when the "ranks" share a device). */
+typedef struct hsb_peer_out {
+  int32_t n_ranks;
+  int32_t rank;
+  int64_t cols_per_rank;
+  int64_t ld;
+  double* const* h_slots;
+  double* const* s_slots;
+} hsb_peer_out;
+
+/* CUDA IPC for the receive slots: a 64-byte handle of a device allocation,
+ * and its mapping in another process (cudaIpcGetMemHandle / OpenMemHandle). */
+HSB_API hsb_status hsb_ipc_handle(hsb_ctx* ctx, void* dev_ptr, uint8_t handle[64]);
+HSB_API hsb_status hsb_ipc_open(hsb_ctx* ctx, const uint8_t handle[64], void** dev_ptr);
+HSB_API hsb_status hsb_ipc_close(hsb_ctx* ctx, void* dev_ptr);
+
 typedef struct {
   /* Output location: HSB_LOC_HOST -> h/s are host pointers,
    * HSB_LOC_DEVICE -> device pointers.  Both n_g x n_g column-major complex128,
@@ -175,6 +197,11 @@ typedef struct {
   int64_t ld;
   double* h;
   double* s;
+  /* Optional (INT8 engine, fused, device outputs): scatter this rank's partial
+   * H and S straight into the owners' receive slots (hsb_peer_out) from the
+   * reconstruction epilogue, instead of writing h / s.  The reduce-scatter of
+   * an atom-sharded build then only sums each owner's slots. */
+  const struct hsb_peer_out* peer;
   /* Optional cudaEvent_t, recorded on the stream as soon as S is final (before
    * the H contraction), so a caller can start consuming S -- e.g. its
    * reduce-scatter -- while H computes.  With device inputs, device outputs

@@ -47,9 +47,14 @@ class HsbProblem(ctypes.Structure):
     ]
 
 
+class HsbPeerOut(ctypes.Structure):
+    _fields_ = [("n_ranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("cols_per_rank", ctypes.c_int64),
+                ("ld", ctypes.c_int64), ("h_slots", _P), ("s_slots", _P)]
+
+
 class HsbOutput(ctypes.Structure):
     _fields_ = [("location", ctypes.c_int32), ("reserved", ctypes.c_int32), ("ld", ctypes.c_int64),
-                ("h", _P), ("s", _P), ("s_ready", _P)]
+                ("h", _P), ("s", _P), ("peer", ctypes.POINTER(HsbPeerOut)), ("s_ready", _P)]
 
 
 class HsbTimings(ctypes.Structure):
@@ -95,6 +100,9 @@ def load():
             "hsb_ctx_trim": (i32, [_P]),
             "hsb_ctx_set_complex_mult": (i32, [_P, i32]),
             "hsb_ctx_set_engine": (i32, [_P, i32, i32]),
+            "hsb_ipc_handle": (i32, [_P, _P, ctypes.c_char_p]),
+            "hsb_ipc_open": (i32, [_P, ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]),
+            "hsb_ipc_close": (i32, [_P, _P]),
             "hsb_zherk": (i32, [_P, _P, i64, i64, dbl, _P, i64, dbl, _P, i64, u32]),
             "hsb_zher2k": (i32, [_P, _P, i64, i64, dbl, dbl, _P, i64, _P, i64, dbl, _P, i64, u32]),
             "hsb_zgemm": (i32, [_P, _P, ch, ch, i64, i64, i64, dbl, dbl, _P, i64, _P, i64, dbl, dbl,
@@ -108,7 +116,7 @@ def load():
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.hsb_abi_version() != 3:
+        if lib.hsb_abi_version() != 4:
             raise RuntimeError("libhsb200.so ABI version mismatch; rebuild it")
         _lib = lib
         return lib

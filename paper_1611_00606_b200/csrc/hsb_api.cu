@@ -250,6 +250,9 @@ struct ZrkCall {
   // optional (INT8 engine): run in column groups and record, after each, an
   // event and the end column of the columns that are final
   std::vector<std::pair<cudaEvent_t, int64_t>>* chunk_events = nullptr;
+  // optional (INT8 engine): scatter the result into peer receive slots
+  const hsb_peer_out* peer = nullptr;
+  bool peer_is_h = false;
 };
 
 // Lower-triangle tile order for the persistent 3M kernel.  The 148 CTAs run
@@ -459,6 +462,16 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
   cp.c = z.c;
   cp.ldc = z.ldc;
   cp.flags = z.flags;
+  cp.peer = nullptr;
+  cp.P = cp.rank = 0;
+  cp.cpr = cp.pld = 0;
+  if (z.peer) {
+    cp.peer = reinterpret_cast<double2* const*>(z.peer_is_h ? z.peer->h_slots : z.peer->s_slots);
+    cp.P = z.peer->n_ranks;
+    cp.rank = z.peer->rank;
+    cp.cpr = z.peer->cols_per_rank;
+    cp.pld = z.peer->ld;
+  }
 
   // With a host download waiting on per-column counters (done_cnt), the
   // product runs in column groups of 6 tiles (contiguous in the tile list):
@@ -501,6 +514,8 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
 }
 
 hsb_status run_zrk(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launches) {
+  if (z.peer && !(ctx->engine == HSB_ENGINE_INT8 && z.triangle && z.batch == 1 && z.m == z.n))
+    return fail(ctx, HSB_ERR_UNSUPPORTED, "peer output needs the INT8 engine on a triangle call");
   if (ctx->engine == HSB_ENGINE_INT8 && z.triangle && z.batch == 1 && z.m == z.n && z.m > 0) {
     bool plain = true;
     for (const Seg& s : z.segs) plain = plain && s.l.batch == 1 && s.r.batch == 1;
@@ -644,7 +659,7 @@ OperandView atom_mats(const double* base, int64_t n_atoms, int64_t n_l) {
 // =============================================================================
 extern "C" {
 
-int32_t hsb_abi_version(void) { return 3; }
+int32_t hsb_abi_version(void) { return 4; }
 
 hsb_status hsb_ctx_create(int32_t device, hsb_ctx** out) {
   hsb_ctx* ctx = nullptr;
@@ -705,6 +720,32 @@ hsb_status hsb_ctx_set_engine(hsb_ctx* ctx, int32_t engine, int32_t min_bits) {
     return fail(ctx, HSB_ERR_INPUT, "min_bits must be 0 (default 40) or in [30, 48]");
   ctx->engine = engine;
   ctx->oz_min_bits = min_bits ? min_bits : 40;
+  return HSB_OK;
+}
+
+hsb_status hsb_ipc_handle(hsb_ctx* ctx, void* dev_ptr, uint8_t handle[64]) {
+  if (!ctx || !dev_ptr || !handle) return fail(ctx, HSB_ERR_INPUT, "NULL argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "CUDA IPC handle size");
+  cudaSetDevice(ctx->device);
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, dev_ptr));
+  std::memcpy(handle, &h, 64);
+  return HSB_OK;
+}
+
+hsb_status hsb_ipc_open(hsb_ctx* ctx, const uint8_t handle[64], void** dev_ptr) {
+  if (!ctx || !dev_ptr || !handle) return fail(ctx, HSB_ERR_INPUT, "NULL argument");
+  cudaSetDevice(ctx->device);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  CK(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return HSB_OK;
+}
+
+hsb_status hsb_ipc_close(hsb_ctx* ctx, void* dev_ptr) {
+  if (!ctx || !dev_ptr) return fail(ctx, HSB_ERR_INPUT, "NULL argument");
+  cudaSetDevice(ctx->device);
+  CK(cudaIpcCloseMemHandle(dev_ptr));
   return HSB_OK;
 }
 
@@ -882,7 +923,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   const int64_t na = p->n_atoms, nl = p->n_l, ng = p->n_g;
   if (na < 1 || nl < 1 || ng < 1) return fail(ctx, HSB_ERR_INPUT, "dimensions must be positive");
   if (out->ld < ng) return fail(ctx, HSB_ERR_DIMENSION, "output leading dimension < n_g");
-  if (!out->h || !out->s) return fail(ctx, HSB_ERR_INPUT, "output pointers are NULL");
+  if (!out->peer && (!out->h || !out->s)) return fail(ctx, HSB_ERR_INPUT, "output pointers are NULL");
   if (na > 65535) return fail(ctx, HSB_ERR_UNSUPPORTED, "more than 65535 atoms");
   const int64_t K = na * nl;
   if (K > (int64_t{1} << 31)) return fail(ctx, HSB_ERR_UNSUPPORTED, "stack too tall");
@@ -898,6 +939,14 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   // Host inputs + fused launches: upload B, start U norm and the (UB)^H(UB)
   // half of S, and stage A on the copy stream meanwhile.
   const bool overlap_upload = host_in && !unfused;
+  const hsb_peer_out* peer = out->peer;
+  if (peer) {
+    if (unfused || ctx->engine != HSB_ENGINE_INT8 || out->location != HSB_LOC_DEVICE)
+      return fail(ctx, HSB_ERR_UNSUPPORTED, "peer output needs the fused INT8 engine and device outputs");
+    if (peer->n_ranks < 1 || peer->rank < 0 || peer->rank >= peer->n_ranks || peer->ld < ng ||
+        peer->cols_per_rank * peer->n_ranks < ng || !peer->h_slots || !peer->s_slots)
+      return fail(ctx, HSB_ERR_INPUT, "inconsistent hsb_peer_out");
+  }
   // INT8 engine + pinned host S: S runs in column groups whose downloads
   // start as each group is final (events), overlapping the rest of S and H
   std::vector<std::pair<cudaEvent_t, int64_t>> s_chunks;
@@ -1129,6 +1178,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     s.segs.push_back({plain(UB, K, ng, K), plain(UB, K, ng, K)});
     s.tl = &tl, s.sect = "s", s.core = "s_core";
     if (chunk_s) s.chunk_events = &s_chunks;
+    s.peer = peer;
     CKS(run_zrk(ctx, st, s, &launches));
     CK(tl.mark(st, "s"));
   }
@@ -1213,6 +1263,8 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     if (n_hpd > 0) h.segs.push_back({plain(Y, k_hpd, ng, K), plain(Y, k_hpd, ng, K)});
     if (n_nh > 0) h.segs.push_back({plain(ANH, k_nh, ng, k_nh), plain(XNH, k_nh, ng, K)});
     h.tl = &tl, h.sect = "h", h.core = "h_core";
+    h.peer = peer;
+    h.peer_is_h = true;
     if (stream_h) {  // per-column-block completion counters in mapped host memory
       const size_t nb = static_cast<size_t>(ntiles);
       if (ctx->done_cnt_len < nb) {

@@ -527,6 +527,17 @@ __global__ void __launch_bounds__(128) ozaki_crt_kernel(const OzCrtParams p) {
     }
   }
   const double2 v = crt_finish<NM>(p, P, Q, W, m, n);
+  if (p.peer) {
+    // fused scatter: write straight into the owning rank's receive slot (NVLink
+    // peer memory); the owner only sums its slots afterwards
+    const int qn = static_cast<int>(n / p.cpr);
+    p.peer[qn][(p.rank * p.cpr + (n - qn * p.cpr)) * p.pld + m] = v;
+    if ((p.flags & kMirror) && m > n) {
+      const int qm = static_cast<int>(m / p.cpr);
+      p.peer[qm][(p.rank * p.cpr + (m - qm * p.cpr)) * p.pld + n] = make_double2(v.x, -v.y);
+    }
+    return;
+  }
   double2* C = reinterpret_cast<double2*>(p.c);
   C[m + static_cast<int64_t>(n) * p.ldc] = v;
   if ((p.flags & kMirror) && m > n) C[n + static_cast<int64_t>(m) * p.ldc] = make_double2(v.x, -v.y);

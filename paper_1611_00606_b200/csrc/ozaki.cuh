@@ -92,6 +92,11 @@ struct OzCrtParams {
   double* c;                 // interleaved complex128, column-major
   int64_t ldc;
   uint32_t flags;            // kLowerOnly | kMirror | kZeroImagDiag (zrk.cuh)
+  // peer output (hsb_peer_out): element (m, n) goes to slot `rank` of the owner of
+  // column n: peer[n / cpr] + ((rank * cpr + n % cpr) * pld + m), instead of c
+  double2* const* peer;
+  int32_t P, rank;
+  int64_t cpr, pld;
 };
 
 cudaError_t launch_ozaki_colexp(const double* x, int64_t ldx, int64_t k, int64_t cols, int32_t* exp_out,

@@ -175,6 +175,132 @@ def build_hs_sharded_device(dp, h, s, hb, sb, policy=None, group=None, comm_stre
     return hb, sb
 
 
+class PeerSlots:
+    """Receive slots for the fused reduce-scatter (hsb_peer_out).
+
+    Rank q owns columns [q * cols, (q + 1) * cols) and holds ``h_recv`` and
+    ``s_recv``: (n_ranks, cols, n_g) complex128 tensors; slot r receives rank
+    r's partial H / S for those columns, written over NVLink by rank r's
+    reconstruction epilogue (the INT8 engine's CRT kernel stores each
+    element straight into its owner's slot).  After every rank's build has
+    completed, the owner's block is the sum of its slots (``finish``).
+
+    ``PeerSlots.group(...)`` wires real ranks (one process per GPU: CUDA IPC
+    handles exchanged through torch.distributed); ``PeerSlots.emulated(...)``
+    wires several "ranks" inside one process on one device (tests).
+    """
+
+    def __init__(self, n_ranks, rank, cols, n_g, h_recv, s_recv, h_ptrs, s_ptrs, opened=()):
+        import torch
+
+        self.n_ranks, self.rank, self.cols, self.n_g = n_ranks, rank, cols, n_g
+        self.h_recv, self.s_recv = h_recv, s_recv
+        dev = h_recv.device
+        self._h_tab = torch.tensor(h_ptrs, dtype=torch.int64, device=dev)
+        self._s_tab = torch.tensor(s_ptrs, dtype=torch.int64, device=dev)
+        self._opened = list(opened)
+
+    @staticmethod
+    def alloc(n_ranks, n_g, device):
+        import torch
+
+        cols = -(-n_g // n_ranks)
+        shape = (n_ranks, cols, n_g)
+        return (torch.zeros(shape, dtype=torch.complex128, device=device),
+                torch.zeros(shape, dtype=torch.complex128, device=device), cols)
+
+    @classmethod
+    def emulated(cls, n_ranks, n_g, device):
+        """All ranks in this process: returns one PeerSlots per rank."""
+        bufs = [cls.alloc(n_ranks, n_g, device) for _ in range(n_ranks)]
+        hp = [b[0].data_ptr() for b in bufs]
+        sp = [b[1].data_ptr() for b in bufs]
+        return [cls(n_ranks, r, bufs[r][2], n_g, bufs[r][0], bufs[r][1], hp, sp) for r in range(n_ranks)]
+
+    @classmethod
+    def group(cls, n_g, device, group=None):
+        """One process per GPU: allocate this rank's slots, exchange CUDA IPC
+        handles with every rank of ``group`` and open the peers' slots."""
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import _lib
+
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        h_recv, s_recv, cols = cls.alloc(world, n_g, device)
+        lib = _lib.load()
+        ctx = _lib.context(device.index if device.index is not None else 0)
+
+        def handle(t):
+            buf = ctypes.create_string_buffer(64)
+            _lib.check(lib.hsb_ipc_handle(ctx, ctypes.c_void_p(t.data_ptr()), buf), ctx)
+            return buf.raw
+
+        mine = (handle(h_recv), handle(s_recv))
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        hp, sp, opened = [], [], []
+        for q, (hh, sh) in enumerate(allh):
+            if q == rank:
+                hp.append(h_recv.data_ptr())
+                sp.append(s_recv.data_ptr())
+                continue
+            for raw, lst in ((hh, hp), (sh, sp)):
+                ptr = ctypes.c_void_p()
+                _lib.check(lib.hsb_ipc_open(ctx, raw, ctypes.byref(ptr)), ctx)
+                lst.append(ptr.value)
+                opened.append(ptr.value)
+        return cls(world, rank, cols, n_g, h_recv, s_recv, hp, sp, opened)
+
+    def struct(self):
+        from . import _lib
+
+        st = _lib.HsbPeerOut()
+        st.n_ranks, st.rank, st.cols_per_rank, st.ld = self.n_ranks, self.rank, self.cols, self.n_g
+        st.h_slots, st.s_slots = self._h_tab.data_ptr(), self._s_tab.data_ptr()
+        return st
+
+    def finish(self, hb=None, sb=None):
+        """This rank's column blocks (cols, n_g) = sums of its receive slots.
+        Call once every rank's build has completed (e.g. after a barrier)."""
+        import torch
+
+        hb = torch.sum(self.h_recv, dim=0) if hb is None else torch.sum(self.h_recv, dim=0, out=hb)
+        sb = torch.sum(self.s_recv, dim=0) if sb is None else torch.sum(self.s_recv, dim=0, out=sb)
+        return hb, sb
+
+    def close(self):
+        import ctypes
+
+        from . import _lib
+
+        if not self._opened:
+            return
+        lib = _lib.load()
+        ctx = _lib.context(self.h_recv.device.index or 0)
+        for ptr in self._opened:
+            lib.hsb_ipc_close(ctx, ctypes.c_void_p(ptr))
+        self._opened = []
+
+
+def build_hs_sharded_fused(dp, slots: "PeerSlots", policy=None, group=None):
+    """Atom-sharded step with the fused reduce-scatter: this rank's partial H
+    and S go straight from the reconstruction epilogue into the owners' slots
+    (no NCCL collective on the data path); a barrier, then each owner sums
+    its slots.  Returns this rank's (cols, n_g) blocks of H and S."""
+    import torch
+    import torch.distributed as dist
+
+    from .pipeline import build_hs_device
+
+    build_hs_device(dp, policy=policy, peer=slots, wait=False)
+    torch.cuda.current_stream(slots.h_recv.device).synchronize()
+    if dist.is_initialized():
+        dist.barrier(group=group)
+    return slots.finish()
+
+
 def kpoint_assignment(n_kpoints: int, world: int, rank: int) -> list[int]:
     """k-points handled by ``rank`` (round robin, no communication)."""
     return list(range(rank, n_kpoints, world))

@@ -354,7 +354,7 @@ class DeviceProblem:
 
 
 def build_hs_device(dp: DeviceProblem, h=None, s=None, policy=None, force_nonhpd: bool = False,
-                    stream=None, s_ready=None, wait: bool = True):
+                    stream=None, s_ready=None, wait: bool = True, peer=None):
     """Device-resident build: returns (H, S, SplitCounts, timings, atom_info).
 
     H and S are torch complex128 (n_g, n_g) tensors holding the column-major
@@ -362,7 +362,9 @@ def build_hs_device(dp: DeviceProblem, h=None, s=None, policy=None, force_nonhpd
     ``H.conj()``).  Inputs are not modified.  ``s_ready`` (a torch.cuda.Event)
     is recorded on the stream as soon as S is final.  With ``wait=False`` the
     call returns once the work is enqueued (split counts, timings and atom
-    info are then None); the results are ready in stream order.
+    info are then None); the results are ready in stream order.  ``peer``
+    (distributed.PeerSlots) scatters this rank's partial H and S into the
+    owners' receive slots instead of h and s (INT8 engine).
     """
     import torch
 
@@ -377,14 +379,15 @@ def build_hs_device(dp: DeviceProblem, h=None, s=None, policy=None, force_nonhpd
         tns = getattr(dp, name)
         if tuple(tns.shape) != shape or tns.dtype != dtype or not tns.is_contiguous() or tns.device != dev:
             raise InputError(f"{name} must be a contiguous {dtype} tensor of shape {shape} on {dev}")
-    if h is None:
-        h = torch.empty((n_g, n_g), dtype=torch.complex128, device=dev)
-    if s is None:
-        s = torch.empty((n_g, n_g), dtype=torch.complex128, device=dev)
-    for name, t in (("h", h), ("s", s)):
-        if t.dtype != torch.complex128 or t.dim() != 2 or t.shape[1] != n_g or t.shape[0] < n_g \
-                or not t.is_contiguous() or t.device != dev:
-            raise InputError(f"{name} must be a contiguous complex128 tensor of shape (>= {n_g}, {n_g})")
+    if peer is None:
+        if h is None:
+            h = torch.empty((n_g, n_g), dtype=torch.complex128, device=dev)
+        if s is None:
+            s = torch.empty((n_g, n_g), dtype=torch.complex128, device=dev)
+        for name, t in (("h", h), ("s", s)):
+            if t.dtype != torch.complex128 or t.dim() != 2 or t.shape[1] != n_g or t.shape[0] < n_g \
+                    or not t.is_contiguous() or t.device != dev:
+                raise InputError(f"{name} must be a contiguous complex128 tensor of shape (>= {n_g}, {n_g})")
     prob = _lib.HsbProblem()
     prob.n_atoms, prob.n_l, prob.n_g = n_a, n_l, n_g
     prob.location = _lib.HSB_LOC_DEVICE
@@ -394,10 +397,14 @@ def build_hs_device(dp: DeviceProblem, h=None, s=None, policy=None, force_nonhpd
     out = _lib.HsbOutput()
     out.location = _lib.HSB_LOC_DEVICE
     out.ld = n_g
-    out.h, out.s = h.data_ptr(), s.data_ptr()
+    out.h = h.data_ptr() if peer is None else None
+    out.s = s.data_ptr() if peer is None else None
     if s_ready is not None:
         s_ready.record(torch.cuda.current_stream(dev))  # materialise the CUDA event
         out.s_ready = s_ready.cuda_event
+    if peer is not None:
+        peer_struct = peer.struct()
+        out.peer = ctypes.pointer(peer_struct)
     if stream is None:
         stream = torch.cuda.current_stream(dev)
     tim, info = _call_build(pol, prob, out, ctypes.c_void_p(stream.cuda_stream), force_nonhpd, n_a, wait=wait)
