@@ -76,7 +76,7 @@ HSB_API hsb_status hsb_ctx_set_complex_mult(hsb_ctx* ctx, int32_t algo);
  *   (tcgen05.mma kind::i8) by the Chinese-remainder / Ozaki-II scheme:
  *   operands rounded to min_bits-bit integers per column (relative error
  *   ~2^-min_bits of each column's max), then exact modular INT8 products and
- *   CRT reconstruction.  min_bits = 0 selects the default 40 (~1e-12 relative
+ *   CRT reconstruction.  min_bits = 0 selects the default 39 (~3e-12 relative
  *   Frobenius; the north star's bound is 1e-10).  Batched per-atom products
  *   (Loop 1 / Loop 2) and rectangular GEMMs always use DMMA. */
 #define HSB_ENGINE_DMMA 0

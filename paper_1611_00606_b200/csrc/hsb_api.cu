@@ -60,7 +60,7 @@ struct hsb_ctx {
   int64_t tile_list_T = 0;             // tile rows of the cached grouped triangle order
   std::vector<int2> tile_list_host;    // its host copy (source of an async upload)
   int32_t engine = HSB_ENGINE_DMMA;    // triangle contractions: FP64 DMMA or INT8 CRT emulation
-  int32_t oz_min_bits = 40;            // INT8 engine: operand integer bits (accuracy ~2^-bits)
+  int32_t oz_min_bits = 39;            // INT8 engine: operand integer bits (accuracy ~2^-bits)
   int64_t oz_tiles_n = 0;              // cached INT8-engine tile list (n of the output)
   std::vector<int2> oz_tiles_host;
   std::vector<int32_t> oz_tile_index_host;
@@ -344,13 +344,16 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
       ktot += s.l.k;
     }
   if (segs.size() > static_cast<size_t>(kOzMaxSeg)) return fail(ctx, HSB_ERR_UNSUPPORTED, "too many segments");
-  // moduli: the fewest with b >= oz_min_bits, where |Re'|,|Im'| <= 3 K 2^2b < M/2
+  // moduli: the fewest with b >= oz_min_bits.  With |x'| + |y'| <= 2^b per
+  // element, |Re'| = |sum x'x' + y'y'| and |Im'| = |sum x'_L y'_R - y'_L x'_R|
+  // are both <= K 2^2b; the explicit CRT needs |X| < M/2, kept with one bit of
+  // margin: 2b <= log2 M - 2 - log2 K.
   int n_mod = 0, b = 0;
   {
     double log2m = 0;
     for (int i = 0; i < kOzMaxMod; ++i) {
       log2m += std::log2(static_cast<double>(oz_mod(i)));
-      const int bi = static_cast<int>(std::floor((log2m - 2.0 - std::log2(3.0 * std::max<int64_t>(ktot, 1))) / 2.0)) - 1;
+      const int bi = static_cast<int>(std::floor((log2m - 2.0 - std::log2(static_cast<double>(std::max<int64_t>(ktot, 1)))) / 2.0));
       if (i + 1 >= 11 && (bi >= ctx->oz_min_bits || i + 1 == kOzMaxMod)) {
         n_mod = i + 1;
         b = std::min(bi, ctx->oz_min_bits + 4);
@@ -719,7 +722,7 @@ hsb_status hsb_ctx_set_engine(hsb_ctx* ctx, int32_t engine, int32_t min_bits) {
   if (min_bits != 0 && (min_bits < 30 || min_bits > 48))
     return fail(ctx, HSB_ERR_INPUT, "min_bits must be 0 (default 40) or in [30, 48]");
   ctx->engine = engine;
-  ctx->oz_min_bits = min_bits ? min_bits : 40;
+  ctx->oz_min_bits = min_bits ? min_bits : 39;
   return HSB_OK;
 }
 

@@ -15,18 +15,19 @@ from __future__ import annotations
 import math
 
 MODULI = (256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193)
-DEFAULT_BITS = 40
+DEFAULT_BITS = 39
 
 
 def int8_moduli(k_total: int, min_bits: int = 0) -> tuple[int, int]:
     """(n_mod, b): the fewest moduli (>= 11) such that the integer bits
-    b = floor((log2 M - 2 - log2(3 K)) / 2) - 1 reach ``min_bits``
-    (|Re'|, |Im'| <= 3 K 2^(2b) must stay below M / 16)."""
+    b = floor((log2 M - 2 - log2 K) / 2) reach ``min_bits``: with
+    |x'| + |y'| <= 2^b per element, |Re'| and |Im'| are <= K 2^(2b), which must
+    stay below M / 2 (one bit of margin kept)."""
     want = min_bits or DEFAULT_BITS
     log2m = 0.0
     for i, p in enumerate(MODULI):
         log2m += math.log2(p)
-        b = math.floor((log2m - 2.0 - math.log2(3.0 * max(k_total, 1))) / 2.0) - 1
+        b = math.floor((log2m - 2.0 - math.log2(max(k_total, 1))) / 2.0)
         if i + 1 >= 11 and (b >= want or i + 1 == len(MODULI)):
             return i + 1, min(b, want + 4)
     raise AssertionError("unreachable")

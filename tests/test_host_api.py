@@ -149,11 +149,12 @@ def test_int8_engine_moduli_choice():
     for k in (1, 98, 7744, 11616, 46464):
         n_mod, b = int8_moduli(k)
         log2m = sum(math.log2(p) for p in MODULI[:n_mod])
-        assert b >= 40 and 3 * k * 2.0 ** (2 * b) < 2.0 ** log2m / 16
+        assert b >= 39 and k * 2.0 ** (2 * b) < 2.0 ** log2m / 4  # |Re'|, |Im'| <= K 2^2b < M/2, 1 bit spare
         if n_mod > 11:
             prev = sum(math.log2(p) for p in MODULI[:n_mod - 1])
-            assert math.floor((prev - 2 - math.log2(3 * k)) / 2) - 1 < 40
+            assert math.floor((prev - 2 - math.log2(k)) / 2) < 39
+    assert int8_moduli(11616) == (12, 39) and int8_moduli(46464)[0] == 13
     assert all(math.gcd(a, b) == 1 for i, a in enumerate(MODULI) for b in MODULI[i + 1:])
-    assert int8_gemm_ops(8000, 11616) == 2 * 3 * 13 * 11616 * 8000 * 8001 // 2
+    assert int8_gemm_ops(8000, 11616) == 2 * 3 * 12 * 11616 * 8000 * 8001 // 2
     with pytest.raises(InputError):
         GpuPolicy(engine="fp16")
