@@ -148,7 +148,7 @@ def context(device: int = 0, complex_mult: str | None = None, engine: str | None
     ``complex_mult`` ("3m" | "4m") selects the real-product form of the
     complex contractions for the calls that follow (hsb_ctx_set_complex_mult);
     ``engine`` ("dmma" | "int8") the engine of the triangle contractions
-    (hsb_ctx_set_engine; ``int8_bits`` 0 = default 40).
+    (hsb_ctx_set_engine; ``int8_bits`` 0 = default 39).
     """
     lib = load()
     if complex_mult is not None and complex_mult not in COMPLEX_MULT:

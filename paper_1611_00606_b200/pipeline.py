@@ -50,7 +50,7 @@ class GpuPolicy:
     ``engine`` emulates the S and H contractions on the INT8 tensor cores
     ("int8", default: Chinese-remainder / Ozaki-II scheme, operands rounded
     to ``int8_bits`` bits per column, ~1e-12 relative Frobenius at the
-    default 40, 3.4x faster at C3; see csrc/ozaki.cuh) or runs them on the
+    default 39, 4.2x faster at C3; see csrc/ozaki.cuh) or runs them on the
     FP64 DMMA tensor cores ("dmma": ~1e-15).
     """
 
