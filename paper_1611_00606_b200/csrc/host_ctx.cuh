@@ -1,0 +1,209 @@
+// host_ctx.cuh — internal to libhsb200 (not part of the ABI): the context,
+// workspace and error helpers, the section timeline, and the contraction
+// dispatcher's call description shared by hsb_api.cu and contract.cu.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <atomic>
+#include <thread>
+#include <chrono>
+#include <cstdlib>
+#include <cstdio>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/hsb200.h"
+#include "aux_kernels.cuh"
+#include "match.cuh"
+#include "ozaki.cuh"
+#include "staging.cuh"
+#include "zrk.cuh"
+
+
+using namespace hsb;
+
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+struct hsb_ctx {
+  int device = 0;
+  std::string err;
+  PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  std::map<std::string, DevBuf> bufs;
+  void* pinned = nullptr;  // small pinned host scratch (routing info / offsets)
+  size_t pinned_bytes = 0;
+  hsb::Stager stager;                 // pinned-slot host<->device transfers
+  int* done_cnt = nullptr;            // mapped pinned per-column-block tile counters
+  size_t done_cnt_len = 0;
+  cudaStream_t copy_stream = nullptr;  // overlaps S download with the H contraction
+  int64_t tile_list_T = 0;             // tile rows of the cached grouped triangle order
+  std::vector<int2> tile_list_host;    // its host copy (source of an async upload)
+  int32_t engine = HSB_ENGINE_DMMA;    // triangle contractions: FP64 DMMA or INT8 CRT emulation
+  int32_t oz_min_bits = 39;            // INT8 engine: operand integer bits (accuracy ~2^-bits)
+  int64_t oz_tiles_n = 0;              // cached INT8-engine tile list (n of the output)
+  std::vector<int2> oz_tiles_host;
+  std::vector<int32_t> oz_tile_index_host;
+  int32_t cplx = HSB_CPLX_3M;          // complex product form of the zrk kernels
+};
+
+inline thread_local std::string g_create_err;  // errors of hsb_ctx_create (no context yet)
+
+// Host wall-clock phase stamps for diagnosing the host-buffer path.
+struct HostClock {
+  using clk = std::chrono::steady_clock;
+  bool on = std::getenv("HSB_DEBUG_TIMING") != nullptr;
+  clk::time_point t0 = clk::now(), last = t0;
+  std::string log;
+  void mark(const char* what) {
+    if (!on) return;
+    auto now = clk::now();
+    log += std::string(what) + " " + std::to_string(std::chrono::duration<double, std::milli>(now - last).count()) + " ms; ";
+    last = now;
+  }
+  void report() {
+    if (on) std::fprintf(stderr, "[hsb timing] %s\n", log.c_str());
+  }
+};
+
+
+namespace hsb_host {
+
+
+inline hsb_status fail(hsb_ctx* ctx, hsb_status st, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  else g_create_err = msg;
+  return st;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(ctx, HSB_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define CKS(expr)                     \
+  do {                                \
+    hsb_status s_ = (expr);           \
+    if (s_ != HSB_OK) return s_;      \
+  } while (0)
+
+// grow-only named device workspace (cudaMalloc); pinned host scratch
+hsb_status ws(hsb_ctx* ctx, const char* name, size_t bytes, void** out);
+hsb_status pinned(hsb_ctx* ctx, size_t bytes, void** out);
+
+struct Seg {
+  OperandView l, r;
+};
+
+// Section timeline on the compute stream: each mark closes the interval since
+// the previous mark and charges it to a section tag.
+struct Timeline {
+  std::vector<std::pair<std::string, cudaEvent_t>> marks;
+  ~Timeline() {
+    for (auto& m : marks) cudaEventDestroy(m.second);
+  }
+  cudaError_t mark(cudaStream_t st, const char* tag) {
+    cudaEvent_t e;
+    cudaError_t err = cudaEventCreate(&e);
+    if (err != cudaSuccess) return err;
+    marks.push_back({tag, e});
+    return cudaEventRecord(e, st);
+  }
+  double total(const char* tag) const {
+    double s = 0;
+    for (size_t i = 1; i < marks.size(); ++i)
+      if (marks[i].first == tag) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second);
+        s += ms * 1e-3;
+      }
+    return s;
+  }
+  double span() const {
+    float ms = 0.f;
+    if (marks.size() > 1) cudaEventElapsedTime(&ms, marks.front().second, marks.back().second);
+    return ms * 1e-3;
+  }
+};
+
+inline cudaError_t timeline_mark(Timeline* tl, cudaStream_t st, const char* tag) { return tl->mark(st, tag); }
+
+struct ZrkCall {
+  std::vector<Seg> segs;
+  int64_t m = 0, n = 0;
+  bool triangle = false;
+  bool conj = true;
+  uint32_t flags = 0;
+  double alpha_re = 1, alpha_im = 0, beta_re = 0, beta_im = 0;
+  double* c = nullptr;
+  int64_t ldc = 0;
+  int64_t batch = 1;
+  int64_t c_bstride = 0;
+  const int32_t* c_rowoff = nullptr;
+  int* done_cnt = nullptr;
+  // optional: mark the contraction kernel alone on this timeline, charging the
+  // work before it to `sect` and the kernel itself to `core`
+  Timeline* tl = nullptr;
+  const char* sect = nullptr;
+  const char* core = nullptr;
+  // optional (INT8 engine): run in column groups and record, after each, an
+  // event and the end column of the columns that are final
+  std::vector<std::pair<cudaEvent_t, int64_t>>* chunk_events = nullptr;
+  // optional (INT8 engine): scatter the result into peer receive slots
+  const hsb_peer_out* peer = nullptr;
+  bool peer_is_h = false;
+};
+
+
+// plain stacked operand: k x cols, leading dimension ld
+inline OperandView plain(const double* base, int64_t k, int64_t cols, int64_t ld) {
+  OperandView v;
+  v.base = base;
+  v.k = k;
+  v.cols = cols;
+  v.ld = ld;
+  v.batch = 1;
+  v.bstride = 0;
+  v.bpos = 2;
+  return v;
+}
+// per-atom row blocks of a stacked K x cols array (rows a*n_l .. a*n_l+n_l-1)
+inline OperandView atom_rows(const double* stacked, int64_t n_atoms, int64_t n_l, int64_t cols, int64_t ld) {
+  OperandView v;
+  v.base = stacked;
+  v.k = n_l;
+  v.cols = cols;
+  v.ld = ld;
+  v.batch = n_atoms;
+  v.bstride = n_l;
+  v.bpos = 1;
+  return v;
+}
+// n_atoms contiguous n_l x n_l matrices
+inline OperandView atom_mats(const double* base, int64_t n_atoms, int64_t n_l) {
+  OperandView v;
+  v.base = base;
+  v.k = n_l;
+  v.cols = n_l;
+  v.ld = n_l;
+  v.batch = n_atoms;
+  v.bstride = n_l * n_l;
+  v.bpos = 2;
+  return v;
+}
+
+
+// the contraction dispatcher (contract.cu): DMMA 3M / 4M kernels or the INT8 engine
+hsb_status run_zrk(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launches);
+
+}  // namespace hsb_host

@@ -15,649 +15,9 @@
 //
 // With HSB_OPT_UNFUSED the large updates run as one launch per reference
 // section, in the reference's order, followed by a separate mirror.
-#include <cuda.h>
-#include <cuda_runtime.h>
-#include <cudaTypedefs.h>
-#include <stdint.h>
+#include "host_ctx.cuh"
 
-#include <algorithm>
-#include <atomic>
-#include <thread>
-#include <chrono>
-#include <cstdlib>
-#include <cstdio>
-#include <cmath>
-#include <cstring>
-#include <map>
-#include <string>
-#include <vector>
-
-#include "../../include/hsb200.h"
-#include "aux_kernels.cuh"
-#include "match.cuh"
-#include "ozaki.cuh"
-#include "staging.cuh"
-#include "zrk.cuh"
-
-using namespace hsb;
-
-struct DevBuf {
-  void* ptr = nullptr;
-  size_t bytes = 0;
-};
-
-struct hsb_ctx {
-  int device = 0;
-  std::string err;
-  PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  std::map<std::string, DevBuf> bufs;
-  void* pinned = nullptr;  // small pinned host scratch (routing info / offsets)
-  size_t pinned_bytes = 0;
-  hsb::Stager stager;                 // pinned-slot host<->device transfers
-  int* done_cnt = nullptr;            // mapped pinned per-column-block tile counters
-  size_t done_cnt_len = 0;
-  cudaStream_t copy_stream = nullptr;  // overlaps S download with the H contraction
-  int64_t tile_list_T = 0;             // tile rows of the cached grouped triangle order
-  std::vector<int2> tile_list_host;    // its host copy (source of an async upload)
-  int32_t engine = HSB_ENGINE_DMMA;    // triangle contractions: FP64 DMMA or INT8 CRT emulation
-  int32_t oz_min_bits = 39;            // INT8 engine: operand integer bits (accuracy ~2^-bits)
-  int64_t oz_tiles_n = 0;              // cached INT8-engine tile list (n of the output)
-  std::vector<int2> oz_tiles_host;
-  std::vector<int32_t> oz_tile_index_host;
-  int32_t cplx = HSB_CPLX_3M;          // complex product form of the zrk kernels
-};
-
-static thread_local std::string g_create_err;
-
-// Host wall-clock phase stamps for diagnosing the host-buffer path.
-struct HostClock {
-  using clk = std::chrono::steady_clock;
-  bool on = std::getenv("HSB_DEBUG_TIMING") != nullptr;
-  clk::time_point t0 = clk::now(), last = t0;
-  std::string log;
-  void mark(const char* what) {
-    if (!on) return;
-    auto now = clk::now();
-    log += std::string(what) + " " + std::to_string(std::chrono::duration<double, std::milli>(now - last).count()) + " ms; ";
-    last = now;
-  }
-  void report() {
-    if (on) std::fprintf(stderr, "[hsb timing] %s\n", log.c_str());
-  }
-};
-
-namespace {
-
-hsb_status fail(hsb_ctx* ctx, hsb_status st, const std::string& msg) {
-  if (ctx) ctx->err = msg;
-  else g_create_err = msg;
-  return st;
-}
-
-#define CK(call)                                                                          \
-  do {                                                                                    \
-    cudaError_t e_ = (call);                                                              \
-    if (e_ != cudaSuccess)                                                                \
-      return fail(ctx, HSB_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
-  } while (0)
-
-#define CKS(expr)                     \
-  do {                                \
-    hsb_status s_ = (expr);           \
-    if (s_ != HSB_OK) return s_;      \
-  } while (0)
-
-hsb_status ws(hsb_ctx* ctx, const char* name, size_t bytes, void** out) {
-  DevBuf& b = ctx->bufs[name];
-  if (b.bytes < bytes) {
-    if (b.ptr) cudaFree(b.ptr);
-    b.ptr = nullptr;
-    b.bytes = 0;
-    cudaError_t e = cudaMalloc(&b.ptr, bytes ? bytes : 16);
-    if (e != cudaSuccess) {
-      b.ptr = nullptr;
-      cudaGetLastError();
-      return fail(ctx, HSB_ERR_NOMEM, std::string("device allocation of ") + std::to_string(bytes) +
-                                          " bytes for '" + name + "' failed: " + cudaGetErrorString(e));
-    }
-    b.bytes = bytes;
-  }
-  *out = b.ptr;
-  return HSB_OK;
-}
-
-hsb_status pinned(hsb_ctx* ctx, size_t bytes, void** out) {
-  if (ctx->pinned_bytes < bytes) {
-    if (ctx->pinned) cudaFreeHost(ctx->pinned);
-    ctx->pinned = nullptr;
-    ctx->pinned_bytes = 0;
-    if (cudaMallocHost(&ctx->pinned, bytes) != cudaSuccess) {
-      cudaGetLastError();
-      return fail(ctx, HSB_ERR_NOMEM, "pinned host allocation failed");
-    }
-    ctx->pinned_bytes = bytes;
-  }
-  *out = ctx->pinned;
-  return HSB_OK;
-}
-
-// ----------------------------------------------------------- TMA descriptors
-hsb_status encode_operand(hsb_ctx* ctx, CUtensorMap* map, const OperandView& v) {
-  if (reinterpret_cast<uintptr_t>(v.base) % 16 != 0)
-    return fail(ctx, HSB_ERR_INPUT, "operand base address must be 16-byte aligned");
-  cuuint64_t dims[3], strides[2];
-  cuuint32_t box[3], estr[3] = {1, 1, 1};
-  const cuuint64_t col_stride = static_cast<cuuint64_t>(v.ld) * 16;
-  const cuuint64_t bat_stride =
-      static_cast<cuuint64_t>(v.batch > 1 ? v.bstride : std::max<int64_t>(1, v.ld * std::max<int64_t>(1, v.cols))) * 16;
-  dims[0] = static_cast<cuuint64_t>(2 * v.k);
-  box[0] = kBK;
-  if (v.bpos == 1) {
-    dims[1] = static_cast<cuuint64_t>(v.batch);
-    dims[2] = static_cast<cuuint64_t>(v.cols);
-    strides[0] = bat_stride;
-    strides[1] = col_stride;
-    box[1] = 1;
-    box[2] = kBM;
-  } else {
-    dims[1] = static_cast<cuuint64_t>(v.cols);
-    dims[2] = static_cast<cuuint64_t>(v.batch);
-    strides[0] = col_stride;
-    strides[1] = bat_stride;
-    box[1] = kBM;
-    box[2] = 1;
-  }
-  CUresult r = ctx->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(v.base), dims, strides,
-                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS)
-    return fail(ctx, HSB_ERR_CUDA, "cuTensorMapEncodeTiled failed (code " + std::to_string(static_cast<int>(r)) +
-                                       ") for k=" + std::to_string(v.k) + " cols=" + std::to_string(v.cols) +
-                                       " ld=" + std::to_string(v.ld));
-  return HSB_OK;
-}
-
-// 2-D TMA map over one real sum plane (k x cols, leading dimension ldp doubles),
-// box {8 complex k, 64 cols}, no swizzle (zrk3m_kernel.cu, PLANES).
-hsb_status encode_plane(hsb_ctx* ctx, CUtensorMap* map, const double* base, int64_t k, int64_t cols, int64_t ldp) {
-  cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(cols)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldp) * 8};
-  cuuint32_t box[2] = {8, static_cast<cuuint32_t>(kBM)}, estr[2] = {1, 1};
-  CUresult r = ctx->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
-                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS)
-    return fail(ctx, HSB_ERR_CUDA, "cuTensorMapEncodeTiled failed for a sum plane (code " +
-                                       std::to_string(static_cast<int>(r)) + ")");
-  return HSB_OK;
-}
-
-struct Seg {
-  OperandView l, r;
-};
-
-// Section timeline on the compute stream: each mark closes the interval since
-// the previous mark and charges it to a section tag.
-struct Timeline {
-  std::vector<std::pair<std::string, cudaEvent_t>> marks;
-  ~Timeline() {
-    for (auto& m : marks) cudaEventDestroy(m.second);
-  }
-  cudaError_t mark(cudaStream_t st, const char* tag) {
-    cudaEvent_t e;
-    cudaError_t err = cudaEventCreate(&e);
-    if (err != cudaSuccess) return err;
-    marks.push_back({tag, e});
-    return cudaEventRecord(e, st);
-  }
-  double total(const char* tag) const {
-    double s = 0;
-    for (size_t i = 1; i < marks.size(); ++i)
-      if (marks[i].first == tag) {
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second);
-        s += ms * 1e-3;
-      }
-    return s;
-  }
-  double span() const {
-    float ms = 0.f;
-    if (marks.size() > 1) cudaEventElapsedTime(&ms, marks.front().second, marks.back().second);
-    return ms * 1e-3;
-  }
-};
-
-cudaError_t timeline_mark(Timeline* tl, cudaStream_t st, const char* tag) { return tl->mark(st, tag); }
-
-struct ZrkCall {
-  std::vector<Seg> segs;
-  int64_t m = 0, n = 0;
-  bool triangle = false;
-  bool conj = true;
-  uint32_t flags = 0;
-  double alpha_re = 1, alpha_im = 0, beta_re = 0, beta_im = 0;
-  double* c = nullptr;
-  int64_t ldc = 0;
-  int64_t batch = 1;
-  int64_t c_bstride = 0;
-  const int32_t* c_rowoff = nullptr;
-  int* done_cnt = nullptr;
-  // optional: mark the contraction kernel alone on this timeline, charging the
-  // work before it to `sect` and the kernel itself to `core`
-  Timeline* tl = nullptr;
-  const char* sect = nullptr;
-  const char* core = nullptr;
-  // optional (INT8 engine): run in column groups and record, after each, an
-  // event and the end column of the columns that are final
-  std::vector<std::pair<cudaEvent_t, int64_t>>* chunk_events = nullptr;
-  // optional (INT8 engine): scatter the result into peer receive slots
-  const hsb_peer_out* peer = nullptr;
-  bool peer_is_h = false;
-};
-
-// Lower-triangle tile order for the persistent 3M kernel.  The 148 CTAs run
-// consecutive list entries concurrently and advance through k in near
-// lockstep, so the operand panels they share stay in L2.  Column-major tile
-// order puts ~148 distinct row panels in flight at once (each streamed from
-// HBM: 117 GB per C3 H launch); kTileGroup x kTileGroup blocks of tiles
-// (column groups left to right, row groups top to bottom, i >= j) put 2 x 12.
-// Column groups still complete left to right, which the H download stream
-// relies on (done_cnt prefix).
-constexpr int kTileGroup = 12;
-hsb_status tile_order(hsb_ctx* ctx, int64_t T, cudaStream_t st, const int2** out) {
-  void* buf;
-  CKS(ws(ctx, "tile_list", static_cast<size_t>(T * (T + 1) / 2) * sizeof(int2), &buf));
-  if (ctx->tile_list_T != T) {
-    std::vector<int2>& v = ctx->tile_list_host;
-    v.clear();
-    v.reserve(static_cast<size_t>(T * (T + 1) / 2));
-    for (int64_t j0 = 0; j0 < T; j0 += kTileGroup)
-      for (int64_t i0 = j0; i0 < T; i0 += kTileGroup)
-        for (int64_t j = j0; j < std::min<int64_t>(j0 + kTileGroup, T); ++j)
-          for (int64_t i = std::max(i0, j); i < std::min<int64_t>(i0 + kTileGroup, T); ++i)
-            v.push_back(make_int2(static_cast<int>(i), static_cast<int>(j)));
-    CK(cudaMemcpyAsync(buf, v.data(), v.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
-    ctx->tile_list_T = T;
-  }
-  *out = static_cast<const int2*>(buf);
-  return HSB_OK;
-}
-
-// ---------------------------------------------------------------- INT8 engine
-// Lower-triangle C = alpha sum_s op(L_s)^T R_s + beta C on the INT8 tensor
-// cores (ozaki.cuh): column exponents, residue planes of every distinct
-// operand, one persistent tcgen05 GEMM launch over (product, modulus, tile),
-// CRT reconstruction + mirror.
-hsb_status oz_encode(hsb_ctx* ctx, CUtensorMap* map, const int8_t* planes, int64_t k, int64_t cols, int64_t kpad,
-                     int n_mod, int box_rows) {
-  cuuint64_t dims[3] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(n_mod)};
-  cuuint64_t strides[2] = {static_cast<cuuint64_t>(kpad), static_cast<cuuint64_t>(kpad * cols)};
-  cuuint32_t box[3] = {static_cast<cuuint32_t>(kOzBK), static_cast<cuuint32_t>(box_rows), 1}, es[3] = {1, 1, 1};
-  CUresult r = ctx->encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(planes), dims, strides, box, es,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS)
-    return fail(ctx, HSB_ERR_CUDA, "cuTensorMapEncodeTiled failed for residue planes (code " +
-                                       std::to_string(static_cast<int>(r)) + ")");
-  return HSB_OK;
-}
-
-// 256 x 256 tiles (tile row tm >= tile col tn) of the lower triangle, in
-// groups of 6 x 6 tiles for L2 reuse
-hsb_status oz_tiles(hsb_ctx* ctx, int64_t n, cudaStream_t st, const int2** out, int* count,
-                    const int32_t** index) {
-  const int64_t T = (n + kOzBN - 1) / kOzBN;
-  std::vector<int2>& v = ctx->oz_tiles_host;
-  std::vector<int32_t>& ix = ctx->oz_tile_index_host;
-  if (ctx->oz_tiles_n != n) {
-    v.clear();
-    for (int64_t j0 = 0; j0 < T; j0 += 6)
-      for (int64_t i0 = j0; i0 < T; i0 += 6)
-        for (int64_t j = j0; j < std::min<int64_t>(j0 + 6, T); ++j)
-          for (int64_t i = std::max(i0, j); i < std::min<int64_t>(i0 + 6, T); ++i)
-            v.push_back(make_int2(static_cast<int>(i), static_cast<int>(j)));
-    ix.assign(static_cast<size_t>(T * T), -1);
-    for (size_t t = 0; t < v.size(); ++t) ix[static_cast<size_t>(v[t].x * T + v[t].y)] = static_cast<int32_t>(t);
-  }
-  void *buf, *ibuf;
-  CKS(ws(ctx, "oz_tiles", v.size() * sizeof(int2), &buf));
-  CKS(ws(ctx, "oz_tile_index", ix.size() * sizeof(int32_t), &ibuf));
-  if (ctx->oz_tiles_n != n) {
-    CK(cudaMemcpyAsync(buf, v.data(), v.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(ibuf, ix.data(), ix.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-    ctx->oz_tiles_n = n;
-  }
-  *out = static_cast<const int2*>(buf);
-  *count = static_cast<int>(v.size());
-  *index = static_cast<const int32_t*>(ibuf);
-  return HSB_OK;
-}
-
-hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launches) {
-  const int64_t n = z.m;
-  std::vector<Seg> segs;
-  int64_t ktot = 0;
-  for (const Seg& s : z.segs)
-    if (s.l.k > 0) {
-      if (s.l.k != s.r.k) return fail(ctx, HSB_ERR_DIMENSION, "segment operands disagree in reduction length");
-      segs.push_back(s);
-      ktot += s.l.k;
-    }
-  if (segs.size() > static_cast<size_t>(kOzMaxSeg)) return fail(ctx, HSB_ERR_UNSUPPORTED, "too many segments");
-  // moduli: the fewest with b >= oz_min_bits.  With |x'| + |y'| <= 2^b per
-  // element, |Re'| = |sum x'x' + y'y'| and |Im'| = |sum x'_L y'_R - y'_L x'_R|
-  // are both <= K 2^2b; the explicit CRT needs |X| < M/2, kept with one bit of
-  // margin: 2b <= log2 M - 2 - log2 K.
-  int n_mod = 0, b = 0;
-  {
-    double log2m = 0;
-    for (int i = 0; i < kOzMaxMod; ++i) {
-      log2m += std::log2(static_cast<double>(oz_mod(i)));
-      const int bi = static_cast<int>(std::floor((log2m - 2.0 - std::log2(static_cast<double>(std::max<int64_t>(ktot, 1)))) / 2.0));
-      if (i + 1 >= 11 && (bi >= ctx->oz_min_bits || i + 1 == kOzMaxMod)) {
-        n_mod = i + 1;
-        b = std::min(bi, ctx->oz_min_bits + 4);
-        break;
-      }
-    }
-  }
-  if (b < 30) return fail(ctx, HSB_ERR_UNSUPPORTED, "reduction too long for the INT8 engine's moduli");
-  // exponents: one array for both sides (m == n), max over every operand
-  void* ebuf;
-  CKS(ws(ctx, "oz_exp", static_cast<size_t>(n) * sizeof(int32_t), &ebuf));
-  int32_t* e = static_cast<int32_t*>(ebuf);
-  CK(launch_ozaki_init_exp(e, n, st));
-  {
-    std::vector<const OperandView*> seen;
-    auto colexp = [&](const OperandView& v) -> hsb_status {
-      for (const OperandView* q : seen)
-        if (q->base == v.base && q->k == v.k && q->ld == v.ld) return HSB_OK;
-      seen.push_back(&v);
-      CK(launch_ozaki_colexp(v.base, v.ld, v.k, v.cols, e, st));
-      return HSB_OK;
-    };
-    for (const Seg& s : segs) {
-      CKS(colexp(s.l));
-      CKS(colexp(s.r));
-    }
-  }
-  // residue planes of each distinct operand
-  struct Src {
-    const double* base;
-    int64_t k, ld;
-    int8_t* planes;
-    int64_t kpad;
-  };
-  std::vector<Src> srcs;
-  auto planes_of = [&](const OperandView& v, Src* out) -> hsb_status {
-    for (const Src& q : srcs)
-      if (q.base == v.base && q.k == v.k && q.ld == v.ld) {
-        *out = q;
-        return HSB_OK;
-      }
-    Src q{v.base, v.k, v.ld, nullptr, (v.k + 15) / 16 * 16};
-    const std::string name = "oz_res" + std::to_string(srcs.size());
-    void* buf;
-    CKS(ws(ctx, name.c_str(), static_cast<size_t>(4) * n_mod * n * q.kpad, &buf));
-    q.planes = static_cast<int8_t*>(buf);
-    CK(launch_ozaki_residues(v.base, v.ld, v.k, n, e, b, n_mod, q.planes, q.kpad, st));
-    srcs.push_back(q);
-    *out = q;
-    return HSB_OK;
-  };
-  OzGemmParams gp;
-  std::memset(&gp, 0, sizeof(gp));
-  // products: P = re.re, Q = im.im, W = (re -/+ im)(re + im)
-  const int lp[3] = {kOzRe, kOzIm, z.conj ? kOzMinus : kOzPlus};
-  const int rp[3] = {kOzRe, kOzIm, kOzPlus};
-  for (size_t si = 0; si < segs.size(); ++si) {
-    Src L, R;
-    CKS(planes_of(segs[si].l, &L));
-    CKS(planes_of(segs[si].r, &R));
-    const int64_t pl = static_cast<int64_t>(n_mod) * n * L.kpad, pr = static_cast<int64_t>(n_mod) * n * R.kpad;
-    for (int pi = 0; pi < 3; ++pi) {
-      CKS(oz_encode(ctx, &gp.map[pi][si][0], L.planes + lp[pi] * pl, L.k, n, L.kpad, n_mod, 128));
-      CKS(oz_encode(ctx, &gp.map[pi][si][1], R.planes + rp[pi] * pr, R.k, n, R.kpad, n_mod, 128));
-    }
-    gp.seg_chunk0[si + 1] = gp.seg_chunk0[si] + static_cast<int32_t>((segs[si].l.k + kOzBK - 1) / kOzBK);
-  }
-  gp.nseg = static_cast<int32_t>(segs.size());
-  // slabs of ~16 KB of k (see ozaki.cuh), balanced
-  const int32_t total_chunks = gp.seg_chunk0[gp.nseg];
-  constexpr int32_t kSlabChunks = 16384 / kOzBK;
-  gp.nslab = std::max(1, std::min<int32_t>(kOzMaxSlab, (total_chunks + kSlabChunks - 1) / kSlabChunks));
-  for (int sl = 0; sl <= gp.nslab; ++sl)
-    gp.slab_chunk0[sl] = static_cast<int32_t>(static_cast<int64_t>(total_chunks) * sl / gp.nslab);
-  gp.n_mod = n_mod;
-  gp.n = static_cast<int32_t>(n);
-  const int32_t* tile_index = nullptr;
-  int total_tiles = 0;
-  CKS(oz_tiles(ctx, n, st, &gp.tile_list, &total_tiles, &tile_index));
-  gp.mod_stride = static_cast<int64_t>(total_tiles) * kOzTileBytes;
-  gp.slab_stride = gp.mod_stride * n_mod;
-  gp.prod_stride = gp.slab_stride * gp.nslab;
-  void* rbuf;
-  CKS(ws(ctx, "oz_out", static_cast<size_t>(3 * gp.prod_stride), &rbuf));
-  gp.res = static_cast<int8_t*>(rbuf);
-  void* cbuf;
-  CKS(ws(ctx, "oz_counter", 16, &cbuf));
-  gp.counter = static_cast<int32_t*>(cbuf);
-  if (gp.nseg == 0) CK(cudaMemsetAsync(rbuf, 0, static_cast<size_t>(3 * gp.prod_stride), st));
-
-  OzCrtParams cp;
-  cp.res = gp.res;
-  cp.mod_stride = gp.mod_stride;
-  cp.slab_stride = gp.slab_stride;
-  cp.prod_stride = gp.prod_stride;
-  cp.tile_index = tile_index;
-  cp.T = static_cast<int32_t>((n + kOzBN - 1) / kOzBN);
-  cp.nslab = gp.nslab;
-  cp.n_mod = n_mod;
-  cp.n = static_cast<int32_t>(n);
-  cp.b = b;
-  cp.conj = z.conj ? 1 : 0;
-  cp.el = e;
-  cp.er = e;
-  cp.alpha_re = z.alpha_re;
-  cp.alpha_im = z.alpha_im;
-  cp.beta_re = z.beta_re;
-  cp.beta_im = z.beta_im;
-  cp.c = z.c;
-  cp.ldc = z.ldc;
-  cp.flags = z.flags;
-  cp.peer = nullptr;
-  cp.P = cp.rank = 0;
-  cp.cpr = cp.pld = 0;
-  if (z.peer) {
-    cp.peer = reinterpret_cast<double2* const*>(z.peer_is_h ? z.peer->h_slots : z.peer->s_slots);
-    cp.P = z.peer->n_ranks;
-    cp.rank = z.peer->rank;
-    cp.cpr = z.peer->cols_per_rank;
-    cp.pld = z.peer->ld;
-  }
-
-  // With a host download waiting on per-column counters (done_cnt), the
-  // product runs in column groups of 6 tiles (contiguous in the tile list):
-  // once groups 0..g are done their columns are final (the mirror of an
-  // entry of an earlier group lands in a later column), so their download
-  // overlaps the remaining groups.  Otherwise one GEMM + one CRT launch.
-  const int64_t T = (n + kOzBN - 1) / kOzBN;
-  const int64_t T64 = (n + kBN - 1) / kBN;  // the host's 64-column blocks
-  const std::vector<int2>& tl_host = ctx->oz_tiles_host;
-  const int64_t group = (z.done_cnt || z.chunk_events) ? 6 : T;
-  int t0 = 0;
-  for (int64_t j0 = 0; j0 < T; j0 += group) {
-    const int64_t j1 = std::min<int64_t>(j0 + group, T);
-    int t1 = t0;
-    while (t1 < total_tiles && tl_host[static_cast<size_t>(t1)].y < j1) ++t1;
-    if (gp.nseg > 0 && t1 > t0) {
-      gp.tile0 = t0;
-      gp.ntiles = t1 - t0;
-      if (z.tl) CK(timeline_mark(z.tl, st, z.sect));
-      CK(launch_ozaki_gemm(gp, st));
-      if (z.tl) CK(timeline_mark(z.tl, st, z.core));
-    }
-    const int64_t c0 = j0 * kOzBN, c1 = std::min<int64_t>(j1 * kOzBN, n);
-    cp.n0 = static_cast<int32_t>(c0);
-    CK(launch_ozaki_crt_cols(cp, c1 - c0, st));
-    if (z.done_cnt) {
-      const int64_t b0 = c0 / kBN, b1 = (j1 == T) ? T64 : c1 / kBN;
-      CK(launch_fill_i32(z.done_cnt + b0, b1 - b0, static_cast<int32_t>(T64), st));
-    }
-    if (z.chunk_events) {
-      cudaEvent_t ev;
-      CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-      z.chunk_events->push_back({ev, c1});
-      CK(cudaEventRecord(ev, st));
-    }
-    t0 = t1;
-  }
-  if (launches) *launches += 3 + 2 * static_cast<int>(segs.size()) + static_cast<int>(srcs.size());
-  return HSB_OK;
-}
-
-hsb_status run_zrk(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launches) {
-  if (z.peer && !(ctx->engine == HSB_ENGINE_INT8 && z.triangle && z.batch == 1 && z.m == z.n))
-    return fail(ctx, HSB_ERR_UNSUPPORTED, "peer output needs the INT8 engine on a triangle call");
-  if (ctx->engine == HSB_ENGINE_INT8 && z.triangle && z.batch == 1 && z.m == z.n && z.m > 0) {
-    bool plain = true;
-    for (const Seg& s : z.segs) plain = plain && s.l.batch == 1 && s.r.batch == 1;
-    if (plain) return run_ozaki(ctx, st, z, launches);
-  }
-  if (z.m <= 0 || z.n <= 0 || z.batch <= 0) return HSB_OK;
-  if (z.segs.size() > static_cast<size_t>(kMaxSeg)) return fail(ctx, HSB_ERR_UNSUPPORTED, "too many segments");
-  if (z.triangle && z.m != z.n) return fail(ctx, HSB_ERR_DIMENSION, "triangle mode needs a square output");
-  if (z.m > (int64_t{1} << 30) || z.n > (int64_t{1} << 30))
-    return fail(ctx, HSB_ERR_UNSUPPORTED, "output dimension too large");
-  ZrkParams p;
-  std::memset(&p, 0, sizeof(p));
-  // 3M on plain (unbatched) operands: Re-Im / Re+Im planes of each distinct
-  // operand, computed once here and fed to the kernel by TMA
-  const bool g3 = ctx->cplx == HSB_CPLX_3M;
-  bool planes = g3 && z.batch == 1;
-  for (const Seg& s : z.segs)
-    if (s.l.batch != 1 || s.r.batch != 1) planes = false;
-  struct PlaneSrc {
-    const double* base;
-    int64_t k, cols, ld, ldp;
-    double* minus;
-    double* plus;
-  };
-  std::vector<PlaneSrc> srcs;
-  auto plane_of = [&](const OperandView& v, bool minus, const double** out, int64_t* ldp) -> hsb_status {
-    for (const PlaneSrc& q : srcs)
-      if (q.base == v.base && q.k == v.k && q.cols == v.cols && q.ld == v.ld) {
-        *out = minus ? q.minus : q.plus;
-        *ldp = q.ldp;
-        return HSB_OK;
-      }
-    PlaneSrc q{v.base, v.k, v.cols, v.ld, v.k + (v.k & 1), nullptr, nullptr};
-    const std::string name = "zplane" + std::to_string(srcs.size());
-    void* buf;
-    CKS(ws(ctx, name.c_str(), static_cast<size_t>(2 * q.ldp) * q.cols * 8, &buf));
-    q.minus = static_cast<double*>(buf);
-    q.plus = q.minus + q.ldp * q.cols;
-    CK(launch_sum_planes(q.base, q.ld, q.k, q.cols, q.minus, q.plus, q.ldp, st));
-    srcs.push_back(q);
-    *out = minus ? q.minus : q.plus;
-    *ldp = q.ldp;
-    return HSB_OK;
-  };
-  int nseg = 0, total = 0;
-  for (const Seg& s : z.segs) {
-    if (s.l.k <= 0) continue;
-    if (s.l.k != s.r.k) return fail(ctx, HSB_ERR_DIMENSION, "segment operands disagree in reduction length");
-    CKS(encode_operand(ctx, &p.lmap[nseg], s.l));
-    CKS(encode_operand(ctx, &p.rmap[nseg], s.r));
-    if (planes) {
-      const double *lp, *rp;
-      int64_t ldl, ldr;
-      // left factor: Re-Im for L^H R (conj), Re+Im for L^T R
-      CKS(plane_of(s.l, z.conj, &lp, &ldl));
-      CKS(plane_of(s.r, false, &rp, &ldr));
-      CKS(encode_plane(ctx, &p.lsum[nseg], lp, s.l.k, s.l.cols, ldl));
-      CKS(encode_plane(ctx, &p.rsum[nseg], rp, s.r.k, s.r.cols, ldr));
-    }
-    const int64_t chunks = (2 * s.l.k + kBK - 1) / kBK;
-    if (chunks > (int64_t{1} << 30)) return fail(ctx, HSB_ERR_UNSUPPORTED, "reduction too long");
-    p.seg[nseg].kchunks = static_cast<int32_t>(chunks);
-    p.seg[nseg].lbpos = s.l.bpos;
-    p.seg[nseg].rbpos = s.r.bpos;
-    total += static_cast<int>(chunks);
-    ++nseg;
-  }
-  p.nseg = nseg;
-  p.total_chunks = total;
-  p.m = static_cast<int32_t>(z.m);
-  p.n = static_cast<int32_t>(z.n);
-  p.tiles_m = static_cast<int32_t>((z.m + kBM - 1) / kBM);
-  p.tiles_n = static_cast<int32_t>((z.n + kBN - 1) / kBN);
-  p.triangle = z.triangle ? 1 : 0;
-  p.flags = z.flags;
-  p.alpha_re = z.alpha_re;
-  p.alpha_im = z.alpha_im;
-  p.beta_re = z.beta_re;
-  p.beta_im = z.beta_im;
-  p.c = z.c;
-  p.ldc = z.ldc;
-  p.c_bstride = z.c_bstride;
-  p.c_rowoff = z.c_rowoff;
-  p.done_cnt = z.triangle ? z.done_cnt : nullptr;
-  int64_t grid_x = z.triangle ? static_cast<int64_t>(p.tiles_m) * (p.tiles_m + 1) / 2
-                              : static_cast<int64_t>(p.tiles_m) * p.tiles_n;
-  if (grid_x > 0x7fffffff || z.batch > 65535) return fail(ctx, HSB_ERR_UNSUPPORTED, "grid too large");
-  if (g3 && z.triangle && z.batch == 1 && p.tiles_m > kTileGroup) CKS(tile_order(ctx, p.tiles_m, st, &p.tile_list));
-  if (z.tl) CK(timeline_mark(z.tl, st, z.sect));
-  if (g3) {
-    if (grid_x * z.batch > 0x7fffffff) return fail(ctx, HSB_ERR_UNSUPPORTED, "grid too large");
-    CK(launch_zrk3m(p, z.conj, planes, static_cast<int>(grid_x), static_cast<int>(z.batch), st));
-    if (launches) *launches += static_cast<int>(srcs.size());
-  } else {
-    CK(launch_zrk(p, z.conj, static_cast<int>(grid_x), static_cast<int>(z.batch), st));
-  }
-  if (z.tl) CK(timeline_mark(z.tl, st, z.core));
-  if (launches) ++*launches;
-  return HSB_OK;
-}
-
-// plain stacked operand: k x cols, leading dimension ld
-OperandView plain(const double* base, int64_t k, int64_t cols, int64_t ld) {
-  OperandView v;
-  v.base = base;
-  v.k = k;
-  v.cols = cols;
-  v.ld = ld;
-  v.batch = 1;
-  v.bstride = 0;
-  v.bpos = 2;
-  return v;
-}
-// per-atom row blocks of a stacked K x cols array (rows a*n_l .. a*n_l+n_l-1)
-OperandView atom_rows(const double* stacked, int64_t n_atoms, int64_t n_l, int64_t cols, int64_t ld) {
-  OperandView v;
-  v.base = stacked;
-  v.k = n_l;
-  v.cols = cols;
-  v.ld = ld;
-  v.batch = n_atoms;
-  v.bstride = n_l;
-  v.bpos = 1;
-  return v;
-}
-// n_atoms contiguous n_l x n_l matrices
-OperandView atom_mats(const double* base, int64_t n_atoms, int64_t n_l) {
-  OperandView v;
-  v.base = base;
-  v.k = n_l;
-  v.cols = n_l;
-  v.ld = n_l;
-  v.batch = n_atoms;
-  v.bstride = n_l * n_l;
-  v.bpos = 2;
-  return v;
-}
-
-}  // namespace
+using namespace hsb_host;
 
 // =============================================================================
 extern "C" {
