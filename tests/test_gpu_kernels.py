@@ -154,3 +154,39 @@ def test_int8_engine_is_column_scale_invariant():
     norm[norm == 0] = 1.0
     assert np.all(got[:, 7] == 0) and np.all(got[7, :] == 0)
     assert np.max(np.abs(got - want) / norm) < 1e-10
+
+
+@pytest.mark.parametrize("engine", ["int8", "dmma"])
+@pytest.mark.parametrize("opa", ["C", "T"])
+def test_gemmt_lower_only_through_the_abi(engine, opa):
+    # hsb_zgemm with HSB_LOWER_ONLY (GEMMT): a triangle call; with opa 'T' the
+    # INT8 engine takes its non-conjugating path (Re = P - Q, Im = W - P - Q)
+    import ctypes
+
+    import torch
+
+    from paper_1611_00606_b200 import _lib
+
+    rng = np.random.default_rng(11)
+    k, n = 333, 290
+    a, b = _cm(rng, k, n), _cm(rng, k, n)
+    c0 = _cm(rng, n, n)
+    dev = torch.device("cuda", 0)
+    da = torch.from_numpy(np.ascontiguousarray(a.T)).to(dev)   # row-major (n, k) = column-major k x n
+    db = torch.from_numpy(np.ascontiguousarray(b.T)).to(dev)
+    dc = torch.from_numpy(np.ascontiguousarray(c0.T)).to(dev)
+    lib = _lib.load()
+    ctx = _lib.context(0, "3m", engine)
+    st = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    _lib.check(lib.hsb_zgemm(ctx, st, opa.encode(), b"N", n, n, k, 1.0, 0.0, da.data_ptr(), k, db.data_ptr(), k,
+                             0.5, 0.0, dc.data_ptr(), n, _lib.HSB_LOWER_ONLY), ctx)
+    torch.cuda.synchronize()
+    got = dc.cpu().numpy().T
+    opm = a.conj().T if opa == "C" else a.T
+    want = opm @ b + 0.5 * c0
+    low = np.tril_indices(n)
+    err = np.linalg.norm(got[low] - want[low]) / (1 + np.linalg.norm(want[low]))
+    assert err < (TOL_INT8 if engine == "int8" else TOL)
+    up = np.triu_indices(n, 1)
+    assert np.array_equal(got[up], c0[up])  # the strict upper triangle is untouched
+    _lib.context(0, "3m", "int8")  # restore the default engine for later tests
