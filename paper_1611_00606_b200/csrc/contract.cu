@@ -272,24 +272,30 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
   int total_tiles = 0;
   CKS(oz_tiles(ctx, n, st, &gp.tile_list, &total_tiles, &tile_index));
   gp.mod_stride = static_cast<int64_t>(total_tiles) * kOzTileBytes;
-  gp.slab_stride = gp.mod_stride * n_mod;
-  gp.prod_stride = gp.slab_stride * gp.nslab;
+  gp.prod_stride = gp.mod_stride * n_mod;
+  gp.tiles_total = total_tiles;
   void* rbuf;
   CKS(ws(ctx, "oz_out", static_cast<size_t>(3 * gp.prod_stride), &rbuf));
   gp.res = static_cast<int8_t*>(rbuf);
   void* cbuf;
   CKS(ws(ctx, "oz_counter", 16, &cbuf));
   gp.counter = static_cast<int32_t*>(cbuf);
+  gp.slab_cnt = nullptr;
+  if (gp.nslab > 1) {
+    const size_t nc = static_cast<size_t>(3) * n_mod * total_tiles;
+    void* sbuf;
+    CKS(ws(ctx, "oz_slab_cnt", nc * sizeof(int32_t), &sbuf));
+    gp.slab_cnt = static_cast<int32_t*>(sbuf);
+    CK(cudaMemsetAsync(sbuf, 0, nc * sizeof(int32_t), st));
+  }
   if (gp.nseg == 0) CK(cudaMemsetAsync(rbuf, 0, static_cast<size_t>(3 * gp.prod_stride), st));
 
   OzCrtParams cp;
   cp.res = gp.res;
   cp.mod_stride = gp.mod_stride;
-  cp.slab_stride = gp.slab_stride;
   cp.prod_stride = gp.prod_stride;
   cp.tile_index = tile_index;
   cp.T = static_cast<int32_t>((n + kOzBN - 1) / kOzBN);
-  cp.nslab = gp.nslab;
   cp.n_mod = n_mod;
   cp.n = static_cast<int32_t>(n);
   cp.b = b;

@@ -398,8 +398,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int rloc = static_cast<int>(rank) * kOzHalf + q * 32 + lane;  // row within the tile
       const int row = tm * 256 + rloc;
-      int8_t* out = p.res + prod * p.prod_stride + slab * p.slab_stride + mod * p.mod_stride +
-                    static_cast<int64_t>(t) * kOzTileBytes + rloc;
+      int8_t* out = p.res + prod * p.prod_stride + mod * p.mod_stride + static_cast<int64_t>(t) * kOzTileBytes + rloc;
+      int32_t* cnt = p.nslab > 1 ? p.slab_cnt + (static_cast<int64_t>(prod) * p.n_mod + mod) * p.tiles_total + t
+                                 : nullptr;
+      if (slab > 0) {  // slab s-1 of this tile: all 8 epilogue warps (2 CTAs x 4) finished
+        if (lane == 0)
+          while (*reinterpret_cast<volatile int32_t*>(cnt) < 8 * slab) __nanosleep(256);
+        __syncwarp();
+        __threadfence();
+      }
       const int col0 = tn * 256;
       const int ncol = min(kOzBN, p.n - col0);
       for (int c = 0; c < kOzBN / 32; ++c) {
@@ -409,10 +416,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
         if (row < p.n) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            const int r = sym_mod_d(static_cast<double>(static_cast<int32_t>(v[j])), pd, inv);
-            out[(c * 32 + j) * 256] = static_cast<int8_t>(r);
+            int r = sym_mod_d(static_cast<double>(static_cast<int32_t>(v[j])), pd, inv);
+            int8_t* o = out + (c * 32 + j) * 256;
+            if (slab > 0) r = sym_adj(r + __ldcg(o), ip);  // the residue of the sum of the slabs
+            *o = static_cast<int8_t>(r);
           }
         }
+      }
+      if (cnt) {
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(cnt, 1);
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -496,35 +510,20 @@ __device__ __forceinline__ double2 crt_finish(const OzCrtParams& p, const int (&
 // loads and the C[m, n] store are coalesced; the mirror C[n, m] = conj(C[m, n])
 // is a strided store (matcore.hermitian_mirror, matcore.py:89-105).  Measured
 // faster than shared-memory-transposed variants, which run fewer threads per
-// SM.  ONE_SLAB: straight-line code, all 3 x NM loads in flight at once.
-template <int NM, bool ONE_SLAB>
+// SM.
+template <int NM>
 __global__ void __launch_bounds__(128) ozaki_crt_kernel(const OzCrtParams p) {
   const int n = p.n0 + blockIdx.y;  // column
   const int m = (p.n0 & ~127) + blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= p.n || m < n) return;
   const int t = p.tile_index[(m >> 8) * p.T + (n >> 8)];
   const int8_t* r0 = p.res + static_cast<int64_t>(t) * kOzTileBytes + (n & 255) * 256 + (m & 255);
-  int P[NM], Q[NM], W[NM];
-  if (ONE_SLAB) {
+  int P[NM], Q[NM], W[NM];  // straight-line: all 3 x NM loads in flight together
 #pragma unroll
-    for (int i = 0; i < NM; ++i) {
-      P[i] = r0[i * p.mod_stride];
-      Q[i] = r0[p.prod_stride + i * p.mod_stride];
-      W[i] = r0[2 * p.prod_stride + i * p.mod_stride];
-    }
-  } else {
-    // the residue of a sum is the sum of the k slabs' residues
-#pragma unroll
-    for (int i = 0; i < NM; ++i) P[i] = Q[i] = W[i] = 0;
-    for (int sl = 0; sl < p.nslab; ++sl) {
-      const int8_t* q = r0 + sl * p.slab_stride;
-#pragma unroll
-      for (int i = 0; i < NM; ++i) {
-        P[i] += q[i * p.mod_stride];
-        Q[i] += q[p.prod_stride + i * p.mod_stride];
-        W[i] += q[2 * p.prod_stride + i * p.mod_stride];
-      }
-    }
+  for (int i = 0; i < NM; ++i) {
+    P[i] = r0[i * p.mod_stride];
+    Q[i] = r0[p.prod_stride + i * p.mod_stride];
+    W[i] = r0[2 * p.prod_stride + i * p.mod_stride];
   }
   const double2 v = crt_finish<NM>(p, P, Q, W, m, n);
   if (p.peer) {
@@ -649,13 +648,9 @@ cudaError_t launch_ozaki_crt_cols(const OzCrtParams& p, int64_t ncols, cudaStrea
   if (ncols > 65535) return cudaErrorInvalidConfiguration;
   // rows m >= n0 only: the first row block starts at n0
   const dim3 grid(static_cast<unsigned>((p.n - (p.n0 & ~127) + 127) / 128), static_cast<unsigned>(ncols)), block(128);
-  const bool one = p.nslab == 1;
-#define HSB_OZ_CRT(NMV)                                                        \
-  case NMV:                                                                  \
-    if (one)                                                                 \
-      ozaki_crt_kernel<NMV, true><<<grid, block, 0, st>>>(p);                \
-    else                                                                     \
-      ozaki_crt_kernel<NMV, false><<<grid, block, 0, st>>>(p);               \
+#define HSB_OZ_CRT(NMV)                                   \
+  case NMV:                                             \
+    ozaki_crt_kernel<NMV><<<grid, block, 0, st>>>(p);   \
     break;
   switch (p.n_mod) {
     HSB_OZ_CRT(11)

@@ -54,9 +54,12 @@ constexpr int kOzTileBytes = 256 * 256;  // one tile of int8 residues, column-ma
 
 // The reduction (the concatenated segments, in 128-byte k chunks) is split into
 // slabs of ~16 KB of k: each work item covers one slab of one tile, so the
-// operand panels a wave of tiles streams (256 rows x slab) stay L2-resident
-// even for long reductions (C4: 46464 bytes of k), and the per-slab residues
-// are summed in the CRT (the product is linear).
+// operand panels the tiles in flight stream (256 rows x slab) stay L2-resident
+// even for long reductions (C4: 46464 bytes of k; DRAM 878 -> 345 GB per H
+// GEMM).  Slab s > 0 of a tile adds its residues into slab s-1's in place
+// (mod p): its epilogue warps wait on a per-(product, modulus, tile) counter
+// that slab s-1's warps bump -- work is claimed in order, so the counted item
+// was claimed earlier by a resident CTA pair and the wait always ends.
 struct OzGemmParams {
   // maps[prod][seg][side]: 3-D int8 maps {k, cols, modulus}, box {128, 128, 1}
   CUtensorMap map[3][kOzMaxSeg][2];
@@ -68,20 +71,20 @@ struct OzGemmParams {
   int32_t ntiles;       // tiles of this launch: tile_list[tile0 .. tile0 + ntiles)
   int32_t tile0;
   const int2* tile_list;  // (tile row, tile col) of the 256 x 256 tiles on or below the diagonal
-  int8_t* res;          // residues [prod][slab][modulus][tile][256 x 256 col-major]
+  int8_t* res;          // residues [prod][modulus][tile][256 x 256 col-major]
   int64_t mod_stride;   // bytes between moduli (all tiles of the triangle * kOzTileBytes)
-  int64_t slab_stride;  // bytes between slabs (mod_stride * n_mod)
-  int64_t prod_stride;  // bytes between products (slab_stride * nslab)
+  int64_t prod_stride;  // bytes between products (mod_stride * n_mod)
   int32_t* counter;     // work-stealing counter (zeroed by the launcher)
+  int32_t* slab_cnt;    // nslab > 1: per (prod, modulus, tile), epilogue warps finished (zeroed)
+  int32_t tiles_total;  // tiles of the whole triangle (slab_cnt / residue indexing)
 };
 
 struct OzCrtParams {
   const int8_t* res;
-  int64_t mod_stride, slab_stride, prod_stride;
+  int64_t mod_stride, prod_stride;
   const int32_t* tile_index;  // T x T: tile_list position of tile (tm, tn), tm >= tn
   int32_t T;                  // tiles per side
   int32_t n0;                 // first output column of this launch (grid.y columns follow)
-  int32_t nslab;
   int32_t n_mod;
   int32_t n;
   int32_t b;                 // operand integer bits
