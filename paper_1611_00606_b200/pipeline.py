@@ -205,7 +205,7 @@ def build_hs(p, policy=None, force_nonhpd: bool = False) -> BuildOutput:
     return _build_host(p, policy, force_nonhpd)
 
 
-def _build_host(p, policy, force_nonhpd, slot: int = 0, stream=None) -> BuildOutput:
+def _build_host(p, policy, force_nonhpd, slot: int = 0, stream=None, s_ready=None) -> BuildOutput:
     validate_instance(p, check_stack_values=False)  # A/B values are checked while staging
     pol = _policy(policy)
     dims = Dims(p.dims.n_atoms, p.dims.n_l, p.dims.n_g)
@@ -216,6 +216,8 @@ def _build_host(p, policy, force_nonhpd, slot: int = 0, stream=None) -> BuildOut
     out.location = _lib.HSB_LOC_HOST
     out.ld = dims.n_g
     out.h, out.s = h.ctypes.data, s.ctypes.data
+    if s_ready is not None:
+        out.s_ready = s_ready
     tim, info = _call_build(pol, prob, out, stream, force_nonhpd, dims.n_atoms, slot)
     t = _timings_dict(tim)
     led = ledger_from_timings(dims, info, t, force_nonhpd)
@@ -231,6 +233,7 @@ def iter_hs_kpoints(instances, policy=None, force_nonhpd: bool = False, depth: i
     beyond the one being consumed, so pinned output memory stays bounded when
     the caller drops each result after use."""
     import threading
+    import time
 
     import torch
 
@@ -244,24 +247,52 @@ def iter_hs_kpoints(instances, policy=None, force_nonhpd: bool = False, depth: i
         return
     dev = torch.device("cuda", pol.device)
     streams = [torch.cuda.Stream(device=dev) for _ in range(depth)]
+    if pol.pinned_outputs:
+        # up to depth + 1 results (two matrices each) are alive at once: have the
+        # caching pinned allocator hold that many blocks before the lanes start,
+        # so no 1 GB cudaHostAlloc lands in the middle of the pipeline
+        n_max = max(int(p.dims.n_g) for p in instances)
+        warm = [_host_matrix(n_max, True) for _ in range(2 * (depth + 1))]
+        del warm
     results = [None] * len(instances)
     ready = [threading.Event() for _ in instances]
-    credits = threading.Semaphore(depth)
+    # window: k-point i may start once fewer than depth results ahead of it are
+    # unconsumed (i < consumed + depth), so a fast lane cannot use up the
+    # window with later k-points while the consumer waits for an earlier one
+    window = threading.Condition()
+    consumed = [0]
     failure = []
+
+    # stagger: lane k starts once lane k-1's first S is final (its event), so the
+    # lanes alternate between transfers and kernels instead of running in lockstep
+    s_events = [torch.cuda.Event() for _ in range(depth)]
+    for ev in s_events:
+        ev.record(torch.cuda.current_stream(dev))  # materialise the CUDA events
+    entered = [threading.Event() for _ in range(depth)]
 
     def lane(slot):  # one thread per context: k-points slot, slot + depth, ...
         st = ctypes.c_void_p(streams[slot].cuda_stream)
         try:
-            for i in range(slot, len(instances), depth):
-                credits.acquire()
+            if slot > 0:
+                entered[slot - 1].wait()
+                time.sleep(0.005)  # lane slot-1 enqueues its S event within its first milliseconds
+                s_events[slot - 1].synchronize()
+            for n_done, i in enumerate(range(slot, len(instances), depth)):
+                with window:
+                    window.wait_for(lambda: failure or i < consumed[0] + depth)
                 if failure:
                     return
-                results[i] = _build_host(instances[i], pol, force_nonhpd, slot=slot, stream=st)
+                if n_done == 0:
+                    entered[slot].set()
+                results[i] = _build_host(instances[i], pol, force_nonhpd, slot=slot, stream=st,
+                                         s_ready=s_events[slot].cuda_event if n_done == 0 else None)
                 ready[i].set()
         except BaseException as exc:  # noqa: BLE001 - re-raised in the consumer
             failure.append(exc)
             for e in ready:
                 e.set()
+        finally:
+            entered[slot].set()
 
     threads = [threading.Thread(target=lane, args=(k,), daemon=True) for k in range(depth)]
     for t in threads:
@@ -272,13 +303,15 @@ def iter_hs_kpoints(instances, policy=None, force_nonhpd: bool = False, depth: i
             if failure:
                 raise failure[0]
             r, results[i] = results[i], None
-            credits.release()
+            with window:
+                consumed[0] = i + 1
+                window.notify_all()
             yield r
     finally:
-        if not failure:  # stop lanes that are still waiting for a credit
+        if not failure:  # stop lanes that are still waiting for the window
             failure.append(GeneratorExit())
-        for _ in range(len(instances)):
-            credits.release()
+        with window:
+            window.notify_all()
         for t in threads:
             t.join()
 

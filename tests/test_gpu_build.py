@@ -196,3 +196,22 @@ def test_kpoint_pipeline_matches_serial_builds(cm):
         assert a.s.matrix.tobytes() == b.s.matrix.tobytes()
         assert (a.split.hpd, a.split.nonhpd) == (b.split.hpd, b.split.nonhpd)
         assert rel_frob_error(b.h.matrix, brute.h_brute(p)) < TOL
+
+
+@pytest.mark.timeout(120)
+def test_kpoint_iterator_early_exit_and_slow_consumer():
+    # the window flow control must neither deadlock when a lane runs ahead
+    # (staggered start) nor leave lanes blocked when the consumer stops early
+    import time
+
+    from paper_1611_00606_b200 import iter_hs_kpoints
+
+    ps = [generate(ProblemSpec(Dims(2, 16, 120), seed=90 + i)) for i in range(7)]
+    got = []
+    for i, out in enumerate(iter_hs_kpoints(ps, _pol("int8"), depth=2)):
+        time.sleep(0.02)  # slow consumer
+        got.append(out.split.hpd + out.split.nonhpd)
+        if i == 3:
+            break  # generator closed with lanes still running
+    assert got == [2, 2, 2, 2]
+    assert len(list(iter_hs_kpoints(ps, _pol("int8"), depth=3))) == 7
