@@ -10,13 +10,13 @@
 //   A    = c [ j_l(KR) udot'_l - K j_l'(KR) udot_l ] / D_l
 //   B    = c [ K j_l'(KR) u_l  - j_l(KR) u'_l      ] / D_l,   D_l = u udot' - udot u'
 //
-// One CTA per G column.  The per-column special functions are computed once
-// into shared memory (Y_lm by the normalised associated-Legendre recurrence,
-// one lane per m; j_l by upward recurrence for x >= lmax+1, Miller's downward
-// recurrence below that, a 3-term series for x < 1e-3; structure phases by
-// sincos), then all threads stream the n_atoms * N_L rows of the column of A
-// and B with coalesced 16-byte stores: the kernel is HBM-write bound
-// (2 * K * 16 bytes per column).
+// One CTA per kMatchCols G columns.  The per-column special functions are
+// computed once into shared memory (Y_lm by the normalised associated-Legendre
+// recurrence, one lane per m; j_l by upward recurrence for x >= lmax+1,
+// Miller's downward recurrence below that, a 3-term series for x < 1e-3;
+// structure phases by sincos), then all threads stream the n_atoms * N_L rows
+// of the columns of A and B with coalesced 16-byte stores: the kernel is
+// HBM-write bound (2 * K * 16 bytes per column).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -89,52 +89,87 @@ __device__ void spherical_bessel(double x, int nmax, double* j) {
   for (int l = 0; l <= nmax; ++l) j[l] *= scale;
 }
 
-__global__ void match_coeffs_kernel(MatchParams p, double2* __restrict__ A, double2* __restrict__ B) {
+// kMatchCols G columns per CTA: the special functions of the kMatchCols
+// columns are computed concurrently (warps 4..7: Y_lm, one column at a time each;
+// warps 0..3: radial factors and structure phases of all of them), then all
+// threads stream the kMatchCols columns.  At C3 (K = 3872 rows) one column is
+// only 124 KB of stores, so one column per CTA left the HBM 43 % idle behind
+// the per-column prologue.
+constexpr int kMatchCols = 8;
+constexpr int kMatchThreads = 256;
+
+__global__ void __launch_bounds__(kMatchThreads) match_coeffs_kernel(MatchParams p, double2* __restrict__ A,
+                                                                      double2* __restrict__ B) {
   extern __shared__ double smem_d[];
   const int lmax = p.lmax, nlm = (lmax + 1) * (lmax + 1), nl1 = lmax + 1;
-  double2* ys = reinterpret_cast<double2*>(smem_d);          // nlm: pre i^l conj(Y_lm)
-  double2* phase = ys + nlm;                                  // n_atoms
-  double* fa = reinterpret_cast<double*>(phase + p.n_atoms);  // n_types * (lmax+1)
-  double* fb = fa + p.n_types * nl1;
-  unsigned char* lidx = reinterpret_cast<unsigned char*>(fb + p.n_types * nl1);  // nlm
+  double2* ys = reinterpret_cast<double2*>(smem_d);                     // [col][nlm]: pre i^l conj(Y_lm)
+  double2* phase = ys + kMatchCols * nlm;                               // [col][n_atoms]
+  double* fa = reinterpret_cast<double*>(phase + kMatchCols * p.n_atoms);  // [col][n_types * (lmax+1)]
+  double* fb = fa + kMatchCols * p.n_types * nl1;
+  unsigned char* lidx = reinterpret_cast<unsigned char*>(fb + kMatchCols * p.n_types * nl1);  // nlm
 
-  const int g = blockIdx.x;
-  const int tid = threadIdx.x;
-  const int* gv = p.gvec + 3 * g;
-  const double f0 = p.kpt[0] + gv[0], f1 = p.kpt[1] + gv[1], f2 = p.kpt[2] + gv[2];
-  const double kx = f0 * p.recip[0] + f1 * p.recip[3] + f2 * p.recip[6];
-  const double ky = f0 * p.recip[1] + f1 * p.recip[4] + f2 * p.recip[7];
-  const double kz = f0 * p.recip[2] + f1 * p.recip[5] + f2 * p.recip[8];
-  const double rho = sqrt(kx * kx + ky * ky);
-  const double kn = sqrt(kx * kx + ky * ky + kz * kz);
+  const int64_t g0 = static_cast<int64_t>(blockIdx.x) * kMatchCols;
+  const int ncols = static_cast<int>(p.n_g - g0 < kMatchCols ? p.n_g - g0 : kMatchCols);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  auto kvec = [&](int c, double& kx, double& ky, double& kz) {
+    const int* gv = p.gvec + 3 * (g0 + c);
+    const double f0 = p.kpt[0] + gv[0], f1 = p.kpt[1] + gv[1], f2 = p.kpt[2] + gv[2];
+    kx = f0 * p.recip[0] + f1 * p.recip[3] + f2 * p.recip[6];
+    ky = f0 * p.recip[1] + f1 * p.recip[4] + f2 * p.recip[7];
+    kz = f0 * p.recip[2] + f1 * p.recip[5] + f2 * p.recip[8];
+  };
 
-  // ---- radial factors per (type, l)
-  for (int t = tid; t < p.n_types; t += blockDim.x) {
-    double j[kMaxL + 2];
-    const double x = kn * p.rmt[t];
-    spherical_bessel(x, lmax + 1, j);
-    for (int l = 0; l <= lmax; ++l) {
-      const double dj = (l == 0) ? -j[1] : (l * j[l - 1] - (l + 1) * j[l + 1]) / (2 * l + 1);
-      const double* r = p.radial + (t * nl1 + l) * 4;  // u, u', udot, udot'
-      const double d = r[0] * r[3] - r[2] * r[1];
-      fa[t * nl1 + l] = (j[l] * r[3] - kn * dj * r[2]) / d;
-      fb[t * nl1 + l] = (kn * dj * r[0] - j[l] * r[1]) / d;
+  if (warp < 4) {
+    // ---- radial factors per (column, type, l)
+    for (int i = tid; i < ncols * p.n_types; i += 128) {
+      const int c = i / p.n_types, t = i - c * p.n_types;
+      double kx, ky, kz;
+      kvec(c, kx, ky, kz);
+      const double kn = sqrt(kx * kx + ky * ky + kz * kz);
+      double j[kMaxL + 2];
+      spherical_bessel(kn * p.rmt[t], lmax + 1, j);
+      for (int l = 0; l <= lmax; ++l) {
+        const double dj = (l == 0) ? -j[1] : (l * j[l - 1] - (l + 1) * j[l + 1]) / (2 * l + 1);
+        const double* r = p.radial + (t * nl1 + l) * 4;  // u, u', udot, udot'
+        const double d = r[0] * r[3] - r[2] * r[1];
+        fa[(c * p.n_types + t) * nl1 + l] = (j[l] * r[3] - kn * dj * r[2]) / d;
+        fb[(c * p.n_types + t) * nl1 + l] = (kn * dj * r[0] - j[l] * r[1]) / d;
+      }
     }
-  }
-  // ---- spherical harmonics: lane m of warp 1 runs the l recurrence for m
-  if (tid >= 32 && tid < 64) {
-    const int m = tid - 32;
+    // ---- structure phases per (column, atom)
+    for (int i = tid; i < ncols * p.n_atoms; i += 128) {
+      const int c = i / p.n_atoms, a = i - c * p.n_atoms;
+      double kx, ky, kz;
+      kvec(c, kx, ky, kz);
+      const double* tau = p.tau + 3 * a;
+      double sn, cs;
+      sincos(kx * tau[0] + ky * tau[1] + kz * tau[2], &sn, &cs);
+      phase[c * p.n_atoms + a] = make_double2(cs, sn);
+    }
+    for (int L = tid; L < nlm; L += 128) {
+      int l = 0;
+      while ((l + 1) * (l + 1) <= L) ++l;
+      lidx[L] = static_cast<unsigned char>(l);
+    }
+  } else {
+    // ---- spherical harmonics: warp 4 + w handles columns w, w + 4, ...; lane m
+    // runs the l recurrence for m
+    for (int c = warp - 4; c < ncols; c += 4) {
+    const int m = lane;
     if (m <= lmax) {
+      double kx, ky, kz;
+      kvec(c, kx, ky, kz);
+      const double rho = sqrt(kx * kx + ky * ky);
+      const double kn = sqrt(kx * kx + ky * ky + kz * kz);
       const double ct = kn > 0.0 ? kz / kn : 1.0;
       const double st = kn > 0.0 ? rho / kn : 0.0;
       const double cp = rho > 0.0 ? kx / rho : 1.0, sp = rho > 0.0 ? ky / rho : 0.0;
-      // e^{i m phi}
-      double2 em = make_double2(1.0, 0.0);
+      double2 em = make_double2(1.0, 0.0);  // e^{i m phi}
       for (int q = 0; q < m; ++q) em = cmul(em, make_double2(cp, sp));
-      // P_mm (normalised, Condon-Shortley phase)
-      double pmm = 0.28209479177387814;  // 1/sqrt(4 pi)
+      double pmm = 0.28209479177387814;  // P_mm, normalised, Condon-Shortley phase; 1/sqrt(4 pi)
       for (int q = 1; q <= m; ++q) pmm *= -sqrt((2.0 * q + 1.0) / (2.0 * q)) * st;
       double plm2 = 0.0, plm1 = pmm;
+      double2* yc = ys + c * nlm;
       for (int l = m; l <= lmax; ++l) {
         double plm;
         if (l == m) {
@@ -152,48 +187,46 @@ __global__ void match_coeffs_kernel(MatchParams p, double2* __restrict__ A, doub
         }
         // Y_lm = plm e^{i m phi};  Y_{l,-m} = (-1)^m conj(Y_lm)
         const double2 y = make_double2(plm * em.x, plm * em.y);
-        // i^l
-        const int lr = l & 3;
+        const int lr = l & 3;  // i^l
         const double2 il = lr == 0 ? make_double2(1, 0) : lr == 1 ? make_double2(0, 1)
                          : lr == 2 ? make_double2(-1, 0) : make_double2(0, -1);
         const double2 cy = cmul(il, make_double2(y.x, -y.y));  // i^l conj(Y_lm)
-        ys[l * l + l + m] = make_double2(p.pre * cy.x, p.pre * cy.y);
+        yc[l * l + l + m] = make_double2(p.pre * cy.x, p.pre * cy.y);
         if (m > 0) {
           const double sgn = (m & 1) ? -1.0 : 1.0;  // conj(Y_{l,-m}) = (-1)^m Y_lm
           const double2 cyn = cmul(il, make_double2(sgn * y.x, sgn * y.y));
-          ys[l * l + l - m] = make_double2(p.pre * cyn.x, p.pre * cyn.y);
+          yc[l * l + l - m] = make_double2(p.pre * cyn.x, p.pre * cyn.y);
         }
-        lidx[l * l + l + m] = static_cast<unsigned char>(l);
-        lidx[l * l + l - m] = static_cast<unsigned char>(l);
       }
     }
-  }
-  // ---- structure phases
-  for (int a = tid; a < p.n_atoms; a += blockDim.x) {
-    const double* tau = p.tau + 3 * a;
-    double s, c;
-    sincos(kx * tau[0] + ky * tau[1] + kz * tau[2], &s, &c);
-    phase[a] = make_double2(c, s);
+    }
   }
   __syncthreads();
 
-  // ---- stream the column: rows (atom, L)
+  // ---- stream the columns: rows (atom, L), 16-byte coalesced stores
   const int64_t K = static_cast<int64_t>(p.n_atoms) * nlm;
-  double2* colA = A + static_cast<int64_t>(g) * p.ld;
-  double2* colB = B + static_cast<int64_t>(g) * p.ld;
-  for (int64_t r = tid; r < K; r += blockDim.x) {
-    const int a = static_cast<int>(r / nlm), L = static_cast<int>(r - static_cast<int64_t>(a) * nlm);
-    const int t = p.type_of[a], l = lidx[L];
-    const double2 base = cmul(ys[L], phase[a]);
-    const double ca = fa[t * nl1 + l], cb = fb[t * nl1 + l];
-    colA[r] = make_double2(base.x * ca, base.y * ca);
-    colB[r] = make_double2(base.x * cb, base.y * cb);
+  for (int c = 0; c < ncols; ++c) {
+    double2* colA = A + (g0 + c) * p.ld;
+    double2* colB = B + (g0 + c) * p.ld;
+    const double2* yc = ys + c * nlm;
+    const double2* ph = phase + c * p.n_atoms;
+    const double* fac = fa + c * p.n_types * nl1;
+    const double* fbc = fb + c * p.n_types * nl1;
+    for (int64_t r = tid; r < K; r += kMatchThreads) {
+      const int a = static_cast<int>(r / nlm), L = static_cast<int>(r - static_cast<int64_t>(a) * nlm);
+      const int t = p.type_of[a], l = lidx[L];
+      const double2 base = cmul(yc[L], ph[a]);
+      const double ca = fac[t * nl1 + l], cb = fbc[t * nl1 + l];
+      colA[r] = make_double2(base.x * ca, base.y * ca);
+      colB[r] = make_double2(base.x * cb, base.y * cb);
+    }
   }
 }
 
 size_t match_smem_bytes(const MatchParams& p) {
   const size_t nlm = static_cast<size_t>(p.lmax + 1) * (p.lmax + 1);
-  return nlm * 16 + static_cast<size_t>(p.n_atoms) * 16 + 2 * static_cast<size_t>(p.n_types) * (p.lmax + 1) * 8 +
+  return kMatchCols * (nlm * 16 + static_cast<size_t>(p.n_atoms) * 16 +
+                       2 * static_cast<size_t>(p.n_types) * (p.lmax + 1) * 8) +
          nlm + 16;
 }
 
@@ -204,8 +237,10 @@ cudaError_t launch_match_coeffs(const MatchParams& p, double* A, double* B, cuda
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  match_coeffs_kernel<<<static_cast<unsigned>(p.n_g), 256, smem, st>>>(p, reinterpret_cast<double2*>(A),
-                                                                       reinterpret_cast<double2*>(B));
+  const int64_t blocks = (p.n_g + kMatchCols - 1) / kMatchCols;
+  if (blocks <= 0) return cudaSuccess;
+  match_coeffs_kernel<<<static_cast<unsigned>(blocks), kMatchThreads, smem, st>>>(
+      p, reinterpret_cast<double2*>(A), reinterpret_cast<double2*>(B));
   return cudaGetLastError();
 }
 
