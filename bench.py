@@ -92,7 +92,8 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.lines: list[str] = []
+        self.lines: list[tuple[float, str]] = []  # (host time, csv line)
+        self.window = (0.0, float("inf"))
 
     def start(self):
         try:
@@ -106,7 +107,20 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def wait_first(self, timeout: float = 5.0) -> None:
+        """nvidia-smi takes a few hundred ms to print its first sample: wait for
+        it, so the samples that follow can fall inside a short timed region."""
+        t0 = time.perf_counter()
+        while self.proc is not None and not self.lines and time.perf_counter() - t0 < timeout:
+            time.sleep(0.01)
+
+    def begin(self) -> None:
+        self.window = (time.perf_counter(), float("inf"))
+
+    def end(self) -> None:
+        self.window = (self.window[0], time.perf_counter())
 
     def stop(self) -> dict:
         if self.proc is None:
@@ -119,7 +133,10 @@ class ClockSampler:
         self._t.join(timeout=2)
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
+        lo, hi = self.window
+        # a line read at t was sampled up to one interval (0.1 s) before t
+        inside = [line for t, line in self.lines if lo <= t <= hi + 0.1]
+        for line in inside:
             f = [x.strip() for x in line.split(",")]
             if len(f) < 9:
                 continue
@@ -191,7 +208,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C3", choices=sorted(CONFIG_DESC))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -278,11 +295,16 @@ def main():
     barrier()
     sampler = ClockSampler(dev_index)
     sampler.start()
+    sampler.wait_first()
+    step()  # keep the GPU busy while nvidia-smi starts (an extra untimed warm-up step)
+    barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler.begin()
     ev0.record(stream)
     ts = [step() for _ in range(args.steps)]
     ev1.record(stream)
     barrier()
+    sampler.end()
     clocks = sampler.stop()
     ms = ev0.elapsed_time(ev1) / args.steps
     ms = hsdist.max_over_ranks(ms, dev)
@@ -380,6 +402,7 @@ def main():
                 _ = out.h.matrix[0, 0]
             torch.cuda.synchronize(dev)
             single_ms = (time.perf_counter() - t0) / args.steps * 1e3
+            pcie = (out.timings["h2d_bytes"], out.timings["d2h_bytes"])  # counted by the library per copy
             del out
             # (b) the K steps as one k-point batch through build_hs_kpoints: two
             # contexts/streams overlap one step's PCIe transfers with the next
@@ -403,6 +426,8 @@ def main():
         h2d = sum(np.asarray(b).nbytes for name in ("a_blocks", "b_blocks", "t_aa", "t_ab", "t_bb", "u_norms")
                   for b in getattr(p, name))
         d2h = 2 * n_g * (ncols // world) * 16
+        if world == 1:
+            h2d, d2h = pcie  # H and S cross PCIe as lower triangles (host mirror completes them)
         e2e = {"value": flops_full / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
                "inputs": "pageable numpy" if args.pageable_inputs else "pinned numpy (pin_instance)",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}

@@ -165,6 +165,18 @@ typedef struct {
                                       (S1, U norm, S2, H1, H2, H3 separately,
                                       mirror last) instead of the fused
                                       H and S launches */
+#define HSB_OPT_VALIDATE     0x4u  /* host inputs: check the T blocks and u
+                                      (finite, T_AA / T_BB Hermitian within
+                                      1e-14 (1 + ||T||_F), u > 0) in the order
+                                      of probgen.validate_instance
+                                      (probgen.py:140-168) before any transfer;
+                                      A / B finiteness is always checked while
+                                      they are staged */
+#define HSB_OPT_FULL_D2H     0x8u  /* pinned host outputs: download both
+                                      triangles of H and S instead of the lower
+                                      triangles + host-side conjugate mirror
+                                      (the default on the streamed INT8 path;
+                                      same bytes in the result) */
 
 /* Receive slots of an atom-sharded build across n_ranks GPUs (north star (3);
  * SURVEY 8f row 2).  Rank q owns columns [q * cols_per_rank, (q + 1) *
@@ -221,12 +233,16 @@ typedef struct {
   int32_t n_hpd, n_nonhpd;  /* builder.SplitCounts (builder.py:51-54) */
   int32_t launches;         /* kernels launched by this call */
   int32_t reserved;
+  double h2d_bytes, d2h_bytes;  /* PCIe bytes moved by this call (host inputs /
+                                   outputs; lower-triangle downloads count once) */
 } hsb_timings;
 
 /* Build H and S.  `atom_info` (optional, n_atoms int32) receives the
  * potrf_lower info per atom: 0 = Cholesky succeeded (HPD path), j>0 = first
  * non-positive leading minor (kernels.py:296-325), -1 = forced non-HPD.
- * Validation (probgen.validate_instance) is done by the host layer. */
+ * Shapes are the caller's (host layer's) to validate; values of T and u with
+ * HSB_OPT_VALIDATE; A and B non-finite values are always reported
+ * (HSB_ERR_INVARIANT). */
 HSB_API hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p,
                         uint32_t opts, const hsb_output* out,
                         hsb_timings* timings, int32_t* atom_info);

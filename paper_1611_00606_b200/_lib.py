@@ -25,6 +25,8 @@ HSB_LOC_HOST = 0
 HSB_LOC_DEVICE = 1
 HSB_OPT_FORCE_NONHPD = 0x1
 HSB_OPT_UNFUSED = 0x2
+HSB_OPT_VALIDATE = 0x4
+HSB_OPT_FULL_D2H = 0x8
 HSB_CPLX_4M = 0
 HSB_CPLX_3M = 1
 COMPLEX_MULT = {"4m": HSB_CPLX_4M, "3m": HSB_CPLX_3M}
@@ -62,7 +64,7 @@ class HsbTimings(ctypes.Structure):
                 ("loop1", "loop2", "unorm", "s1", "s2", "h1", "h2", "h3", "h2d", "d2h", "total",
                  "s_core", "h_core")] + [
         ("n_hpd", ctypes.c_int32), ("n_nonhpd", ctypes.c_int32), ("launches", ctypes.c_int32),
-        ("reserved", ctypes.c_int32)]
+        ("reserved", ctypes.c_int32), ("h2d_bytes", ctypes.c_double), ("d2h_bytes", ctypes.c_double)]
 
 
 class HsbPhys(ctypes.Structure):
@@ -116,7 +118,7 @@ def load():
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.hsb_abi_version() != 4:
+        if lib.hsb_abi_version() != 5:
             raise RuntimeError("libhsb200.so ABI version mismatch; rebuild it")
         _lib = lib
         return lib

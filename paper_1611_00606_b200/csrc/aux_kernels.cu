@@ -292,6 +292,67 @@ __global__ void fill_i32_kernel(int32_t* p, int64_t n, int32_t v) {
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
     p[i] = v;
 }
+// Loop 2 routing on the device (the HPD / non-HPD split of builder.py:135-160):
+// from every atom's potrf info, the row offset of its product in R = [Y_hpd ;
+// X_nh] and the gather lists of the non-HPD atoms, all in atom order.  info
+// is also exported to mapped host memory, so the host learns the split
+// without a copy-engine transfer queued behind other streams' bulk copies.
+// One block; chunked block-wide scan over the atoms.
+__global__ void route_atoms_kernel(const int32_t* __restrict__ info, int na, int nl, int32_t* __restrict__ offs,
+                                   int32_t* __restrict__ info_host) {
+  __shared__ int s_warp[32];
+  __shared__ int s_base;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  int cnt = 0;
+  for (int i = tid; i < na; i += blockDim.x) cnt += info[i] == 0;
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(~0u, cnt, o);
+  if (lane == 0) s_warp[warp] = cnt;
+  if (tid == 0) s_base = 0;
+  __syncthreads();
+  int n_hpd = 0;
+  for (int w = 0; w < nw; ++w) n_hpd += s_warp[w];
+  __syncthreads();
+  for (int c0 = 0; c0 < na; c0 += blockDim.x) {
+    const int i = c0 + tid;
+    const int v = i < na ? info[i] : 1;
+    const bool hpd = i < na && v == 0;
+    const unsigned m = __ballot_sync(~0u, hpd);
+    if (lane == 0) s_warp[warp] = __popc(m);
+    __syncthreads();
+    int ih = s_base + __popc(m & ((1u << lane) - 1));  // HPD atoms before atom i
+    for (int w = 0; w < warp; ++w) ih += s_warp[w];
+    if (i < na) {
+      info_host[i] = v;
+      if (hpd) {
+        offs[i] = ih * nl;
+      } else {
+        const int in = i - ih;  // non-HPD atoms before atom i
+        offs[i] = (n_hpd + in) * nl;
+        offs[na + in] = i * nl;  // A_nh source rows
+        offs[2 * na + in] = in * nl;  // A_nh destination rows
+      }
+    }
+    __syncthreads();
+    if (tid == 0)
+      for (int w = 0; w < nw; ++w) s_base += s_warp[w];
+    __syncthreads();
+  }
+}
+cudaError_t launch_route_atoms(const int32_t* info, int na, int nl, int32_t* offs, int32_t* info_host,
+                               cudaStream_t st) {
+  route_atoms_kernel<<<1, 1024, 0, st>>>(info, na, nl, offs, info_host);
+  return cudaGetLastError();
+}
+
+__global__ void copy_i32_kernel(const int32_t* __restrict__ src, int32_t* __restrict__ dst, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[i];
+}
+cudaError_t launch_copy_i32(const int32_t* src, int32_t* dst, int n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  copy_i32_kernel<<<grid_for(n, 256, 64), 256, 0, st>>>(src, dst, n);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fill_i32(int32_t* p, int64_t n, int32_t v, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   fill_i32_kernel<<<grid_for(n, 256, 1024), 256, 0, st>>>(p, n, v);
@@ -326,7 +387,7 @@ cudaError_t launch_stack_blocks(const double* raw, double* dst, int n_atoms, int
 
 cudaError_t launch_first_nonfinite(const double* v, int n_blocks, int64_t doubles_per_block, int* flag,
                                    cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(flag, 0x7f, sizeof(int), st);
+  cudaError_t e = launch_fill_i32(flag, 1, 0x7f7f7f7f, st);
   if (e != cudaSuccess) return e;
   const int64_t total = static_cast<int64_t>(n_blocks) * doubles_per_block;
   first_nonfinite_kernel<<<grid_for(total, 256, 148 * 16), 256, 0, st>>>(

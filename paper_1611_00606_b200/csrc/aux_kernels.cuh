@@ -20,6 +20,11 @@ cudaError_t launch_diag_scale(const double* src, int64_t lds, double* dst, int64
                               int64_t rows, int64_t cols, cudaStream_t st);
 cudaError_t launch_mirror(double* c, int64_t ldc, int n, cudaStream_t st);
 cudaError_t launch_fill_i32(int32_t* p, int64_t n, int32_t v, cudaStream_t st);
+// device-side Loop 2 routing (offsets of R / gather lists) + info export to mapped host memory
+cudaError_t launch_route_atoms(const int32_t* info, int na, int nl, int32_t* offs, int32_t* info_host,
+                               cudaStream_t st);
+// small int32 copies by a kernel (e.g. into mapped host memory: no copy-engine queue)
+cudaError_t launch_copy_i32(const int32_t* src, int32_t* dst, int n, cudaStream_t st);
 cudaError_t launch_sum_planes(const double* x, int64_t ldx, int64_t rows, int64_t cols, double* minus,
                               double* plus, int64_t ldp, cudaStream_t st);
 cudaError_t launch_gather_rows(const double* src, int64_t lds, double* dst, int64_t ldd, const int32_t* src_off,

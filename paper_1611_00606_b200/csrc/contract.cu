@@ -286,7 +286,7 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
     void* sbuf;
     CKS(ws(ctx, "oz_slab_cnt", nc * sizeof(int32_t), &sbuf));
     gp.slab_cnt = static_cast<int32_t*>(sbuf);
-    CK(cudaMemsetAsync(sbuf, 0, nc * sizeof(int32_t), st));
+    CK(launch_fill_i32(static_cast<int32_t*>(sbuf), static_cast<int64_t>(nc), 0, st));
   }
   if (gp.nseg == 0) CK(cudaMemsetAsync(rbuf, 0, static_cast<size_t>(3 * gp.prod_stride), st));
 

@@ -138,6 +138,49 @@ struct Timeline {
 
 inline cudaError_t timeline_mark(Timeline* tl, cudaStream_t st, const char* tag) { return tl->mark(st, tag); }
 
+// Absolute GPU timeline across calls and contexts (HSB_TRACE=1): events on
+// any stream, resolved after the call against one process-wide base event
+// and printed as "[hsb trace] <ctx> <tag> <ms>".  Diagnostics only.
+struct GpuTrace {
+  bool on = std::getenv("HSB_TRACE") != nullptr;
+  const void* who = nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> marks;
+  static cudaEvent_t base() {
+    static cudaEvent_t b = [] {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, 0);
+      cudaEventSynchronize(e);
+      return e;
+    }();
+    return b;
+  }
+  ~GpuTrace() {
+    for (auto& m : marks) cudaEventDestroy(m.second);
+  }
+  void mark(cudaStream_t st, const std::string& tag) {
+    if (!on) return;
+    base();
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    marks.push_back({tag, e});
+    cudaEventRecord(e, st);
+  }
+  void report() {
+    if (!on) return;
+    std::string s;
+    for (auto& m : marks) {
+      float ms = -1.f;
+      cudaEventSynchronize(m.second);
+      cudaEventElapsedTime(&ms, base(), m.second);
+      char buf[160];
+      std::snprintf(buf, sizeof buf, "[hsb trace] %p %s %.3f\n", who, m.first.c_str(), ms);
+      s += buf;
+    }
+    std::fputs(s.c_str(), stderr);
+  }
+};
+
 struct ZrkCall {
   std::vector<Seg> segs;
   int64_t m = 0, n = 0;

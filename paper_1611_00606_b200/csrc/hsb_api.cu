@@ -15,6 +15,16 @@
 //
 // With HSB_OPT_UNFUSED the large updates run as one launch per reference
 // section, in the reference's order, followed by a separate mirror.
+#include <omp.h>
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
+
+#include <condition_variable>
+#include <deque>
+#include <mutex>
+#include <thread>
+
 #include "host_ctx.cuh"
 
 using namespace hsb_host;
@@ -22,7 +32,7 @@ using namespace hsb_host;
 // =============================================================================
 extern "C" {
 
-int32_t hsb_abi_version(void) { return 4; }
+int32_t hsb_abi_version(void) { return 5; }
 
 hsb_status hsb_ctx_create(int32_t device, hsb_ctx** out) {
   hsb_ctx* ctx = nullptr;
@@ -279,6 +289,176 @@ ZrkCall tri_call(double* c, int64_t ldc, int64_t n, uint32_t flags, double beta)
 
 }  // namespace
 
+// probgen.validate_instance value checks of the small host inputs
+// (probgen.py:155-168): finiteness of T_AA, T_AB, T_BB, u (fields in that
+// order, atoms in order), then T_AA / T_BB Hermitian within
+// 1e-14 (1 + ||T||_F) (matcore.hermitian_defect, matcore.py:108-114), then
+// u > 0.  Host threads, no Python (the k-point lanes run it concurrently).
+// Hermitian outputs cross PCIe as lower triangles (each downloaded column
+// range [c0, c1) carries rows >= c0) and are completed on the host: once a
+// range has landed (its event), rows [c0, c1) of the columns >= c1 are the
+// conjugate transpose of the arrived panel.  Those rows of later columns are
+// never written by a later download (it starts at its own c0 >= c1), so the
+// host threads and the DMA engine touch disjoint bytes.  Halves the D2H bytes
+// (the e2e bound of the pinned-host path) for ~1 GB/s-per-core host work.
+struct HostMirror {
+  struct Job {
+    cudaEvent_t ev;
+    double* m;
+    int64_t ld, n, c0, c1;
+  };
+  // a worker thread waits for each range's event and mirrors it, so the
+  // caller keeps issuing downloads meanwhile
+  std::deque<Job> q;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::thread worker;
+  bool closing = false;
+  cudaError_t err = cudaSuccess;
+  int device = 0;
+  int threads = mirror_threads();
+  static int mirror_threads() {
+    static const int n = [] {
+      const char* e = std::getenv("HSB_MIRROR_THREADS");
+      const int v = e ? std::atoi(e) : 0;
+      return v > 0 ? v : std::max(1, omp_get_max_threads());
+    }();
+    return n;
+  }
+  ~HostMirror() { finish(); }
+  cudaError_t push(cudaStream_t cs, double* m, int64_t ld, int64_t n, int64_t c0, int64_t c1) {
+    if (c1 >= n) return cudaSuccess;  // nothing above the diagonal blocks
+    cudaEvent_t e;
+    cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    if (r != cudaSuccess) return r;
+    r = cudaEventRecord(e, cs);
+    if (r != cudaSuccess) {
+      cudaEventDestroy(e);
+      return r;
+    }
+    if (!worker.joinable()) {
+      cudaGetDevice(&device);
+      worker = std::thread([this] { loop(); });
+    }
+    std::lock_guard<std::mutex> lk(mu);
+    q.push_back({e, m, ld, n, c0, c1});
+    cv.notify_one();
+    return cudaSuccess;
+  }
+  void loop() {
+    cudaSetDevice(device);
+    for (;;) {
+      Job j;
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [this] { return closing || !q.empty(); });
+        if (q.empty()) return;
+        j = q.front();
+        q.pop_front();
+      }
+      cudaError_t e = cudaEventSynchronize(j.ev);
+      cudaEventDestroy(j.ev);
+      if (e != cudaSuccess) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (err == cudaSuccess) err = e;
+        continue;
+      }
+      run(j, threads);
+    }
+  }
+  static void run(const Job& j, int threads) {
+    constexpr int64_t tb = 64;
+    const int64_t ntj = (j.n - j.c1 + tb - 1) / tb, nti = (j.c1 - j.c0 + tb - 1) / tb;
+    double* m = j.m;
+    const int64_t ld = j.ld;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(threads)
+    for (int64_t t = 0; t < ntj * nti; ++t) {
+      const int64_t j0 = j.c1 + (t / nti) * tb, i0 = j.c0 + (t % nti) * tb;
+      const int64_t j1 = std::min(j.n, j0 + tb), i1 = std::min(j.c1, i0 + tb);
+      // (r, c) upper  <-  conj (c, r) lower; destination runs are contiguous
+      // in r and written with non-temporal stores (no read-for-ownership)
+      for (int64_t c = j0; c < j1; ++c)
+        for (int64_t r = i0; r < i1; ++r) {
+#if defined(__SSE2__)
+          const __m128d sign = _mm_set_pd(-0.0, 0.0);
+          _mm_stream_pd(m + 2 * (r + c * ld), _mm_xor_pd(_mm_load_pd(m + 2 * (c + r * ld)), sign));
+#else
+          m[2 * (r + c * ld)] = m[2 * (c + r * ld)];
+          m[2 * (r + c * ld) + 1] = -m[2 * (c + r * ld) + 1];
+#endif
+        }
+#if defined(__SSE2__)
+      _mm_sfence();
+#endif
+    }
+  }
+  // wait until every queued range is mirrored
+  cudaError_t finish() {
+    if (worker.joinable()) {
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        closing = true;
+        cv.notify_one();
+      }
+      worker.join();
+    }
+    return err;
+  }
+};
+
+static hsb_status validate_small_inputs(hsb_ctx* ctx, const hsb_problem* p) {
+  const int64_t na = p->n_atoms, nl = p->n_l;
+  enum { FIN_TAA, FIN_TAB, FIN_TBB, FIN_U, HERM_TAA, HERM_TBB, POS_U, NCHK };
+  int64_t first[NCHK];
+  for (auto& f : first) f = na;
+  const double* const* tf[3] = {p->t_aa, p->t_ab, p->t_bb};
+#pragma omp parallel for schedule(dynamic, 4) num_threads(std::max(1, std::min(8, omp_get_max_threads())))
+  for (int64_t a = 0; a < na; ++a) {
+    bool bad[NCHK] = {};
+    for (int f = 0; f < 3; ++f) {
+      const double* t = tf[f][a];
+      for (int64_t i = 0; i < 2 * nl * nl; ++i)
+        if (!std::isfinite(t[i])) {
+          bad[FIN_TAA + f] = true;
+          break;
+        }
+    }
+    const double* u = p->u_norms[a];
+    for (int64_t i = 0; i < nl; ++i) {
+      if (!std::isfinite(u[i])) bad[FIN_U] = true;
+      if (!(u[i] > 0)) bad[POS_U] = true;
+    }
+    for (int f = 0; f < 2; ++f) {
+      const double* t = f == 0 ? p->t_aa[a] : p->t_bb[a];  // column-major complex
+      double defect = 0, fro = 0;
+      for (int64_t j = 0; j < nl; ++j)
+        for (int64_t i = 0; i < nl; ++i) {
+          const double xr = t[2 * (i + j * nl)], xi = t[2 * (i + j * nl) + 1];
+          const double yr = t[2 * (j + i * nl)], yi = -t[2 * (j + i * nl) + 1];
+          defect = std::max(defect, std::hypot(xr - yr, xi - yi));
+          fro += xr * xr + xi * xi;
+        }
+      for (int64_t i = 0; i < nl; ++i) defect = std::max(defect, std::fabs(t[2 * (i + i * nl) + 1]));
+      if (defect > 1e-14 * (1.0 + std::sqrt(fro))) bad[f == 0 ? HERM_TAA : HERM_TBB] = true;
+    }
+    for (int c = 0; c < NCHK; ++c)
+      if (bad[c]) {
+#pragma omp critical(hsb_validate)
+        first[c] = std::min(first[c], a);
+      }
+  }
+  static const char* name[NCHK] = {"t_aa", "t_ab", "t_bb", "u_norms", "t_aa", "t_bb", "u_norms"};
+  static const char* what[NCHK] = {"contains non-finite entries", "contains non-finite entries",
+                                   "contains non-finite entries", "contains non-finite entries",
+                                   "is not Hermitian within 1e-14", "is not Hermitian within 1e-14",
+                                   "has non-positive entries"};
+  for (int c = 0; c < NCHK; ++c)
+    if (first[c] < na)
+      return fail(ctx, HSB_ERR_INVARIANT,
+                  std::string(name[c]) + "[" + std::to_string(first[c]) + "] " + what[c]);
+  return HSB_OK;
+}
+
 hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32_t opts, const hsb_output* out,
                         hsb_timings* tm, int32_t* atom_info) {
   if (!ctx) return fail(nullptr, HSB_ERR_INPUT, "ctx is NULL");
@@ -292,6 +472,10 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   if (K > (int64_t{1} << 31)) return fail(ctx, HSB_ERR_UNSUPPORTED, "stack too tall");
   if (p->location != HSB_LOC_HOST && p->location != HSB_LOC_DEVICE)
     return fail(ctx, HSB_ERR_INPUT, "unknown problem location");
+  if ((opts & HSB_OPT_VALIDATE) && p->location == HSB_LOC_HOST) {
+    if (!p->t_aa || !p->t_ab || !p->t_bb || !p->u_norms) return fail(ctx, HSB_ERR_INPUT, "host block arrays are NULL");
+    CKS(validate_small_inputs(ctx, p));
+  }
   cudaSetDevice(ctx->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (!ctx->copy_stream) CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
@@ -322,9 +506,13 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   const bool chunk_s = !unfused && ctx->engine == HSB_ENGINE_INT8 && out->location == HSB_LOC_HOST &&
                        host_is_pinned(out->s);
   int launches = 0;
+  double h2d_bytes = 0, d2h_bytes = 0;  // PCIe bytes this call moves (host in / out)
   Timeline tl;
   HostClock hc;  // host-side phase stamps, printed when HSB_DEBUG_TIMING is set
+  GpuTrace tr;    // absolute GPU timeline, printed when HSB_TRACE is set
+  tr.who = ctx;
   CK(tl.mark(st, "start"));
+  tr.mark(st, "start");
 
   // ------------------------------------------------------------ buffers
   const size_t stack_bytes = static_cast<size_t>(K) * ng * 16;
@@ -382,12 +570,16 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   if (static_cast<size_t>(nl) * (nl + 1) / 2 * 16 > kPotrfSmemMax)
     CKS(ws(ctx, "potrf_scr", static_cast<size_t>(na) * nl * (nl + 1) / 2 * 16, &potrf_scr));
   CKS(pinned(ctx, (static_cast<size_t>(na) * 4 + 2) * 4, &hostbuf));
+  // info and the non-finite flags come back through mapped host memory, written
+  // by kernels: a copy-engine transfer would queue behind other streams' bulk
+  // downloads (k-point lanes) and stall this call's compute stream
   int32_t* info_h = static_cast<int32_t*>(hostbuf);
-  int32_t* offs_h = info_h + na;  // 3 * na entries: R row offset, A_nh source rows, A_nh dest rows
+  int32_t* hostbuf_dev = nullptr;
+  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hostbuf_dev), hostbuf, 0));
   double* Z = static_cast<double*>(zbuf);
   double* UB = static_cast<double*>(ub);
   double* R = static_cast<double*>(rbuf);  // [Y_hpd ; X_nh]
-  int32_t* flag_h = offs_h + 3 * na;  // first non-finite atom of A / B (pinned uploads)
+  int32_t* flag_h = info_h + na;  // first non-finite atom of A / B (pinned uploads)
   flag_h[0] = flag_h[1] = -1;
 
   auto stage_stack = [&](int m, cudaStream_t s) -> hsb_status {
@@ -407,6 +599,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
       const size_t blk = static_cast<size_t>(nl) * ng * 16;
       for (int64_t i = 0; i < na; ++i)
         CK(cudaMemcpyAsync(static_cast<char*>(raw) + i * blk, blocks[i], blk, cudaMemcpyHostToDevice, s));
+      h2d_bytes += static_cast<double>(blk) * na;
       CK(launch_stack_blocks(static_cast<double*>(raw), dst, static_cast<int>(na), static_cast<int>(nl), ng, s));
       ++launches;
       void* flag;
@@ -414,11 +607,13 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
       CK(launch_first_nonfinite(static_cast<double*>(raw), static_cast<int>(na), static_cast<int64_t>(nl) * ng * 2,
                                 static_cast<int*>(flag), s));
       ++launches;
-      CK(cudaMemcpyAsync(flag_h + m, flag, 4, cudaMemcpyDeviceToHost, s));  // checked after the final sync
+      CK(launch_copy_i32(static_cast<int32_t*>(flag), hostbuf_dev + na + m, 1, s));  // checked after the final sync
+      ++launches;
       hc.mark(m == 0 ? "h2d A pinned" : "h2d B pinned");
       return HSB_OK;
     }
     CK(ctx->stager.h2d_stack(dst, blocks, na, nl, ng, s, &bad));
+    h2d_bytes += static_cast<double>(stack_bytes);
     hc.mark(m == 0 ? "h2d A stack" : "h2d B stack");
     if (bad >= 0) {
       cudaStreamSynchronize(st);
@@ -446,9 +641,11 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
                       static_cast<size_t>(nl) * 8, static_cast<size_t>(nl) * 8, 1});
     }
     CK(ctx->stager.h2d(jobs, st));
+    for (const auto& j : jobs) h2d_bytes += static_cast<double>(j.width) * j.height;
     hc.mark("h2d T,u");
     CKS(stage_stack(1, st));
     CK(cudaEventRecord(ev_b_up, st));
+    tr.mark(st, "h2d_b");
     if (!overlap_upload) CKS(stage_stack(0, st));
     CK(tl.mark(st, "h2d"));
   }
@@ -457,7 +654,9 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   CK(launch_potrf_route(TAA, static_cast<double*>(q), static_cast<int32_t*>(info_d), static_cast<int>(na),
                         static_cast<int>(nl), force_nonhpd, static_cast<double*>(potrf_scr), st));
   ++launches;
-  CK(cudaMemcpyAsync(info_h, info_d, na * 4, cudaMemcpyDeviceToHost, st));
+  CK(launch_route_atoms(static_cast<int32_t*>(info_d), static_cast<int>(na), static_cast<int>(nl),
+                        static_cast<int32_t*>(offs_d), hostbuf_dev, st));
+  ++launches;
   cudaEvent_t ev_info;
   CK(cudaEventCreateWithFlags(&ev_info, cudaEventDisableTiming));
   struct EvDel {
@@ -502,6 +701,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     // two uploads do not split the PCIe bandwidth B is waited on
     CK(cudaStreamWaitEvent(cs, ev_b_up, 0));
     CKS(stage_stack(0, cs));
+    tr.mark(cs, "h2d_a");
     cudaEvent_t ev_a;
     CK(cudaEventCreateWithFlags(&ev_a, cudaEventDisableTiming));
     EvDel ev_a_del{ev_a};
@@ -549,6 +749,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   CK(cudaEventCreateWithFlags(&ev_s, cudaEventDisableTiming));
   EvDel ev_s_del{ev_s};
   CK(cudaEventRecord(ev_s, st));
+  tr.mark(st, "s_done");
   if (out->s_ready) CK(cudaEventRecord(static_cast<cudaEvent_t>(out->s_ready), st));
 
   // ------------------------------------------- routing (host, overlaps S)
@@ -556,22 +757,9 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   CK(cudaEventSynchronize(ev_info));
   hc.mark("routing wait");
   int64_t n_hpd = 0, n_nh = 0;
+  std::atomic_thread_fence(std::memory_order_acquire);
   for (int64_t i = 0; i < na; ++i) (info_h[i] == 0 ? n_hpd : n_nh)++;
-  {
-    int64_t ih = 0, in = 0;
-    for (int64_t i = 0; i < na; ++i) {
-      if (info_h[i] == 0) {
-        offs_h[i] = static_cast<int32_t>(ih++ * nl);
-      } else {
-        offs_h[i] = static_cast<int32_t>((n_hpd + in) * nl);
-        offs_h[na + in] = static_cast<int32_t>(i * nl);      // A_nh source rows
-        offs_h[2 * na + in] = static_cast<int32_t>(in * nl);  // A_nh dest rows
-        ++in;
-      }
-    }
-  }
   if (atom_info) std::memcpy(atom_info, info_h, na * 4);
-  CK(cudaMemcpyAsync(offs_d, offs_h, na * 3 * 4, cudaMemcpyHostToDevice, st));
   const int32_t* offs_dev = static_cast<int32_t*>(offs_d);
 
   // ------------------------------------------- Loop 2, part 2 (builder.py:162-185)
@@ -602,6 +790,9 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   // Stream H to pinned host memory while the H contraction runs (fused path)
   const int64_t ntiles = (ng + kBN - 1) / kBN;
   const bool stream_h = !unfused && out->location == HSB_LOC_HOST && host_is_pinned(out->h);
+  // lower-triangle downloads + host mirror: the streamed (chunked) paths only
+  const bool lower_d2h = stream_h && chunk_s && !(opts & HSB_OPT_FULL_D2H);
+  HostMirror mirror;
 
   // -------------------------------------------------- H (builder.py:91-104, 187-200)
   if (unfused) {
@@ -642,8 +833,10 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
       CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dptr), ctx->done_cnt, 0));
       h.done_cnt = dptr;
     }
+    tr.mark(st, "loop2_done");
     CKS(run_zrk(ctx, st, h, &launches));
     CK(tl.mark(st, "h"));
+    tr.mark(st, "h_done");
   }
 
   // --------------------------------------------------------------- outputs
@@ -651,19 +844,35 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     // S is final at ev_s: its download runs on the copy stream, concurrently
     // with the H contraction; H follows on the compute stream.
     const size_t row = static_cast<size_t>(ng) * 16;
+    // columns [c0, c1) of a final matrix to the host, on the copy stream.
+    // lower_d2h: one copy per 256-column block [a, b) of rows >= a, and a host
+    // mirror job for rows [a, b) of the columns >= b once it has landed
+    auto download = [&](double* dst, const double* src, int64_t c0, int64_t c1) -> hsb_status {
+      const int64_t step = lower_d2h ? 256 : c1 - c0;
+      for (int64_t a = c0; a < c1; a += step) {
+        const int64_t b = std::min(c1, a + step), r0 = lower_d2h ? a : 0;
+        CK(cudaMemcpy2DAsync(reinterpret_cast<char*>(dst) + (a * out->ld + r0) * 16, out->ld * 16,
+                             reinterpret_cast<const char*>(src) + (a * ldo + r0) * 16, ldo * 16, (ng - r0) * 16,
+                             b - a, cudaMemcpyDeviceToHost, cs));
+        d2h_bytes += 16.0 * (ng - r0) * (b - a);
+        if (lower_d2h) CK(mirror.push(cs, dst, out->ld, ng, a, b));
+      }
+      return HSB_OK;
+    };
     if (!s_chunks.empty()) {
       // column groups of S download as soon as each is final
       int64_t c0 = 0;
       for (const auto& c : s_chunks) {
         CK(cudaStreamWaitEvent(cs, c.first, 0));
-        if (c.second > c0)
-          CK(cudaMemcpy2DAsync(reinterpret_cast<char*>(out->s) + c0 * out->ld * 16, out->ld * 16,
-                               reinterpret_cast<const char*>(S) + c0 * ldo * 16, ldo * 16, row, c.second - c0,
-                               cudaMemcpyDeviceToHost, cs));
+        if (c.second > c0) {
+          CKS(download(out->s, S, c0, c.second));
+        }
+        tr.mark(cs, "d2h_s " + std::to_string(c.second));
         c0 = c.second;
       }
     } else {
       CK(cudaStreamWaitEvent(cs, ev_s, 0));
+      d2h_bytes += 16.0 * ng * ng;
       CK(ctx->stager.d2h({{out->s, static_cast<size_t>(out->ld) * 16, S, static_cast<size_t>(ldo) * 16, row,
                            static_cast<size_t>(ng)}},
                          cs));
@@ -687,9 +896,8 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
         if (c - sent >= batch || (c == T && c > sent)) {
           std::atomic_thread_fence(std::memory_order_acquire);
           const int64_t c0 = sent * kBN, c1 = std::min<int64_t>(c * kBN, ng);
-          CK(cudaMemcpy2DAsync(reinterpret_cast<char*>(out->h) + c0 * out->ld * 16, out->ld * 16,
-                               reinterpret_cast<const char*>(H) + c0 * ldo * 16, ldo * 16, row, c1 - c0,
-                               cudaMemcpyDeviceToHost, cs));
+          CKS(download(out->h, H, c0, c1));
+          tr.mark(cs, "d2h_h " + std::to_string(c1));
           sent = c;
         } else {
           std::this_thread::sleep_for(std::chrono::microseconds(50));
@@ -697,6 +905,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
       }
       hc.mark("stream H");
     } else {
+      d2h_bytes += 16.0 * ng * ng;
       CK(ctx->stager.d2h({{out->h, static_cast<size_t>(out->ld) * 16, H, static_cast<size_t>(ldo) * 16, row,
                            static_cast<size_t>(ng)}},
                          st));
@@ -711,8 +920,10 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   hc.mark("enqueue H + d2h");
   if (!tm && !host_in && out->location == HSB_LOC_DEVICE) return HSB_OK;  // asynchronous: stream order
   CK(cudaEventSynchronize(tl.marks.back().second));
+  CK(mirror.finish());
   hc.mark("final sync");
   hc.report();
+  tr.report();
   for (int m = 0; m < 2; ++m)
     if (flag_h[m] >= 0 && flag_h[m] < na)  // pinned uploads are scanned on the device; outputs are discarded
       return fail(ctx, HSB_ERR_INVARIANT, std::string(m == 0 ? "a_blocks" : "b_blocks") + "[" +
@@ -742,6 +953,8 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     tm->n_hpd = static_cast<int32_t>(n_hpd);
     tm->n_nonhpd = static_cast<int32_t>(n_nh);
     tm->launches = launches;
+    tm->h2d_bytes = h2d_bytes;
+    tm->d2h_bytes = d2h_bytes;
   }
   return HSB_OK;
 }

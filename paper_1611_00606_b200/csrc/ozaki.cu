@@ -6,6 +6,7 @@
 #include <cstring>
 #include <mutex>
 
+#include "aux_kernels.cuh"
 #include "ozaki.cuh"
 #include "ptx.cuh"
 #include "zrk.cuh"
@@ -627,7 +628,7 @@ cudaError_t launch_ozaki_gemm(const OzGemmParams& p, cudaStream_t st) {
   if (nwork > 0x7fffffff) return cudaErrorInvalidConfiguration;
   const int pairs = static_cast<int>(nwork < n_sm / 2 ? nwork : n_sm / 2);
   const int grid = 2 * pairs;
-  e = cudaMemsetAsync(p.counter, 0, sizeof(int32_t), st);
+  e = launch_fill_i32(p.counter, 1, 0, st);  // a kernel, not a copy-engine memset
   if (e != cudaSuccess) return e;
   ozaki_gemm_kernel<<<grid, kOzThreads, kOzSmem, st>>>(p);
   return cudaGetLastError();

@@ -26,7 +26,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .hs_types import Dims, Fill, HermitianResult, InputError, SplitCounts
+from .hs_types import Dims, Fill, HermitianResult, InputError, InvariantError, SplitCounts
 from .instances import validate_instance
 from .ledger import FlopLedger, KernelKind, flops_of
 
@@ -52,6 +52,10 @@ class GpuPolicy:
     to ``int8_bits`` bits per column, ~1e-12 relative Frobenius at the
     default 39, 4.2x faster at C3; see csrc/ozaki.cuh) or runs them on the
     FP64 DMMA tensor cores ("dmma": ~1e-15).
+
+    ``lower_d2h`` (pinned outputs, INT8 engine): H and S cross PCIe as lower
+    triangles and host threads fill the upper triangles (conjugate mirror)
+    as column ranges land -- half the download bytes; identical results.
     """
 
     device: int = 0
@@ -60,6 +64,7 @@ class GpuPolicy:
     complex_mult: str = "3m"
     engine: str = "int8"
     int8_bits: int = 0
+    lower_d2h: bool = True
 
     def __post_init__(self):
         if int(self.device) != self.device or self.device < 0:
@@ -192,6 +197,10 @@ def _call_build(pol, prob, out, stream, force_nonhpd, n_a, slot: int = 0, wait: 
     lib = _lib.load()
     ctx = _lib.context(pol.device, pol.complex_mult, pol.engine, pol.int8_bits, slot)
     opts = (_lib.HSB_OPT_FORCE_NONHPD if force_nonhpd else 0) | (0 if pol.fused else _lib.HSB_OPT_UNFUSED)
+    if not pol.lower_d2h:
+        opts |= _lib.HSB_OPT_FULL_D2H
+    if prob.location == _lib.HSB_LOC_HOST:
+        opts |= _lib.HSB_OPT_VALIDATE  # T / u values are checked natively, before any transfer
     tim = _lib.HsbTimings()
     info = (ctypes.c_int32 * n_a)()
     # no timings -> the library returns without waiting (device in/out only)
@@ -205,8 +214,19 @@ def build_hs(p, policy=None, force_nonhpd: bool = False) -> BuildOutput:
     return _build_host(p, policy, force_nonhpd)
 
 
+def _validate_shapes(p) -> None:
+    """Shapes and block counts here; values natively (HSB_OPT_VALIDATE for T
+    and u, staging for A and B).  On a shape error the full reference-order
+    validation runs, so an earlier field's value error still wins."""
+    try:
+        validate_instance(p, check_stack_values=False, check_block_values=False)
+    except InvariantError:
+        validate_instance(p)
+        raise
+
+
 def _build_host(p, policy, force_nonhpd, slot: int = 0, stream=None, s_ready=None) -> BuildOutput:
-    validate_instance(p, check_stack_values=False)  # A/B values are checked while staging
+    _validate_shapes(p)
     pol = _policy(policy)
     dims = Dims(p.dims.n_atoms, p.dims.n_l, p.dims.n_g)
     prob, _keep = _host_problem(p)
@@ -328,7 +348,7 @@ def build_hs_into(p, h, s, policy=None, force_nonhpd: bool = False, stream=None)
     multi-GPU path, whose partial H/S go straight into a reduce-scatter."""
     import torch
 
-    validate_instance(p, check_stack_values=False)
+    _validate_shapes(p)
     pol = _policy(policy)
     n_g = int(p.dims.n_g)
     for name, t in (("h", h), ("s", s)):

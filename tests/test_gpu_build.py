@@ -113,6 +113,49 @@ def test_rejects_invalid_instance_before_work():
         build_hs(p)
 
 
+def _corrupt(p, edits):
+    for field, atom, idx, value in edits:
+        blk = getattr(p, field)[atom]
+        if idx == "shape":
+            getattr(p, field)[atom] = blk[:-1]
+        else:
+            blk[idx] = value
+    return p
+
+
+@pytest.mark.parametrize("edits", [
+    [("t_aa", 1, (0, 2), 1.0 + 0.5j)],                          # off-diagonal defect
+    [("t_bb", 2, (3, 3), 1.0 + 1e-9j)],                         # imaginary diagonal
+    [("t_ab", 0, (1, 1), np.nan)],
+    [("u_norms", 1, 2, -1.0)],
+    [("u_norms", 2, 0, np.inf)],
+    [("t_bb", 0, (0, 1), 2.0), ("t_aa", 2, (1, 1), np.inf)],     # finiteness before Hermitian
+    [("t_bb", 1, (2, 2), np.nan), ("t_ab", 2, (0, 0), np.nan)],  # field order
+    [("t_aa", 2, (0, 1), 3.0), ("t_aa", 1, (0, 1), 3.0)],        # atom order
+    [("u_norms", 0, 0, -1.0), ("t_bb", 2, (0, 1), 3.0)],        # Hermitian before u > 0
+    [("t_bb", 1, "shape", None), ("t_aa", 2, (0, 0), np.nan)],   # shape after an earlier value error
+    [("t_aa", 1, "shape", None), ("t_bb", 0, (0, 0), np.nan)],
+])
+def test_native_value_checks_follow_reference_order(edits):
+    # HSB_OPT_VALIDATE checks T / u natively; the message and the precedence
+    # must be those of validate_instance (probgen.py:140-168)
+    from paper_1611_00606_b200 import validate_instance
+
+    p = _corrupt(generate(ProblemSpec(Dims(3, 6, 20), seed=21)), edits)
+    with pytest.raises(InvariantError) as ref:
+        validate_instance(p)
+    with pytest.raises(InvariantError) as got:
+        build_hs(p)
+    assert str(got.value) == str(ref.value)
+
+
+def test_native_value_checks_accept_roundoff_hermitian():
+    p = generate(ProblemSpec(Dims(3, 6, 20), seed=22))
+    p.t_aa[1][0, 2] += 1e-16  # below 1e-14 (1 + ||T||_F)
+    out = build_hs(p)
+    assert rel_frob_error(out.s.matrix, brute.s_brute(p)) < TOL
+
+
 def test_psd_and_hermitian():
     # acceptance criterion 6 (pkg/tests/test_acceptance.py:119-133)
     for seed, frac in ((0, 0.0), (1, 0.5), (2, 1.0)):
@@ -154,6 +197,22 @@ def test_nonfinite_stack_values_raise_invariant_error(field):
     q = generate(ProblemSpec(Dims(3, 5, 40), seed=2))
     out = build_hs(q)
     assert rel_frob_error(out.s.matrix, brute.s_brute(q)) < TOL
+
+
+@pytest.mark.parametrize("dims", [Dims(3, 17, 700), Dims(6, 25, 1283)])
+def test_lower_triangle_download_matches_full_download(dims):
+    # default pinned INT8 path: H / S cross PCIe as lower triangles and the
+    # host fills the upper triangles; bitwise the same as full downloads
+    p = generate(ProblemSpec(dims, seed=31, nonhpd_fraction=0.3))
+    a = build_hs(p, GpuPolicy(lower_d2h=True))
+    b = build_hs(p, GpuPolicy(lower_d2h=False))
+    c = build_hs(p, GpuPolicy(pinned_outputs=False))
+    for x in (a, c):
+        assert x.h.matrix.tobytes() == b.h.matrix.tobytes()
+        assert x.s.matrix.tobytes() == b.s.matrix.tobytes()
+    a.h.check()
+    a.s.check()
+    assert rel_frob_error(a.h.matrix, brute.h_brute(p)) < TOL
 
 
 def test_pageable_outputs_path():

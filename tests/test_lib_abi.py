@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_loader_and_abi_version():
     lib = _lib.load()
-    assert lib.hsb_abi_version() == 4
+    assert lib.hsb_abi_version() == 5
 
 
 def test_binding_struct_layout_matches_header():
@@ -37,7 +37,7 @@ def test_binding_struct_layout_matches_header():
     assert ctypes.sizeof(_lib.HsbProblem) == 32 + 12 * 8
     assert ctypes.sizeof(_lib.HsbOutput) == 8 + 8 + 32
     assert ctypes.sizeof(_lib.HsbPeerOut) == 8 + 8 + 8 + 16
-    assert ctypes.sizeof(_lib.HsbTimings) == 13 * 8 + 16
+    assert ctypes.sizeof(_lib.HsbTimings) == 13 * 8 + 16 + 2 * 8
 
 
 def test_kernels_are_sm100a_only():
