@@ -140,6 +140,17 @@ hsb_status oz_encode(hsb_ctx* ctx, CUtensorMap* map, const int8_t* planes, int64
   return HSB_OK;
 }
 
+// side of the tile groups (bands of G tile columns), HSB_OZ_GROUP for experiments;
+// the column-group launches of the streamed paths follow the same bands
+static int64_t oz_tile_group() {
+  static const int64_t g = [] {
+    const char* e = std::getenv("HSB_OZ_GROUP");
+    const int v = e ? std::atoi(e) : 0;
+    return static_cast<int64_t>(v > 0 ? v : 6);
+  }();
+  return g;
+}
+
 // 256 x 256 tiles (tile row tm >= tile col tn) of the lower triangle, in
 // groups of 6 x 6 tiles for L2 reuse
 hsb_status oz_tiles(hsb_ctx* ctx, int64_t n, cudaStream_t st, const int2** out, int* count,
@@ -147,12 +158,19 @@ hsb_status oz_tiles(hsb_ctx* ctx, int64_t n, cudaStream_t st, const int2** out, 
   const int64_t T = (n + kOzBN - 1) / kOzBN;
   std::vector<int2>& v = ctx->oz_tiles_host;
   std::vector<int32_t>& ix = ctx->oz_tile_index_host;
+  const int64_t G = oz_tile_group();
+  static const int64_t GR = [] {  // HSB_OZ_GROUP_ROWS: rows of a group (default = G)
+    const char* e = std::getenv("HSB_OZ_GROUP_ROWS");
+    const int v = e ? std::atoi(e) : 0;
+    return static_cast<int64_t>(v);
+  }();
+  const int64_t gr = GR > 0 ? GR : G;
   if (ctx->oz_tiles_n != n) {
     v.clear();
-    for (int64_t j0 = 0; j0 < T; j0 += 6)
-      for (int64_t i0 = j0; i0 < T; i0 += 6)
-        for (int64_t j = j0; j < std::min<int64_t>(j0 + 6, T); ++j)
-          for (int64_t i = std::max(i0, j); i < std::min<int64_t>(i0 + 6, T); ++i)
+    for (int64_t j0 = 0; j0 < T; j0 += G)
+      for (int64_t i0 = j0; i0 < T; i0 += gr)
+        for (int64_t j = j0; j < std::min<int64_t>(j0 + G, T); ++j)
+          for (int64_t i = std::max(i0, j); i < std::min<int64_t>(i0 + gr, T); ++i)
             v.push_back(make_int2(static_cast<int>(i), static_cast<int>(j)));
     ix.assign(static_cast<size_t>(T * T), -1);
     for (size_t t = 0; t < v.size(); ++t) ix[static_cast<size_t>(v[t].x * T + v[t].y)] = static_cast<int32_t>(t);
@@ -321,14 +339,15 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
   }
 
   // With a host download waiting on per-column counters (done_cnt), the
-  // product runs in column groups of 6 tiles (contiguous in the tile list):
+  // product runs in column groups of G tiles (contiguous in the tile list):
   // once groups 0..g are done their columns are final (the mirror of an
   // entry of an earlier group lands in a later column), so their download
   // overlaps the remaining groups.  Otherwise one GEMM + one CRT launch.
   const int64_t T = (n + kOzBN - 1) / kOzBN;
   const int64_t T64 = (n + kBN - 1) / kBN;  // the host's 64-column blocks
   const std::vector<int2>& tl_host = ctx->oz_tiles_host;
-  const int64_t group = (z.done_cnt || z.chunk_events) ? 6 : T;
+  // (the tile list is ordered in bands of kOzTileGroup columns, see oz_tiles)
+  const int64_t group = (z.done_cnt || z.chunk_events) ? oz_tile_group() : T;
   int t0 = 0;
   for (int64_t j0 = 0; j0 < T; j0 += group) {
     const int64_t j1 = std::min<int64_t>(j0 + group, T);

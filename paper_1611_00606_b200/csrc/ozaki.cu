@@ -66,51 +66,86 @@ __global__ void ozaki_colexp_kernel(const double2* __restrict__ x, int64_t ldx, 
 }
 
 // ------------------------------------------------------------ 2. residues
-// thread = 4 consecutive k of one column; writes char4 into each of the
-// 4 planes x n_mod moduli: out[((plane * n_mod + i) * cols + col) * kpad + k]
-__global__ void ozaki_residue_kernel(const double2* __restrict__ x, int64_t ldx, int64_t k, int64_t cols,
-                                     const int32_t* __restrict__ col_exp, int b, int n_mod,
-                                     int8_t* __restrict__ out, int64_t kpad) {
-  const int64_t k4 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
-  if (k4 >= kpad) return;
-  const int64_t plane_stride = static_cast<int64_t>(n_mod) * cols * kpad;
+// 1 / p, correctly rounded (compile-time division)
+__constant__ double oz_inv_rt[kOzMaxMod] = {
+    1.0 / 256, 1.0 / 255, 1.0 / 253, 1.0 / 251, 1.0 / 247, 1.0 / 241, 1.0 / 239, 1.0 / 233,
+    1.0 / 229, 1.0 / 227, 1.0 / 223, 1.0 / 217, 1.0 / 211, 1.0 / 199, 1.0 / 197, 1.0 / 193};
+
+// 2^e for |e| <= 1022 from the exponent bits
+__device__ __forceinline__ double pow2i(int e) { return __longlong_as_double(static_cast<long long>(e + 1023) << 52); }
+
+// residue of an exactly-integer double |v| < 2^46 modulo p, as the low word of
+// r + 1.5 * 2^52 with r = v - p * rn(v / p): q = rn(v * fl(1/p)) through the
+// magic constant (the product's error, |v| 2^-61, is far below the 2^-9
+// distance of v / p from a half-integer for odd p), r = v - p q exactly.
+// r lies in [-(p-1)/2, (p-1)/2] for odd p and in [-128, 128] for p = 256
+// (a tie rounds to even; 128 and -128 are the same residue mod 256 and the
+// same int8).  No FRND, no division.
+__device__ __forceinline__ int sym_mod_magic(double v, double p, double inv_p) {
+  constexpr double M = 6755399441055744.0;  // 1.5 * 2^52
+  const double q = fma(v, inv_p, M) - M;
+  return static_cast<int>(__double2loint(fma(-p, q, v) + M));
+}
+
+// thread = 8 consecutive k of one column; writes 8 bytes into each of the
+// 4 planes x NM moduli: out[((plane * NM + i) * cols + col) * kpad + k]
+constexpr int kOzResK = 8;
+template <int NM>
+__global__ void __launch_bounds__(128, 4) ozaki_residue_kernel(const double2* __restrict__ x, int64_t ldx, int64_t k,
+                                                            int64_t cols, const int32_t* __restrict__ col_exp, int b,
+                                                            int8_t* __restrict__ out, int64_t kpad) {
+  const int64_t k0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kOzResK;
+  if (k0 >= kpad) return;
+  const int64_t mod_stride = cols * kpad;
+  const int64_t plane_stride = NM * mod_stride;
   for (int64_t c = blockIdx.y; c < cols; c += gridDim.y) {
     // x * 2^(b - e) in two exact power-of-two steps (each factor stays finite)
-    const int sh = b - col_exp[c];
-    const double s1 = ldexp(1.0, sh / 2), s2 = ldexp(1.0, sh - sh / 2);
-    double xr[4], xi[4];
+    const int sh = b - __ldg(col_exp + c);
+    const double s1 = pow2i(sh / 2), s2 = pow2i(sh - sh / 2);
+    double xr[kOzResK], xi[kOzResK];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (k4 + j < k) {
-        const double2 v = x[c * ldx + k4 + j];
+    for (int j = 0; j < kOzResK; ++j) {
+      if (k0 + j < k) {
+        const double2 v = x[c * ldx + k0 + j];
         xr[j] = rint((v.x * s1) * s2);
         xi[j] = rint((v.y * s1) * s2);
       } else {
         xr[j] = xi[j] = 0.0;
       }
     }
-    int8_t* o = out + c * kpad + k4;
-    for (int i = 0; i < n_mod; ++i) {
-      const int ip = oz_mod_rt[i];
-      const double p = ip, inv = 1.0 / p;
-      char4 re, im, mi, pl;
-      int rr[4], ri[4];
+    int8_t* o0 = out + c * kpad + k0;
+    int8_t* o1 = o0 + plane_stride;
+    int8_t* o2 = o1 + plane_stride;
+    int8_t* o3 = o2 + plane_stride;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        rr[j] = sym_mod_d(xr[j], p, inv);
-        ri[j] = sym_mod_d(xi[j], p, inv);
+    for (int i = 0; i < NM; ++i) {
+      const int ip = oz_mod(i);
+      const double p = ip, inv = oz_inv_rt[i];
+      int rr[kOzResK], ri[kOzResK], mi[kOzResK], pl[kOzResK];
+#pragma unroll
+      for (int j = 0; j < kOzResK; ++j) {
+        rr[j] = sym_mod_magic(xr[j], p, inv);
+        ri[j] = sym_mod_magic(xi[j], p, inv);
+        if (ip == 256) {  // the low byte is the residue
+          mi[j] = rr[j] - ri[j];
+          pl[j] = rr[j] + ri[j];
+        } else {  // |x' -+ y'| <= 2^b: exact doubles, reduced like x' and y'
+          mi[j] = sym_mod_magic(xr[j] - xi[j], p, inv);
+          pl[j] = sym_mod_magic(xr[j] + xi[j], p, inv);
+        }
       }
-      re = make_char4(rr[0], rr[1], rr[2], rr[3]);
-      im = make_char4(ri[0], ri[1], ri[2], ri[3]);
-      mi = make_char4(sym_adj(rr[0] - ri[0], ip), sym_adj(rr[1] - ri[1], ip), sym_adj(rr[2] - ri[2], ip),
-                      sym_adj(rr[3] - ri[3], ip));
-      pl = make_char4(sym_adj(rr[0] + ri[0], ip), sym_adj(rr[1] + ri[1], ip), sym_adj(rr[2] + ri[2], ip),
-                      sym_adj(rr[3] + ri[3], ip));
-      const int64_t mo = static_cast<int64_t>(i) * cols * kpad;
-      *reinterpret_cast<char4*>(o + kOzRe * plane_stride + mo) = re;
-      *reinterpret_cast<char4*>(o + kOzIm * plane_stride + mo) = im;
-      *reinterpret_cast<char4*>(o + kOzMinus * plane_stride + mo) = mi;
-      *reinterpret_cast<char4*>(o + kOzPlus * plane_stride + mo) = pl;
+      const auto pack = [](const int* v) {
+        return make_int2(__byte_perm(__byte_perm(v[0], v[1], 0x40), __byte_perm(v[2], v[3], 0x40), 0x5410),
+                         __byte_perm(__byte_perm(v[4], v[5], 0x40), __byte_perm(v[6], v[7], 0x40), 0x5410));
+      };
+      *reinterpret_cast<int2*>(o0) = pack(rr);
+      *reinterpret_cast<int2*>(o1) = pack(ri);
+      *reinterpret_cast<int2*>(o2) = pack(mi);
+      *reinterpret_cast<int2*>(o3) = pack(pl);
+      o0 += mod_stride;
+      o1 += mod_stride;
+      o2 += mod_stride;
+      o3 += mod_stride;
     }
   }
 }
@@ -609,10 +644,19 @@ cudaError_t launch_ozaki_colexp(const double* x, int64_t ldx, int64_t k, int64_t
 cudaError_t launch_ozaki_residues(const double* x, int64_t ldx, int64_t k, int64_t cols, const int32_t* col_exp,
                                   int b, int n_mod, int8_t* out, int64_t kpad, cudaStream_t st) {
   if (cols <= 0 || kpad <= 0) return cudaSuccess;
-  const int64_t threads_k = kpad / 4;
+  const int64_t threads_k = kpad / kOzResK;
   dim3 grid(static_cast<unsigned>((threads_k + 127) / 128), static_cast<unsigned>(cols < 65535 ? cols : 65535));
-  ozaki_residue_kernel<<<grid, 128, 0, st>>>(reinterpret_cast<const double2*>(x), ldx, k, cols, col_exp, b, n_mod,
-                                            out, kpad);
+  const double2* xx = reinterpret_cast<const double2*>(x);
+  switch (n_mod) {
+#define HSB_OZ_RES(NM) \
+  case NM:             \
+    ozaki_residue_kernel<NM><<<grid, 128, 0, st>>>(xx, ldx, k, cols, col_exp, b, out, kpad); \
+    break;
+    HSB_OZ_RES(11) HSB_OZ_RES(12) HSB_OZ_RES(13) HSB_OZ_RES(14) HSB_OZ_RES(15) HSB_OZ_RES(16)
+#undef HSB_OZ_RES
+    default:
+      return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 
