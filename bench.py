@@ -335,7 +335,7 @@ def main():
                 "frac": alg / h_core / 1e12 / peak_tops,
                 "peak_source": peak_src,
                 "algorithmic_ops_per_launch": alg,
-                "op_form": f"3 real products x {n_mod} moduli x K_tot {k_tot_h} x N(N+1)/2, 2 ops per MAC "
+                "op_form": f"2 real products (split complex) x {n_mod} moduli x K_tot {k_tot_h} x N(N+1)/2, 2 ops per MAC "
                            f"(operands rounded to {bits} bits)",
                 "model_flops_per_launch": h_flops, "model_tflops": h_flops / h_core / 1e12,
                 "avg_launch_ms": h_core * 1e3}

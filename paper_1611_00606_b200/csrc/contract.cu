@@ -201,7 +201,7 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
     }
   if (segs.size() > static_cast<size_t>(kOzMaxSeg)) return fail(ctx, HSB_ERR_UNSUPPORTED, "too many segments");
   // moduli: the fewest with b >= oz_min_bits.  With |x'| + |y'| <= 2^b per
-  // element, |Re'| = |sum x'x' + y'y'| and |Im'| = |sum x'_L y'_R - y'_L x'_R|
+  // element, |Re C'| = |sum x'x' + y'y'| and |Im C'| = |sum x'_L y'_R - y'_L x'_R|
   // are both <= K 2^2b; the explicit CRT needs |X| < M/2, kept with one bit of
   // margin: 2b <= log2 M - 2 - log2 K.
   int n_mod = 0, b = 0;
@@ -254,7 +254,7 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
     Src q{v.base, v.k, v.ld, nullptr, (v.k + 15) / 16 * 16};
     const std::string name = "oz_res" + std::to_string(srcs.size());
     void* buf;
-    CKS(ws(ctx, name.c_str(), static_cast<size_t>(4) * n_mod * n * q.kpad, &buf));
+    CKS(ws(ctx, name.c_str(), static_cast<size_t>(kOzPlanes) * n_mod * n * q.kpad, &buf));
     q.planes = static_cast<int8_t*>(buf);
     CK(launch_ozaki_residues(v.base, v.ld, v.k, n, e, b, n_mod, q.planes, q.kpad, st));
     srcs.push_back(q);
@@ -263,15 +263,15 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
   };
   OzGemmParams gp;
   std::memset(&gp, 0, sizeof(gp));
-  // products: P = re.re, Q = im.im, W = (re -/+ im)(re + im)
-  const int lp[3] = {kOzRe, kOzIm, z.conj ? kOzMinus : kOzPlus};
-  const int rp[3] = {kOzRe, kOzIm, kOzPlus};
+  // products phi1(C), phi2(C) (ozaki.cuh): conjugation swaps the left planes
+  const int lp[kOzProds] = {z.conj ? kOzPhi2 : kOzPhi1, z.conj ? kOzPhi1 : kOzPhi2};
+  const int rp[kOzProds] = {kOzPhi1, kOzPhi2};
   for (size_t si = 0; si < segs.size(); ++si) {
     Src L, R;
     CKS(planes_of(segs[si].l, &L));
     CKS(planes_of(segs[si].r, &R));
     const int64_t pl = static_cast<int64_t>(n_mod) * n * L.kpad, pr = static_cast<int64_t>(n_mod) * n * R.kpad;
-    for (int pi = 0; pi < 3; ++pi) {
+    for (int pi = 0; pi < kOzProds; ++pi) {
       CKS(oz_encode(ctx, &gp.map[pi][si][0], L.planes + lp[pi] * pl, L.k, n, L.kpad, n_mod, 128));
       CKS(oz_encode(ctx, &gp.map[pi][si][1], R.planes + rp[pi] * pr, R.k, n, R.kpad, n_mod, 128));
     }
@@ -293,20 +293,20 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
   gp.prod_stride = gp.mod_stride * n_mod;
   gp.tiles_total = total_tiles;
   void* rbuf;
-  CKS(ws(ctx, "oz_out", static_cast<size_t>(3 * gp.prod_stride), &rbuf));
+  CKS(ws(ctx, "oz_out", static_cast<size_t>(kOzProds * gp.prod_stride), &rbuf));
   gp.res = static_cast<int8_t*>(rbuf);
   void* cbuf;
   CKS(ws(ctx, "oz_counter", 16, &cbuf));
   gp.counter = static_cast<int32_t*>(cbuf);
   gp.slab_cnt = nullptr;
   if (gp.nslab > 1) {
-    const size_t nc = static_cast<size_t>(3) * n_mod * total_tiles;
+    const size_t nc = static_cast<size_t>(kOzProds) * n_mod * total_tiles;
     void* sbuf;
     CKS(ws(ctx, "oz_slab_cnt", nc * sizeof(int32_t), &sbuf));
     gp.slab_cnt = static_cast<int32_t*>(sbuf);
     CK(launch_fill_i32(static_cast<int32_t*>(sbuf), static_cast<int64_t>(nc), 0, st));
   }
-  if (gp.nseg == 0) CK(cudaMemsetAsync(rbuf, 0, static_cast<size_t>(3 * gp.prod_stride), st));
+  if (gp.nseg == 0) CK(cudaMemsetAsync(rbuf, 0, static_cast<size_t>(kOzProds * gp.prod_stride), st));
 
   OzCrtParams cp;
   cp.res = gp.res;

@@ -1,7 +1,7 @@
 // ozaki.cu — kernels of the INT8-tensor-core emulated FP64 contraction
-// (scheme in ozaki.cuh): column exponents, residue planes, the tcgen05
-// kind::i8 modular GEMM over lower-triangle tiles, and the CRT
-// reconstruction with the 3M combination and the Hermitian mirror.
+// (scheme in ozaki.cuh): column exponents, split-complex residue planes, the
+// tcgen05 kind::i8 modular GEMM over lower-triangle tiles, and the CRT
+// reconstruction with the Hermitian mirror.
 #include <climits>
 #include <cstring>
 #include <mutex>
@@ -13,16 +13,16 @@
 
 namespace hsb {
 
-__constant__ int32_t oz_mod_rt[kOzMaxMod] = {256, 255, 253, 251, 247, 241, 239, 233,
-                                             229, 227, 223, 217, 211, 199, 197, 193};
+__constant__ int32_t oz_mod_rt[kOzMaxMod] = {241, 233, 229, 221, 205, 197, 193, 181,
+                                             173, 157, 149, 137, 113, 109, 101, 97};
 
 // ------------------------------------------------------------ small helpers
 __device__ __forceinline__ int sym_lo(int p) { return -(p >> 1); }
 
 // symmetric residue of an exactly-integer double |v| < 2^46: r = v - p*floor(v/p + 1/2)
-// lies in [-p/2, p/2) ([-(p-1)/2, (p-1)/2] for odd p) with no correction:
-// for p = 2^8 the quotient is exact; for odd p, v/p is never within
-// 1/(2p) = 2^-9 of a half-integer while the product's error is ~2^-15.
+// lies in [-(p-1)/2, (p-1)/2] (every modulus is odd) with no correction:
+// v/p is never within 1/(2p) >= 2^-9 of a half-integer while the product's
+// error is ~2^-15.
 // The integer is read from the mantissa (magic 1.5 * 2^52) instead of F2I.
 __device__ __forceinline__ int sym_mod_d(double v, double p, double inv_p) {
   const double q = floor(fma(v, inv_p, 0.5));
@@ -68,8 +68,8 @@ __global__ void ozaki_colexp_kernel(const double2* __restrict__ x, int64_t ldx, 
 // ------------------------------------------------------------ 2. residues
 // 1 / p, correctly rounded (compile-time division)
 __constant__ double oz_inv_rt[kOzMaxMod] = {
-    1.0 / 256, 1.0 / 255, 1.0 / 253, 1.0 / 251, 1.0 / 247, 1.0 / 241, 1.0 / 239, 1.0 / 233,
-    1.0 / 229, 1.0 / 227, 1.0 / 223, 1.0 / 217, 1.0 / 211, 1.0 / 199, 1.0 / 197, 1.0 / 193};
+    1.0 / 241, 1.0 / 233, 1.0 / 229, 1.0 / 221, 1.0 / 205, 1.0 / 197, 1.0 / 193, 1.0 / 181,
+    1.0 / 173, 1.0 / 157, 1.0 / 149, 1.0 / 137, 1.0 / 113, 1.0 / 109, 1.0 / 101, 1.0 / 97};
 
 // 2^e for |e| <= 1022 from the exponent bits
 __device__ __forceinline__ double pow2i(int e) { return __longlong_as_double(static_cast<long long>(e + 1023) << 52); }
@@ -77,21 +77,27 @@ __device__ __forceinline__ double pow2i(int e) { return __longlong_as_double(sta
 // residue of an exactly-integer double |v| < 2^46 modulo p, as the low word of
 // r + 1.5 * 2^52 with r = v - p * rn(v / p): q = rn(v * fl(1/p)) through the
 // magic constant (the product's error, |v| 2^-61, is far below the 2^-9
-// distance of v / p from a half-integer for odd p), r = v - p q exactly.
-// r lies in [-(p-1)/2, (p-1)/2] for odd p and in [-128, 128] for p = 256
-// (a tie rounds to even; 128 and -128 are the same residue mod 256 and the
-// same int8).  No FRND, no division.
+// distance of v / p from a half-integer for odd p), r = v - p q exactly,
+// in [-(p-1)/2, (p-1)/2].  No FRND, no division.
 __device__ __forceinline__ int sym_mod_magic(double v, double p, double inv_p) {
   constexpr double M = 6755399441055744.0;  // 1.5 * 2^52
   const double q = fma(v, inv_p, M) - M;
   return static_cast<int>(__double2loint(fma(-p, q, v) + M));
 }
 
+// symmetric residue of a small integer |v| < 2^14 modulo an odd p: v / p is
+// never within 1/(2p) of a half-integer, and the float quotient's error is
+// below |v / p| 2^-23 < 2^-15
+__device__ __forceinline__ int sym_mod_small(int v, int p, float inv_p) {
+  return v - p * __float2int_rn(__int2float_rn(v) * inv_p);
+}
+
 // thread = 8 consecutive k of one column; writes 8 bytes into each of the
-// 4 planes x NM moduli: out[((plane * NM + i) * cols + col) * kpad + k]
+// 2 planes x NM moduli: out[((plane * NM + i) * cols + col) * kpad + k],
+// plane 0 = phi1(z') = x' + j y', plane 1 = phi2(z') = x' - j y' (mod p_i)
 constexpr int kOzResK = 8;
 template <int NM>
-__global__ void __launch_bounds__(128, 4) ozaki_residue_kernel(const double2* __restrict__ x, int64_t ldx, int64_t k,
+__global__ void __launch_bounds__(128, 3) ozaki_residue_kernel(const double2* __restrict__ x, int64_t ldx, int64_t k,
                                                             int64_t cols, const int32_t* __restrict__ col_exp, int b,
                                                             int8_t* __restrict__ out, int64_t kpad) {
   const int64_t k0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kOzResK;
@@ -115,37 +121,27 @@ __global__ void __launch_bounds__(128, 4) ozaki_residue_kernel(const double2* __
     }
     int8_t* o0 = out + c * kpad + k0;
     int8_t* o1 = o0 + plane_stride;
-    int8_t* o2 = o1 + plane_stride;
-    int8_t* o3 = o2 + plane_stride;
 #pragma unroll
     for (int i = 0; i < NM; ++i) {
-      const int ip = oz_mod(i);
-      const double p = ip, inv = oz_inv_rt[i];
-      int rr[kOzResK], ri[kOzResK], mi[kOzResK], pl[kOzResK];
+      const double p = oz_mod(i), inv = oz_inv_rt[i];
+      const int jm = oz_sqrtm1(i);
+      const float invf = 1.0f / oz_mod(i);
+      int u[kOzResK], w[kOzResK];
 #pragma unroll
       for (int j = 0; j < kOzResK; ++j) {
-        rr[j] = sym_mod_magic(xr[j], p, inv);
-        ri[j] = sym_mod_magic(xi[j], p, inv);
-        if (ip == 256) {  // the low byte is the residue
-          mi[j] = rr[j] - ri[j];
-          pl[j] = rr[j] + ri[j];
-        } else {  // |x' -+ y'| <= 2^b: exact doubles, reduced like x' and y'
-          mi[j] = sym_mod_magic(xr[j] - xi[j], p, inv);
-          pl[j] = sym_mod_magic(xr[j] + xi[j], p, inv);
-        }
+        const int rr = sym_mod_magic(xr[j], p, inv);
+        const int t = jm * sym_mod_magic(xi[j], p, inv);  // |t| <= 107 * 120
+        u[j] = sym_mod_small(rr + t, oz_mod(i), invf);
+        w[j] = sym_mod_small(rr - t, oz_mod(i), invf);
       }
       const auto pack = [](const int* v) {
         return make_int2(__byte_perm(__byte_perm(v[0], v[1], 0x40), __byte_perm(v[2], v[3], 0x40), 0x5410),
                          __byte_perm(__byte_perm(v[4], v[5], 0x40), __byte_perm(v[6], v[7], 0x40), 0x5410));
       };
-      *reinterpret_cast<int2*>(o0) = pack(rr);
-      *reinterpret_cast<int2*>(o1) = pack(ri);
-      *reinterpret_cast<int2*>(o2) = pack(mi);
-      *reinterpret_cast<int2*>(o3) = pack(pl);
+      *reinterpret_cast<int2*>(o0) = pack(u);
+      *reinterpret_cast<int2*>(o1) = pack(w);
       o0 += mod_stride;
       o1 += mod_stride;
-      o2 += mod_stride;
-      o3 += mod_stride;
     }
   }
 }
@@ -291,7 +287,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
-  const int nwork = 3 * p.nslab * p.n_mod * p.ntiles;
+  const int nwork = kOzProds * p.nslab * p.n_mod * p.ntiles;
   // consumer side of the queue (every role except the leader's producer)
   auto take = [&](int seq) -> int {
     const int j = seq & (kOzQ - 1);
@@ -482,33 +478,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
 }
 
 // ------------------------------------------------------------ 4. CRT
-// Explicit CRT in exact double limbs.  With M = prod p_i, y_i = (M/p_i) *
-// ((M/p_i)^-1 mod p_i) and any representatives r_i (|r_i| <= 384 per slab, <= 16 slabs):
+// Explicit CRT in exact double limbs.  With M = prod p_i and residues
+// X = c_i r_i (mod p_i) for representatives r_i (|r_i| <= p_i - 1) and unit
+// constants c_i (1/2 for Re = (phi1 + phi2)/2, 1/(2 j_i) for
+// Im = (phi1 - phi2)/(2 j_i)), the weights y_i = (M/p_i) * ((c_i (M/p_i)^-1) mod p_i) give
 //     X = sum_i r_i y_i - k M,   k = rint(sum_i r_i (y_i / M)),
-// exact for |X| < M/4 (the host's choice of b leaves >= 4 bits of margin).
+// exact for |X| < M/4 (the host's choice of b keeps |X| <= M/4).
 // y_i and M are split into 4 limbs of 32 bits; every limb sum
 // S_j = sum_i r_i y_ij (< 2^45) and T_j = S_j - k M_j is an exact double, so
 // X = ((T3 2^32 + T2) 2^32 + T1) 2^32 + T0 is rounded once, at the end.
 struct OzCrtConst {
-  double y[kOzMaxMod][4];   // limbs of y_i, least significant first
-  double f[kOzMaxMod];      // y_i / M
-  double m[4];              // limbs of M
+  double y[2][kOzMaxMod][4];   // [Re, Im] limbs of y_i, least significant first
+  double f[2][kOzMaxMod];      // y_i / M
+  double m[4];                 // limbs of M
 };
 constexpr int kOzMinMod = 11;
 __constant__ OzCrtConst c_oz_crt[kOzMaxMod - kOzMinMod + 1];  // one table per n_mod = 11 .. 16
 
-template <int NM>
+template <int NM, int PART>
 __device__ __forceinline__ double crt_value(const int (&r)[NM]) {
   const OzCrtConst& C = c_oz_crt[NM - kOzMinMod];
   double fk = 0.0, s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
     const double ri = static_cast<double>(r[i]);
-    fk = fma(ri, C.f[i], fk);
-    s0 = fma(ri, C.y[i][0], s0);
-    s1 = fma(ri, C.y[i][1], s1);
-    s2 = fma(ri, C.y[i][2], s2);
-    s3 = fma(ri, C.y[i][3], s3);
+    fk = fma(ri, C.f[PART][i], fk);
+    s0 = fma(ri, C.y[PART][i][0], s0);
+    s1 = fma(ri, C.y[PART][i][1], s1);
+    s2 = fma(ri, C.y[PART][i][2], s2);
+    s3 = fma(ri, C.y[PART][i][3], s3);
   }
   const double k = rint(fk);
   const double t0 = fma(-k, C.m[0], s0), t1 = fma(-k, C.m[1], s1);
@@ -517,20 +515,20 @@ __device__ __forceinline__ double crt_value(const int (&r)[NM]) {
   return fma(fma(fma(t3, kL, t2), kL, t1), kL, t0);
 }
 
-// Finish one element from its per-modulus P, Q, W residue sums.
+// Finish one element from its per-modulus phi1(C), phi2(C) residues (the
+// conjugation of L^H R is in the GEMM's choice of planes).
 template <int NM>
-__device__ __forceinline__ double2 crt_finish(const OzCrtParams& p, const int (&P)[NM], const int (&Q)[NM],
-                                              const int (&W)[NM], int m, int n) {
+__device__ __forceinline__ double2 crt_finish(const OzCrtParams& p, const int (&F1)[NM], const int (&F2)[NM],
+                                              int m, int n) {
   int re[NM], im[NM];
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
-    // L^H R: Re = P + Q, Im = W - P + Q ;  L^T R: Re = P - Q, Im = W - P - Q
-    re[i] = p.conj ? P[i] + Q[i] : P[i] - Q[i];
-    im[i] = p.conj ? W[i] - P[i] + Q[i] : W[i] - P[i] - Q[i];
+    re[i] = F1[i] + F2[i];  // 2 Re C   (mod p_i)
+    im[i] = F1[i] - F2[i];  // 2 j Im C (mod p_i)
   }
   const int sh = p.el[m] + p.er[n] - 2 * p.b;
-  const double xr = ldexp(crt_value<NM>(re), sh);
-  const double xi = ldexp(crt_value<NM>(im), sh);
+  const double xr = ldexp(crt_value<NM, 0>(re), sh);
+  const double xi = ldexp(crt_value<NM, 1>(im), sh);
   double vr = p.alpha_re * xr - p.alpha_im * xi;
   double vi = p.alpha_re * xi + p.alpha_im * xr;
   if (p.beta_re != 0.0 || p.beta_im != 0.0) {
@@ -554,14 +552,13 @@ __global__ void __launch_bounds__(128) ozaki_crt_kernel(const OzCrtParams p) {
   if (m >= p.n || m < n) return;
   const int t = p.tile_index[(m >> 8) * p.T + (n >> 8)];
   const int8_t* r0 = p.res + static_cast<int64_t>(t) * kOzTileBytes + (n & 255) * 256 + (m & 255);
-  int P[NM], Q[NM], W[NM];  // straight-line: all 3 x NM loads in flight together
+  int F1[NM], F2[NM];  // straight-line: all 2 x NM loads in flight together
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
-    P[i] = r0[i * p.mod_stride];
-    Q[i] = r0[p.prod_stride + i * p.mod_stride];
-    W[i] = r0[2 * p.prod_stride + i * p.mod_stride];
+    F1[i] = r0[i * p.mod_stride];
+    F2[i] = r0[p.prod_stride + i * p.mod_stride];
   }
-  const double2 v = crt_finish<NM>(p, P, Q, W, m, n);
+  const double2 v = crt_finish<NM>(p, F1, F2, m, n);
   if (p.peer) {
     // fused scatter: write straight into the owning rank's receive slot (NVLink
     // peer memory); the owner only sums its slots afterwards
@@ -593,19 +590,23 @@ static OzCrtConst oz_crt_table(int n_mod) {
     }
   };
   const double Md = static_cast<double>(M);
+  auto inverse = [](int a, int p) {
+    a = ((a % p) + p) % p;
+    for (int x = 1; x < p; ++x)
+      if ((a * x) % p == 1) return x;
+    return 0;
+  };
   for (int i = 0; i < n_mod; ++i) {
     const int pi = oz_mod(i);
     const u128 Mi = M / static_cast<u128>(pi);
-    const int mi_mod = static_cast<int>(Mi % static_cast<u128>(pi));
-    int inv = 0;
-    for (int x = 1; x < pi; ++x)
-      if ((mi_mod * x) % pi == 1) {
-        inv = x;
-        break;
-      }
-    const u128 y = Mi * static_cast<u128>(inv);  // < M
-    limbs(y, c.y[i]);
-    c.f[i] = static_cast<double>(y) / Md;
+    const int mi_inv = inverse(static_cast<int>(Mi % static_cast<u128>(pi)), pi);
+    // Re: c = 1/2 ; Im: c = 1/(2 j)
+    const int cpart[2] = {inverse(2, pi), inverse(2 * oz_sqrtm1(i), pi)};
+    for (int part = 0; part < 2; ++part) {
+      const u128 y = Mi * static_cast<u128>((cpart[part] * mi_inv) % pi);  // < M
+      limbs(y, c.y[part][i]);
+      c.f[part][i] = static_cast<double>(y) / Md;
+    }
   }
   limbs(M, c.m);
   return c;
@@ -667,7 +668,7 @@ cudaError_t launch_ozaki_gemm(const OzGemmParams& p, cudaStream_t st) {
   cudaGetDevice(&dev);
   e = cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return e;
-  const int64_t nwork = 3LL * p.nslab * p.n_mod * p.ntiles;
+  const int64_t nwork = static_cast<int64_t>(kOzProds) * p.nslab * p.n_mod * p.ntiles;
   if (nwork <= 0) return cudaSuccess;
   if (nwork > 0x7fffffff) return cudaErrorInvalidConfiguration;
   const int pairs = static_cast<int>(nwork < n_sm / 2 ? nwork : n_sm / 2);

@@ -8,20 +8,26 @@
 //  1. column scaling: e^L_m = exponent of max over all segments and k of
 //     |Re L| + |Im L| in column m (ozaki_colexp_kernel); same for R.
 //  2. integer operands: x' = rint(Re X * 2^(b - e_col)), y' = rint(Im X * ...),
-//     |x'| + |y'| <= 2^b; four exact integer planes re = x', im = y',
-//     minus = x' - y', plus = x' + y' and their symmetric residues modulo
-//     n_mod pairwise-coprime moduli p_i <= 256 as int8 (ozaki_residue_kernel).
-//  3. 3M products, exact in int32 per modulus (tcgen05 INT8 GEMM, TMEM
-//     accumulators, ozaki_gemm_kernel):
-//        P_i = re(L)^T re(R),  Q_i = im(L)^T im(R),  W_i = minus(L)^T plus(R)
-//     reduced mod p_i in the epilogue and stored as int8 residues.
-//  4. reconstruction (ozaki_crt_kernel): Re' = P + Q, Im' = W - P + Q (mod p_i,
-//     exact integers), Garner mixed-radix with symmetric digits -> double,
-//     scaled by 2^(e^L_m + e^R_n - 2b); alpha/beta, Im(diag) = 0, mirror.
+//     |x'| + |y'| <= 2^b, i.e. a Gaussian integer z' = x' + i y'.
+//  3. split complex arithmetic: every modulus p_i is odd with all prime
+//     factors = 1 (mod 4), so -1 has a square root j_i mod p_i and
+//        Z_p[i] -> Z_p x Z_p,  z = x + i y -> (x + j y, x - j y)
+//     is a ring isomorphism (phi1, phi2); conjugation swaps the components.
+//     Two planes per modulus, phi1(z') and phi2(z') as symmetric int8
+//     residues (ozaki_residue_kernel), and two real products per modulus,
+//     exact in int32 (tcgen05 INT8 GEMM, TMEM accumulators, ozaki_gemm_kernel):
+//        L^H R:  phi1(C) = phi2(L)^T phi1(R),  phi2(C) = phi1(L)^T phi2(R)
+//        L^T R:  phi1(C) = phi1(L)^T phi1(R),  phi2(C) = phi2(L)^T phi2(R)
+//     reduced mod p_i in the epilogue and stored as int8 residues: 2 integer
+//     GEMMs per modulus instead of the 3 of a Gauss/3M split.
+//  4. reconstruction (ozaki_crt_kernel): Re C = (phi1 + phi2) / 2,
+//     Im C = (phi1 - phi2) / (2 j) mod p_i, the constants folded into the
+//     explicit CRT weights; scaled by 2^(e^L_m + e^R_n - 2b); alpha/beta,
+//     Im(diag) = 0, mirror.
 //
 // Exactness: every step after the rounding in (2) is exact integer
-// arithmetic as long as |Re'|, |Im'| < M/2 = prod p_i / 2, which fixes b from
-// K_tot (the host picks n_mod so that b >= 40).  The only error is the
+// arithmetic as long as |Re C'|, |Im C'| < M/2 = prod p_i / 2, which fixes b
+// from K_tot (the host picks n_mod so that b >= 39).  The only error is the
 // operand rounding, ~2^-b relative to each column's max: ~1e-12 relative
 // Frobenius, inside the north star's 1e-10 (measured in tests/).
 #pragma once
@@ -36,18 +42,30 @@ constexpr int kOzMaxSeg = 4;
 constexpr int kOzBM = 256;   // output tile rows   (CTA pair: 128 TMEM lanes each)
 constexpr int kOzBN = 256;   // output tile cols   (TMEM columns per accumulator)
 constexpr int kOzBK = 128;   // k bytes per stage  (128B swizzle row)
-// pairwise coprime, descending; the first n_mod are used
+// pairwise coprime, descending, every prime factor = 1 (mod 4)
+// (221 = 13 * 17, 205 = 5 * 41); the first n_mod are used
 __host__ __device__ constexpr int oz_mod(int i) {
   switch (i) {
-    case 0: return 256;  case 1: return 255;  case 2: return 253;  case 3: return 251;
-    case 4: return 247;  case 5: return 241;  case 6: return 239;  case 7: return 233;
-    case 8: return 229;  case 9: return 227;  case 10: return 223; case 11: return 217;
-    case 12: return 211; case 13: return 199; case 14: return 197; default: return 193;
+    case 0: return 241;  case 1: return 233;  case 2: return 229;  case 3: return 221;
+    case 4: return 205;  case 5: return 197;  case 6: return 193;  case 7: return 181;
+    case 8: return 173;  case 9: return 157;  case 10: return 149; case 11: return 137;
+    case 12: return 113; case 13: return 109; case 14: return 101; default: return 97;
+  }
+}
+// j_i: a square root of -1 modulo oz_mod(i), symmetric representative
+__host__ __device__ constexpr int oz_sqrtm1(int i) {
+  switch (i) {
+    case 0: return 64;   case 1: return 89;   case 2: return 107;  case 3: return 21;
+    case 4: return 32;   case 5: return 14;   case 6: return 81;   case 7: return 19;
+    case 8: return 80;   case 9: return 28;   case 10: return 44;  case 11: return 37;
+    case 12: return 15;  case 13: return 33;  case 14: return 10;  default: return 22;
   }
 }
 
 // planes of a residue buffer: [plane][modulus][col][kpad] int8
-enum OzPlane { kOzRe = 0, kOzIm = 1, kOzMinus = 2, kOzPlus = 3 };
+enum OzPlane { kOzPhi1 = 0, kOzPhi2 = 1 };
+constexpr int kOzPlanes = 2;
+constexpr int kOzProds = 2;   // integer GEMMs per modulus: phi1(C), phi2(C)
 
 constexpr int kOzMaxSlab = 16;
 constexpr int kOzTileBytes = 256 * 256;  // one tile of int8 residues, column-major
@@ -62,7 +80,7 @@ constexpr int kOzTileBytes = 256 * 256;  // one tile of int8 residues, column-ma
 // was claimed earlier by a resident CTA pair and the wait always ends.
 struct OzGemmParams {
   // maps[prod][seg][side]: 3-D int8 maps {k, cols, modulus}, box {128, 128, 1}
-  CUtensorMap map[3][kOzMaxSeg][2];
+  CUtensorMap map[kOzProds][kOzMaxSeg][2];
   int32_t seg_chunk0[kOzMaxSeg + 1];    // first global k chunk of each segment (+ total)
   int32_t slab_chunk0[kOzMaxSlab + 1];  // first global k chunk of each slab (+ total)
   int32_t nseg, nslab;

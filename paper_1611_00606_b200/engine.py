@@ -2,9 +2,11 @@
 
 The engine emulates the FP64 complex contractions C = sum_s L_s^H R_s by the
 Chinese-remainder (Ozaki-II) scheme: operands are rounded per column to
-``b``-bit integers, their residues modulo ``n_mod`` pairwise-coprime moduli
-p_i <= 256 are multiplied exactly on the INT8 tensor cores (3 real products
-per modulus, Gauss/3M), and the integers are reconstructed by the CRT.
+``b``-bit Gaussian integers, their residues modulo ``n_mod`` pairwise-coprime
+odd moduli p_i < 256 whose prime factors are all 1 (mod 4) are split by the
+isomorphism Z_p[i] = Z_p x Z_p (x + iy -> x +- j y, j^2 = -1 mod p), so each
+modulus costs 2 exact real products on the INT8 tensor cores, and the
+integers are reconstructed by the CRT.
 
 ``int8_moduli`` restates the library's choice (hsb_api.cu ``run_ozaki``) so
 reports can count the work; the library is the authority.
@@ -14,7 +16,10 @@ from __future__ import annotations
 
 import math
 
-MODULI = (256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193)
+MODULI = (241, 233, 229, 221, 205, 197, 193, 181, 173, 157, 149, 137, 113, 109, 101, 97)
+# a square root of -1 modulo each modulus (csrc/ozaki.cuh oz_sqrtm1)
+SQRT_M1 = (64, 89, 107, 21, 32, 14, 81, 19, 80, 28, 44, 37, 15, 33, 10, 22)
+PRODUCTS = 2
 DEFAULT_BITS = 39
 
 
@@ -35,6 +40,6 @@ def int8_moduli(k_total: int, min_bits: int = 0) -> tuple[int, int]:
 
 def int8_gemm_ops(n: int, k_total: int, min_bits: int = 0) -> int:
     """Algorithmic INT8 tensor-core ops (2 per MAC) of one triangle
-    contraction: 3 real products x n_mod moduli x K_tot x n(n+1)/2."""
+    contraction: 2 real products x n_mod moduli x K_tot x n(n+1)/2."""
     n_mod, _ = int8_moduli(k_total, min_bits)
-    return 2 * 3 * n_mod * k_total * (n * (n + 1) // 2)
+    return 2 * PRODUCTS * n_mod * k_total * (n * (n + 1) // 2)

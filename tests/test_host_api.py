@@ -139,22 +139,76 @@ def test_report_summarize_and_table5():
 
 
 def test_int8_engine_moduli_choice():
-    # engine.int8_moduli restates hsb_api.cu run_ozaki: the fewest moduli with
-    # b >= 40 bits and 3 K 2^(2b) below M/16
+    # engine.int8_moduli restates contract.cu run_ozaki: the fewest moduli with
+    # b >= 39 bits and K 2^(2b) below M/4
     import math
 
     from paper_1611_00606_b200 import int8_gemm_ops, int8_moduli
-    from paper_1611_00606_b200.engine import MODULI
+    from paper_1611_00606_b200.engine import MODULI, SQRT_M1
 
     for k in (1, 98, 7744, 11616, 46464):
         n_mod, b = int8_moduli(k)
         log2m = sum(math.log2(p) for p in MODULI[:n_mod])
-        assert b >= 39 and k * 2.0 ** (2 * b) < 2.0 ** log2m / 4  # |Re'|, |Im'| <= K 2^2b < M/2, 1 bit spare
+        assert b >= 39 and k * 2.0 ** (2 * b) < 2.0 ** log2m / 4  # |Re C'|, |Im C'| <= K 2^2b < M/2, 1 bit spare
         if n_mod > 11:
             prev = sum(math.log2(p) for p in MODULI[:n_mod - 1])
             assert math.floor((prev - 2 - math.log2(k)) / 2) < 39
-    assert int8_moduli(11616) == (12, 39) and int8_moduli(46464)[0] == 13
+    assert int8_moduli(11616) == (13, 41) and int8_moduli(46464) == (13, 40)
     assert all(math.gcd(a, b) == 1 for i, a in enumerate(MODULI) for b in MODULI[i + 1:])
-    assert int8_gemm_ops(8000, 11616) == 2 * 3 * 12 * 11616 * 8000 * 8001 // 2
+    # split complex arithmetic: odd moduli < 256, -1 a square mod each
+    assert all(p % 2 == 1 and p < 256 and (j * j + 1) % p == 0 and abs(j) <= p // 2
+               for p, j in zip(MODULI, SQRT_M1))
+    assert int8_gemm_ops(8000, 11616) == 2 * 2 * 13 * 11616 * 8000 * 8001 // 2
     with pytest.raises(InputError):
         GpuPolicy(engine="fp16")
+
+
+def _sym(v, p):
+    r = v % p
+    return r - p if r > p // 2 else r
+
+
+def test_int8_split_complex_crt_exact():
+    # CPU restatement of the INT8 engine's integer arithmetic (csrc/ozaki.cuh):
+    # Gaussian-integer operands, residues phi1 = x + j y, phi2 = x - j y mod p_i
+    # (int8 range), two real products per modulus (conjugation swaps the left
+    # planes), reconstruction Re = (phi1 + phi2)/2, Im = (phi1 - phi2)/(2j) by the
+    # explicit CRT with folded weights -- exact for |Re C|, |Im C| < M/2.
+    import random
+
+    from paper_1611_00606_b200.engine import MODULI, SQRT_M1, int8_moduli
+
+    rng = random.Random(5)
+    for conj in (True, False):
+        k = 300
+        n_mod, b = int8_moduli(k)
+        mods, roots = MODULI[:n_mod], SQRT_M1[:n_mod]
+        M = 1
+        for p in mods:
+            M *= p
+
+        def gauss():
+            x = rng.randint(-2 ** (b - 1), 2 ** (b - 1))
+            y = rng.choice((-1, 1)) * (2 ** b - abs(x) - rng.randint(0, 3))
+            return complex(0), x, y
+
+        L = [gauss()[1:] for _ in range(k)]
+        R = [gauss()[1:] for _ in range(k)]
+        cre = sum((lx * rx + ly * ry) if conj else (lx * rx - ly * ry) for (lx, ly), (rx, ry) in zip(L, R))
+        cim = sum((lx * ry - ly * rx) if conj else (lx * ry + ly * rx) for (lx, ly), (rx, ry) in zip(L, R))
+        assert abs(cre) < M // 2 and abs(cim) < M // 2
+        x_re = x_im = 0
+        for p, j in zip(mods, roots):
+            phi = [[_sym(x + j * y, p) for x, y in V] for V in (L, R)]
+            psi = [[_sym(x - j * y, p) for x, y in V] for V in (L, R)]
+            assert all(-128 <= v <= 127 for v in phi[0] + psi[0])
+            lp1, lp2 = (psi[0], phi[0]) if conj else (phi[0], psi[0])
+            f1 = _sym(sum(a * c for a, c in zip(lp1, phi[1])), p)
+            f2 = _sym(sum(a * c for a, c in zip(lp2, psi[1])), p)
+            mi = M // p
+            inv_mi = pow(mi, -1, p)
+            x_re += (f1 + f2) * (mi * (pow(2, -1, p) * inv_mi % p))
+            x_im += (f1 - f2) * (mi * (pow(2 * j, -1, p) * inv_mi % p))
+        x_re -= M * round(x_re / M)
+        x_im -= M * round(x_im / M)
+        assert (x_re, x_im) == (cre, cim)
