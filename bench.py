@@ -408,9 +408,11 @@ def main():
             # contexts/streams overlap one step's PCIe transfers with the next
             # step's kernels (every step still uploads its inputs and downloads
             # its H and S inside the timed region)
-            # a second context doubles the device workspace: pipeline only when it fits
+            # every further context adds one call's device workspace: pipeline
+            # as deep as it fits (three stages: upload, kernels, download)
             free, _total = torch.cuda.mem_get_info(dev)
-            depth = 2 if free > 1.2 * torch.cuda.memory_reserved(dev) + 0.5 * _total else 1
+            per_ctx = 1.1 * (_total - free) + 0.02 * _total  # everything allocated so far ~ one context
+            depth = max(1, min(3, 1 + int(free // per_ctx)))
             for o in iter_hs_kpoints([p] * (depth + 2), policy, depth=depth):
                 del o  # warm the second context and the pinned-output cache (depth + 1 in flight)
             t0 = time.perf_counter()

@@ -220,6 +220,23 @@ typedef struct {
    * and timings == NULL, hsb_build_hs returns without waiting for the device
    * (the work completes in stream order). */
   void* s_ready;
+  /* Optional cudaEvent_t ordering of pipelined host-path calls (k-point lanes,
+   * each on its own context and stream): this call's host->device copies
+   * start after h2d_after, and h2d_done is recorded once they have landed;
+   * its kernels start after compute_after, and compute_done is recorded after
+   * the last one (H final).  Chaining call i+1's *_after to call i's *_done
+   * keeps the upload engine and the SMs each working on one k-point at a
+   * time, in order, while other calls' downloads run concurrently (ABI 6).
+   * An event is only waited on once the previous call has recorded it:
+   * order_in points at the previous call's order_out, which this library
+   * sets to 1 after recording h2d_done and to 2 after compute_done (or on any
+   * early return); host threads of consecutive calls synchronise on it. */
+  void* h2d_after;
+  void* h2d_done;
+  void* compute_after;
+  void* compute_done;
+  const int32_t* order_in;
+  int32_t* order_out;
 } hsb_output;
 
 /* Section timings (seconds, from CUDA events) in the reference's section

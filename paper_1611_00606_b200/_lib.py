@@ -56,7 +56,9 @@ class HsbPeerOut(ctypes.Structure):
 
 class HsbOutput(ctypes.Structure):
     _fields_ = [("location", ctypes.c_int32), ("reserved", ctypes.c_int32), ("ld", ctypes.c_int64),
-                ("h", _P), ("s", _P), ("peer", ctypes.POINTER(HsbPeerOut)), ("s_ready", _P)]
+                ("h", _P), ("s", _P), ("peer", ctypes.POINTER(HsbPeerOut)), ("s_ready", _P),
+                ("h2d_after", _P), ("h2d_done", _P), ("compute_after", _P), ("compute_done", _P),
+                ("order_in", ctypes.POINTER(ctypes.c_int32)), ("order_out", ctypes.POINTER(ctypes.c_int32))]
 
 
 class HsbTimings(ctypes.Structure):
@@ -118,7 +120,7 @@ def load():
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.hsb_abi_version() != 5:
+        if lib.hsb_abi_version() != 6:
             raise RuntimeError("libhsb200.so ABI version mismatch; rebuild it")
         _lib = lib
         return lib

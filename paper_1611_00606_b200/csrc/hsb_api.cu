@@ -22,6 +22,7 @@
 
 #include <condition_variable>
 #include <deque>
+#include <functional>
 #include <mutex>
 #include <thread>
 
@@ -32,7 +33,7 @@ using namespace hsb_host;
 // =============================================================================
 extern "C" {
 
-int32_t hsb_abi_version(void) { return 5; }
+int32_t hsb_abi_version(void) { return 6; }
 
 hsb_status hsb_ctx_create(int32_t device, hsb_ctx** out) {
   hsb_ctx* ctx = nullptr;
@@ -321,7 +322,9 @@ struct HostMirror {
     static const int n = [] {
       const char* e = std::getenv("HSB_MIRROR_THREADS");
       const int v = e ? std::atoi(e) : 0;
-      return v > 0 ? v : std::max(1, omp_get_max_threads());
+      // default: half the cores -- the mirror shares the host's DRAM with the
+      // lanes' DMA traffic, and more threads slow the uploads (probes/host_contention.cu)
+      return v > 0 ? v : std::max(1, omp_get_max_threads() / 2);
     }();
     return n;
   }
@@ -511,6 +514,30 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   HostClock hc;  // host-side phase stamps, printed when HSB_DEBUG_TIMING is set
   GpuTrace tr;    // absolute GPU timeline, printed when HSB_TRACE is set
   tr.who = ctx;
+  // ordering against the previous pipelined call (hsb_output.h2d_after ...):
+  // wait until it has recorded the event, then make the stream wait on it
+  struct OrderGuard {  // never leave the next call waiting (early returns)
+    int32_t* f;
+    ~OrderGuard() {
+      if (f) __atomic_store_n(f, 2, __ATOMIC_RELEASE);
+    }
+  } order_guard{out->order_out};
+  auto order_wait = [&](void* ev, int32_t level, cudaStream_t s) -> cudaError_t {
+    if (!ev) return cudaSuccess;
+    if (out->order_in)
+      while (__atomic_load_n(out->order_in, __ATOMIC_ACQUIRE) < level)
+        std::this_thread::sleep_for(std::chrono::microseconds(20));
+    return cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev), 0);
+  };
+  auto order_done = [&](void* ev, int32_t level, cudaStream_t s) -> cudaError_t {
+    if (ev) {
+      const cudaError_t e = cudaEventRecord(static_cast<cudaEvent_t>(ev), s);
+      if (e != cudaSuccess) return e;
+    }
+    if (out->order_out) __atomic_store_n(out->order_out, level, __ATOMIC_RELEASE);
+    return cudaSuccess;
+  };
+  if (host_in) CK(order_wait(out->h2d_after, 1, st));
   CK(tl.mark(st, "start"));
   tr.mark(st, "start");
 
@@ -582,7 +609,9 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   int32_t* flag_h = info_h + na;  // first non-finite atom of A / B (pinned uploads)
   flag_h[0] = flag_h[1] = -1;
 
-  auto stage_stack = [&](int m, cudaStream_t s) -> hsb_status {
+  // dma_done: recorded on s once the DMAs have landed, before the restack
+  // kernels (which may wait for SMs held by another call's kernels)
+  auto stage_stack = [&](int m, cudaStream_t s, const std::function<cudaError_t()>& dma_done) -> hsb_status {
     // A (m = 0) or B (m = 1) into the stacked layout.  Pinned blocks: one
     // contiguous DMA per atom into an atom-major buffer, then a device
     // restack (HBM speed).  Pageable blocks: host threads gather stacked
@@ -600,6 +629,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
       for (int64_t i = 0; i < na; ++i)
         CK(cudaMemcpyAsync(static_cast<char*>(raw) + i * blk, blocks[i], blk, cudaMemcpyHostToDevice, s));
       h2d_bytes += static_cast<double>(blk) * na;
+      if (dma_done) CK(dma_done());
       CK(launch_stack_blocks(static_cast<double*>(raw), dst, static_cast<int>(na), static_cast<int>(nl), ng, s));
       ++launches;
       void* flag;
@@ -614,6 +644,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     }
     CK(ctx->stager.h2d_stack(dst, blocks, na, nl, ng, s, &bad));
     h2d_bytes += static_cast<double>(stack_bytes);
+    if (dma_done) CK(dma_done());
     hc.mark(m == 0 ? "h2d A stack" : "h2d B stack");
     if (bad >= 0) {
       cudaStreamSynchronize(st);
@@ -643,12 +674,14 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     CK(ctx->stager.h2d(jobs, st));
     for (const auto& j : jobs) h2d_bytes += static_cast<double>(j.width) * j.height;
     hc.mark("h2d T,u");
-    CKS(stage_stack(1, st));
-    CK(cudaEventRecord(ev_b_up, st));
-    tr.mark(st, "h2d_b");
-    if (!overlap_upload) CKS(stage_stack(0, st));
+    CKS(stage_stack(1, st, [&] {
+      tr.mark(st, "h2d_b");
+      return cudaEventRecord(ev_b_up, st);
+    }));
+    if (!overlap_upload) CKS(stage_stack(0, st, [&] { return order_done(out->h2d_done, 1, st); }));
     CK(tl.mark(st, "h2d"));
   }
+  CK(order_wait(out->compute_after, 2, st));
 
   // ------------------------------------------- Loop 2, part 1: Cholesky routing
   CK(launch_potrf_route(TAA, static_cast<double*>(q), static_cast<int32_t*>(info_d), static_cast<int>(na),
@@ -700,8 +733,10 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     // A rides the copy engine while (UB)^H(UB) runs -- after B's DMAs, so the
     // two uploads do not split the PCIe bandwidth B is waited on
     CK(cudaStreamWaitEvent(cs, ev_b_up, 0));
-    CKS(stage_stack(0, cs));
-    tr.mark(cs, "h2d_a");
+    CKS(stage_stack(0, cs, [&] {
+      tr.mark(cs, "h2d_a");
+      return order_done(out->h2d_done, 1, cs);
+    }));
     cudaEvent_t ev_a;
     CK(cudaEventCreateWithFlags(&ev_a, cudaEventDisableTiming));
     EvDel ev_a_del{ev_a};
@@ -838,6 +873,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     CK(tl.mark(st, "h"));
     tr.mark(st, "h_done");
   }
+  CK(order_done(out->compute_done, 2, st));
 
   // --------------------------------------------------------------- outputs
   if (out->location == HSB_LOC_HOST) {
@@ -847,15 +883,21 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     // columns [c0, c1) of a final matrix to the host, on the copy stream.
     // lower_d2h: one copy per 256-column block [a, b) of rows >= a, and a host
     // mirror job for rows [a, b) of the columns >= b once it has landed
+    // HSB_LOWER_D2H (experiments): which matrices cross as lower triangles ("hs", "s", "h", "-")
+    static const std::string lower_which = [] {
+      const char* e = std::getenv("HSB_LOWER_D2H");
+      return std::string(e ? e : "hs");
+    }();
     auto download = [&](double* dst, const double* src, int64_t c0, int64_t c1) -> hsb_status {
-      const int64_t step = lower_d2h ? 256 : c1 - c0;
+      const bool lower = lower_d2h && lower_which.find(dst == out->h ? 'h' : 's') != std::string::npos;
+      const int64_t step = lower ? 256 : c1 - c0;
       for (int64_t a = c0; a < c1; a += step) {
-        const int64_t b = std::min(c1, a + step), r0 = lower_d2h ? a : 0;
+        const int64_t b = std::min(c1, a + step), r0 = lower ? a : 0;
         CK(cudaMemcpy2DAsync(reinterpret_cast<char*>(dst) + (a * out->ld + r0) * 16, out->ld * 16,
                              reinterpret_cast<const char*>(src) + (a * ldo + r0) * 16, ldo * 16, (ng - r0) * 16,
                              b - a, cudaMemcpyDeviceToHost, cs));
         d2h_bytes += 16.0 * (ng - r0) * (b - a);
-        if (lower_d2h) CK(mirror.push(cs, dst, out->ld, ng, a, b));
+        if (lower) CK(mirror.push(cs, dst, out->ld, ng, a, b));
       }
       return HSB_OK;
     };

@@ -225,7 +225,7 @@ def _validate_shapes(p) -> None:
         raise
 
 
-def _build_host(p, policy, force_nonhpd, slot: int = 0, stream=None, s_ready=None) -> BuildOutput:
+def _build_host(p, policy, force_nonhpd, slot: int = 0, stream=None, s_ready=None, order=None) -> BuildOutput:
     _validate_shapes(p)
     pol = _policy(policy)
     dims = Dims(p.dims.n_atoms, p.dims.n_l, p.dims.n_g)
@@ -238,6 +238,8 @@ def _build_host(p, policy, force_nonhpd, slot: int = 0, stream=None, s_ready=Non
     out.h, out.s = h.ctypes.data, s.ctypes.data
     if s_ready is not None:
         out.s_ready = s_ready
+    if order is not None:  # (h2d_after, h2d_done, compute_after, compute_done, order_in, order_out)
+        (out.h2d_after, out.h2d_done, out.compute_after, out.compute_done, out.order_in, out.order_out) = order
     tim, info = _call_build(pol, prob, out, stream, force_nonhpd, dims.n_atoms, slot)
     t = _timings_dict(tim)
     led = ledger_from_timings(dims, info, t, force_nonhpd)
@@ -249,11 +251,15 @@ def iter_hs_kpoints(instances, policy=None, force_nonhpd: bool = False, depth: i
     """Yield ``build_hs`` of each independent k-point (BASELINE config C5) in
     input order, pipelined on one GPU: ``depth`` host threads each drive their
     own context and CUDA stream, so one k-point's uploads and H/S downloads
-    (PCIe) overlap another's kernels.  At most ``depth`` results are in flight
-    beyond the one being consumed, so pinned output memory stays bounded when
-    the caller drops each result after use."""
+    (PCIe) overlap another's kernels.  Consecutive k-points are chained by
+    CUDA events (hsb_output.h2d_after / compute_after): uploads run back to
+    back in k-point order on the host-to-device engine, kernels in k-point
+    order on the SMs, and each k-point's downloads overlap the next one's
+    kernels and the one after's uploads -- a three-stage pipeline at
+    depth >= 3.  At most ``depth`` results are in flight beyond the one being
+    consumed, so pinned output memory stays bounded when the caller drops each
+    result after use."""
     import threading
-    import time
 
     import torch
 
@@ -283,36 +289,45 @@ def iter_hs_kpoints(instances, policy=None, force_nonhpd: bool = False, depth: i
     consumed = [0]
     failure = []
 
-    # stagger: lane k starts once lane k-1's first S is final (its event), so the
-    # lanes alternate between transfers and kernels instead of running in lockstep
-    s_events = [torch.cuda.Event() for _ in range(depth)]
-    for ev in s_events:
+    # ordering: k-point i's uploads wait for k-point i-1's (h2d events), its
+    # kernels for k-point i-1's (compute events).  The library only waits on an
+    # event once the previous call has recorded it (progress flags, one per
+    # k-point).  Events are recycled modulo depth + 2: k-point i + depth + 2
+    # starts only after result i + 1 was consumed, i.e. after k-point i + 1
+    # finished waiting on k-point i's events.
+    n_ev = depth + 2
+    h2d_ev = [torch.cuda.Event() for _ in range(n_ev)]
+    cmp_ev = [torch.cuda.Event() for _ in range(n_ev)]
+    for ev in h2d_ev + cmp_ev:
         ev.record(torch.cuda.current_stream(dev))  # materialise the CUDA events
-    entered = [threading.Event() for _ in range(depth)]
+    torch.cuda.current_stream(dev).synchronize()
+    flags = (ctypes.c_int32 * len(instances))()
+    flag_ptr = ctypes.cast(flags, ctypes.c_void_p).value
+
+    def order_of(i):
+        def fp(j):
+            return ctypes.cast(ctypes.c_void_p(flag_ptr + 4 * j), ctypes.POINTER(ctypes.c_int32))
+        prev = (h2d_ev[(i - 1) % n_ev].cuda_event, cmp_ev[(i - 1) % n_ev].cuda_event, fp(i - 1)) if i > 0 \
+            else (None, None, None)
+        return (prev[0], h2d_ev[i % n_ev].cuda_event, prev[1], cmp_ev[i % n_ev].cuda_event, prev[2], fp(i))
 
     def lane(slot):  # one thread per context: k-points slot, slot + depth, ...
         st = ctypes.c_void_p(streams[slot].cuda_stream)
         try:
-            if slot > 0:
-                entered[slot - 1].wait()
-                time.sleep(0.005)  # lane slot-1 enqueues its S event within its first milliseconds
-                s_events[slot - 1].synchronize()
-            for n_done, i in enumerate(range(slot, len(instances), depth)):
+            for i in range(slot, len(instances), depth):
                 with window:
                     window.wait_for(lambda: failure or i < consumed[0] + depth)
                 if failure:
                     return
-                if n_done == 0:
-                    entered[slot].set()
-                results[i] = _build_host(instances[i], pol, force_nonhpd, slot=slot, stream=st,
-                                         s_ready=s_events[slot].cuda_event if n_done == 0 else None)
+                results[i] = _build_host(instances[i], pol, force_nonhpd, slot=slot, stream=st, order=order_of(i))
                 ready[i].set()
         except BaseException as exc:  # noqa: BLE001 - re-raised in the consumer
             failure.append(exc)
             for e in ready:
                 e.set()
         finally:
-            entered[slot].set()
+            for i in range(slot, len(instances), depth):  # never leave a later k-point waiting
+                flags[i] = max(flags[i], 2)
 
     threads = [threading.Thread(target=lane, args=(k,), daemon=True) for k in range(depth)]
     for t in threads:

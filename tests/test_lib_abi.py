@@ -29,13 +29,13 @@ def test_library_exports_every_declared_symbol():
 
 def test_loader_and_abi_version():
     lib = _lib.load()
-    assert lib.hsb_abi_version() == 5
+    assert lib.hsb_abi_version() == 6
 
 
 def test_binding_struct_layout_matches_header():
     # 3*8 + 2*4 + 6 pointers + 6 pointers
     assert ctypes.sizeof(_lib.HsbProblem) == 32 + 12 * 8
-    assert ctypes.sizeof(_lib.HsbOutput) == 8 + 8 + 32
+    assert ctypes.sizeof(_lib.HsbOutput) == 8 + 8 + 10 * 8  # h, s, peer, s_ready, 4 events, 2 flags
     assert ctypes.sizeof(_lib.HsbPeerOut) == 8 + 8 + 8 + 16
     assert ctypes.sizeof(_lib.HsbTimings) == 13 * 8 + 16 + 2 * 8
 
