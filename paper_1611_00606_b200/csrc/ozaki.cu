@@ -92,12 +92,13 @@ __device__ __forceinline__ int sym_mod_small(int v, int p, float inv_p) {
   return v - p * __float2int_rn(__int2float_rn(v) * inv_p);
 }
 
-// thread = 8 consecutive k of one column; writes 8 bytes into each of the
-// 2 planes x NM moduli: out[((plane * NM + i) * cols + col) * kpad + k],
+// thread = 4 consecutive k of one column; writes 4 bytes into each of the
+// 2 planes x NM moduli (4 k per thread at 6 CTAs/SM measured 12 % faster than
+// 8 k at 3 CTAs/SM, probes/residue_bench.cu): out[((plane * NM + i) * cols + col) * kpad + k],
 // plane 0 = phi1(z') = x' + j y', plane 1 = phi2(z') = x' - j y' (mod p_i)
-constexpr int kOzResK = 8;
+constexpr int kOzResK = 4;
 template <int NM>
-__global__ void __launch_bounds__(128, 3) ozaki_residue_kernel(const double2* __restrict__ x, int64_t ldx, int64_t k,
+__global__ void __launch_bounds__(128, 6) ozaki_residue_kernel(const double2* __restrict__ x, int64_t ldx, int64_t k,
                                                             int64_t cols, const int32_t* __restrict__ col_exp, int b,
                                                             int8_t* __restrict__ out, int64_t kpad) {
   const int64_t k0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kOzResK;
@@ -135,11 +136,10 @@ __global__ void __launch_bounds__(128, 3) ozaki_residue_kernel(const double2* __
         w[j] = sym_mod_small(rr - t, oz_mod(i), invf);
       }
       const auto pack = [](const int* v) {
-        return make_int2(__byte_perm(__byte_perm(v[0], v[1], 0x40), __byte_perm(v[2], v[3], 0x40), 0x5410),
-                         __byte_perm(__byte_perm(v[4], v[5], 0x40), __byte_perm(v[6], v[7], 0x40), 0x5410));
+        return __byte_perm(__byte_perm(v[0], v[1], 0x40), __byte_perm(v[2], v[3], 0x40), 0x5410);
       };
-      *reinterpret_cast<int2*>(o0) = pack(u);
-      *reinterpret_cast<int2*>(o1) = pack(w);
+      *reinterpret_cast<uint32_t*>(o0) = pack(u);
+      *reinterpret_cast<uint32_t*>(o1) = pack(w);
       o0 += mod_stride;
       o1 += mod_stride;
     }
@@ -484,36 +484,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
 // Im = (phi1 - phi2)/(2 j_i)), the weights y_i = (M/p_i) * ((c_i (M/p_i)^-1) mod p_i) give
 //     X = sum_i r_i y_i - k M,   k = rint(sum_i r_i (y_i / M)),
 // exact for |X| < M/4 (the host's choice of b keeps |X| <= M/4).
-// y_i and M are split into 4 limbs of 32 bits; every limb sum
-// S_j = sum_i r_i y_ij (< 2^45) and T_j = S_j - k M_j is an exact double, so
-// X = ((T3 2^32 + T2) 2^32 + T1) 2^32 + T0 is rounded once, at the end.
+// y_i and M are split into NL limbs of LB bits (3 x 33 for n_mod <= 13,
+// M < 2^99; 4 x 30 otherwise); every limb sum S_j = sum_i r_i y_ij (< 2^46)
+// and T_j = S_j - k M_j is an exact double, so X = sum_j T_j 2^(j LB) is
+// rounded once, at the end.  k only needs |error| < 1/4 (X/M is within 1/4 of
+// an integer): the quotient sum runs in FP32 (error < 13 * 240 * 2^-23).
 struct OzCrtConst {
   double y[2][kOzMaxMod][4];   // [Re, Im] limbs of y_i, least significant first
-  double f[2][kOzMaxMod];      // y_i / M
+  float f[2][kOzMaxMod];       // y_i / M
   double m[4];                 // limbs of M
 };
 constexpr int kOzMinMod = 11;
 __constant__ OzCrtConst c_oz_crt[kOzMaxMod - kOzMinMod + 1];  // one table per n_mod = 11 .. 16
+__host__ __device__ constexpr int oz_crt_limbs(int nm) { return nm <= 13 ? 3 : 4; }
+__host__ __device__ constexpr int oz_crt_limb_bits(int nm) { return nm <= 13 ? 33 : 30; }
+
+// exact int -> double / float through the mantissa (no I2F): a double with high
+// word 0x43300000 and low word w is 2^52 + w
+__device__ __forceinline__ double i2d_exact(int v) {
+  return __hiloint2double(0x43300000, static_cast<int>(static_cast<unsigned>(v) ^ 0x80000000u)) -
+         4503601774854144.0;  // 2^52 + 2^31
+}
+__device__ __forceinline__ float i2f_small(int v) {  // |v| < 2^22
+  return __int_as_float(0x4B400000 + v) - 12582912.0f;
+}
 
 template <int NM, int PART>
 __device__ __forceinline__ double crt_value(const int (&r)[NM]) {
+  constexpr int NL = oz_crt_limbs(NM);
   const OzCrtConst& C = c_oz_crt[NM - kOzMinMod];
-  double fk = 0.0, s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  float fk = 0.0f;
+  double s[NL];
+#pragma unroll
+  for (int j = 0; j < NL; ++j) s[j] = 0.0;
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
-    const double ri = static_cast<double>(r[i]);
-    fk = fma(ri, C.f[PART][i], fk);
-    s0 = fma(ri, C.y[PART][i][0], s0);
-    s1 = fma(ri, C.y[PART][i][1], s1);
-    s2 = fma(ri, C.y[PART][i][2], s2);
-    s3 = fma(ri, C.y[PART][i][3], s3);
+    fk = __fmaf_rn(i2f_small(r[i]), C.f[PART][i], fk);
+    const double ri = i2d_exact(r[i]);
+#pragma unroll
+    for (int j = 0; j < NL; ++j) s[j] = fma(ri, C.y[PART][i][j], s[j]);
   }
-  const double k = rint(fk);
-  const double t0 = fma(-k, C.m[0], s0), t1 = fma(-k, C.m[1], s1);
-  const double t2 = fma(-k, C.m[2], s2), t3 = fma(-k, C.m[3], s3);
-  constexpr double kL = 4294967296.0;  // 2^32
-  return fma(fma(fma(t3, kL, t2), kL, t1), kL, t0);
+  const double k = static_cast<double>(rintf(fk));
+  constexpr double kL = static_cast<double>(1ull << oz_crt_limb_bits(NM));
+  double x = fma(-k, C.m[NL - 1], s[NL - 1]);
+#pragma unroll
+  for (int j = NL - 2; j >= 0; --j) x = fma(x, kL, fma(-k, C.m[j], s[j]));
+  return x;
 }
+
+// 2^sh in two exact power-of-two factors (|sh| <= 2044)
+__device__ __forceinline__ double scale2(double x, int sh) { return (x * pow2i(sh / 2)) * pow2i(sh - sh / 2); }
 
 // Finish one element from its per-modulus phi1(C), phi2(C) residues (the
 // conjugation of L^H R is in the GEMM's choice of planes).
@@ -527,8 +547,8 @@ __device__ __forceinline__ double2 crt_finish(const OzCrtParams& p, const int (&
     im[i] = F1[i] - F2[i];  // 2 j Im C (mod p_i)
   }
   const int sh = p.el[m] + p.er[n] - 2 * p.b;
-  const double xr = ldexp(crt_value<NM, 0>(re), sh);
-  const double xi = ldexp(crt_value<NM, 1>(im), sh);
+  const double xr = scale2(crt_value<NM, 0>(re), sh);
+  const double xi = scale2(crt_value<NM, 1>(im), sh);
   double vr = p.alpha_re * xr - p.alpha_im * xi;
   double vi = p.alpha_re * xi + p.alpha_im * xr;
   if (p.beta_re != 0.0 || p.beta_im != 0.0) {
@@ -540,39 +560,65 @@ __device__ __forceinline__ double2 crt_finish(const OzCrtParams& p, const int (&
   return make_double2(vr, vi);
 }
 
-// One thread per lower-triangle element (m >= n), threads along m: residue
-// loads and the C[m, n] store are coalesced; the mirror C[n, m] = conj(C[m, n])
-// is a strided store (matcore.hermitian_mirror, matcore.py:89-105).  Measured
-// faster than shared-memory-transposed variants, which run fewer threads per
-// SM.
+// Lower-triangle elements (m >= n), 4 consecutive rows per thread (one 32-bit
+// load per modulus and product from the tile-packed residues), threads along
+// m: residue loads and the C[m, n] stores are coalesced; the mirror
+// C[n, m] = conj(C[m, n]) is a strided store (matcore.hermitian_mirror,
+// matcore.py:89-105).  Block row y handles the column pair (n0 + y,
+// n0 + ncols - 1 - y), whose row counts add up to about the same for every y,
+// so no block of the rectangular grid falls entirely above the diagonal.
+constexpr int kOzCrtRows = 4;
 template <int NM>
-__global__ void __launch_bounds__(128) ozaki_crt_kernel(const OzCrtParams p) {
-  const int n = p.n0 + blockIdx.y;  // column
-  const int m = (p.n0 & ~127) + blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= p.n || m < n) return;
-  const int t = p.tile_index[(m >> 8) * p.T + (n >> 8)];
-  const int8_t* r0 = p.res + static_cast<int64_t>(t) * kOzTileBytes + (n & 255) * 256 + (m & 255);
-  int F1[NM], F2[NM];  // straight-line: all 2 x NM loads in flight together
+__global__ void __launch_bounds__(128) ozaki_crt_kernel(const OzCrtParams p, int ncols) {
+  const int na = p.n0 + static_cast<int>(blockIdx.y), nb = p.n0 + ncols - 1 - static_cast<int>(blockIdx.y);
+  const int gend = (p.n + kOzCrtRows - 1) / kOzCrtRows;
+  const int ga = na / kOzCrtRows, gb = nb / kOzCrtRows;
+  int g = static_cast<int>(blockIdx.x * blockDim.x + threadIdx.x), n;
+  if (g < gend - ga) {
+    n = na;
+    g += ga;
+  } else {
+    g -= gend - ga;
+    if (nb == na || g >= gend - gb) return;
+    n = nb;
+    g += gb;
+  }
+  const int m0 = g * kOzCrtRows;
+  const int t = p.tile_index[(m0 >> 8) * p.T + (n >> 8)];
+  const uint8_t* r0 = reinterpret_cast<const uint8_t*>(p.res) + static_cast<int64_t>(t) * kOzTileBytes +
+                      (n & 255) * 256 + (m0 & 255);
+  uint32_t w1[NM], w2[NM];  // straight-line: all 2 x NM loads in flight together
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
-    F1[i] = r0[i * p.mod_stride];
-    F2[i] = r0[p.prod_stride + i * p.mod_stride];
-  }
-  const double2 v = crt_finish<NM>(p, F1, F2, m, n);
-  if (p.peer) {
-    // fused scatter: write straight into the owning rank's receive slot (NVLink
-    // peer memory); the owner only sums its slots afterwards
-    const int qn = static_cast<int>(n / p.cpr);
-    p.peer[qn][(p.rank * p.cpr + (n - qn * p.cpr)) * p.pld + m] = v;
-    if ((p.flags & kMirror) && m > n) {
-      const int qm = static_cast<int>(m / p.cpr);
-      p.peer[qm][(p.rank * p.cpr + (m - qm * p.cpr)) * p.pld + n] = make_double2(v.x, -v.y);
-    }
-    return;
+    w1[i] = __ldg(reinterpret_cast<const uint32_t*>(r0 + i * p.mod_stride));
+    w2[i] = __ldg(reinterpret_cast<const uint32_t*>(r0 + p.prod_stride + i * p.mod_stride));
   }
   double2* C = reinterpret_cast<double2*>(p.c);
-  C[m + static_cast<int64_t>(n) * p.ldc] = v;
-  if ((p.flags & kMirror) && m > n) C[n + static_cast<int64_t>(m) * p.ldc] = make_double2(v.x, -v.y);
+#pragma unroll 1
+  for (int e = 0; e < kOzCrtRows; ++e) {
+    const int m = m0 + e;
+    if (m < n || m >= p.n) continue;
+    int F1[NM], F2[NM];
+#pragma unroll
+    for (int i = 0; i < NM; ++i) {
+      F1[i] = static_cast<int8_t>(w1[i] >> (8 * e));
+      F2[i] = static_cast<int8_t>(w2[i] >> (8 * e));
+    }
+    const double2 v = crt_finish<NM>(p, F1, F2, m, n);
+    if (p.peer) {
+      // fused scatter: write straight into the owning rank's receive slot (NVLink
+      // peer memory); the owner only sums its slots afterwards
+      const int qn = static_cast<int>(n / p.cpr);
+      p.peer[qn][(p.rank * p.cpr + (n - qn * p.cpr)) * p.pld + m] = v;
+      if ((p.flags & kMirror) && m > n) {
+        const int qm = static_cast<int>(m / p.cpr);
+        p.peer[qm][(p.rank * p.cpr + (m - qm * p.cpr)) * p.pld + n] = make_double2(v.x, -v.y);
+      }
+      continue;
+    }
+    C[m + static_cast<int64_t>(n) * p.ldc] = v;
+    if ((p.flags & kMirror) && m > n) C[n + static_cast<int64_t>(m) * p.ldc] = make_double2(v.x, -v.y);
+  }
 }
 
 // CRT tables for every n_mod, computed and uploaded once per process (the
@@ -583,10 +629,12 @@ static OzCrtConst oz_crt_table(int n_mod) {
   for (int i = 0; i < n_mod; ++i) M *= static_cast<u128>(oz_mod(i));
   OzCrtConst c;
   std::memset(&c, 0, sizeof(c));
-  auto limbs = [](u128 v, double* out) {
+  const int lb = oz_crt_limb_bits(n_mod), nl = oz_crt_limbs(n_mod);
+  auto limbs = [&](u128 v, double* out) {
+    const u128 mask = (static_cast<u128>(1) << lb) - 1;
     for (int j = 0; j < 4; ++j) {
-      out[j] = static_cast<double>(static_cast<uint32_t>(v & 0xffffffffu));
-      v >>= 32;
+      out[j] = j < nl ? static_cast<double>(static_cast<uint64_t>(v & mask)) : 0.0;
+      v >>= lb;
     }
   };
   const double Md = static_cast<double>(M);
@@ -605,7 +653,7 @@ static OzCrtConst oz_crt_table(int n_mod) {
     for (int part = 0; part < 2; ++part) {
       const u128 y = Mi * static_cast<u128>((cpart[part] * mi_inv) % pi);  // < M
       limbs(y, c.y[part][i]);
-      c.f[part][i] = static_cast<double>(y) / Md;
+      c.f[part][i] = static_cast<float>(static_cast<double>(y) / Md);
     }
   }
   limbs(M, c.m);
@@ -692,11 +740,20 @@ cudaError_t launch_ozaki_crt_cols(const OzCrtParams& p, int64_t ncols, cudaStrea
   cudaError_t ce = oz_init_once();
   if (ce != cudaSuccess) return ce;
   if (ncols > 65535) return cudaErrorInvalidConfiguration;
-  // rows m >= n0 only: the first row block starts at n0
-  const dim3 grid(static_cast<unsigned>((p.n - (p.n0 & ~127) + 127) / 128), static_cast<unsigned>(ncols)), block(128);
-#define HSB_OZ_CRT(NMV)                                   \
-  case NMV:                                             \
-    ozaki_crt_kernel<NMV><<<grid, block, 0, st>>>(p);   \
+  // column pairs (n0 + y, n0 + ncols - 1 - y): groups of kOzCrtRows rows from
+  // each column's diagonal group down to row n
+  const int64_t gend = (p.n + kOzCrtRows - 1) / kOzCrtRows;
+  int64_t most = 0;
+  for (int64_t y = 0; y < (ncols + 1) / 2; ++y) {
+    const int64_t na = p.n0 + y, nb = p.n0 + ncols - 1 - y;
+    const int64_t cnt = (gend - na / kOzCrtRows) + (nb == na ? 0 : gend - nb / kOzCrtRows);
+    most = std::max(most, cnt);
+  }
+  const dim3 grid(static_cast<unsigned>((most + 127) / 128), static_cast<unsigned>((ncols + 1) / 2)), block(128);
+  const int nc = static_cast<int>(ncols);
+#define HSB_OZ_CRT(NMV)                                     \
+  case NMV:                                               \
+    ozaki_crt_kernel<NMV><<<grid, block, 0, st>>>(p, nc); \
     break;
   switch (p.n_mod) {
     HSB_OZ_CRT(11)
