@@ -241,15 +241,17 @@ def test_pinned_instance_path_matches_and_checks_values():
         build_hs(q)
 
 
-@pytest.mark.parametrize("cm", ["3m", "int8"])
-def test_kpoint_pipeline_matches_serial_builds(cm):
-    # BASELINE config C5 on one GPU: independent k-points through two contexts
-    # and streams concurrently; each result equals its serial build bitwise
+@pytest.mark.parametrize("cm,depth", [("3m", 2), ("int8", 2), ("int8", 3)])
+def test_kpoint_pipeline_matches_serial_builds(cm, depth):
+    # BASELINE config C5 on one GPU: independent k-points through several
+    # contexts and streams, chained by upload / compute events; each result
+    # equals its serial build bitwise (k-points of different sizes included)
     from paper_1611_00606_b200 import build_hs_kpoints
 
-    ps = [generate(ProblemSpec(Dims(3, 25, 260), seed=40 + i, nonhpd_fraction=0.3)) for i in range(5)]
+    ps = [generate(ProblemSpec(Dims(3, 25, 260 + 37 * (i % 3)), seed=40 + i, nonhpd_fraction=0.3))
+          for i in range(7)]
     serial = [build_hs(p, _pol(cm)) for p in ps]
-    piped = build_hs_kpoints(ps, _pol(cm), depth=2)
+    piped = build_hs_kpoints(ps, _pol(cm), depth=depth)
     for a, b, p in zip(serial, piped, ps):
         assert a.h.matrix.tobytes() == b.h.matrix.tobytes()
         assert a.s.matrix.tobytes() == b.s.matrix.tobytes()
@@ -274,3 +276,24 @@ def test_kpoint_iterator_early_exit_and_slow_consumer():
             break  # generator closed with lanes still running
     assert got == [2, 2, 2, 2]
     assert len(list(iter_hs_kpoints(ps, _pol("int8"), depth=3))) == 7
+
+
+@pytest.mark.timeout(120)
+def test_kpoint_pipeline_failure_mid_batch_does_not_hang():
+    # a k-point that fails validation on the device (non-finite A) must surface
+    # as the reference's InvariantError without leaving later k-points waiting
+    # on its upload / compute events
+    from paper_1611_00606_b200 import iter_hs_kpoints
+
+    from paper_1611_00606_b200 import pin_instance
+
+    ps = [pin_instance(generate(ProblemSpec(Dims(2, 16, 140), seed=120 + i))) for i in range(6)]
+    ps[2].a_blocks[1][3, 5] = complex(float("nan"), 0.0)
+    got = []
+    with pytest.raises(InvariantError, match=r"a_blocks\[1\]"):
+        for out in iter_hs_kpoints(ps, _pol("int8"), depth=3):
+            got.append(out)
+    assert len(got) == 2
+    # the lanes were released: a new batch runs normally
+    ps[2].a_blocks[1][3, 5] = 0.0
+    assert len(list(iter_hs_kpoints(ps, _pol("int8"), depth=3))) == 6
