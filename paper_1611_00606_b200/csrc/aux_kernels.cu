@@ -113,6 +113,20 @@ __global__ void half_mirror_kernel(const double2* __restrict__ t, double2* __res
   }
 }
 
+// out_a = T_a^H (column-major n x n blocks)
+__global__ void conj_transpose_kernel(const double2* __restrict__ t, double2* __restrict__ out, int n,
+                                      int64_t count) {
+  const int64_t nn = static_cast<int64_t>(n) * n;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < count * nn;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t a = idx / nn;
+    const int r = static_cast<int>(idx % nn);
+    const int i = r % n, j = r / n;
+    const double2 w = t[a * nn + j + static_cast<int64_t>(i) * n];
+    out[idx] = make_double2(w.x, -w.y);
+  }
+}
+
 // dst[r, g] = u[r] * src[r, g]   (kernels.diag_scale, kernels.py:328-339)
 __global__ void diag_scale_kernel(const double2* __restrict__ src, int64_t lds,
                                   double2* __restrict__ dst, int64_t ldd,
@@ -269,6 +283,14 @@ cudaError_t launch_half_mirror(const double* t, double* out, int n, int64_t coun
   const int64_t total = count * n * n;
   half_mirror_kernel<<<grid_for(total, 256, 148 * 16), 256, 0, st>>>(
       reinterpret_cast<const double2*>(t), reinterpret_cast<double2*>(out), n, count, scale);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_conj_transpose(const double* t, double* out, int n, int64_t count, cudaStream_t st) {
+  const int64_t total = count * static_cast<int64_t>(n) * n;
+  if (total <= 0) return cudaSuccess;
+  conj_transpose_kernel<<<grid_for(total, 256, 148 * 16), 256, 0, st>>>(reinterpret_cast<const double2*>(t),
+                                                                         reinterpret_cast<double2*>(out), n, count);
   return cudaGetLastError();
 }
 

@@ -715,6 +715,40 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     CK(tl.mark(st, "loop1"));
     return HSB_OK;
   };
+  // Fused path: H = sum_a X_a^H M_a X_a with X_a = [A_a; B_a] and the
+  // Hermitian M_a = [[T_AA, T_AB], [T_AB^H, T_BB]] (Eq. 7; the
+  // reference's Loop 1 / H1 / Loop 2 / H2 / H3 regroup these four terms):
+  // V1_a = T_AA A_a + T_AB B_a and V2_a = T_AB^H A_a + T_BB B_a (batched, into the
+  // Z and R stacks), then H = A^H V1 + B^H V2 over the lower triangle, a
+  // reduction of 2K instead of the 3K of Z^H B + B^H Z + Y^H Y.  The same
+  // product covers HPD and non-HPD T_AA alike; potrf_route still runs for the
+  // reference's split counts.  T_AA and T_BB are read from their lower
+  // triangles (kernels.py:223-231, 296-307), as in the reference.
+  auto vloop = [&]() -> hsb_status {
+    void *taa_full, *tab_h;
+    CKS(ws(ctx, "taa_full", tblk_bytes * na, &taa_full));
+    CKS(ws(ctx, "tab_h", tblk_bytes * na, &tab_h));
+    CK(launch_half_mirror(TAA, static_cast<double*>(taa_full), static_cast<int>(nl), na, 1.0, st));
+    CK(launch_half_mirror(TBB, static_cast<double*>(pbb), static_cast<int>(nl), na, 1.0, st));
+    CK(launch_conj_transpose(TAB, static_cast<double*>(tab_h), static_cast<int>(nl), na, st));
+    launches += 3;
+    for (int half = 0; half < 2; ++half) {  // zrk form: sum_s L_s^H R_s
+      ZrkCall z;
+      const double* l0 = half == 0 ? static_cast<const double*>(taa_full) : TAB;              // T_AA | (T_AB^H)^H
+      const double* l1 = half == 0 ? static_cast<const double*>(tab_h) : static_cast<const double*>(pbb);  // (T_AB)^H^H | T_BB
+      z.segs.push_back({atom_mats(l0, na, nl), atom_rows(A, na, nl, ng, K)});
+      z.segs.push_back({atom_mats(l1, na, nl), atom_rows(B, na, nl, ng, K)});
+      z.m = nl;
+      z.n = ng;
+      z.c = half == 0 ? Z : R;
+      z.ldc = K;
+      z.batch = na;
+      z.c_bstride = nl;
+      CKS(run_zrk(ctx, st, z, &launches));
+    }
+    CK(tl.mark(st, "loop1"));
+    return HSB_OK;
+  };
   auto unorm = [&]() -> hsb_status {  // UB = diag(u) B (builder.py:124-127)
     CK(launch_diag_scale(B, K, UB, K, U, K, ng, st));
     ++launches;
@@ -749,7 +783,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     if (chunk_s) s1.chunk_events = &s_chunks;
     CKS(run_zrk(ctx, st, s1, &launches));
     CK(tl.mark(st, "s1"));
-    CKS(loop1());
+    CKS(vloop());
   } else if (unfused) {
     CKS(loop1());
     ZrkCall h1 = tri_call(H, ldo, ng, kLowerOnly | kZeroImagDiag, 0.0);  // builder.h_cross (builder.py:91-104)
@@ -769,7 +803,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     ++launches;
     CK(tl.mark(st, "s2"));
   } else {
-    CKS(loop1());
+    CKS(vloop());
     CKS(unorm());
     ZrkCall s = tri_call(S, ldo, ng, kLowerOnly | kMirror, 0.0);
     s.segs.push_back({plain(A, K, ng, K), plain(A, K, ng, K)});
@@ -798,8 +832,9 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   const int32_t* offs_dev = static_cast<int32_t*>(offs_d);
 
   // ------------------------------------------- Loop 2, part 2 (builder.py:162-185)
+  // (unfused path only: the fused H uses V1, V2)
   double* ANH = nullptr;
-  {
+  if (unfused) {
     ZrkCall z;
     z.segs.push_back({atom_mats(static_cast<double*>(q), na, nl), atom_rows(A, na, nl, ng, K)});
     z.m = nl;
@@ -847,10 +882,8 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     CK(tl.mark(st, "h3"));
   } else {
     ZrkCall h = tri_call(H, ldo, ng, kLowerOnly | kMirror, 0.0);
-    h.segs.push_back({plain(Z, K, ng, K), plain(B, K, ng, K)});
-    h.segs.push_back({plain(B, K, ng, K), plain(Z, K, ng, K)});
-    if (n_hpd > 0) h.segs.push_back({plain(Y, k_hpd, ng, K), plain(Y, k_hpd, ng, K)});
-    if (n_nh > 0) h.segs.push_back({plain(ANH, k_nh, ng, k_nh), plain(XNH, k_nh, ng, K)});
+    h.segs.push_back({plain(A, K, ng, K), plain(Z, K, ng, K)});  // A^H V1
+    h.segs.push_back({plain(B, K, ng, K), plain(R, K, ng, K)});  // B^H V2
     h.tl = &tl, h.sect = "h", h.core = "h_core";
     h.peer = peer;
     h.peer_is_h = true;
