@@ -576,8 +576,11 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   const size_t out_bytes = static_cast<size_t>(ng) * ng * 16;
   if (out->location == HSB_LOC_HOST) {
     void *h, *s;
-    CKS(ws(ctx, "out_h", out_bytes, &h));
-    CKS(ws(ctx, "out_s", out_bytes, &s));
+    // host inputs: the pinned blocks land in these buffers first (raw_b in
+    // out_s, raw_a in out_h; see stage_stack), so they hold a stack as well
+    const size_t ob = host_in ? std::max(out_bytes, stack_bytes) : out_bytes;
+    CKS(ws(ctx, "out_h", ob, &h));
+    CKS(ws(ctx, "out_s", ob, &s));
     H = static_cast<double*>(h);
     S = static_cast<double*>(s);
     ldo = ng;
@@ -624,7 +627,13 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     int64_t bad = -1;
     if (all_pinned) {
       void* raw;
-      CKS(ws(ctx, m == 0 ? "raw_a" : "raw_b", stack_bytes, &raw));
+      // atom-major landing buffer; with host outputs it aliases an output
+      // buffer written only after the restack: B's (stream order on st:
+      // restack, U norm, then S) in out_s, A's (restacked on the copy stream
+      // before the compute stream waits for it) in out_h
+      const bool alias = out->location == HSB_LOC_HOST;
+      CKS(ws(ctx, alias ? (m == 0 ? "out_h" : "out_s") : (m == 0 ? "raw_a" : "raw_b"),
+             alias ? std::max(out_bytes, stack_bytes) : stack_bytes, &raw));
       const size_t blk = static_cast<size_t>(nl) * ng * 16;
       for (int64_t i = 0; i < na; ++i)
         CK(cudaMemcpyAsync(static_cast<char*>(raw) + i * blk, blocks[i], blk, cudaMemcpyHostToDevice, s));
