@@ -189,6 +189,28 @@ hsb_status oz_tiles(hsb_ctx* ctx, int64_t n, cudaStream_t st, const int2** out, 
   return HSB_OK;
 }
 
+// moduli: the fewest with b >= oz_min_bits.  With |x'| + |y'| <= 2^b per
+// element, |Re C'| = |sum x'x' + y'y'| and |Im C'| = |sum x'_L y'_R - y'_L x'_R|
+// are both <= K 2^2b; the explicit CRT needs |X| < M/2, kept with one bit of
+// margin: 2b <= log2 M - 2 - log2 K.
+hsb_status oz_choose(hsb_ctx* ctx, int64_t ktot, int* n_mod_out, int* b_out) {
+  int n_mod = 0, b = 0;
+  double log2m = 0;
+  for (int i = 0; i < kOzMaxMod; ++i) {
+    log2m += std::log2(static_cast<double>(oz_mod(i)));
+    const int bi = static_cast<int>(std::floor((log2m - 2.0 - std::log2(static_cast<double>(std::max<int64_t>(ktot, 1)))) / 2.0));
+    if (i + 1 >= 11 && (bi >= ctx->oz_min_bits || i + 1 == kOzMaxMod)) {
+      n_mod = i + 1;
+      b = std::min(bi, ctx->oz_min_bits + 4);
+      break;
+    }
+  }
+  if (b < 30) return fail(ctx, HSB_ERR_UNSUPPORTED, "reduction too long for the INT8 engine's moduli");
+  *n_mod_out = n_mod;
+  *b_out = b;
+  return HSB_OK;
+}
+
 hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launches) {
   const int64_t n = z.m;
   std::vector<Seg> segs;
@@ -200,30 +222,22 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
       ktot += s.l.k;
     }
   if (segs.size() > static_cast<size_t>(kOzMaxSeg)) return fail(ctx, HSB_ERR_UNSUPPORTED, "too many segments");
-  // moduli: the fewest with b >= oz_min_bits.  With |x'| + |y'| <= 2^b per
-  // element, |Re C'| = |sum x'x' + y'y'| and |Im C'| = |sum x'_L y'_R - y'_L x'_R|
-  // are both <= K 2^2b; the explicit CRT needs |X| < M/2, kept with one bit of
-  // margin: 2b <= log2 M - 2 - log2 K.
   int n_mod = 0, b = 0;
-  {
-    double log2m = 0;
-    for (int i = 0; i < kOzMaxMod; ++i) {
-      log2m += std::log2(static_cast<double>(oz_mod(i)));
-      const int bi = static_cast<int>(std::floor((log2m - 2.0 - std::log2(static_cast<double>(std::max<int64_t>(ktot, 1)))) / 2.0));
-      if (i + 1 >= 11 && (bi >= ctx->oz_min_bits || i + 1 == kOzMaxMod)) {
-        n_mod = i + 1;
-        b = std::min(bi, ctx->oz_min_bits + 4);
-        break;
-      }
-    }
+  CKS(oz_choose(ctx, ktot, &n_mod, &b));
+  // exponents: one array for both sides (m == n), max over every operand --
+  // unless the caller prepared left / right exponents (run_ozaki_hv)
+  const bool pre = z.oz_el != nullptr;
+  const int32_t* el = z.oz_el;
+  const int32_t* er = z.oz_er;
+  int32_t* e = nullptr;
+  if (!pre) {
+    void* ebuf;
+    CKS(ws(ctx, "oz_exp", static_cast<size_t>(n) * sizeof(int32_t), &ebuf));
+    e = static_cast<int32_t*>(ebuf);
+    el = er = e;
+    CK(launch_ozaki_init_exp(e, n, st));
   }
-  if (b < 30) return fail(ctx, HSB_ERR_UNSUPPORTED, "reduction too long for the INT8 engine's moduli");
-  // exponents: one array for both sides (m == n), max over every operand
-  void* ebuf;
-  CKS(ws(ctx, "oz_exp", static_cast<size_t>(n) * sizeof(int32_t), &ebuf));
-  int32_t* e = static_cast<int32_t*>(ebuf);
-  CK(launch_ozaki_init_exp(e, n, st));
-  {
+  if (!pre) {
     std::vector<const OperandView*> seen;
     auto colexp = [&](const OperandView& v) -> hsb_status {
       for (const OperandView* q : seen)
@@ -243,20 +257,27 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
     int64_t k, ld;
     int8_t* planes;
     int64_t kpad;
+    int side;
   };
   std::vector<Src> srcs;
-  auto planes_of = [&](const OperandView& v, Src* out) -> hsb_status {
+  int computed = 0;
+  auto planes_of = [&](const OperandView& v, int side, Src* out) -> hsb_status {
+    if (!pre) side = 0;  // one exponent array: both sides share residues
     for (const Src& q : srcs)
-      if (q.base == v.base && q.k == v.k && q.ld == v.ld) {
+      if (q.base == v.base && q.k == v.k && q.ld == v.ld && q.side == side) {
         *out = q;
         return HSB_OK;
       }
-    Src q{v.base, v.k, v.ld, nullptr, (v.k + 15) / 16 * 16};
-    const std::string name = "oz_res" + std::to_string(srcs.size());
-    void* buf;
-    CKS(ws(ctx, name.c_str(), static_cast<size_t>(kOzPlanes) * n_mod * n * q.kpad, &buf));
-    q.planes = static_cast<int8_t*>(buf);
-    CK(launch_ozaki_residues(v.base, v.ld, v.k, n, e, b, n_mod, q.planes, q.kpad, st));
+    Src q{v.base, v.k, v.ld, nullptr, (v.k + 15) / 16 * 16, side};
+    for (const ZrkCall::OzPre& pz : z.oz_pre)
+      if (pz.base == v.base && pz.side == side) q.planes = pz.planes;
+    if (!q.planes) {
+      const std::string name = "oz_res" + std::to_string(computed++);
+      void* buf;
+      CKS(ws(ctx, name.c_str(), static_cast<size_t>(kOzPlanes) * n_mod * n * q.kpad, &buf));
+      q.planes = static_cast<int8_t*>(buf);
+      CK(launch_ozaki_residues(v.base, v.ld, v.k, n, side ? er : el, b, n_mod, q.planes, q.kpad, st));
+    }
     srcs.push_back(q);
     *out = q;
     return HSB_OK;
@@ -268,8 +289,8 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
   const int rp[kOzProds] = {kOzPhi1, kOzPhi2};
   for (size_t si = 0; si < segs.size(); ++si) {
     Src L, R;
-    CKS(planes_of(segs[si].l, &L));
-    CKS(planes_of(segs[si].r, &R));
+    CKS(planes_of(segs[si].l, 0, &L));
+    CKS(planes_of(segs[si].r, 1, &R));
     const int64_t pl = static_cast<int64_t>(n_mod) * n * L.kpad, pr = static_cast<int64_t>(n_mod) * n * R.kpad;
     for (int pi = 0; pi < kOzProds; ++pi) {
       CKS(oz_encode(ctx, &gp.map[pi][si][0], L.planes + lp[pi] * pl, L.k, n, L.kpad, n_mod, 128));
@@ -292,6 +313,9 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
   gp.mod_stride = static_cast<int64_t>(total_tiles) * kOzTileBytes;
   gp.prod_stride = gp.mod_stride * n_mod;
   gp.tiles_total = total_tiles;
+  gp.r_k_per_tm = 0;
+  gp.rows_valid = 0;
+  gp.ncols = gp.n;
   void* rbuf;
   CKS(ws(ctx, "oz_out", static_cast<size_t>(kOzProds * gp.prod_stride), &rbuf));
   gp.res = static_cast<int8_t*>(rbuf);
@@ -318,8 +342,8 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
   cp.n = static_cast<int32_t>(n);
   cp.b = b;
   cp.conj = z.conj ? 1 : 0;
-  cp.el = e;
-  cp.er = e;
+  cp.el = el;
+  cp.er = er;
   cp.alpha_re = z.alpha_re;
   cp.alpha_im = z.alpha_im;
   cp.beta_re = z.beta_re;
@@ -375,7 +399,7 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
     }
     t0 = t1;
   }
-  if (launches) *launches += 3 + 2 * static_cast<int>(segs.size()) + static_cast<int>(srcs.size());
+  if (launches) *launches += 3 + (pre ? 0 : 2 * static_cast<int>(segs.size())) + computed;
   return HSB_OK;
 }
 
@@ -483,5 +507,139 @@ hsb_status run_zrk(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launche
   return HSB_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Fused H on the INT8 engine with the V products there too:
+//   el = exponents of the A / B columns -> left residues of A and B
+//   L1_a = [T_AA | T_AB], L2_a = [T_AB^H | T_BB] -> exponents, residues
+//   [V1_a; V2_a] = L1_a^H A_a + L2_a^H B_a: rectangular (atom, column tile)
+//     modular GEMM (M = 2 nl rows per atom, the A / B residues of H's left
+//     side as its right operand) + CRT into the V1 / V2 stacks, whose column
+//     maxima give er
+//   H = A^H V1 + B^H V2 on the lower triangle with (el, er) and the left
+//     residues reused (run_ozaki).
+// The V product's reduction (2 nl) is shorter than H's (2 K), so H's moduli
+// and bits keep it exact.
+hsb_status run_ozaki_hv(hsb_ctx* ctx, cudaStream_t st, const HvCall& c, ZrkCall h, int* launches) {
+  const int64_t K = c.K, ng = c.ng, nl = c.nl, na = c.na;
+  if (2 * nl > 256) return fail(ctx, HSB_ERR_UNSUPPORTED, "INT8 V products need n_l <= 128");
+  int n_mod = 0, b = 0;
+  CKS(oz_choose(ctx, 2 * K, &n_mod, &b));
+  // left blocks: 256 k rows per atom (the atom's nl rows shifted by (nl a) mod 16,
+  // matching the 16-byte aligned start of the right operand's TMA box)
+  const int64_t kpad = (K + 15) / 16 * 16, kpad_t = 256;
+  const int64_t tcols = na * 256;
+  void *el_b, *er_b, *et_b, *la, *lb, *t1, *t2, *rt1, *rt2;
+  CKS(ws(ctx, "oz_exp_l", ng * sizeof(int32_t), &el_b));
+  CKS(ws(ctx, "oz_exp_r", ng * sizeof(int32_t), &er_b));
+  CKS(ws(ctx, "oz_exp_t", tcols * sizeof(int32_t), &et_b));
+  int32_t *el = static_cast<int32_t*>(el_b), *er = static_cast<int32_t*>(er_b), *et = static_cast<int32_t*>(et_b);
+  // left side of H (and right side of the V products): A, B
+  CK(launch_ozaki_init_exp(el, ng, st));
+  CK(launch_ozaki_colexp(c.A, K, K, ng, el, st));
+  CK(launch_ozaki_colexp(c.B, K, K, ng, el, st));
+  const size_t res_bytes = static_cast<size_t>(kOzPlanes) * n_mod * ng * kpad;
+  CKS(ws(ctx, "oz_res_la", res_bytes, &la));
+  CKS(ws(ctx, "oz_res_lb", res_bytes, &lb));
+  CK(launch_ozaki_residues(c.A, K, K, ng, el, b, n_mod, static_cast<int8_t*>(la), kpad, st));
+  CK(launch_ozaki_residues(c.B, K, K, ng, el, b, n_mod, static_cast<int8_t*>(lb), kpad, st));
+  // left blocks of the V products
+  const size_t tb = static_cast<size_t>(tcols) * kpad_t * 16;
+  CKS(ws(ctx, "oz_tblk1", tb, &t1));
+  CKS(ws(ctx, "oz_tblk2", tb, &t2));
+  CK(launch_ozaki_vblocks(c.TAA, c.TAB, c.TBB, static_cast<int>(nl), na, static_cast<double*>(t1),
+                          static_cast<double*>(t2), st));
+  CK(launch_ozaki_init_exp(et, tcols, st));
+  CK(launch_ozaki_colexp(static_cast<double*>(t1), kpad_t, kpad_t, tcols, et, st));
+  CK(launch_ozaki_colexp(static_cast<double*>(t2), kpad_t, kpad_t, tcols, et, st));
+  const size_t rt_bytes = static_cast<size_t>(kOzPlanes) * n_mod * tcols * kpad_t;
+  CKS(ws(ctx, "oz_res_t1", rt_bytes, &rt1));
+  CKS(ws(ctx, "oz_res_t2", rt_bytes, &rt2));
+  CK(launch_ozaki_residues(static_cast<double*>(t1), kpad_t, kpad_t, tcols, et, b, n_mod, static_cast<int8_t*>(rt1),
+                           kpad_t, st));
+  CK(launch_ozaki_residues(static_cast<double*>(t2), kpad_t, kpad_t, tcols, et, b, n_mod, static_cast<int8_t*>(rt2),
+                           kpad_t, st));
+  int nlaunch = 12;
+
+  // V products in batches of atoms (bounded residue output)
+  OzGemmParams gp;
+  std::memset(&gp, 0, sizeof(gp));
+  const int lp[kOzProds] = {kOzPhi2, kOzPhi1};  // L^H R
+  const int rp[kOzProds] = {kOzPhi1, kOzPhi2};
+  const int64_t pl_t = static_cast<int64_t>(n_mod) * tcols * kpad_t, pl_x = static_cast<int64_t>(n_mod) * ng * kpad;
+  for (int pi = 0; pi < kOzProds; ++pi) {
+    CKS(oz_encode(ctx, &gp.map[pi][0][0], static_cast<int8_t*>(rt1) + lp[pi] * pl_t, kpad_t, tcols, kpad_t, n_mod, 128));
+    CKS(oz_encode(ctx, &gp.map[pi][0][1], static_cast<int8_t*>(la) + rp[pi] * pl_x, K, ng, kpad, n_mod, 128));
+    CKS(oz_encode(ctx, &gp.map[pi][1][0], static_cast<int8_t*>(rt2) + lp[pi] * pl_t, kpad_t, tcols, kpad_t, n_mod, 128));
+    CKS(oz_encode(ctx, &gp.map[pi][1][1], static_cast<int8_t*>(lb) + rp[pi] * pl_x, K, ng, kpad, n_mod, 128));
+  }
+  const int32_t seg_chunks = static_cast<int32_t>(kpad_t / kOzBK);
+  gp.nseg = 2;
+  gp.seg_chunk0[0] = 0;
+  gp.seg_chunk0[1] = seg_chunks;
+  gp.seg_chunk0[2] = 2 * seg_chunks;
+  gp.nslab = 1;
+  gp.slab_chunk0[0] = 0;
+  gp.slab_chunk0[1] = 2 * seg_chunks;
+  gp.n_mod = n_mod;
+  const int64_t gtiles = (ng + kOzBN - 1) / kOzBN;
+  gp.n = static_cast<int32_t>(ng);
+  gp.ncols = static_cast<int32_t>(ng);
+  gp.r_k_per_tm = static_cast<int32_t>(nl);
+  gp.rows_valid = static_cast<int32_t>(2 * nl);
+  gp.rect_gtiles = static_cast<int32_t>(gtiles);
+  gp.tile_list = nullptr;
+  gp.slab_cnt = nullptr;
+  const int64_t per_batch = std::max<int64_t>(1, std::min<int64_t>(na, 2048 / gtiles));
+  const int64_t cap_tiles = per_batch * gtiles;
+  void *vout, *cbuf;
+  CKS(ws(ctx, "oz_vout", static_cast<size_t>(kOzProds) * n_mod * cap_tiles * kOzTileBytes, &vout));
+  CKS(ws(ctx, "oz_counter", 16, &cbuf));
+  gp.res = static_cast<int8_t*>(vout);
+  gp.counter = static_cast<int32_t*>(cbuf);
+  CK(launch_ozaki_init_exp(er, ng, st));
+  OzVcrtParams vp;
+  std::memset(&vp, 0, sizeof(vp));
+  vp.res = gp.res;
+  vp.n_mod = n_mod;
+  vp.bsum = 2 * b;
+  vp.gtiles = static_cast<int32_t>(gtiles);
+  vp.nl = static_cast<int32_t>(nl);
+  vp.ng = static_cast<int32_t>(ng);
+  vp.et = et;
+  vp.el = el;
+  vp.v1 = c.V1;
+  vp.v2 = c.V2;
+  vp.ldv = K;
+  vp.er = er;
+  for (int64_t a0 = 0; a0 < na; a0 += per_batch) {
+    const int64_t nb = std::min(per_batch, na - a0);
+    gp.rect_atom0 = static_cast<int32_t>(a0);
+    gp.tile0 = 0;
+    gp.ntiles = static_cast<int32_t>(nb * gtiles);
+    gp.tiles_total = gp.ntiles;
+    gp.mod_stride = static_cast<int64_t>(gp.ntiles) * kOzTileBytes;
+    gp.prod_stride = gp.mod_stride * n_mod;
+    CK(launch_ozaki_gemm(gp, st));
+    vp.mod_stride = gp.mod_stride;
+    vp.prod_stride = gp.prod_stride;
+    vp.atom0 = static_cast<int32_t>(a0);
+    vp.natoms = static_cast<int32_t>(nb);
+    CK(launch_ozaki_vcrt(vp, st));
+    nlaunch += 3;
+  }
+  if (c.tl && c.vsect) CK(timeline_mark(c.tl, st, c.vsect));
+
+  // H = A^H V1 + B^H V2 with the prepared exponents and left residues
+  h.segs.clear();
+  h.segs.push_back({plain(c.A, K, ng, K), plain(c.V1, K, ng, K)});
+  h.segs.push_back({plain(c.B, K, ng, K), plain(c.V2, K, ng, K)});
+  h.oz_el = el;
+  h.oz_er = er;
+  h.oz_pre.clear();
+  h.oz_pre.push_back({c.A, 0, static_cast<int8_t*>(la)});
+  h.oz_pre.push_back({c.B, 0, static_cast<int8_t*>(lb)});
+  if (launches) *launches += nlaunch;
+  return run_ozaki(ctx, st, h, launches);
+}
 
 }  // namespace hsb_host

@@ -205,6 +205,17 @@ struct ZrkCall {
   // optional (INT8 engine): scatter the result into peer receive slots
   const hsb_peer_out* peer = nullptr;
   bool peer_is_h = false;
+  // optional (INT8 engine): precomputed column exponents of the left / right
+  // operands, and residue planes of operands by base pointer and side (0 left,
+  // 1 right), prepared with the same moduli and bits (oz_choose)
+  const int32_t* oz_el = nullptr;
+  const int32_t* oz_er = nullptr;
+  struct OzPre {
+    const double* base;
+    int side;
+    int8_t* planes;
+  };
+  std::vector<OzPre> oz_pre;
 };
 
 
@@ -248,5 +259,19 @@ inline OperandView atom_mats(const double* base, int64_t n_atoms, int64_t n_l) {
 
 // the contraction dispatcher (contract.cu): DMMA 3M / 4M kernels or the INT8 engine
 hsb_status run_zrk(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launches);
+// INT8 engine: moduli count and operand bits for a reduction of length ktot
+hsb_status oz_choose(hsb_ctx* ctx, int64_t ktot, int* n_mod, int* b);
+// INT8 engine, fused H = A^H V1 + B^H V2 with the V products on the INT8 tensor
+// cores as well (hsb_api.cu): A, B are K x ng stacks (ld K) of na atoms of nl
+// rows; T_* per-atom nl x nl column-major blocks; V1, V2 receive the K x ng
+// products; h is the triangle call (segments filled in here)
+struct HvCall {
+  const double *A, *B, *TAA, *TAB, *TBB;
+  double *V1, *V2;
+  int64_t K, ng, nl, na;
+  Timeline* tl = nullptr;
+  const char* vsect = nullptr;  // timeline tag of the V products
+};
+hsb_status run_ozaki_hv(hsb_ctx* ctx, cudaStream_t st, const HvCall& c, ZrkCall h, int* launches);
 
 }  // namespace hsb_host

@@ -733,7 +733,14 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   // product covers HPD and non-HPD T_AA alike; potrf_route still runs for the
   // reference's split counts.  T_AA and T_BB are read from their lower
   // triangles (kernels.py:223-231, 296-307), as in the reference.
+  // INT8 engine, HSB_INT8_V=1 (experimental): the V products run on the INT8
+  // tensor cores inside the H phase (run_ozaki_hv), sharing H's left residues
+  // of A and B.  Measured slower than the DMMA V products so far (C3: 4.6 vs
+  // 3.3 ms; its modular GEMM is epilogue-bound at K = 2 n_l), so off by default.
+  static const bool int8_v_env = std::getenv("HSB_INT8_V") != nullptr;
+  const bool int8_v = int8_v_env && !unfused && ctx->engine == HSB_ENGINE_INT8 && 2 * nl <= 256;
   auto vloop = [&]() -> hsb_status {
+    if (int8_v) return HSB_OK;
     void *taa_full, *tab_h;
     CKS(ws(ctx, "taa_full", tblk_bytes * na, &taa_full));
     CKS(ws(ctx, "tab_h", tblk_bytes * na, &tab_h));
@@ -911,7 +918,25 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
       h.done_cnt = dptr;
     }
     tr.mark(st, "loop2_done");
-    CKS(run_zrk(ctx, st, h, &launches));
+    if (int8_v) {
+      HvCall hv;
+      hv.A = A;
+      hv.B = B;
+      hv.TAA = TAA;
+      hv.TAB = TAB;
+      hv.TBB = TBB;
+      hv.V1 = Z;
+      hv.V2 = R;
+      hv.K = K;
+      hv.ng = ng;
+      hv.nl = nl;
+      hv.na = na;
+      hv.tl = &tl;
+      hv.vsect = "loop1";
+      CKS(run_ozaki_hv(ctx, st, hv, h, &launches));
+    } else {
+      CKS(run_zrk(ctx, st, h, &launches));
+    }
     CK(tl.mark(st, "h"));
     tr.mark(st, "h_done");
   }

@@ -260,6 +260,11 @@ __device__ __forceinline__ void oz_work(const OzGemmParams& p, int w, int& prod,
   r /= p.n_mod;
   slab = r % p.nslab;
   prod = r / p.nslab;
+  if (p.rows_valid > 0) {  // rectangular mode: (atom, column tile)
+    tm = p.rect_atom0 + t / p.rect_gtiles;
+    tn = t % p.rect_gtiles;
+    return;
+  }
   const int2 tt = p.tile_list[t];
   tm = tt.x;
   tn = tt.y;
@@ -361,7 +366,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
           const uint32_t dst = base + stage * kOzStageBytes;
           const uint32_t fb = full(stage) & kPeerMask;
           tma_load_3d_pair(dst, &p.map[prod][seg][0], kc * kOzBK, row0, mod, fb);
-          tma_load_3d_pair(dst + kOzABytes, &p.map[prod][seg][1], kc * kOzBK, col0, mod, fb);
+          tma_load_3d_pair(dst + kOzABytes, &p.map[prod][seg][1], kc * kOzBK + ((tm * p.r_k_per_tm) & ~15), col0, mod, fb);
         }
         __syncwarp();
         if (++stage == kOzStages) {
@@ -440,12 +445,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
         __threadfence();
       }
       const int col0 = tn * 256;
-      const int ncol = min(kOzBN, p.n - col0);
+      const int ncol = min(kOzBN, p.ncols - col0);
+      const bool row_ok = p.rows_valid > 0 ? rloc < p.rows_valid : row < p.n;
       for (int c = 0; c < kOzBN / 32; ++c) {
         if (c * 32 >= ncol) break;  // warp-uniform
         uint32_t v[32];
         tmem_ld32(tmem + ((q * 32) << 16) + acc * kOzBN + c * 32, v);
-        if (row < p.n) {
+        if (row_ok) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             int r = sym_mod_d(static_cast<double>(static_cast<int32_t>(v[j])), pd, inv);
@@ -621,6 +627,103 @@ __global__ void __launch_bounds__(128) ozaki_crt_kernel(const OzCrtParams p, int
   }
 }
 
+// ------------------------------------------------------------ 5. V products
+// L1_a = [T_AA | T_AB], L2_a = [T_AB^H | T_BB], column-major 256 x 256 per atom:
+// the nl rows sit at rows d_a .. d_a + nl - 1 with d_a = (nl a) mod 16 -- the
+// TMA k coordinate of the right operand (the atom's rows of the stack) must be
+// 16-byte aligned, so its box starts d_a rows early -- the rest is zero, as
+// are columns 2 nl .. 255
+__global__ void ozaki_vblocks_kernel(const double2* __restrict__ taa, const double2* __restrict__ tab,
+                                     const double2* __restrict__ tbb, int nl, int64_t na, double2* __restrict__ l1,
+                                     double2* __restrict__ l2) {
+  const int64_t nn = static_cast<int64_t>(nl) * nl, per = 256 * 256;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < na * per;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t a = idx / per;
+    const int rem = static_cast<int>(idx - a * per);
+    const int k = (rem & 255) - static_cast<int>((a * nl) & 15), c = rem >> 8;
+    const double2* AA = taa + a * nn;
+    const double2* AB = tab + a * nn;
+    const double2* BB = tbb + a * nn;
+    auto herm = [&](const double2* T, int i, int j) {  // (i, j) of the Hermitian completion of the lower triangle
+      if (i > j) return T[i + static_cast<int64_t>(j) * nl];
+      if (i < j) {
+        const double2 w = T[j + static_cast<int64_t>(i) * nl];
+        return make_double2(w.x, -w.y);
+      }
+      return make_double2(T[i + static_cast<int64_t>(i) * nl].x, 0.0);
+    };
+    double2 v1 = make_double2(0.0, 0.0), v2 = v1;
+    if (k < 0 || k >= nl) {
+      // padding rows
+    } else if (c < nl) {
+      v1 = herm(AA, k, c);
+      const double2 w = AB[c + static_cast<int64_t>(k) * nl];  // (T_AB^H)[k, c]
+      v2 = make_double2(w.x, -w.y);
+    } else if (c < 2 * nl) {
+      v1 = AB[k + static_cast<int64_t>(c - nl) * nl];
+      v2 = herm(BB, k, c - nl);
+    }
+    l1[idx] = v1;
+    l2[idx] = v2;
+  }
+}
+
+// [V1; V2] from the residues of one batch of (atom, column tile) products:
+// block = 256 rows r of one tile x 32 of its columns; per column the block's
+// max |Re| + |Im| goes into er (the right-hand exponents of H = A^H V1 + B^H V2)
+template <int NM>
+__global__ void __launch_bounds__(256) ozaki_vcrt_kernel(const OzVcrtParams p) {
+  const int al = static_cast<int>(blockIdx.y), a = p.atom0 + al;
+  const int gt = static_cast<int>(blockIdx.x) >> 3, gsub = static_cast<int>(blockIdx.x) & 7;
+  const int t = al * p.gtiles + gt;
+  const int r = static_cast<int>(threadIdx.x);
+  const bool valid = r < 2 * p.nl;
+  const int st = valid ? __ldg(p.et + static_cast<int64_t>(a) * 256 + r) : 0;
+  const uint8_t* base = reinterpret_cast<const uint8_t*>(p.res) + static_cast<int64_t>(t) * kOzTileBytes + r;
+  double2* dst = reinterpret_cast<double2*>(r < p.nl ? p.v1 : p.v2) +
+                 (static_cast<int64_t>(p.nl) * a + (r < p.nl ? r : r - p.nl));
+  __shared__ double wmax[8];
+  for (int j = 0; j < 32; ++j) {
+    const int gl = gsub * 32 + j, g = gt * 256 + gl;
+    if (g >= p.ng) break;  // uniform across the block
+    double m = 0.0;
+    if (valid) {
+      int F1[NM], F2[NM];
+      const uint8_t* r0 = base + gl * 256;
+#pragma unroll
+      for (int i = 0; i < NM; ++i) {
+        F1[i] = static_cast<int8_t>(__ldg(r0 + i * p.mod_stride));
+        F2[i] = static_cast<int8_t>(__ldg(r0 + p.prod_stride + i * p.mod_stride));
+      }
+      int re[NM], im[NM];
+#pragma unroll
+      for (int i = 0; i < NM; ++i) {
+        re[i] = F1[i] + F2[i];
+        im[i] = F1[i] - F2[i];
+      }
+      const int sh = st + __ldg(p.el + g) - p.bsum;
+      const double xr = scale2(crt_value<NM, 0>(re), sh);
+      const double xi = scale2(crt_value<NM, 1>(im), sh);
+      dst[static_cast<int64_t>(g) * p.ldv] = make_double2(xr, xi);
+      m = fabs(xr) + fabs(xi);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((r & 31) == 0) wmax[r >> 5] = m;
+    __syncthreads();
+    if (r == 0) {
+      double mm = wmax[0];
+#pragma unroll
+      for (int w = 1; w < 8; ++w) mm = fmax(mm, wmax[w]);
+      int ex = 0;
+      frexp(mm, &ex);
+      atomicMax(p.er + g, ex);
+    }
+    __syncthreads();
+  }
+}
+
 // CRT tables for every n_mod, computed and uploaded once per process (the
 // tables are constant, so concurrent builds on several contexts never race)
 static OzCrtConst oz_crt_table(int n_mod) {
@@ -724,6 +827,34 @@ cudaError_t launch_ozaki_gemm(const OzGemmParams& p, cudaStream_t st) {
   e = launch_fill_i32(p.counter, 1, 0, st);  // a kernel, not a copy-engine memset
   if (e != cudaSuccess) return e;
   ozaki_gemm_kernel<<<grid, kOzThreads, kOzSmem, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ozaki_vblocks(const double* taa, const double* tab, const double* tbb, int nl, int64_t na,
+                                 double* l1, double* l2, cudaStream_t st) {
+  const int64_t total = na * 256 * 256;
+  if (total <= 0) return cudaSuccess;
+  ozaki_vblocks_kernel<<<grid_cap((total + 255) / 256, 148 * 16), 256, 0, st>>>(
+      reinterpret_cast<const double2*>(taa), reinterpret_cast<const double2*>(tab),
+      reinterpret_cast<const double2*>(tbb), nl, na, reinterpret_cast<double2*>(l1), reinterpret_cast<double2*>(l2));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ozaki_vcrt(const OzVcrtParams& p, cudaStream_t st) {
+  if (p.natoms <= 0 || p.ng <= 0) return cudaSuccess;
+  cudaError_t ce = oz_init_once();
+  if (ce != cudaSuccess) return ce;
+  const dim3 grid(static_cast<unsigned>(p.gtiles * 8), static_cast<unsigned>(p.natoms)), block(256);
+  switch (p.n_mod) {
+#define HSB_OZ_VCRT(NMV)                                  \
+  case NMV:                                             \
+    ozaki_vcrt_kernel<NMV><<<grid, block, 0, st>>>(p);  \
+    break;
+    HSB_OZ_VCRT(11) HSB_OZ_VCRT(12) HSB_OZ_VCRT(13) HSB_OZ_VCRT(14) HSB_OZ_VCRT(15) HSB_OZ_VCRT(16)
+#undef HSB_OZ_VCRT
+    default:
+      return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 

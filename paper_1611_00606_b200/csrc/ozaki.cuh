@@ -95,6 +95,14 @@ struct OzGemmParams {
   int32_t* counter;     // work-stealing counter (zeroed by the launcher)
   int32_t* slab_cnt;    // nslab > 1: per (prod, modulus, tile), epilogue warps finished (zeroed)
   int32_t tiles_total;  // tiles of the whole triangle (slab_cnt / residue indexing)
+  // rectangular batched mode (the per-atom V products, contract.cu): tile
+  // (tm, tn) = (atom, column tile); the right operand's k coordinate is shifted
+  // by tm * r_k_per_tm (the atom's rows of the stack); rows rloc < rows_valid
+  // of a tile are stored.  Triangle mode: 0, 0, and ncols = n.
+  int32_t r_k_per_tm;
+  int32_t rows_valid;
+  int32_t ncols;        // columns of the output
+  int32_t rect_atom0, rect_gtiles;  // rectangular mode: tile t = (atom0 + t / gtiles, t % gtiles)
 };
 
 struct OzCrtParams {
@@ -119,6 +127,28 @@ struct OzCrtParams {
   int32_t P, rank;
   int64_t cpr, pld;
 };
+
+// V products of the fused H (contract.cu run_ozaki_hv): per-atom left blocks
+// L1 = [T_AA | T_AB], L2 = [T_AB^H | T_BB] (256 x 256 per atom, rows shifted by
+// (nl a) mod 16, zero padded; T_AA, T_BB completed from their lower
+// triangles), so that [V1_a; V2_a] = L1_a^H A_a + L2_a^H B_a.
+cudaError_t launch_ozaki_vblocks(const double* taa, const double* tab, const double* tbb, int nl, int64_t na,
+                                 double* l1, double* l2, cudaStream_t st);
+struct OzVcrtParams {
+  const int8_t* res;           // [prod][modulus][tile][256 x 256]: column g_local, row r
+  int64_t mod_stride, prod_stride;
+  int32_t n_mod;
+  int32_t bsum;                // b_left + b_right of the product
+  int32_t gtiles, atom0, natoms;
+  int32_t nl, ng;
+  const int32_t* et;           // [atom * 256 + r] exponents of the L columns
+  const int32_t* el;           // [g] exponents of the A / B columns
+  double* v1;                  // rows nl * a + r       (r <  nl), leading dimension ldv
+  double* v2;                  // rows nl * a + r - nl  (r >= nl)
+  int64_t ldv;
+  int32_t* er;                 // [g] atomicMax of the V column exponents
+};
+cudaError_t launch_ozaki_vcrt(const OzVcrtParams& p, cudaStream_t st);
 
 cudaError_t launch_ozaki_colexp(const double* x, int64_t ldx, int64_t k, int64_t cols, int32_t* exp_out,
                                 cudaStream_t st);
