@@ -29,6 +29,17 @@ __device__ __forceinline__ int sym_mod_d(double v, double p, double inv_p) {
   const double r = fma(-p, q, v) + 6755399441055744.0;
   return static_cast<int>(__double2loint(r));
 }
+// symmetric residue of an int32 v modulo an odd p < 256 in FP32:
+// t = (v >> 16) (2^16 mod p) + (v & 0xffff) = v (mod p), |t| < 2^22; the
+// quotient rn(t fl(1/p)) through the 1.5 * 2^23 magic constant is exact (its
+// error, below 1/(4p), is under the 1/(2p) distance of t/p from a half-integer)
+__device__ __forceinline__ int sym_mod_i32(int v, float pf, float invf, int c16) {
+  constexpr float M = 12582912.0f;
+  const int t = (v >> 16) * c16 + (v & 0xffff);
+  const float tf = __int_as_float(0x4B400000 + t) - M;
+  const float q = __fadd_rn(__fmaf_rn(tf, invf, M), -M);
+  return __float_as_int(__fadd_rn(__fmaf_rn(-pf, q, tf), M)) - 0x4B400000;
+}
 __device__ __forceinline__ int sym_adj(int r, int p) {
   const int lo = sym_lo(p);
   if (r < lo) r += p;
@@ -430,7 +441,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
       int prod, slab, mod, t, tm, tn;
       oz_work(p, w, prod, slab, mod, t, tm, tn);
       const int ip = oz_mod_rt[mod];
-      const double pd = ip, inv = 1.0 / pd;
+      const float pf = static_cast<float>(ip), invf = 1.0f / pf;
+      const int c16 = ((65536 % ip) > ip / 2) ? (65536 % ip) - ip : (65536 % ip);
       mbar_wait(tfull(acc), acc_phase);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int rloc = static_cast<int>(rank) * kOzHalf + q * 32 + lane;  // row within the tile
@@ -454,7 +466,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
         if (row_ok) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            int r = sym_mod_d(static_cast<double>(static_cast<int32_t>(v[j])), pd, inv);
+            int r = sym_mod_i32(static_cast<int32_t>(v[j]), pf, invf, c16);
             int8_t* o = out + (c * 32 + j) * 256;
             if (slab > 0) r = sym_adj(r + __ldcg(o), ip);  // the residue of the sum of the slabs
             *o = static_cast<int8_t>(r);
