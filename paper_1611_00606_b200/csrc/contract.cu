@@ -292,9 +292,9 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
     CKS(planes_of(segs[si].l, 0, &L));
     CKS(planes_of(segs[si].r, 1, &R));
     const int64_t pl = static_cast<int64_t>(n_mod) * n * L.kpad, pr = static_cast<int64_t>(n_mod) * n * R.kpad;
-    for (int pi = 0; pi < kOzProds; ++pi) {
-      CKS(oz_encode(ctx, &gp.map[pi][si][0], L.planes + lp[pi] * pl, L.k, n, L.kpad, n_mod, 128));
-      CKS(oz_encode(ctx, &gp.map[pi][si][1], R.planes + rp[pi] * pr, R.k, n, R.kpad, n_mod, 128));
+    for (int pi = 0; pi < kOzProds; ++pi) {  // MMA A operand: the right factor (output columns)
+      CKS(oz_encode(ctx, &gp.map[pi][si][0], R.planes + rp[pi] * pr, R.k, n, R.kpad, n_mod, 128));
+      CKS(oz_encode(ctx, &gp.map[pi][si][1], L.planes + lp[pi] * pl, L.k, n, L.kpad, n_mod, 128));
     }
     gp.seg_chunk0[si + 1] = gp.seg_chunk0[si] + static_cast<int32_t>((segs[si].l.k + kOzBK - 1) / kOzBK);
   }
@@ -313,9 +313,8 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
   gp.mod_stride = static_cast<int64_t>(total_tiles) * kOzTileBytes;
   gp.prod_stride = gp.mod_stride * n_mod;
   gp.tiles_total = total_tiles;
-  gp.r_k_per_tm = 0;
-  gp.rows_valid = 0;
-  gp.ncols = gp.n;
+  gp.a_k_per_tm = 0;
+  gp.nrows = gp.n;
   void* rbuf;
   CKS(ws(ctx, "oz_out", static_cast<size_t>(kOzProds * gp.prod_stride), &rbuf));
   gp.res = static_cast<int8_t*>(rbuf);
@@ -567,10 +566,11 @@ hsb_status run_ozaki_hv(hsb_ctx* ctx, cudaStream_t st, const HvCall& c, ZrkCall 
   const int rp[kOzProds] = {kOzPhi1, kOzPhi2};
   const int64_t pl_t = static_cast<int64_t>(n_mod) * tcols * kpad_t, pl_x = static_cast<int64_t>(n_mod) * ng * kpad;
   for (int pi = 0; pi < kOzProds; ++pi) {
-    CKS(oz_encode(ctx, &gp.map[pi][0][0], static_cast<int8_t*>(rt1) + lp[pi] * pl_t, kpad_t, tcols, kpad_t, n_mod, 128));
-    CKS(oz_encode(ctx, &gp.map[pi][0][1], static_cast<int8_t*>(la) + rp[pi] * pl_x, K, ng, kpad, n_mod, 128));
-    CKS(oz_encode(ctx, &gp.map[pi][1][0], static_cast<int8_t*>(rt2) + lp[pi] * pl_t, kpad_t, tcols, kpad_t, n_mod, 128));
-    CKS(oz_encode(ctx, &gp.map[pi][1][1], static_cast<int8_t*>(lb) + rp[pi] * pl_x, K, ng, kpad, n_mod, 128));
+    // MMA A operand: the stacks' columns g (k shifted to the atom's rows); B: the left blocks
+    CKS(oz_encode(ctx, &gp.map[pi][0][0], static_cast<int8_t*>(la) + rp[pi] * pl_x, K, ng, kpad, n_mod, 128));
+    CKS(oz_encode(ctx, &gp.map[pi][0][1], static_cast<int8_t*>(rt1) + lp[pi] * pl_t, kpad_t, tcols, kpad_t, n_mod, 128));
+    CKS(oz_encode(ctx, &gp.map[pi][1][0], static_cast<int8_t*>(lb) + rp[pi] * pl_x, K, ng, kpad, n_mod, 128));
+    CKS(oz_encode(ctx, &gp.map[pi][1][1], static_cast<int8_t*>(rt2) + lp[pi] * pl_t, kpad_t, tcols, kpad_t, n_mod, 128));
   }
   const int32_t seg_chunks = static_cast<int32_t>(kpad_t / kOzBK);
   gp.nseg = 2;
@@ -583,9 +583,8 @@ hsb_status run_ozaki_hv(hsb_ctx* ctx, cudaStream_t st, const HvCall& c, ZrkCall 
   gp.n_mod = n_mod;
   const int64_t gtiles = (ng + kOzBN - 1) / kOzBN;
   gp.n = static_cast<int32_t>(ng);
-  gp.ncols = static_cast<int32_t>(ng);
-  gp.r_k_per_tm = static_cast<int32_t>(nl);
-  gp.rows_valid = static_cast<int32_t>(2 * nl);
+  gp.nrows = 1 << 30;  // every row r of the left blocks is stored (the CRT reads r < 2 nl)
+  gp.a_k_per_tm = static_cast<int32_t>(nl);
   gp.rect_gtiles = static_cast<int32_t>(gtiles);
   gp.tile_list = nullptr;
   gp.slab_cnt = nullptr;

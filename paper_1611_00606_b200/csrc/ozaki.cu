@@ -271,7 +271,7 @@ __device__ __forceinline__ void oz_work(const OzGemmParams& p, int w, int& prod,
   r /= p.n_mod;
   slab = r % p.nslab;
   prod = r / p.nslab;
-  if (p.rows_valid > 0) {  // rectangular mode: (atom, column tile)
+  if (p.rect_gtiles > 0) {  // rectangular mode: (atom, column tile)
     tm = p.rect_atom0 + t / p.rect_gtiles;
     tn = t % p.rect_gtiles;
     return;
@@ -365,8 +365,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
       if (w >= nwork) break;
       int prod, slab, mod, t, tm, tn;
       oz_work(p, w, prod, slab, mod, t, tm, tn);
-      const int row0 = tm * 256 + static_cast<int>(rank) * kOzHalf;
-      const int col0 = tn * 256 + static_cast<int>(rank) * kOzHalf;
+      // MMA A operand (TMEM lanes, the epilogue threads) = tile column tn,
+      // B operand (TMEM columns) = tile row tm: each thread then holds 32
+      // consecutive rows of one output column, stored as 32 contiguous bytes
+      const int a0 = tn * 256 + static_cast<int>(rank) * kOzHalf;
+      const int b0 = tm * 256 + static_cast<int>(rank) * kOzHalf;
+      const int a_kofs = (tm * p.a_k_per_tm) & ~15;
       int seg = 0;
       for (int c = p.slab_chunk0[slab]; c < p.slab_chunk0[slab + 1]; ++c) {
         while (c >= p.seg_chunk0[seg + 1]) ++seg;
@@ -376,8 +380,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
           if (leader) mbar_expect_tx(full(stage), 2 * kOzStageBytes);
           const uint32_t dst = base + stage * kOzStageBytes;
           const uint32_t fb = full(stage) & kPeerMask;
-          tma_load_3d_pair(dst, &p.map[prod][seg][0], kc * kOzBK, row0, mod, fb);
-          tma_load_3d_pair(dst + kOzABytes, &p.map[prod][seg][1], kc * kOzBK + ((tm * p.r_k_per_tm) & ~15), col0, mod, fb);
+          tma_load_3d_pair(dst, &p.map[prod][seg][0], kc * kOzBK + a_kofs, a0, mod, fb);
+          tma_load_3d_pair(dst + kOzABytes, &p.map[prod][seg][1], kc * kOzBK, b0, mod, fb);
         }
         __syncwarp();
         if (++stage == kOzStages) {
@@ -445,9 +449,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
       const int c16 = ((65536 % ip) > ip / 2) ? (65536 % ip) - ip : (65536 % ip);
       mbar_wait(tfull(acc), acc_phase);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int rloc = static_cast<int>(rank) * kOzHalf + q * 32 + lane;  // row within the tile
-      const int row = tm * 256 + rloc;
-      int8_t* out = p.res + prod * p.prod_stride + mod * p.mod_stride + static_cast<int64_t>(t) * kOzTileBytes + rloc;
+      // thread = output column tn * 256 + cloc (TMEM lane); registers = rows
+      const int cloc = static_cast<int>(rank) * kOzHalf + q * 32 + lane;
+      int8_t* out = p.res + prod * p.prod_stride + mod * p.mod_stride + static_cast<int64_t>(t) * kOzTileBytes +
+                    cloc * 256;
       int32_t* cnt = p.nslab > 1 ? p.slab_cnt + (static_cast<int64_t>(prod) * p.n_mod + mod) * p.tiles_total + t
                                  : nullptr;
       if (slab > 0) {  // slab s-1 of this tile: all 8 epilogue warps (2 CTAs x 4) finished
@@ -456,21 +461,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
         __syncwarp();
         __threadfence();
       }
-      const int col0 = tn * 256;
-      const int ncol = min(kOzBN, p.ncols - col0);
-      const bool row_ok = p.rows_valid > 0 ? rloc < p.rows_valid : row < p.n;
+      const int nrow = min(kOzBN, p.nrows - tm * 256);
+      const bool col_ok = tn * 256 + cloc < p.n;
       for (int c = 0; c < kOzBN / 32; ++c) {
-        if (c * 32 >= ncol) break;  // warp-uniform
+        if (c * 32 >= nrow) break;  // warp-uniform
         uint32_t v[32];
         tmem_ld32(tmem + ((q * 32) << 16) + acc * kOzBN + c * 32, v);
-        if (row_ok) {
+        if (col_ok) {
+          uint32_t w[8];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            int r = sym_mod_i32(static_cast<int32_t>(v[j]), pf, invf, c16);
-            int8_t* o = out + (c * 32 + j) * 256;
-            if (slab > 0) r = sym_adj(r + __ldcg(o), ip);  // the residue of the sum of the slabs
-            *o = static_cast<int8_t>(r);
+          for (int j = 0; j < 8; ++j) {
+            int r4[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) r4[i] = sym_mod_i32(static_cast<int32_t>(v[4 * j + i]), pf, invf, c16);
+            w[j] = __byte_perm(__byte_perm(r4[0], r4[1], 0x40), __byte_perm(r4[2], r4[3], 0x40), 0x5410);
           }
+          uint4* o = reinterpret_cast<uint4*>(out + c * 32);
+          if (slab > 0) {  // the residue of the sum of the slabs
+            const uint4 o0 = __ldcg(o), o1 = __ldcg(o + 1);
+            const uint32_t ow[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              uint32_t x = 0;
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int a = static_cast<int8_t>(w[j] >> (8 * i)), b = static_cast<int8_t>(ow[j] >> (8 * i));
+                x |= (static_cast<uint32_t>(sym_adj(a + b, ip)) & 0xffu) << (8 * i);
+              }
+              w[j] = x;
+            }
+          }
+          o[0] = make_uint4(w[0], w[1], w[2], w[3]);
+          o[1] = make_uint4(w[4], w[5], w[6], w[7]);
         }
       }
       if (cnt) {

@@ -95,14 +95,16 @@ struct OzGemmParams {
   int32_t* counter;     // work-stealing counter (zeroed by the launcher)
   int32_t* slab_cnt;    // nslab > 1: per (prod, modulus, tile), epilogue warps finished (zeroed)
   int32_t tiles_total;  // tiles of the whole triangle (slab_cnt / residue indexing)
-  // rectangular batched mode (the per-atom V products, contract.cu): tile
-  // (tm, tn) = (atom, column tile); the right operand's k coordinate is shifted
-  // by tm * r_k_per_tm (the atom's rows of the stack); rows rloc < rows_valid
-  // of a tile are stored.  Triangle mode: 0, 0, and ncols = n.
-  int32_t r_k_per_tm;
-  int32_t rows_valid;
-  int32_t ncols;        // columns of the output
-  int32_t rect_atom0, rect_gtiles;  // rectangular mode: tile t = (atom0 + t / gtiles, t % gtiles)
+  // The MMA's A operand (map[..][..][0], TMEM lanes) covers tile column tn,
+  // its B operand (map[..][..][1]) tile row tm; residue tiles are stored with
+  // the rows of one column contiguous.  Output columns < n and rows < nrows are
+  // valid.  Rectangular batched mode (the per-atom V products, contract.cu,
+  // rect_gtiles > 0): tile t = (tm, tn) = (atom0 + t / gtiles, t % gtiles); the
+  // A operand's k coordinate is shifted by (tm * a_k_per_tm) & ~15 (the atom's
+  // rows of the stack, 16-byte aligned for TMA).  Triangle mode: 0, nrows = n.
+  int32_t a_k_per_tm;
+  int32_t nrows;
+  int32_t rect_atom0, rect_gtiles;
 };
 
 struct OzCrtParams {
