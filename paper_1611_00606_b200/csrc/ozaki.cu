@@ -170,7 +170,12 @@ constexpr int kOzHalf = 128;                      // rows of A and of B per CTA
 constexpr int kOzABytes = kOzHalf * kOzBK;        // 16 KB
 constexpr int kOzStageBytes = 2 * kOzABytes;      // 32 KB
 constexpr int kOzSmem = kOzStages * kOzStageBytes + 1024 + 256;
-constexpr int kOzThreads = 192;  // warp 0 TMA, warp 1 MMA (leader) + TMEM owner, warps 2-5 epilogue
+// warp 0 TMA, warp 1 MMA (leader) + TMEM owner, warps 2-9 epilogue: two warps per
+// TMEM lane quarter, each reducing half of the accumulator's columns, so short
+// reductions (few k chunks per tile: small configs, atom shards) are not
+// epilogue-bound
+constexpr int kOzEpiWarps = 8;
+constexpr int kOzThreads = (2 + kOzEpiWarps) * 32;
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;       // shared::cluster address of the leader's copy
 
 __device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
@@ -321,11 +326,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(tfull(s), 1);
-      mbar_init(tempty(s), 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+      mbar_init(tempty(s), 2 * kOzEpiWarps);  // epilogue warps x 2 CTAs (leader's copy is used)
     }
     for (int j = 0; j < kOzQ; ++j) {
       mbar_init(wfull(j), 1);
-      mbar_init(wempty(j), 10);  // leader: MMA + 4 epilogue warps; peer: producer + 4 epilogue warps
+      mbar_init(wempty(j), 2 + 2 * kOzEpiWarps);  // leader: MMA + epilogue warps; peer: producer + epilogue warps
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -436,7 +441,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
   } else {
     // ------------------------------------------------------------ epilogue (both CTAs)
     // warp w owns TMEM lanes 32*(w%4) .. +31 = rows of this CTA's half; residue mod p, int8
-    const int q = warp & 3;
+    const int q = warp & 3;                        // TMEM lane quarter (warp id mod 4)
+    const int half = (warp - 2) / 4;               // columns [128 half, 128 half + 128)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int seq = 0;; ++seq) {
@@ -455,15 +461,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
                     cloc * 256;
       int32_t* cnt = p.nslab > 1 ? p.slab_cnt + (static_cast<int64_t>(prod) * p.n_mod + mod) * p.tiles_total + t
                                  : nullptr;
-      if (slab > 0) {  // slab s-1 of this tile: all 8 epilogue warps (2 CTAs x 4) finished
+      if (slab > 0) {  // slab s-1 of this tile: all epilogue warps of both CTAs finished
         if (lane == 0)
-          while (*reinterpret_cast<volatile int32_t*>(cnt) < 8 * slab) __nanosleep(256);
+          while (*reinterpret_cast<volatile int32_t*>(cnt) < 2 * kOzEpiWarps * slab) __nanosleep(256);
         __syncwarp();
         __threadfence();
       }
       const int nrow = min(kOzBN, p.nrows - tm * 256);
       const bool col_ok = tn * 256 + cloc < p.n;
-      for (int c = 0; c < kOzBN / 32; ++c) {
+      for (int c = half * (kOzBN / 64); c < (half + 1) * (kOzBN / 64); ++c) {
         if (c * 32 >= nrow) break;  // warp-uniform
         uint32_t v[32];
         tmem_ld32(tmem + ((q * 32) << 16) + acc * kOzBN + c * 32, v);
