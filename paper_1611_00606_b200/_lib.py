@@ -179,3 +179,13 @@ def release_all() -> None:
         for ctx in _ctxs.values():
             lib.hsb_ctx_destroy(ctx)
         _ctxs.clear()
+
+
+def trim_all(device: int | None = None) -> None:
+    """Release the cached device workspace of every context (of ``device``);
+    the next call on a context re-allocates what it needs."""
+    lib = load()
+    with _lock:
+        for (dev, _slot), ctx in _ctxs.items():
+            if device is None or dev == device:
+                check(lib.hsb_ctx_trim(ctx), ctx)
