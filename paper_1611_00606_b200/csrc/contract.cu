@@ -241,9 +241,9 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
     std::vector<const OperandView*> seen;
     auto colexp = [&](const OperandView& v) -> hsb_status {
       for (const OperandView* q : seen)
-        if (q->base == v.base && q->k == v.k && q->ld == v.ld) return HSB_OK;
+        if (q->base == v.base && q->k == v.k && q->ld == v.ld && q->rscale == v.rscale) return HSB_OK;
       seen.push_back(&v);
-      CK(launch_ozaki_colexp(v.base, v.ld, v.k, v.cols, e, st));
+      CK(launch_ozaki_colexp(v.base, v.ld, v.k, v.cols, e, st, v.rscale));
       return HSB_OK;
     };
     for (const Seg& s : segs) {
@@ -258,25 +258,26 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
     int8_t* planes;
     int64_t kpad;
     int side;
+    const double* rscale;
   };
   std::vector<Src> srcs;
   int computed = 0;
   auto planes_of = [&](const OperandView& v, int side, Src* out) -> hsb_status {
     if (!pre) side = 0;  // one exponent array: both sides share residues
     for (const Src& q : srcs)
-      if (q.base == v.base && q.k == v.k && q.ld == v.ld && q.side == side) {
+      if (q.base == v.base && q.k == v.k && q.ld == v.ld && q.side == side && q.rscale == v.rscale) {
         *out = q;
         return HSB_OK;
       }
-    Src q{v.base, v.k, v.ld, nullptr, (v.k + 15) / 16 * 16, side};
+    Src q{v.base, v.k, v.ld, nullptr, (v.k + 15) / 16 * 16, side, v.rscale};
     for (const ZrkCall::OzPre& pz : z.oz_pre)
-      if (pz.base == v.base && pz.side == side) q.planes = pz.planes;
+      if (pz.base == v.base && pz.side == side && !v.rscale) q.planes = pz.planes;
     if (!q.planes) {
       const std::string name = "oz_res" + std::to_string(computed++);
       void* buf;
       CKS(ws(ctx, name.c_str(), static_cast<size_t>(kOzPlanes) * n_mod * n * q.kpad, &buf));
       q.planes = static_cast<int8_t*>(buf);
-      CK(launch_ozaki_residues(v.base, v.ld, v.k, n, side ? er : el, b, n_mod, q.planes, q.kpad, st));
+      CK(launch_ozaki_residues(v.base, v.ld, v.k, n, side ? er : el, b, n_mod, q.planes, q.kpad, st, v.rscale));
     }
     srcs.push_back(q);
     *out = q;

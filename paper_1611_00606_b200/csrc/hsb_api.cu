@@ -594,7 +594,10 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   CKS(ws(ctx, "info", static_cast<size_t>(na) * 4, &info_d));
   CKS(ws(ctx, "pbb", tblk_bytes * na, &pbb));
   CKS(ws(ctx, "z", stack_bytes, &zbuf));
-  CKS(ws(ctx, "ub", stack_bytes, &ub));
+  // the INT8 engine's fused paths scale B by u on the fly (UB not materialised)
+  const bool u_fused = !unfused && ctx->engine == HSB_ENGINE_INT8;
+  ub = nullptr;
+  if (!u_fused) CKS(ws(ctx, "ub", stack_bytes, &ub));
   CKS(ws(ctx, "r", stack_bytes, &rbuf));
   CKS(ws(ctx, "offs", static_cast<size_t>(na) * 3 * 4, &offs_d));
   if (static_cast<size_t>(nl) * (nl + 1) / 2 * 16 > kPotrfSmemMax)
@@ -765,7 +768,16 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     CK(tl.mark(st, "loop1"));
     return HSB_OK;
   };
+  // INT8 engine (fused paths): UB is never materialised -- its column exponents
+  // and residues read B and scale each row by u on the fly, rounding the product
+  // exactly as diag_scale_kernel does
+  auto ub_view = [&]() {
+    OperandView v = plain(u_fused ? B : UB, K, ng, K);
+    if (u_fused) v.rscale = U;
+    return v;
+  };
   auto unorm = [&]() -> hsb_status {  // UB = diag(u) B (builder.py:124-127)
+    if (u_fused) return HSB_OK;
     CK(launch_diag_scale(B, K, UB, K, U, K, ng, st));
     ++launches;
     CK(tl.mark(st, "unorm"));
@@ -776,7 +788,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   if (overlap_upload) {
     CKS(unorm());
     ZrkCall s2 = tri_call(S, ldo, ng, kLowerOnly, 0.0);
-    s2.segs.push_back({plain(UB, K, ng, K), plain(UB, K, ng, K)});
+    s2.segs.push_back({ub_view(), ub_view()});
     s2.tl = &tl, s2.sect = "s2", s2.core = "s2_core";
     CKS(run_zrk(ctx, st, s2, &launches));
     CK(tl.mark(st, "s2"));
@@ -823,7 +835,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     CKS(unorm());
     ZrkCall s = tri_call(S, ldo, ng, kLowerOnly | kMirror, 0.0);
     s.segs.push_back({plain(A, K, ng, K), plain(A, K, ng, K)});
-    s.segs.push_back({plain(UB, K, ng, K), plain(UB, K, ng, K)});
+    s.segs.push_back({ub_view(), ub_view()});
     s.tl = &tl, s.sect = "s", s.core = "s_core";
     if (chunk_s) s.chunk_events = &s_chunks;
     s.peer = peer;

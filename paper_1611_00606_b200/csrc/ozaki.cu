@@ -56,14 +56,18 @@ __global__ void ozaki_init_exp_kernel(int32_t* e, int64_t n) {
 
 // one warp per column: e = frexp exponent of max_k |Re x| + |Im x| (max < 2^e)
 __global__ void ozaki_colexp_kernel(const double2* __restrict__ x, int64_t ldx, int64_t k, int64_t cols,
-                                    int32_t* __restrict__ e) {
+                                    int32_t* __restrict__ e, const double* __restrict__ rscale) {
   const int warps = blockDim.x >> 5;
   for (int64_t c = static_cast<int64_t>(blockIdx.x) * warps + (threadIdx.x >> 5); c < cols;
        c += static_cast<int64_t>(gridDim.x) * warps) {
     double m = 0.0;
     const double2* col = x + c * ldx;
     for (int64_t r = threadIdx.x & 31; r < k; r += 32) {
-      const double2 v = col[r];
+      double2 v = col[r];
+      if (rscale) {
+        const double u = __ldg(rscale + r);
+        v = make_double2(u * v.x, u * v.y);
+      }
       m = fmax(m, fabs(v.x) + fabs(v.y));
     }
 #pragma unroll
@@ -111,7 +115,8 @@ constexpr int kOzResK = 4;
 template <int NM>
 __global__ void __launch_bounds__(128, 6) ozaki_residue_kernel(const double2* __restrict__ x, int64_t ldx, int64_t k,
                                                             int64_t cols, const int32_t* __restrict__ col_exp, int b,
-                                                            int8_t* __restrict__ out, int64_t kpad) {
+                                                            int8_t* __restrict__ out, int64_t kpad,
+                                                            const double* __restrict__ rscale) {
   const int64_t k0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kOzResK;
   if (k0 >= kpad) return;
   const int64_t mod_stride = cols * kpad;
@@ -124,7 +129,11 @@ __global__ void __launch_bounds__(128, 6) ozaki_residue_kernel(const double2* __
 #pragma unroll
     for (int j = 0; j < kOzResK; ++j) {
       if (k0 + j < k) {
-        const double2 v = x[c * ldx + k0 + j];
+        double2 v = x[c * ldx + k0 + j];
+        if (rscale) {  // fl(u x), as diag_scale_kernel rounds it
+          const double u = __ldg(rscale + k0 + j);
+          v = make_double2(u * v.x, u * v.y);
+        }
         xr[j] = rint((v.x * s1) * s2);
         xi[j] = rint((v.y * s1) * s2);
       } else {
@@ -826,15 +835,15 @@ cudaError_t launch_ozaki_init_exp(int32_t* e, int64_t n, cudaStream_t st) {
 }
 
 cudaError_t launch_ozaki_colexp(const double* x, int64_t ldx, int64_t k, int64_t cols, int32_t* exp_out,
-                                cudaStream_t st) {
+                                cudaStream_t st, const double* rscale) {
   if (cols <= 0 || k <= 0) return cudaSuccess;
   ozaki_colexp_kernel<<<grid_cap((cols + 7) / 8, 148 * 16), 256, 0, st>>>(reinterpret_cast<const double2*>(x), ldx,
-                                                                          k, cols, exp_out);
+                                                                          k, cols, exp_out, rscale);
   return cudaGetLastError();
 }
 
 cudaError_t launch_ozaki_residues(const double* x, int64_t ldx, int64_t k, int64_t cols, const int32_t* col_exp,
-                                  int b, int n_mod, int8_t* out, int64_t kpad, cudaStream_t st) {
+                                  int b, int n_mod, int8_t* out, int64_t kpad, cudaStream_t st, const double* rscale) {
   if (cols <= 0 || kpad <= 0) return cudaSuccess;
   const int64_t threads_k = kpad / kOzResK;
   dim3 grid(static_cast<unsigned>((threads_k + 127) / 128), static_cast<unsigned>(cols < 65535 ? cols : 65535));
@@ -842,7 +851,7 @@ cudaError_t launch_ozaki_residues(const double* x, int64_t ldx, int64_t k, int64
   switch (n_mod) {
 #define HSB_OZ_RES(NM) \
   case NM:             \
-    ozaki_residue_kernel<NM><<<grid, 128, 0, st>>>(xx, ldx, k, cols, col_exp, b, out, kpad); \
+    ozaki_residue_kernel<NM><<<grid, 128, 0, st>>>(xx, ldx, k, cols, col_exp, b, out, kpad, rscale); \
     break;
     HSB_OZ_RES(11) HSB_OZ_RES(12) HSB_OZ_RES(13) HSB_OZ_RES(14) HSB_OZ_RES(15) HSB_OZ_RES(16)
 #undef HSB_OZ_RES

@@ -152,11 +152,13 @@ struct OzVcrtParams {
 };
 cudaError_t launch_ozaki_vcrt(const OzVcrtParams& p, cudaStream_t st);
 
+// rscale (optional): the operand is diag(rscale) x (S's U-normed B without a
+// materialised copy; the product rounds exactly as diag_scale_kernel's)
 cudaError_t launch_ozaki_colexp(const double* x, int64_t ldx, int64_t k, int64_t cols, int32_t* exp_out,
-                                cudaStream_t st);
+                                cudaStream_t st, const double* rscale = nullptr);
 cudaError_t launch_ozaki_init_exp(int32_t* e, int64_t n, cudaStream_t st);
 cudaError_t launch_ozaki_residues(const double* x, int64_t ldx, int64_t k, int64_t cols, const int32_t* col_exp,
-                                  int b, int n_mod, int8_t* out, int64_t kpad, cudaStream_t st);
+                                  int b, int n_mod, int8_t* out, int64_t kpad, cudaStream_t st, const double* rscale = nullptr);
 cudaError_t launch_ozaki_gemm(const OzGemmParams& p, cudaStream_t st);
 cudaError_t launch_ozaki_crt(const OzCrtParams& p, cudaStream_t st);
 cudaError_t launch_ozaki_crt_cols(const OzCrtParams& p, int64_t ncols, cudaStream_t st);

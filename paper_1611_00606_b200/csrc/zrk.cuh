@@ -88,6 +88,7 @@ struct OperandView {
   int64_t batch;        // >= 1
   int64_t bstride;      // complex elements between batches
   int32_t bpos;         // 1: dims (2k, batch, cols); 2: dims (2k, cols, batch)
+  const double* rscale = nullptr;  // INT8 engine only: real row factors (x[r, c] * rscale[r])
 };
 
 }  // namespace hsb
