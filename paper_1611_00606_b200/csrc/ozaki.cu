@@ -3,6 +3,7 @@
 // tcgen05 kind::i8 modular GEMM over lower-triangle tiles, and the CRT
 // reconstruction with the Hermitian mirror.
 #include <climits>
+#include <cmath>
 #include <cstring>
 #include <mutex>
 
@@ -543,10 +544,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
 // M < 2^99; 4 x 30 otherwise); every limb sum S_j = sum_i r_i y_ij (< 2^46)
 // and T_j = S_j - k M_j is an exact double, so X = sum_j T_j 2^(j LB) is
 // rounded once, at the end.  k only needs |error| < 1/4 (X/M is within 1/4 of
-// an integer): the quotient sum runs in FP32 (error < 13 * 240 * 2^-23).
+// an integer): the quotient sum runs in int32 with 19-bit weights.
 struct OzCrtConst {
   double y[2][kOzMaxMod][4];   // [Re, Im] limbs of y_i, least significant first
-  float f[2][kOzMaxMod];       // y_i / M
+  int32_t f[2][kOzMaxMod];     // rn(2^19 y_i / M): the quotient sum in int32
   double m[4];                 // limbs of M
 };
 constexpr int kOzMinMod = 11;
@@ -560,26 +561,26 @@ __device__ __forceinline__ double i2d_exact(int v) {
   return __hiloint2double(0x43300000, static_cast<int>(static_cast<unsigned>(v) ^ 0x80000000u)) -
          4503601774854144.0;  // 2^52 + 2^31
 }
-__device__ __forceinline__ float i2f_small(int v) {  // |v| < 2^22
-  return __int_as_float(0x4B400000 + v) - 12582912.0f;
-}
 
 template <int NM, int PART>
 __device__ __forceinline__ double crt_value(const int (&r)[NM]) {
   constexpr int NL = oz_crt_limbs(NM);
   const OzCrtConst& C = c_oz_crt[NM - kOzMinMod];
-  float fk = 0.0f;
+  int32_t fk = 0;
   double s[NL];
 #pragma unroll
   for (int j = 0; j < NL; ++j) s[j] = 0.0;
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
-    fk = __fmaf_rn(i2f_small(r[i]), C.f[PART][i], fk);
+    fk += r[i] * C.f[PART][i];
     const double ri = i2d_exact(r[i]);
 #pragma unroll
     for (int j = 0; j < NL; ++j) s[j] = fma(ri, C.y[PART][i][j], s[j]);
   }
-  const double k = static_cast<double>(rintf(fk));
+  // k = rn(sum r_i y_i / M): |r_i| <= 240 and 2^19 y_i / M < 2^19 keep the sum in
+  // int32 (13 * 240 * 2^19 < 2^31); the rounded weights err by <= 13 * 240 *
+  // 2^-20 < 0.003, far inside the 1/4 margin of X / M from a half-integer
+  const double k = i2d_exact((fk + (1 << 18)) >> 19);
   constexpr double kL = static_cast<double>(1ull << oz_crt_limb_bits(NM));
   double x = fma(-k, C.m[NL - 1], s[NL - 1]);
 #pragma unroll
@@ -805,7 +806,7 @@ static OzCrtConst oz_crt_table(int n_mod) {
     for (int part = 0; part < 2; ++part) {
       const u128 y = Mi * static_cast<u128>((cpart[part] * mi_inv) % pi);  // < M
       limbs(y, c.y[part][i]);
-      c.f[part][i] = static_cast<float>(static_cast<double>(y) / Md);
+      c.f[part][i] = static_cast<int32_t>(std::llround(static_cast<double>(y) / Md * 524288.0));
     }
   }
   limbs(M, c.m);
