@@ -272,7 +272,7 @@ cudaError_t launch_potrf_route(const double* t_aa, double* q, int32_t* info, int
                                          static_cast<int>(kPotrfSmemMax));
     if (e != cudaSuccess) return e;
   }
-  potrf_route_kernel<<<n_atoms, 256, smem, st>>>(
+  potrf_route_kernel<<<n_atoms, 1024, smem, st>>>(
       reinterpret_cast<const double2*>(t_aa), reinterpret_cast<double2*>(q), info, n, force_nonhpd ? 1 : 0,
       use_smem ? nullptr : reinterpret_cast<double2*>(gscratch));
   return cudaGetLastError();
