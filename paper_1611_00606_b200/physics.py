@@ -246,8 +246,9 @@ def match_coeffs_device(system: PhysicalSystem, kpt, gset, device: int = 0, stre
 
 
 def build_hs_physical(system: PhysicalSystem, kpt, gset, t_aa, t_ab, t_bb, policy=None,
-                      force_nonhpd: bool = False):
-    """North-star entry point: physical inputs in, H and S out (device tensors).
+                      force_nonhpd: bool = False, host_outputs: bool = False):
+    """North-star entry point: physical inputs in, H and S out (device tensors,
+    or column-major numpy arrays with ``host_outputs``).
 
     Matching coefficients are generated on the device and consumed in place
     by the H/S pipeline (no host round trip).  Returns
@@ -268,4 +269,4 @@ def build_hs_physical(system: PhysicalSystem, kpt, gset, t_aa, t_ab, t_bb, polic
 
     u = torch.from_numpy(np.concatenate(system.u_norms())).to(dev)
     dp = DeviceProblem(dims, a, b, mats(t_aa), mats(t_ab), mats(t_bb), u)
-    return build_hs_device(dp, policy=pol, force_nonhpd=force_nonhpd)
+    return build_hs_device(dp, policy=pol, force_nonhpd=force_nonhpd, host_outputs=host_outputs)

@@ -422,7 +422,7 @@ class DeviceProblem:
 
 
 def build_hs_device(dp: DeviceProblem, h=None, s=None, policy=None, force_nonhpd: bool = False,
-                    stream=None, s_ready=None, wait: bool = True, peer=None):
+                    stream=None, s_ready=None, wait: bool = True, peer=None, host_outputs: bool = False):
     """Device-resident build: returns (H, S, SplitCounts, timings, atom_info).
 
     H and S are torch complex128 (n_g, n_g) tensors holding the column-major
@@ -432,7 +432,10 @@ def build_hs_device(dp: DeviceProblem, h=None, s=None, policy=None, force_nonhpd
     call returns once the work is enqueued (split counts, timings and atom
     info are then None); the results are ready in stream order.  ``peer``
     (distributed.PeerSlots) scatters this rank's partial H and S into the
-    owners' receive slots instead of h and s (INT8 engine).
+    owners' receive slots instead of h and s (INT8 engine).  ``host_outputs``
+    returns H and S as column-major numpy arrays in (pinned) host memory
+    instead, downloaded while the contractions run (the drop-in path's output
+    streaming, lower triangles completed by the host mirror).
     """
     import torch
 
@@ -447,7 +450,12 @@ def build_hs_device(dp: DeviceProblem, h=None, s=None, policy=None, force_nonhpd
         tns = getattr(dp, name)
         if tuple(tns.shape) != shape or tns.dtype != dtype or not tns.is_contiguous() or tns.device != dev:
             raise InputError(f"{name} must be a contiguous {dtype} tensor of shape {shape} on {dev}")
-    if peer is None:
+    if host_outputs:
+        if peer is not None or h is not None or s is not None or not wait:
+            raise InputError("host_outputs excludes peer, h, s and wait=False")
+        pol0 = _policy(policy)
+        h_host, s_host = _host_matrix(n_g, pol0.pinned_outputs), _host_matrix(n_g, pol0.pinned_outputs)
+    elif peer is None:
         if h is None:
             h = torch.empty((n_g, n_g), dtype=torch.complex128, device=dev)
         if s is None:
@@ -463,10 +471,13 @@ def build_hs_device(dp: DeviceProblem, h=None, s=None, policy=None, force_nonhpd
     prob.t_aa_dev, prob.t_ab_dev, prob.t_bb_dev = dp.t_aa.data_ptr(), dp.t_ab.data_ptr(), dp.t_bb.data_ptr()
     prob.u_dev = dp.u.data_ptr()
     out = _lib.HsbOutput()
-    out.location = _lib.HSB_LOC_DEVICE
+    out.location = _lib.HSB_LOC_HOST if host_outputs else _lib.HSB_LOC_DEVICE
     out.ld = n_g
-    out.h = h.data_ptr() if peer is None else None
-    out.s = s.data_ptr() if peer is None else None
+    if host_outputs:
+        out.h, out.s = h_host.ctypes.data, s_host.ctypes.data
+    else:
+        out.h = h.data_ptr() if peer is None else None
+        out.s = s.data_ptr() if peer is None else None
     if s_ready is not None:
         s_ready.record(torch.cuda.current_stream(dev))  # materialise the CUDA event
         out.s_ready = s_ready.cuda_event
@@ -478,4 +489,6 @@ def build_hs_device(dp: DeviceProblem, h=None, s=None, policy=None, force_nonhpd
     tim, info = _call_build(pol, prob, out, ctypes.c_void_p(stream.cuda_stream), force_nonhpd, n_a, wait=wait)
     if not wait:
         return h, s, None, None, None
+    if host_outputs:
+        h, s = h_host, s_host
     return h, s, SplitCounts(tim.n_hpd, tim.n_nonhpd), _timings_dict(tim), info

@@ -68,3 +68,21 @@ def test_physical_build_matches_oracle_pipeline(engine, lmax, kpt):
     assert (split.hpd, split.nonhpd) == (ref["hpd"], ref["nonhpd"])
     assert rel_frob_error(h.cpu().numpy().T, ref["h"]) < 1e-10
     assert rel_frob_error(s.cpu().numpy().T, ref["s"]) < 1e-10
+
+
+@pytest.mark.parametrize("engine", ["int8", "dmma"])
+def test_physical_build_host_outputs_match_device(engine):
+    # the north-star entry point with H and S streamed to host memory (lower
+    # triangles + host mirror on the INT8 path) equals the device-resident build
+    from paper_1611_00606_b200 import GpuPolicy
+
+    system, k, kmax, g = synthetic_system(5, 2, 8, 1300, seed=5)
+    t_aa, t_ab, t_bb = synthetic_t_matrices(system, seed=5, nonhpd_fraction=0.2)
+    pol = GpuPolicy(engine=engine)
+    h, s, split, _, _ = build_hs_physical(system, k, g, t_aa, t_ab, t_bb, policy=pol)
+    hh, sh, split_h, t, _ = build_hs_physical(system, k, g, t_aa, t_ab, t_bb, policy=pol, host_outputs=True)
+    torch.cuda.synchronize()
+    assert isinstance(hh, np.ndarray) and hh.shape == (len(g), len(g))
+    assert (split.hpd, split.nonhpd) == (split_h.hpd, split_h.nonhpd)
+    assert np.array_equal(hh, h.cpu().numpy().T) and np.array_equal(sh, s.cpu().numpy().T)
+    assert t["d2h_bytes"] > 0
