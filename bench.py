@@ -453,33 +453,51 @@ def main():
                         "single_call_value": flops_full / (single_ms * 1e-3) / 1e12})
 
     # ------------------------------------------- north-star entry point, end to end
-    # atoms/types, lmax, G set, radial data and T matrices in (host), matching
-    # coefficients on the device, H and S out in host memory
+    # atoms/types, lmax, G sets, radial data and T matrices in (host), matching
+    # coefficients on the device, H and S out in pinned host memory: K distinct
+    # k-points of the config's system (ragged G sets, ~N_G each; config C5's
+    # shape) through physics.iter_hs_physical_kpoints
     e2e_phys = None
     if world == 1 and not args.no_e2e:
         from paper_1611_00606_b200 import physics
 
         lmax = int(round(dims.n_l ** 0.5)) - 1
         n_types = {"C1": 1, "C2": 2}.get(args.config, 4)
-        system, kpt, _kmax, gset = physics.synthetic_system(dims.n_atoms, n_types, lmax, dims.n_g, seed=args.seed)
+        system, kpt0, kmax, _ = physics.synthetic_system(dims.n_atoms, n_types, lmax, dims.n_g, seed=args.seed)
         t_aa, t_ab, t_bb = physics.synthetic_t_matrices(system, seed=args.seed)
-        n_gp = int(gset.shape[0])
-        flops_p = float(sum(section_flops(Dims(dims.n_atoms, dims.n_l, n_gp), 0).values()))
-        for _ in range(max(2, args.warmup)):
-            out = physics.build_hs_physical(system, kpt, gset, t_aa, t_ab, t_bb, policy, host_outputs=True)
-        del out
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            hh, sh, _, tp, _ = physics.build_hs_physical(system, kpt, gset, t_aa, t_ab, t_bb, policy,
-                                                         host_outputs=True)
-            _ = hh[0, 0]
-        phys_ms = (time.perf_counter() - t0) / args.steps * 1e3
-        h2d_p = sum(np.asarray(x).nbytes for m in (t_aa, t_ab, t_bb) for x in m) + gset.nbytes
-        e2e_phys = {"value": flops_p / (phys_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": phys_ms,
-                    "n_g": n_gp, "h2d_bytes_per_step": int(h2d_p), "d2h_bytes_per_step": int(tp["d2h_bytes"]),
-                    "api": "physics.build_hs_physical(host_outputs=True), one call per step: host wall time "
-                           "(matching coefficients on the device, H and S to pinned host memory)"}
-        del hh, sh
+        krng = np.random.default_rng(args.seed + 17)
+        kpts = [kpt0] + [krng.uniform(-0.5, 0.5, 3) for _ in range(args.steps - 1)]
+        gsets = [physics.gvector_set(system.lattice, k, kmax) for k in kpts]
+        flops_p = sum(float(sum(section_flops(Dims(dims.n_atoms, dims.n_l, int(g.shape[0])), 0).values()))
+                      for g in gsets)
+        depth_p = int(os.environ.get("HSB_PHYS_DEPTH", "3"))
+        try:
+            warm_k = kpts[:1] * (depth_p + 2)
+            for o in physics.iter_hs_physical_kpoints(system, warm_k, gsets[:1] * len(warm_k), t_aa, t_ab, t_bb,
+                                                      policy, depth=depth_p):
+                del o
+            t0 = time.perf_counter()
+            d2h_p = 0
+            for hh, sh, _, tp, _ in physics.iter_hs_physical_kpoints(system, kpts, gsets, t_aa, t_ab, t_bb, policy,
+                                                                     depth=depth_p):
+                _ = hh[-1, 0], sh[-1, 0]
+                d2h_p += int(tp["d2h_bytes"])
+                del hh, sh
+            phys_ms = (time.perf_counter() - t0) / args.steps * 1e3
+            t_bytes = sum(np.asarray(x).nbytes for m in (t_aa, t_ab, t_bb) for x in m) + 8 * dims.n_atoms * dims.n_l
+            h2d_p = t_bytes / args.steps + sum(g.nbytes for g in gsets) / args.steps
+            e2e_phys = {"value": flops_p / args.steps / (phys_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                        "ms_per_step": phys_ms, "depth": depth_p,
+                        "n_g_per_kpoint": [int(g.shape[0]) for g in gsets],
+                        "h2d_bytes_per_step": int(h2d_p), "d2h_bytes_per_step": int(d2h_p / args.steps),
+                        "api": f"physics.iter_hs_physical_kpoints({args.steps} distinct k-points, depth={depth_p}): "
+                               "host wall time per k-point; T/U uploaded once per call (k-independent), G sets "
+                               "and radial data per k-point, matching coefficients on the device, H and S "
+                               "to pinned host memory"}
+        except (torch.OutOfMemoryError, RuntimeError) as exc:
+            if "memory" not in str(exc).lower():
+                raise
+            e2e_phys = {"unavailable": f"out of memory at depth {depth_p}: {exc}"[:200]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -226,23 +226,50 @@ def _phys_struct(system: PhysicalSystem, kpt, gset):
     return s, (g, tau, types, rmt, radial)
 
 
-def match_coeffs_device(system: PhysicalSystem, kpt, gset, device: int = 0, stream=None):
+def match_coeffs_device(system: PhysicalSystem, kpt, gset, device: int = 0, stream=None, slot: int = 0,
+                        out=None):
     """A, B stacks on the device: torch complex128 (n_g, n_atoms*n_l) tensors
-    (= column-major K x n_g), generated by the sm_100a matching kernel."""
+    (= column-major K x n_g), generated by the sm_100a matching kernel.
+    ``out`` = (a, b) writes into caller-owned tensors of that shape; ``slot``
+    picks the library context whose workspace stages the small inputs."""
     import torch
 
     lib = _lib.load()
-    ctx = _lib.context(device)
+    ctx = _lib.context(device, slot=slot)
     dev = torch.device("cuda", device)
     n_g, k = int(gset.shape[0]), system.n_atoms * system.n_l
-    a = torch.empty((n_g, k), dtype=torch.complex128, device=dev)
-    b = torch.empty_like(a)
+    if out is None:
+        a = torch.empty((n_g, k), dtype=torch.complex128, device=dev)
+        b = torch.empty_like(a)
+    else:
+        a, b = out
+        for t in (a, b):
+            if tuple(t.shape) != (n_g, k) or t.dtype != torch.complex128 or not t.is_contiguous() or t.device != dev:
+                raise InputError(f"out tensors must be contiguous complex128 of shape ({n_g}, {k}) on {dev}")
     s, _keep = _phys_struct(system, kpt, gset)
     if stream is None:
         stream = torch.cuda.current_stream(dev)
     _lib.check(lib.hsb_match_coeffs(ctx, ctypes.c_void_p(stream.cuda_stream), ctypes.byref(s), a.data_ptr(),
                                     b.data_ptr(), k), ctx)
     return a, b
+
+
+def _device_t(system: PhysicalSystem, t_aa, t_ab, t_bb, dev):
+    """T_AA, T_AB, T_BB as (n_atoms, n_l, n_l) device stacks and U (K,)."""
+    import torch
+
+    n_a, n_l = system.n_atoms, system.n_l
+
+    def mats(blocks):
+        if len(blocks) != n_a:
+            raise InputError(f"expected {n_a} T blocks, got {len(blocks)}")
+        host = np.stack([np.asarray(x, dtype=np.complex128).T for x in blocks])
+        if host.shape != (n_a, n_l, n_l):
+            raise InputError(f"T blocks must be {n_l} x {n_l}")
+        return torch.from_numpy(np.ascontiguousarray(host)).to(dev)
+
+    u = torch.from_numpy(np.concatenate(system.u_norms())).to(dev)
+    return mats(t_aa), mats(t_ab), mats(t_bb), u
 
 
 def build_hs_physical(system: PhysicalSystem, kpt, gset, t_aa, t_ab, t_bb, policy=None,
@@ -262,11 +289,57 @@ def build_hs_physical(system: PhysicalSystem, kpt, gset, t_aa, t_ab, t_bb, polic
     dev = torch.device("cuda", pol.device)
     a, b = match_coeffs_device(system, kpt, gset, pol.device)
     dims = Dims(system.n_atoms, system.n_l, int(gset.shape[0]))
-
-    def mats(blocks):
-        host = np.stack([np.asarray(x, dtype=np.complex128).T for x in blocks])
-        return torch.from_numpy(np.ascontiguousarray(host)).to(dev)
-
-    u = torch.from_numpy(np.concatenate(system.u_norms())).to(dev)
-    dp = DeviceProblem(dims, a, b, mats(t_aa), mats(t_ab), mats(t_bb), u)
+    dp = DeviceProblem(dims, a, b, *_device_t(system, t_aa, t_ab, t_bb, dev))
     return build_hs_device(dp, policy=pol, force_nonhpd=force_nonhpd, host_outputs=host_outputs)
+
+
+def iter_hs_physical_kpoints(system: PhysicalSystem, kpts, gsets, t_aa, t_ab, t_bb, policy=None,
+                             force_nonhpd: bool = False, depth: int = 3):
+    """Yield (H, S, SplitCounts, timings, atom_info) of ``build_hs_physical(...,
+    host_outputs=True)`` for each k-point in order (BASELINE config C5 from
+    physical inputs), pipelined on one GPU.
+
+    The T matrices and U are k-independent: they are uploaded once and shared
+    by every k-point.  ``depth`` lanes (host threads, each with its own
+    library context, CUDA stream and A/B buffers sized for the largest G set)
+    run in turn: lane i % depth generates k-point i's A and B in its buffers
+    and builds H and S from them; the contractions run in k-point order on the
+    SMs (compute events, as in ``pipeline.iter_hs_kpoints``) while earlier
+    k-points' H and S stream to pinned host memory.  Every result equals the
+    serial ``build_hs_physical`` of that k-point bit for bit.
+    """
+    import torch
+
+    from .pipeline import DeviceProblem, GpuPolicy, _lane_pipeline, build_hs_device
+
+    pol = policy if isinstance(policy, GpuPolicy) else GpuPolicy()
+    if int(depth) != depth or depth < 1:
+        raise InputError(f"depth must be a positive integer, got {depth!r}")
+    kpts, gsets = list(kpts), list(gsets)
+    if len(kpts) != len(gsets):
+        raise InputError(f"{len(kpts)} k-points but {len(gsets)} G sets")
+    if not kpts:
+        return
+    dev = torch.device("cuda", pol.device)
+    tdev = _device_t(system, t_aa, t_ab, t_bb, dev)
+    k = system.n_atoms * system.n_l
+    n_max = max(int(g.shape[0]) for g in gsets)
+    depth = min(int(depth), len(kpts))
+    bufs = [(torch.empty((n_max, k), dtype=torch.complex128, device=dev),
+             torch.empty((n_max, k), dtype=torch.complex128, device=dev)) for _ in range(depth)]
+    torch.cuda.synchronize(dev)  # T uploads and buffers ready before the lanes' streams use them
+
+    def run(i, slot, stream, order):
+        n_g = int(gsets[i].shape[0])
+        a, b = bufs[slot][0][:n_g], bufs[slot][1][:n_g]
+        match_coeffs_device(system, kpts[i], gsets[i], pol.device, stream=stream, slot=slot, out=(a, b))
+        dp = DeviceProblem(Dims(system.n_atoms, system.n_l, n_g), a, b, *tdev)
+        return build_hs_device(dp, policy=pol, force_nonhpd=force_nonhpd, stream=stream, host_outputs=True,
+                               slot=slot, order=order)
+
+    if depth == 1:
+        st = torch.cuda.current_stream(dev)
+        for i in range(len(kpts)):
+            yield run(i, 0, st, None)
+        return
+    yield from _lane_pipeline(len(kpts), depth, pol, n_max, run)

@@ -259,10 +259,6 @@ def iter_hs_kpoints(instances, policy=None, force_nonhpd: bool = False, depth: i
     depth >= 3.  At most ``depth`` results are in flight beyond the one being
     consumed, so pinned output memory stays bounded when the caller drops each
     result after use."""
-    import threading
-
-    import torch
-
     pol = _policy(policy)
     if int(depth) != depth or depth < 1:
         raise InputError(f"depth must be a positive integer, got {depth!r}")
@@ -271,37 +267,54 @@ def iter_hs_kpoints(instances, policy=None, force_nonhpd: bool = False, depth: i
         for p in instances:
             yield build_hs(p, pol, force_nonhpd)
         return
+
+    def run(i, slot, stream, order):
+        return _build_host(instances[i], pol, force_nonhpd, slot=slot, stream=ctypes.c_void_p(stream.cuda_stream),
+                           order=order)
+
+    yield from _lane_pipeline(len(instances), depth, pol, max(int(p.dims.n_g) for p in instances), run)
+
+
+def _lane_pipeline(count: int, depth: int, pol, n_max: int, run):
+    """Run ``run(i, slot, stream, order)`` for i in 0..count-1 on ``depth``
+    lanes (host threads, each with its own context slot and CUDA stream) and
+    yield the results in order.  ``order`` is the hsb_output ordering tuple
+    (h2d_after, h2d_done, compute_after, compute_done, order_in, order_out)
+    that chains item i's uploads and kernels after item i-1's."""
+    import threading
+
+    import torch
+
     dev = torch.device("cuda", pol.device)
     streams = [torch.cuda.Stream(device=dev) for _ in range(depth)]
     if pol.pinned_outputs:
         # up to depth + 1 results (two matrices each) are alive at once: have the
         # caching pinned allocator hold that many blocks before the lanes start,
         # so no 1 GB cudaHostAlloc lands in the middle of the pipeline
-        n_max = max(int(p.dims.n_g) for p in instances)
         warm = [_host_matrix(n_max, True) for _ in range(2 * (depth + 1))]
         del warm
-    results = [None] * len(instances)
-    ready = [threading.Event() for _ in instances]
-    # window: k-point i may start once fewer than depth results ahead of it are
+    results = [None] * count
+    ready = [threading.Event() for _ in range(count)]
+    # window: item i may start once fewer than depth results ahead of it are
     # unconsumed (i < consumed + depth), so a fast lane cannot use up the
-    # window with later k-points while the consumer waits for an earlier one
+    # window with later items while the consumer waits for an earlier one
     window = threading.Condition()
     consumed = [0]
     failure = []
 
-    # ordering: k-point i's uploads wait for k-point i-1's (h2d events), its
-    # kernels for k-point i-1's (compute events).  The library only waits on an
-    # event once the previous call has recorded it (progress flags, one per
-    # k-point).  Events are recycled modulo depth + 2: k-point i + depth + 2
-    # starts only after result i + 1 was consumed, i.e. after k-point i + 1
-    # finished waiting on k-point i's events.
+    # ordering: item i's uploads wait for item i-1's (h2d events), its kernels
+    # for item i-1's (compute events).  The library only waits on an event
+    # once the previous call has recorded it (progress flags, one per item).
+    # Events are recycled modulo depth + 2: item i + depth + 2 starts only
+    # after result i + 1 was consumed, i.e. after item i + 1 finished waiting
+    # on item i's events.
     n_ev = depth + 2
     h2d_ev = [torch.cuda.Event() for _ in range(n_ev)]
     cmp_ev = [torch.cuda.Event() for _ in range(n_ev)]
     for ev in h2d_ev + cmp_ev:
         ev.record(torch.cuda.current_stream(dev))  # materialise the CUDA events
     torch.cuda.current_stream(dev).synchronize()
-    flags = (ctypes.c_int32 * len(instances))()
+    flags = (ctypes.c_int32 * count)()
     flag_ptr = ctypes.cast(flags, ctypes.c_void_p).value
 
     def order_of(i):
@@ -311,29 +324,28 @@ def iter_hs_kpoints(instances, policy=None, force_nonhpd: bool = False, depth: i
             else (None, None, None)
         return (prev[0], h2d_ev[i % n_ev].cuda_event, prev[1], cmp_ev[i % n_ev].cuda_event, prev[2], fp(i))
 
-    def lane(slot):  # one thread per context: k-points slot, slot + depth, ...
-        st = ctypes.c_void_p(streams[slot].cuda_stream)
+    def lane(slot):  # one thread per context: items slot, slot + depth, ...
         try:
-            for i in range(slot, len(instances), depth):
+            for i in range(slot, count, depth):
                 with window:
                     window.wait_for(lambda: failure or i < consumed[0] + depth)
                 if failure:
                     return
-                results[i] = _build_host(instances[i], pol, force_nonhpd, slot=slot, stream=st, order=order_of(i))
+                results[i] = run(i, slot, streams[slot], order_of(i))
                 ready[i].set()
         except BaseException as exc:  # noqa: BLE001 - re-raised in the consumer
             failure.append(exc)
             for e in ready:
                 e.set()
         finally:
-            for i in range(slot, len(instances), depth):  # never leave a later k-point waiting
+            for i in range(slot, count, depth):  # never leave a later item waiting
                 flags[i] = max(flags[i], 2)
 
     threads = [threading.Thread(target=lane, args=(k,), daemon=True) for k in range(depth)]
     for t in threads:
         t.start()
     try:
-        for i in range(len(instances)):
+        for i in range(count):
             ready[i].wait()
             if failure:
                 raise failure[0]
@@ -422,7 +434,8 @@ class DeviceProblem:
 
 
 def build_hs_device(dp: DeviceProblem, h=None, s=None, policy=None, force_nonhpd: bool = False,
-                    stream=None, s_ready=None, wait: bool = True, peer=None, host_outputs: bool = False):
+                    stream=None, s_ready=None, wait: bool = True, peer=None, host_outputs: bool = False,
+                    slot: int = 0, order=None):
     """Device-resident build: returns (H, S, SplitCounts, timings, atom_info).
 
     H and S are torch complex128 (n_g, n_g) tensors holding the column-major
@@ -432,7 +445,9 @@ def build_hs_device(dp: DeviceProblem, h=None, s=None, policy=None, force_nonhpd
     call returns once the work is enqueued (split counts, timings and atom
     info are then None); the results are ready in stream order.  ``peer``
     (distributed.PeerSlots) scatters this rank's partial H and S into the
-    owners' receive slots instead of h and s (INT8 engine).  ``host_outputs``
+    owners' receive slots instead of h and s (INT8 engine).  ``slot`` picks the
+    library context, ``order`` chains the call after a previous pipelined one
+    (see ``_lane_pipeline``).  ``host_outputs``
     returns H and S as column-major numpy arrays in (pinned) host memory
     instead, downloaded while the contractions run (the drop-in path's output
     streaming, lower triangles completed by the host mirror).
@@ -484,9 +499,12 @@ def build_hs_device(dp: DeviceProblem, h=None, s=None, policy=None, force_nonhpd
     if peer is not None:
         peer_struct = peer.struct()
         out.peer = ctypes.pointer(peer_struct)
+    if order is not None:  # (h2d_after, h2d_done, compute_after, compute_done, order_in, order_out)
+        (out.h2d_after, out.h2d_done, out.compute_after, out.compute_done, out.order_in, out.order_out) = order
     if stream is None:
         stream = torch.cuda.current_stream(dev)
-    tim, info = _call_build(pol, prob, out, ctypes.c_void_p(stream.cuda_stream), force_nonhpd, n_a, wait=wait)
+    tim, info = _call_build(pol, prob, out, ctypes.c_void_p(stream.cuda_stream), force_nonhpd, n_a, slot=slot,
+                            wait=wait)
     if not wait:
         return h, s, None, None, None
     if host_outputs:

@@ -86,3 +86,47 @@ def test_physical_build_host_outputs_match_device(engine):
     assert (split.hpd, split.nonhpd) == (split_h.hpd, split_h.nonhpd)
     assert np.array_equal(hh, h.cpu().numpy().T) and np.array_equal(sh, s.cpu().numpy().T)
     assert t["d2h_bytes"] > 0
+
+
+@pytest.mark.parametrize("engine,depth", [("int8", 3), ("dmma", 2), ("int8", 1)])
+def test_physical_kpoint_pipeline_equals_serial(engine, depth):
+    # config C5 from physical inputs: distinct k-points (so distinct, ragged G
+    # sets) through the pipelined iterator equal serial build_hs_physical calls
+    # bit for bit, in order; one k-point is also checked against the oracle
+    from paper_1611_00606_b200 import GpuPolicy
+    from paper_1611_00606_b200.physics import gvector_set, iter_hs_physical_kpoints
+
+    system, _, kmax, _ = synthetic_system(4, 2, 6, 900, seed=11)
+    t_aa, t_ab, t_bb = synthetic_t_matrices(system, seed=11, nonhpd_fraction=0.25)
+    kpts = [np.array(k) for k in [(0.0, 0.0, 0.0), (0.5, 0.25, 0.0), (0.125, -0.375, 0.25), (0.5, 0.5, 0.5),
+                                   (-0.25, 0.0, 0.125)]]
+    gsets = [gvector_set(system.lattice, k, kmax) for k in kpts]
+    assert len({g.shape[0] for g in gsets}) > 1  # ragged sizes
+    pol = GpuPolicy(engine=engine)
+    got = list(iter_hs_physical_kpoints(system, kpts, gsets, t_aa, t_ab, t_bb, policy=pol, depth=depth))
+    assert len(got) == len(kpts)
+    for (hh, sh, split, t, _), k, g in zip(got, kpts, gsets):
+        h, s, split_s, _, _ = build_hs_physical(system, k, g, t_aa, t_ab, t_bb, policy=pol, host_outputs=True)
+        assert hh.shape == (len(g), len(g))
+        assert (split.hpd, split.nonhpd) == (split_s.hpd, split_s.nonhpd)
+        assert np.array_equal(hh, h) and np.array_equal(sh, s)
+    a, b = _oracle(system, kpts[2], gsets[2])
+    n_l = system.n_l
+    p = ProblemInstance(Dims(system.n_atoms, n_l, len(gsets[2])))
+    p.a_blocks = [np.asfortranarray(a[i * n_l:(i + 1) * n_l]) for i in range(system.n_atoms)]
+    p.b_blocks = [np.asfortranarray(b[i * n_l:(i + 1) * n_l]) for i in range(system.n_atoms)]
+    p.t_aa, p.t_ab, p.t_bb, p.u_norms = t_aa, t_ab, t_bb, system.u_norms()
+    ref = alg1.build_hs_cpu(p)
+    assert (got[2][2].hpd, got[2][2].nonhpd) == (ref["hpd"], ref["nonhpd"])
+    assert rel_frob_error(got[2][0], ref["h"]) < 1e-10
+    assert rel_frob_error(got[2][1], ref["s"]) < 1e-10
+
+
+def test_physical_kpoint_pipeline_rejects_mismatched_lists():
+    from paper_1611_00606_b200 import InputError
+    from paper_1611_00606_b200.physics import iter_hs_physical_kpoints
+
+    system, k, _, g = synthetic_system(2, 1, 2, 100, seed=1)
+    t = synthetic_t_matrices(system, seed=1)
+    with pytest.raises(InputError):
+        list(iter_hs_physical_kpoints(system, [k, k], [g], *t))
