@@ -472,8 +472,10 @@ def main():
                       for g in gsets)
         depth_p = int(os.environ.get("HSB_PHYS_DEPTH", "3"))
         try:
-            warm_k = kpts[:1] * (depth_p + 2)
-            for o in physics.iter_hs_physical_kpoints(system, warm_k, gsets[:1] * len(warm_k), t_aa, t_ab, t_bb,
+            # warm contexts and the pinned cache at the largest G set of the batch
+            imax = int(np.argmax([g.shape[0] for g in gsets]))
+            warm_k = [kpts[imax]] * (depth_p + 2)
+            for o in physics.iter_hs_physical_kpoints(system, warm_k, [gsets[imax]] * len(warm_k), t_aa, t_ab, t_bb,
                                                       policy, depth=depth_p):
                 del o
             t0 = time.perf_counter()

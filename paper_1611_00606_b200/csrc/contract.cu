@@ -223,6 +223,10 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
     }
   if (segs.size() > static_cast<size_t>(kOzMaxSeg)) return fail(ctx, HSB_ERR_UNSUPPORTED, "too many segments");
   int n_mod = 0, b = 0;
+  if (z.oz_el && z.oz_ktot > 0) {
+    if (z.oz_ktot < ktot) return fail(ctx, HSB_ERR_UNSUPPORTED, "prepared INT8 planes sized for a shorter reduction");
+    ktot = z.oz_ktot;
+  }
   CKS(oz_choose(ctx, ktot, &n_mod, &b));
   // exponents: one array for both sides (m == n), max over every operand --
   // unless the caller prepared left / right exponents (run_ozaki_hv)
@@ -263,7 +267,7 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
   std::vector<Src> srcs;
   int computed = 0;
   auto planes_of = [&](const OperandView& v, int side, Src* out) -> hsb_status {
-    if (!pre) side = 0;  // one exponent array: both sides share residues
+    if (!pre || el == er) side = 0;  // one exponent array: both sides share residues
     for (const Src& q : srcs)
       if (q.base == v.base && q.k == v.k && q.ld == v.ld && q.side == side && q.rscale == v.rscale) {
         *out = q;

@@ -216,6 +216,9 @@ struct ZrkCall {
     int8_t* planes;
   };
   std::vector<OzPre> oz_pre;
+  // with oz_el: the reduction length the prepared planes were sized for
+  // (oz_choose's moduli and bits), when this call's own is shorter
+  int64_t oz_ktot = 0;
 };
 
 

@@ -784,6 +784,37 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     return HSB_OK;
   };
 
+  // INT8 engine, fused paths: one left exponent per column over A, B and UB
+  // (ozaki_colexp_ab, one pass over A and B) shared by S = A^H A + (UB)^H (UB)
+  // and the left side of H = A^H V1 + B^H V2, so A's residue planes are computed
+  // once for both contractions; H's right side (V1, V2) gets its own exponents.
+  // The planes are sized for the 2K reduction (oz_ktot) of both calls.
+  const bool oz_share = !unfused && ctx->engine == HSB_ENGINE_INT8 && !int8_v;
+  int32_t* oz_el = nullptr;
+  int8_t* oz_res_a = nullptr;
+  auto oz_left = [&]() -> hsb_status {  // A and B resident
+    if (!oz_share) return HSB_OK;
+    int n_mod = 0, bits = 0;
+    CKS(oz_choose(ctx, 2 * K, &n_mod, &bits));
+    const int64_t kpad = (K + 15) / 16 * 16;
+    void *eb, *rb;
+    CKS(ws(ctx, "oz_exp_l", static_cast<size_t>(ng) * 4, &eb));
+    CKS(ws(ctx, "oz_res_a", static_cast<size_t>(hsb::kOzPlanes) * n_mod * ng * kpad, &rb));
+    oz_el = static_cast<int32_t*>(eb);
+    oz_res_a = static_cast<int8_t*>(rb);
+    CK(hsb::launch_ozaki_colexp_ab(A, B, K, K, ng, U, oz_el, st));
+    CK(hsb::launch_ozaki_residues(A, K, K, ng, oz_el, bits, n_mod, oz_res_a, kpad, st));
+    launches += 2;
+    return HSB_OK;
+  };
+  auto oz_use_left = [&](ZrkCall& z, const int32_t* er) {
+    if (!oz_share) return;
+    z.oz_el = oz_el;
+    z.oz_er = er ? er : oz_el;
+    z.oz_pre.push_back({A, 0, oz_res_a});
+    z.oz_ktot = 2 * K;
+  };
+
   // ------------------------------------------------------ Loop 1, U norm, S
   if (overlap_upload) {
     CKS(unorm());
@@ -809,6 +840,8 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     s1.segs.push_back({plain(A, K, ng, K), plain(A, K, ng, K)});
     s1.tl = &tl, s1.sect = "s1", s1.core = "s1_core";
     if (chunk_s) s1.chunk_events = &s_chunks;
+    CKS(oz_left());
+    oz_use_left(s1, nullptr);
     CKS(run_zrk(ctx, st, s1, &launches));
     CK(tl.mark(st, "s1"));
     CKS(vloop());
@@ -839,6 +872,8 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     s.tl = &tl, s.sect = "s", s.core = "s_core";
     if (chunk_s) s.chunk_events = &s_chunks;
     s.peer = peer;
+    CKS(oz_left());
+    oz_use_left(s, nullptr);
     CKS(run_zrk(ctx, st, s, &launches));
     CK(tl.mark(st, "s"));
   }
@@ -947,6 +982,16 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
       hv.vsect = "loop1";
       CKS(run_ozaki_hv(ctx, st, hv, h, &launches));
     } else {
+      if (oz_share) {  // H's right exponents: V1, V2 only
+        void* erb;
+        CKS(ws(ctx, "oz_exp_r", static_cast<size_t>(ng) * 4, &erb));
+        int32_t* er = static_cast<int32_t*>(erb);
+        CK(hsb::launch_ozaki_init_exp(er, ng, st));
+        CK(hsb::launch_ozaki_colexp(Z, K, K, ng, er, st));
+        CK(hsb::launch_ozaki_colexp(R, K, K, ng, er, st));
+        launches += 3;
+        oz_use_left(h, er);
+      }
       CKS(run_zrk(ctx, st, h, &launches));
     }
     CK(tl.mark(st, "h"));

@@ -81,6 +81,35 @@ __global__ void ozaki_colexp_kernel(const double2* __restrict__ x, int64_t ldx, 
   }
 }
 
+// one warp per column, two stacks with the same shape read once: the exponent of
+// max_k over |a|, |b| and |fl(u_k b)| (|Re| + |Im|) -- the left exponent shared by
+// S = A^H A + (UB)^H (UB) and the left side of H = A^H V1 + B^H V2, so A's
+// residue planes serve both contractions
+__global__ void ozaki_colexp_ab_kernel(const double2* __restrict__ a, const double2* __restrict__ b, int64_t ld,
+                                       int64_t k, int64_t cols, const double* __restrict__ u,
+                                       int32_t* __restrict__ e) {
+  const int warps = blockDim.x >> 5;
+  for (int64_t c = static_cast<int64_t>(blockIdx.x) * warps + (threadIdx.x >> 5); c < cols;
+       c += static_cast<int64_t>(gridDim.x) * warps) {
+    double m = 0.0;
+    const double2* ca = a + c * ld;
+    const double2* cb = b + c * ld;
+    for (int64_t r = threadIdx.x & 31; r < k; r += 32) {
+      const double2 va = ca[r], vb = cb[r];
+      const double uk = __ldg(u + r);
+      m = fmax(m, fmax(fabs(va.x) + fabs(va.y), fabs(vb.x) + fabs(vb.y)));
+      m = fmax(m, fabs(uk * vb.x) + fabs(uk * vb.y));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) {
+      int ex = 0;
+      frexp(m, &ex);
+      e[c] = ex;
+    }
+  }
+}
+
 // ------------------------------------------------------------ 2. residues
 // 1 / p, correctly rounded (compile-time division)
 __constant__ double oz_inv_rt[kOzMaxMod] = {
@@ -840,6 +869,14 @@ cudaError_t launch_ozaki_colexp(const double* x, int64_t ldx, int64_t k, int64_t
   if (cols <= 0 || k <= 0) return cudaSuccess;
   ozaki_colexp_kernel<<<grid_cap((cols + 7) / 8, 148 * 16), 256, 0, st>>>(reinterpret_cast<const double2*>(x), ldx,
                                                                           k, cols, exp_out, rscale);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ozaki_colexp_ab(const double* a, const double* b, int64_t ld, int64_t k, int64_t cols,
+                                   const double* u, int32_t* exp_out, cudaStream_t st) {
+  if (cols <= 0 || k <= 0) return cudaSuccess;
+  ozaki_colexp_ab_kernel<<<grid_cap((cols + 7) / 8, 148 * 16), 256, 0, st>>>(
+      reinterpret_cast<const double2*>(a), reinterpret_cast<const double2*>(b), ld, k, cols, u, exp_out);
   return cudaGetLastError();
 }
 
