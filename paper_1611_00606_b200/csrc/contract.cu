@@ -302,6 +302,9 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
       CKS(oz_encode(ctx, &gp.map[pi][si][1], L.planes + lp[pi] * pl, L.k, n, L.kpad, n_mod, 128));
     }
     gp.seg_chunk0[si + 1] = gp.seg_chunk0[si] + static_cast<int32_t>((segs[si].l.k + kOzBK - 1) / kOzBK);
+    static const bool no_kskip = std::getenv("HSB_NO_KSKIP") != nullptr;  // A/B experiments
+    if (!no_kskip)
+      gp.seg_ksteps_last[si] = static_cast<int32_t>((segs[si].l.k - (gp.seg_chunk0[si + 1] - gp.seg_chunk0[si] - 1) * kOzBK + 31) / 32);
   }
   gp.nseg = static_cast<int32_t>(segs.size());
   // slabs of ~16 KB of k (see ozaki.cuh), balanced
@@ -494,6 +497,8 @@ hsb_status run_zrk(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launche
   p.c_bstride = z.c_bstride;
   p.c_rowoff = z.c_rowoff;
   p.done_cnt = z.triangle ? z.done_cnt : nullptr;
+  if (z.col_exp && (!g3 || z.triangle)) return fail(ctx, HSB_ERR_UNSUPPORTED, "column exponents need the 3M rect kernel");
+  p.col_exp = z.col_exp;
   int64_t grid_x = z.triangle ? static_cast<int64_t>(p.tiles_m) * (p.tiles_m + 1) / 2
                               : static_cast<int64_t>(p.tiles_m) * p.tiles_n;
   if (grid_x > 0x7fffffff || z.batch > 65535) return fail(ctx, HSB_ERR_UNSUPPORTED, "grid too large");

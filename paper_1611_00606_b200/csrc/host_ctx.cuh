@@ -194,6 +194,9 @@ struct ZrkCall {
   int64_t c_bstride = 0;
   const int32_t* c_rowoff = nullptr;
   int* done_cnt = nullptr;
+  // optional (3M DMMA kernel, rectangular calls): column exponents of the
+  // output for the INT8 engine, atomicMax-ed into col_exp (initialised by the caller)
+  int32_t* col_exp = nullptr;
   // optional: mark the contraction kernel alone on this timeline, charging the
   // work before it to `sect` and the kernel itself to `core`
   Timeline* tl = nullptr;

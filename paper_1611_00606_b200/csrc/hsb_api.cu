@@ -742,6 +742,9 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   // 3.3 ms; its modular GEMM is epilogue-bound at K = 2 n_l), so off by default.
   static const bool int8_v_env = std::getenv("HSB_INT8_V") != nullptr;
   const bool int8_v = int8_v_env && !unfused && ctx->engine == HSB_ENGINE_INT8 && 2 * nl <= 256;
+  // INT8 engine, fused paths: shared left exponent / A residues (oz_left below)
+  const bool oz_share = !unfused && ctx->engine == HSB_ENGINE_INT8 && !int8_v;
+  int32_t* oz_er_v = nullptr;  // H's right exponents from the V products' epilogue
   auto vloop = [&]() -> hsb_status {
     if (int8_v) return HSB_OK;
     void *taa_full, *tab_h;
@@ -751,8 +754,19 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     CK(launch_half_mirror(TBB, static_cast<double*>(pbb), static_cast<int>(nl), na, 1.0, st));
     CK(launch_conj_transpose(TAB, static_cast<double*>(tab_h), static_cast<int>(nl), na, st));
     launches += 3;
+    // INT8 engine: the V products' epilogue also yields H's right column
+    // exponents (max over V1 and V2), so no separate exponent pass reads them
+    static const bool no_vexp = std::getenv("HSB_NO_VEXP") != nullptr;  // A/B experiments
+    if (oz_share && ctx->cplx == HSB_CPLX_3M && !no_vexp) {
+      void* erb;
+      CKS(ws(ctx, "oz_exp_r", static_cast<size_t>(ng) * 4, &erb));
+      oz_er_v = static_cast<int32_t*>(erb);
+      CK(hsb::launch_ozaki_init_exp(oz_er_v, ng, st));
+      ++launches;
+    }
     for (int half = 0; half < 2; ++half) {  // zrk form: sum_s L_s^H R_s
       ZrkCall z;
+      z.col_exp = oz_er_v;
       const double* l0 = half == 0 ? static_cast<const double*>(taa_full) : TAB;              // T_AA | (T_AB^H)^H
       const double* l1 = half == 0 ? static_cast<const double*>(tab_h) : static_cast<const double*>(pbb);  // (T_AB)^H^H | T_BB
       z.segs.push_back({atom_mats(l0, na, nl), atom_rows(A, na, nl, ng, K)});
@@ -789,7 +803,6 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   // and the left side of H = A^H V1 + B^H V2, so A's residue planes are computed
   // once for both contractions; H's right side (V1, V2) gets its own exponents.
   // The planes are sized for the 2K reduction (oz_ktot) of both calls.
-  const bool oz_share = !unfused && ctx->engine == HSB_ENGINE_INT8 && !int8_v;
   int32_t* oz_el = nullptr;
   int8_t* oz_res_a = nullptr;
   auto oz_left = [&]() -> hsb_status {  // A and B resident
@@ -983,13 +996,16 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
       CKS(run_ozaki_hv(ctx, st, hv, h, &launches));
     } else {
       if (oz_share) {  // H's right exponents: V1, V2 only
-        void* erb;
-        CKS(ws(ctx, "oz_exp_r", static_cast<size_t>(ng) * 4, &erb));
-        int32_t* er = static_cast<int32_t*>(erb);
-        CK(hsb::launch_ozaki_init_exp(er, ng, st));
-        CK(hsb::launch_ozaki_colexp(Z, K, K, ng, er, st));
-        CK(hsb::launch_ozaki_colexp(R, K, K, ng, er, st));
-        launches += 3;
+        int32_t* er = oz_er_v;
+        if (!er) {  // 4M V products: a separate pass
+          void* erb;
+          CKS(ws(ctx, "oz_exp_r", static_cast<size_t>(ng) * 4, &erb));
+          er = static_cast<int32_t*>(erb);
+          CK(hsb::launch_ozaki_init_exp(er, ng, st));
+          CK(hsb::launch_ozaki_colexp(Z, K, K, ng, er, st));
+          CK(hsb::launch_ozaki_colexp(R, K, K, ng, er, st));
+          launches += 3;
+        }
         oz_use_left(h, er);
       }
       CKS(run_zrk(ctx, st, h, &launches));

@@ -451,14 +451,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
         const uint32_t d = tmem + acc * kOzBN;
         uint32_t accum = 0;
         const int slab = (w / p.ntiles / p.n_mod) % p.nslab;
+        int seg = 0;
         for (int c = p.slab_chunk0[slab]; c < p.slab_chunk0[slab + 1]; ++c) {
+          while (c >= p.seg_chunk0[seg + 1]) ++seg;
+          // a segment's last chunk: skip the MMA k steps that only see zero padding
+          const int ksteps = (c == p.seg_chunk0[seg + 1] - 1 && p.seg_ksteps_last[seg] > 0) ? p.seg_ksteps_last[seg]
+                                                                                             : kOzBK / 32;
           mbar_wait(full(stage), phase);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           if (elect_one()) {
             const uint64_t so = static_cast<uint64_t>((stage * kOzStageBytes) >> 4);
 #pragma unroll
             for (int kk = 0; kk < kOzBK / 32; ++kk) {
-              mma_i8_pair(d, da0 + so + 2 * kk, db0 + so + 2 * kk, accum | kk);
+              if (kk < ksteps) mma_i8_pair(d, da0 + so + 2 * kk, db0 + so + 2 * kk, accum | kk);
             }
             mma_commit_pair(empty(stage));
           }

@@ -82,6 +82,8 @@ struct OzGemmParams {
   // maps[prod][seg][side]: 3-D int8 maps {k, cols, modulus}, box {128, 128, 1}
   CUtensorMap map[kOzProds][kOzMaxSeg][2];
   int32_t seg_chunk0[kOzMaxSeg + 1];    // first global k chunk of each segment (+ total)
+  int32_t seg_ksteps_last[kOzMaxSeg];   // 32-byte MMA k steps of a segment's last chunk (0: all 4;
+                                        // the rest of the chunk is zero padding)
   int32_t slab_chunk0[kOzMaxSlab + 1];  // first global k chunk of each slab (+ total)
   int32_t nseg, nslab;
   int32_t n_mod;

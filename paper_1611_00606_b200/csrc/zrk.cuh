@@ -74,6 +74,8 @@ struct ZrkParams {
   const int32_t* c_rowoff;  // optional per-batch row offset (complex), overrides c_bstride
   const int2* tile_list;    // optional (triangle mode, 3M kernel): work order as (tile row,
                             // tile col), grouped for L2 reuse of the operand panels
+  int32_t* col_exp;         // optional (3M kernel, rect mode): atomicMax of the exponent of
+                            // each output column's max |Re| + |Im| (ozaki_colexp_kernel's)
   int* done_cnt;            // optional (triangle mode): per 64-column block, tiles finished
                             // writing into it; host-visible (mapped pinned memory).  A block
                             // is final when its count reaches tiles_m.

@@ -239,6 +239,7 @@ __global__ void __launch_bounds__(k3Threads, 1) zrk3m_kernel(const __grid_consta
 
     // ------------------------------------------------------------ epilogue
     double* C = p.c + 2 * (p.c_rowoff ? static_cast<int64_t>(p.c_rowoff[z]) : z * p.c_bstride);
+    double cmax[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // per column: max |Re| + |Im| of this lane's rows
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int row = tm * kBM + wm * 32 + i * 8 + g;
@@ -263,8 +264,28 @@ __global__ void __launch_bounds__(k3Threads, 1) zrk3m_kernel(const __grid_consta
           if (row == col && (zero_imag || mirror)) vi = 0.0;
           *dst = make_double2(vr, vi);
           if (mirror && row > col) reinterpret_cast<double2*>(C)[col + row * ldc] = make_double2(vr, -vi);
+          cmax[j][e] = fmax(cmax[j][e], fabs(vr) + fabs(vi));
         }
       }
+    }
+    if (p.col_exp) {
+      // the 8 lanes of a column (g = 0..7) hold its 32 rows of this warp: reduce
+      // over g, then one atomicMax of the frexp exponent per column and warp
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          double m = cmax[j][e];
+          m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 4));
+          m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 8));
+          m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 16));
+          const int col = tn * kBN + wn * 16 + j * 8 + 2 * t + e;
+          if (g == 0 && col < p.n) {
+            int ex = 0;
+            frexp(m, &ex);
+            atomicMax(p.col_exp + col, ex);
+          }
+        }
     }
     if (p.done_cnt) {
       // all consumer stores of this tile precede the count (named barrier over
