@@ -658,6 +658,10 @@ __device__ __forceinline__ double2 crt_finish(const OzCrtParams& p, const int (&
 // n0 + ncols - 1 - y), whose row counts add up to about the same for every y,
 // so no block of the rectangular grid falls entirely above the diagonal.
 constexpr int kOzCrtRows = 4;
+#ifndef HSB_CRT_UNROLL
+#define HSB_CRT_UNROLL 1
+#endif
+constexpr int kOzCrtUnroll = HSB_CRT_UNROLL;  // rows unrolled per step (A/B builds)
 template <int NM>
 __global__ void __launch_bounds__(128) ozaki_crt_kernel(const OzCrtParams p, int ncols) {
   const int na = p.n0 + static_cast<int>(blockIdx.y), nb = p.n0 + ncols - 1 - static_cast<int>(blockIdx.y);
@@ -684,7 +688,7 @@ __global__ void __launch_bounds__(128) ozaki_crt_kernel(const OzCrtParams p, int
     w2[i] = __ldg(reinterpret_cast<const uint32_t*>(r0 + p.prod_stride + i * p.mod_stride));
   }
   double2* C = reinterpret_cast<double2*>(p.c);
-#pragma unroll 1
+#pragma unroll kOzCrtUnroll
   for (int e = 0; e < kOzCrtRows; ++e) {
     const int m = m0 + e;
     if (m < n || m >= p.n) continue;
