@@ -275,7 +275,7 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
       }
     Src q{v.base, v.k, v.ld, nullptr, (v.k + 15) / 16 * 16, side, v.rscale};
     for (const ZrkCall::OzPre& pz : z.oz_pre)
-      if (pz.base == v.base && pz.side == side && !v.rscale) q.planes = pz.planes;
+      if (pz.base == v.base && pz.side == side && pz.rscale == v.rscale) q.planes = pz.planes;
     if (!q.planes) {
       const std::string name = "oz_res" + std::to_string(computed++);
       void* buf;

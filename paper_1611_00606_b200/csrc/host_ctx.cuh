@@ -217,6 +217,7 @@ struct ZrkCall {
     const double* base;
     int side;
     int8_t* planes;
+    const double* rscale = nullptr;  // the operand's row factors (OperandView::rscale)
   };
   std::vector<OzPre> oz_pre;
   // with oz_el: the reduction length the prepared planes were sized for

@@ -706,7 +706,9 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   CK(cudaEventCreateWithFlags(&ev_info, cudaEventDisableTiming));
   struct EvDel {
     cudaEvent_t e;
-    ~EvDel() { cudaEventDestroy(e); }
+    ~EvDel() {
+      if (e) cudaEventDestroy(e);
+    }
   } ev_info_del{ev_info};
   CK(cudaEventRecord(ev_info, st));
   CK(tl.mark(st, "loop2"));
@@ -805,19 +807,30 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   // The planes are sized for the 2K reduction (oz_ktot) of both calls.
   int32_t* oz_el = nullptr;
   int8_t* oz_res_a = nullptr;
-  auto oz_left = [&]() -> hsb_status {  // A and B resident
-    if (!oz_share) return HSB_OK;
+  int8_t* oz_res_ub = nullptr;  // S's UB planes, when prepared ahead (oz_left(with_ub))
+  auto oz_left = [&](cudaStream_t s_, bool with_ub) -> hsb_status {  // A and B resident
+    if (!oz_share || oz_el) return HSB_OK;
     int n_mod = 0, bits = 0;
     CKS(oz_choose(ctx, 2 * K, &n_mod, &bits));
     const int64_t kpad = (K + 15) / 16 * 16;
+    const size_t pbytes = static_cast<size_t>(hsb::kOzPlanes) * n_mod * ng * kpad;
     void *eb, *rb;
     CKS(ws(ctx, "oz_exp_l", static_cast<size_t>(ng) * 4, &eb));
-    CKS(ws(ctx, "oz_res_a", static_cast<size_t>(hsb::kOzPlanes) * n_mod * ng * kpad, &rb));
+    CKS(ws(ctx, "oz_res_a", pbytes, &rb));
     oz_el = static_cast<int32_t*>(eb);
     oz_res_a = static_cast<int8_t*>(rb);
-    CK(hsb::launch_ozaki_colexp_ab(A, B, K, K, ng, U, oz_el, st));
-    CK(hsb::launch_ozaki_residues(A, K, K, ng, oz_el, bits, n_mod, oz_res_a, kpad, st));
+    CK(hsb::launch_ozaki_colexp_ab(A, B, K, K, ng, U, oz_el, s_));
+    CK(hsb::launch_ozaki_residues(A, K, K, ng, oz_el, bits, n_mod, oz_res_a, kpad, s_));
     launches += 2;
+    if (with_ub) {
+      // the buffer H's contraction uses for its third operand (V2) afterwards,
+      // in stream order behind S: no extra workspace
+      void* ubb;
+      CKS(ws(ctx, "oz_res2", pbytes, &ubb));
+      oz_res_ub = static_cast<int8_t*>(ubb);
+      CK(hsb::launch_ozaki_residues(B, K, K, ng, oz_el, bits, n_mod, oz_res_ub, kpad, s_, U));
+      ++launches;
+    }
     return HSB_OK;
   };
   auto oz_use_left = [&](ZrkCall& z, const int32_t* er) {
@@ -825,6 +838,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     z.oz_el = oz_el;
     z.oz_er = er ? er : oz_el;
     z.oz_pre.push_back({A, 0, oz_res_a});
+    if (oz_res_ub && !er) z.oz_pre.push_back({B, 0, oz_res_ub, U});  // S only
     z.oz_ktot = 2 * K;
   };
 
@@ -853,7 +867,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     s1.segs.push_back({plain(A, K, ng, K), plain(A, K, ng, K)});
     s1.tl = &tl, s1.sect = "s1", s1.core = "s1_core";
     if (chunk_s) s1.chunk_events = &s_chunks;
-    CKS(oz_left());
+    CKS(oz_left(st, false));
     oz_use_left(s1, nullptr);
     CKS(run_zrk(ctx, st, s1, &launches));
     CK(tl.mark(st, "s1"));
@@ -877,7 +891,27 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     ++launches;
     CK(tl.mark(st, "s2"));
   } else {
+    // INT8 engine: S's operand preparation (exponents, A and UB residues) does
+    // not depend on the V products; it runs on the copy stream, overlapping the
+    // DMMA V products (they leave registers and shared memory for it on every SM)
+    static const bool no_side = std::getenv("HSB_NO_SIDE_PREP") != nullptr;  // A/B experiments
+    const bool side_prep = oz_share && u_fused && !int8_v && !no_side;
+    cudaEvent_t ev_prep_in = nullptr, ev_prep_out = nullptr;
+    if (side_prep) {
+      CK(cudaEventCreateWithFlags(&ev_prep_in, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ev_prep_out, cudaEventDisableTiming));
+    }
+    EvDel ev_prep_in_del{ev_prep_in}, ev_prep_out_del{ev_prep_out};
+    if (side_prep) {
+      CK(cudaEventRecord(ev_prep_in, st));
+      CK(cudaStreamWaitEvent(cs, ev_prep_in, 0));
+    }
     CKS(vloop());
+    if (side_prep) {
+      CKS(oz_left(cs, true));
+      CK(cudaEventRecord(ev_prep_out, cs));
+      CK(cudaStreamWaitEvent(st, ev_prep_out, 0));
+    }
     CKS(unorm());
     ZrkCall s = tri_call(S, ldo, ng, kLowerOnly | kMirror, 0.0);
     s.segs.push_back({plain(A, K, ng, K), plain(A, K, ng, K)});
@@ -885,7 +919,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     s.tl = &tl, s.sect = "s", s.core = "s_core";
     if (chunk_s) s.chunk_events = &s_chunks;
     s.peer = peer;
-    CKS(oz_left());
+    CKS(oz_left(st, false));
     oz_use_left(s, nullptr);
     CKS(run_zrk(ctx, st, s, &launches));
     CK(tl.mark(st, "s"));
