@@ -71,17 +71,33 @@ HSB_API hsb_status hsb_ctx_trim(hsb_ctx* ctx);
 HSB_API hsb_status hsb_ctx_set_complex_mult(hsb_ctx* ctx, int32_t algo);
 
 /* Engine of the lower-triangle contractions (S, H, herk, her2k, gemmt).
- * HSB_ENGINE_DMMA (default): FP64 DMMA tensor cores (complex form above).
+ * HSB_ENGINE_AUTO (default): hsb_build_hs runs the INT8 engine at FP64 width
+ *   (below); the kernel-level calls (hsb_zherk / hsb_zher2k / hsb_zgemm) run
+ *   FP64 DMMA, whose rounding is elementwise like the reference kernels'.
+ * HSB_ENGINE_DMMA: FP64 DMMA tensor cores (complex form above), ~1e-15.
  * HSB_ENGINE_INT8: FP64-accurate emulation on the INT8 tensor cores
  *   (tcgen05.mma kind::i8) by the Chinese-remainder / Ozaki-II scheme:
- *   operands rounded to min_bits-bit integers per column (relative error
- *   ~2^-min_bits of each column's max), then exact modular INT8 products and
- *   CRT reconstruction.  min_bits = 0 selects the default 39 (~3e-12 relative
- *   Frobenius; the north star's bound is 1e-10).  Batched per-atom products
- *   (Loop 1 / Loop 2) and rectangular GEMMs always use DMMA. */
+ *   operands rounded to b-bit integers per column, b >= min_bits (the
+ *   fewest moduli that allow it, up to 20), then exact modular INT8 products
+ *   and CRT reconstruction.  min_bits = 0 selects the default 53: every
+ *   operand keeps a full FP64 mantissa relative to its column's max (the
+ *   largest entries are exact), ~1e-16 relative Frobenius on S and H -- the
+ *   DMMA engine's level.  min_bits in [30, 55]; fewer bits trade accuracy
+ *   (~2^-min_bits of each column's max) for moduli.  Batched per-atom
+ *   products (Loop 1 / Loop 2) and rectangular GEMMs always use DMMA.
+ * Settings are per context; every entry point holds the context's lock, so
+ * calls on one context serialise (use one context per thread to overlap). */
 #define HSB_ENGINE_DMMA 0
 #define HSB_ENGINE_INT8 1
+#define HSB_ENGINE_AUTO 2
 HSB_API hsb_status hsb_ctx_set_engine(hsb_ctx* ctx, int32_t engine, int32_t min_bits);
+
+/* Diagnostic: the INT8 engine's reconstruction table for n_mod moduli
+ * (11..20), as the device uses it -- weights[(part * n_mod + i) * 2 + limb]
+ * (part 0: Re, 1: Im; two 40-bit fixed-point limbs of u_i / p_i) and fl(M).
+ * Host-only (no device call); lets CPU tests check the table against the
+ * Python restatement (engine.crt_weights). */
+HSB_API hsb_status hsb_oz_crt_table(int32_t n_mod, double* weights, double* m);
 
 /* ------------------------------------------------------------------------ */
 /* Kernel level: the five large updates.  Device pointers, caller's stream.  */

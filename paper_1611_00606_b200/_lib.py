@@ -7,6 +7,7 @@ the import of anything that needs it raises ``RuntimeError``.  Build it with
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 import threading
@@ -32,7 +33,9 @@ HSB_CPLX_3M = 1
 COMPLEX_MULT = {"4m": HSB_CPLX_4M, "3m": HSB_CPLX_3M}
 HSB_ENGINE_DMMA = 0
 HSB_ENGINE_INT8 = 1
-ENGINES = {"dmma": HSB_ENGINE_DMMA, "int8": HSB_ENGINE_INT8}
+HSB_ENGINE_AUTO = 2
+ENGINES = {"dmma": HSB_ENGINE_DMMA, "int8": HSB_ENGINE_INT8, "auto": HSB_ENGINE_AUTO}
+ABI_VERSION = 7
 
 _P = ctypes.c_void_p
 _DPP = ctypes.POINTER(ctypes.c_void_p)
@@ -79,6 +82,7 @@ class HsbPhys(ctypes.Structure):
 _lib = None
 _lock = threading.Lock()
 _ctxs: dict[tuple[int, int], ctypes.c_void_p] = {}
+_ctx_locks: dict[tuple[int, int], threading.Lock] = {}
 
 
 def load():
@@ -104,6 +108,7 @@ def load():
             "hsb_ctx_trim": (i32, [_P]),
             "hsb_ctx_set_complex_mult": (i32, [_P, i32]),
             "hsb_ctx_set_engine": (i32, [_P, i32, i32]),
+            "hsb_oz_crt_table": (i32, [i32, _P, _P]),
             "hsb_ipc_handle": (i32, [_P, _P, ctypes.c_char_p]),
             "hsb_ipc_open": (i32, [_P, ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]),
             "hsb_ipc_close": (i32, [_P, _P]),
@@ -120,7 +125,7 @@ def load():
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.hsb_abi_version() != 6:
+        if lib.hsb_abi_version() != ABI_VERSION:
             raise RuntimeError("libhsb200.so ABI version mismatch; rebuild it")
         _lib = lib
         return lib
@@ -151,8 +156,10 @@ def context(device: int = 0, complex_mult: str | None = None, engine: str | None
 
     ``complex_mult`` ("3m" | "4m") selects the real-product form of the
     complex contractions for the calls that follow (hsb_ctx_set_complex_mult);
-    ``engine`` ("dmma" | "int8") the engine of the triangle contractions
-    (hsb_ctx_set_engine; ``int8_bits`` 0 = default 39).
+    ``engine`` ("auto" | "dmma" | "int8") the engine of the triangle
+    contractions (hsb_ctx_set_engine; ``int8_bits`` 0 = default 53).  Settings
+    are sticky per context: callers that change them use ``using`` so no other
+    thread's call runs between the settings and the call.
     """
     lib = load()
     if complex_mult is not None and complex_mult not in COMPLEX_MULT:
@@ -166,11 +173,24 @@ def context(device: int = 0, complex_mult: str | None = None, engine: str | None
             check(lib.hsb_ctx_create(device, ctypes.byref(out)), None)
             ctx = out
             _ctxs[(device, slot)] = ctx
+            _ctx_locks[(device, slot)] = threading.Lock()
         if complex_mult is not None:
             check(lib.hsb_ctx_set_complex_mult(ctx, COMPLEX_MULT[complex_mult]), ctx)
         if engine is not None:
             check(lib.hsb_ctx_set_engine(ctx, ENGINES[engine], int(int8_bits)), ctx)
         return ctx
+
+
+@contextlib.contextmanager
+def using(device: int = 0, complex_mult: str | None = None, engine: str | None = None, int8_bits: int = 0,
+          slot: int = 0):
+    """``context(...)`` held for the duration of a ``with`` block: the settings
+    and the calls inside apply together even when other threads use the same
+    context with other settings (ctypes releases the GIL during the calls; the
+    library serialises the calls themselves per context)."""
+    context(device, slot=slot)  # create it and its lock
+    with _ctx_locks[(device, slot)]:
+        yield context(device, complex_mult, engine, int8_bits, slot)
 
 
 def release_all() -> None:

@@ -3,9 +3,35 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+#include <mutex>
+
 #include "zrk.cuh"
 
 namespace hsb {
+
+// Per-device one-time setup (constant uploads, kernel attributes): both are
+// per device, so a process driving several GPUs must run it on each.
+struct PerDeviceOnce {
+  static constexpr int kMaxDev = 64;
+  std::mutex mu;
+  std::atomic<bool> done[kMaxDev] = {};
+  cudaError_t status[kMaxDev] = {};
+};
+template <class F>
+cudaError_t per_device_once(PerDeviceOnce& o, F&& fn) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= PerDeviceOnce::kMaxDev) return cudaErrorInvalidDevice;
+  if (o.done[dev].load(std::memory_order_acquire)) return o.status[dev];
+  std::lock_guard<std::mutex> g(o.mu);
+  if (!o.done[dev].load(std::memory_order_relaxed)) {
+    o.status[dev] = fn();
+    o.done[dev].store(true, std::memory_order_release);
+  }
+  return o.status[dev];
+}
 
 constexpr size_t kPotrfSmemMax = 200 * 1024;  // packed lower triangle up to n = 158
 

@@ -191,17 +191,19 @@ hsb_status oz_tiles(hsb_ctx* ctx, int64_t n, cudaStream_t st, const int2** out, 
 
 // moduli: the fewest with b >= oz_min_bits.  With |x'| + |y'| <= 2^b per
 // element, |Re C'| = |sum x'x' + y'y'| and |Im C'| = |sum x'_L y'_R - y'_L x'_R|
-// are both <= K 2^2b; the explicit CRT needs |X| < M/2, kept with one bit of
-// margin: 2b <= log2 M - 2 - log2 K.
+// are both <= K 2^2b; the CRT needs |X| < M/2, kept with one bit of margin:
+// 2b <= log2 M - 2 - log2 K.  b may exceed the request (more bits for the
+// entries below their column's max, at no cost) up to kOzMaxBits, the range
+// the residue kernel's magic-constant quotients are exact for.
 hsb_status oz_choose(hsb_ctx* ctx, int64_t ktot, int* n_mod_out, int* b_out) {
   int n_mod = 0, b = 0;
   double log2m = 0;
   for (int i = 0; i < kOzMaxMod; ++i) {
     log2m += std::log2(static_cast<double>(oz_mod(i)));
     const int bi = static_cast<int>(std::floor((log2m - 2.0 - std::log2(static_cast<double>(std::max<int64_t>(ktot, 1)))) / 2.0));
-    if (i + 1 >= 11 && (bi >= ctx->oz_min_bits || i + 1 == kOzMaxMod)) {
+    if (i + 1 >= kOzMinMod && (bi >= ctx->oz_min_bits || i + 1 == kOzMaxMod)) {
       n_mod = i + 1;
-      b = std::min(bi, ctx->oz_min_bits + 4);
+      b = std::min(bi, kOzMaxBits);
       break;
     }
   }

@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -47,12 +48,29 @@ struct hsb_ctx {
   cudaStream_t copy_stream = nullptr;  // overlaps S download with the H contraction
   int64_t tile_list_T = 0;             // tile rows of the cached grouped triangle order
   std::vector<int2> tile_list_host;    // its host copy (source of an async upload)
-  int32_t engine = HSB_ENGINE_DMMA;    // triangle contractions: FP64 DMMA or INT8 CRT emulation
-  int32_t oz_min_bits = 39;            // INT8 engine: operand integer bits (accuracy ~2^-bits)
+  int32_t engine_setting = HSB_ENGINE_AUTO;  // hsb_ctx_set_engine
+  int32_t engine = HSB_ENGINE_DMMA;    // resolved per call (CtxCall): FP64 DMMA or INT8 CRT emulation
+  std::mutex call_mu;                  // one entry point at a time per context (workspace, streams, settings)
+  int32_t oz_min_bits = kOzDefaultBits; // INT8 engine: operand integer bits (accuracy ~2^-bits)
   int64_t oz_tiles_n = 0;              // cached INT8-engine tile list (n of the output)
   std::vector<int2> oz_tiles_host;
   std::vector<int32_t> oz_tile_index_host;
   int32_t cplx = HSB_CPLX_3M;          // complex product form of the zrk kernels
+};
+
+// Entry-point guard: serialises calls on one context (its workspace map, copy
+// stream and staging are not thread-safe; the reference build is externally
+// single-entrant, but its kernels are reentrant) and resolves
+// HSB_ENGINE_AUTO: the pipeline (hsb_build_hs) runs the INT8 engine at FP64
+// width, the kernel-level BLAS calls run FP64 DMMA (elementwise semantics for
+// arbitrary operands).
+struct CtxCall {
+  std::lock_guard<std::mutex> lock;
+  CtxCall(hsb_ctx* ctx, bool pipeline) : lock(ctx->call_mu) {
+    ctx->engine = ctx->engine_setting != HSB_ENGINE_AUTO ? ctx->engine_setting
+                  : pipeline                              ? HSB_ENGINE_INT8
+                                                          : HSB_ENGINE_DMMA;
+  }
 };
 
 inline thread_local std::string g_create_err;  // errors of hsb_ctx_create (no context yet)

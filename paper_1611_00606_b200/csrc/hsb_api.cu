@@ -33,7 +33,7 @@ using namespace hsb_host;
 // =============================================================================
 extern "C" {
 
-int32_t hsb_abi_version(void) { return 6; }
+int32_t hsb_abi_version(void) { return 7; }
 
 hsb_status hsb_ctx_create(int32_t device, hsb_ctx** out) {
   hsb_ctx* ctx = nullptr;
@@ -83,17 +83,26 @@ const char* hsb_last_error(const hsb_ctx* ctx) { return ctx ? ctx->err.c_str() :
 hsb_status hsb_ctx_set_complex_mult(hsb_ctx* ctx, int32_t algo) {
   if (!ctx) return fail(nullptr, HSB_ERR_INPUT, "ctx is NULL");
   if (algo != HSB_CPLX_4M && algo != HSB_CPLX_3M) return fail(ctx, HSB_ERR_INPUT, "unknown complex product form");
+  std::lock_guard<std::mutex> g(ctx->call_mu);
   ctx->cplx = algo;
   return HSB_OK;
 }
 
 hsb_status hsb_ctx_set_engine(hsb_ctx* ctx, int32_t engine, int32_t min_bits) {
   if (!ctx) return fail(nullptr, HSB_ERR_INPUT, "ctx is NULL");
-  if (engine != HSB_ENGINE_DMMA && engine != HSB_ENGINE_INT8) return fail(ctx, HSB_ERR_INPUT, "unknown engine");
-  if (min_bits != 0 && (min_bits < 30 || min_bits > 48))
-    return fail(ctx, HSB_ERR_INPUT, "min_bits must be 0 (default 40) or in [30, 48]");
-  ctx->engine = engine;
-  ctx->oz_min_bits = min_bits ? min_bits : 39;
+  if (engine != HSB_ENGINE_DMMA && engine != HSB_ENGINE_INT8 && engine != HSB_ENGINE_AUTO)
+    return fail(ctx, HSB_ERR_INPUT, "unknown engine");
+  if (min_bits != 0 && (min_bits < 30 || min_bits > kOzMaxBits))
+    return fail(ctx, HSB_ERR_INPUT, "min_bits must be 0 (default 53, a full FP64 mantissa) or in [30, 55]");
+  std::lock_guard<std::mutex> g(ctx->call_mu);
+  ctx->engine_setting = engine;
+  ctx->oz_min_bits = min_bits ? min_bits : kOzDefaultBits;
+  return HSB_OK;
+}
+
+hsb_status hsb_oz_crt_table(int32_t n_mod, double* weights, double* m) {
+  if (!weights || !m) return fail(nullptr, HSB_ERR_INPUT, "NULL output");
+  if (oz_crt_table_host(n_mod, weights, m) != 0) return fail(nullptr, HSB_ERR_INPUT, "n_mod out of range");
   return HSB_OK;
 }
 
@@ -125,6 +134,7 @@ hsb_status hsb_ipc_close(hsb_ctx* ctx, void* dev_ptr) {
 
 hsb_status hsb_ctx_trim(hsb_ctx* ctx) {
   if (!ctx) return fail(nullptr, HSB_ERR_INPUT, "ctx is NULL");
+  CtxCall call_guard(ctx, false);
   cudaSetDevice(ctx->device);
   CK(cudaDeviceSynchronize());
   for (auto& kv : ctx->bufs)
@@ -139,6 +149,7 @@ hsb_status hsb_ctx_trim(hsb_ctx* ctx) {
 hsb_status hsb_zherk(hsb_ctx* ctx, void* stream, int64_t n, int64_t k, double alpha, const double* a, int64_t lda,
                      double beta, double* c, int64_t ldc, uint32_t flags) {
   if (!ctx) return fail(nullptr, HSB_ERR_INPUT, "ctx is NULL");
+  CtxCall call_guard(ctx, false);
   if (n < 0 || k < 0) return fail(ctx, HSB_ERR_DIMENSION, "negative dimension");
   if (n == 0) return HSB_OK;
   if (ldc < n || (k > 0 && lda < k)) return fail(ctx, HSB_ERR_DIMENSION, "leading dimension too small");
@@ -160,6 +171,7 @@ hsb_status hsb_zher2k(hsb_ctx* ctx, void* stream, int64_t n, int64_t k, double a
                       const double* zp, int64_t ldz, const double* b, int64_t ldb, double beta, double* c,
                       int64_t ldc, uint32_t flags) {
   if (!ctx) return fail(nullptr, HSB_ERR_INPUT, "ctx is NULL");
+  CtxCall call_guard(ctx, false);
   if (n < 0 || k < 0) return fail(ctx, HSB_ERR_DIMENSION, "negative dimension");
   if (n == 0) return HSB_OK;
   if (ldc < n || (k > 0 && (ldz < k || ldb < k))) return fail(ctx, HSB_ERR_DIMENSION, "leading dimension too small");
@@ -208,6 +220,7 @@ hsb_status hsb_zgemm(hsb_ctx* ctx, void* stream, char opa, char opb, int64_t m, 
                      double alpha_re, double alpha_im, const double* a, int64_t lda, const double* b, int64_t ldb,
                      double beta_re, double beta_im, double* c, int64_t ldc, uint32_t flags) {
   if (!ctx) return fail(nullptr, HSB_ERR_INPUT, "ctx is NULL");
+  CtxCall call_guard(ctx, false);
   auto valid_op = [](char o) { return o == 'N' || o == 'T' || o == 'C'; };
   if (!valid_op(opa) || !valid_op(opb)) return fail(ctx, HSB_ERR_INPUT, "op must be one of N, T, C");
   if (m < 0 || n < 0 || k < 0) return fail(ctx, HSB_ERR_DIMENSION, "negative dimension");
@@ -267,6 +280,7 @@ hsb_status hsb_zgemm(hsb_ctx* ctx, void* stream, char opa, char opb, int64_t m, 
 
 hsb_status hsb_hermitian_mirror(hsb_ctx* ctx, void* stream, int64_t n, double* c, int64_t ldc) {
   if (!ctx) return fail(nullptr, HSB_ERR_INPUT, "ctx is NULL");
+  CtxCall call_guard(ctx, false);
   if (n < 0 || ldc < n) return fail(ctx, HSB_ERR_DIMENSION, "bad mirror dimensions");
   if (n == 0) return HSB_OK;
   cudaSetDevice(ctx->device);
@@ -465,6 +479,7 @@ static hsb_status validate_small_inputs(hsb_ctx* ctx, const hsb_problem* p) {
 hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32_t opts, const hsb_output* out,
                         hsb_timings* tm, int32_t* atom_info) {
   if (!ctx) return fail(nullptr, HSB_ERR_INPUT, "ctx is NULL");
+  CtxCall call_guard(ctx, true);
   if (!p || !out) return fail(ctx, HSB_ERR_INPUT, "problem/output is NULL");
   const int64_t na = p->n_atoms, nl = p->n_l, ng = p->n_g;
   if (na < 1 || nl < 1 || ng < 1) return fail(ctx, HSB_ERR_INPUT, "dimensions must be positive");
@@ -1178,6 +1193,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
 hsb_status hsb_match_coeffs(hsb_ctx* ctx, void* stream, const hsb_phys* ph, double* a_stack, double* b_stack,
                             int64_t ld) {
   if (!ctx) return fail(nullptr, HSB_ERR_INPUT, "ctx is NULL");
+  CtxCall call_guard(ctx, false);
   if (!ph || !a_stack || !b_stack) return fail(ctx, HSB_ERR_INPUT, "NULL argument");
   if (ph->n_atoms < 1 || ph->n_g < 1 || ph->n_types < 1 || ph->lmax < 0)
     return fail(ctx, HSB_ERR_INPUT, "dimensions must be positive");

@@ -14,8 +14,8 @@
 
 namespace hsb {
 
-__constant__ int32_t oz_mod_rt[kOzMaxMod] = {241, 233, 229, 221, 205, 197, 193, 181,
-                                             173, 157, 149, 137, 113, 109, 101, 97};
+__constant__ int32_t oz_mod_rt[kOzMaxMod] = {241, 233, 229, 221, 205, 197, 193, 181, 173, 157,
+                                             149, 137, 113, 109, 101, 97,  89,  73,  61,  53};
 
 // ------------------------------------------------------------ small helpers
 __device__ __forceinline__ int sym_lo(int p) { return -(p >> 1); }
@@ -113,26 +113,28 @@ __global__ void ozaki_colexp_ab_kernel(const double2* __restrict__ a, const doub
 // ------------------------------------------------------------ 2. residues
 // 1 / p, correctly rounded (compile-time division)
 __constant__ double oz_inv_rt[kOzMaxMod] = {
-    1.0 / 241, 1.0 / 233, 1.0 / 229, 1.0 / 221, 1.0 / 205, 1.0 / 197, 1.0 / 193, 1.0 / 181,
-    1.0 / 173, 1.0 / 157, 1.0 / 149, 1.0 / 137, 1.0 / 113, 1.0 / 109, 1.0 / 101, 1.0 / 97};
+    1.0 / 241, 1.0 / 233, 1.0 / 229, 1.0 / 221, 1.0 / 205, 1.0 / 197, 1.0 / 193, 1.0 / 181, 1.0 / 173, 1.0 / 157,
+    1.0 / 149, 1.0 / 137, 1.0 / 113, 1.0 / 109, 1.0 / 101, 1.0 / 97,  1.0 / 89,  1.0 / 73,  1.0 / 61,  1.0 / 53};
 
 // 2^e for |e| <= 1022 from the exponent bits
 __device__ __forceinline__ double pow2i(int e) { return __longlong_as_double(static_cast<long long>(e + 1023) << 52); }
 
-// residue of an exactly-integer double |v| < 2^46 modulo p, as the low word of
-// r + 1.5 * 2^52 with r = v - p * rn(v / p): q = rn(v * fl(1/p)) through the
-// magic constant (the product's error, |v| 2^-61, is far below the 2^-9
-// distance of v / p from a half-integer for odd p), r = v - p q exactly,
-// in [-(p-1)/2, (p-1)/2].  No FRND, no division.
+// residue of an exactly-integer double |v| <= 2^55 modulo p, as the low word of
+// r + 1.5 * 2^52 with r = v - p * q, q = rn(v * fl(1/p)) through the magic
+// constant: r = v - p q is exact (fma), and since the product's error
+// (|v| 2^-53 / p <= 2^2 / p) may exceed the 1/(2p) distance of v / p from a
+// half-integer once |v| > 2^46, r lies in [-(3p-1)/2, (3p-1)/2] rather than the
+// symmetric range: the callers only combine it into |rr + j ri| < 2^16 and
+// reduce that again with sym_mod_small.  No FRND, no division.
 __device__ __forceinline__ int sym_mod_magic(double v, double p, double inv_p) {
   constexpr double M = 6755399441055744.0;  // 1.5 * 2^52
   const double q = fma(v, inv_p, M) - M;
   return static_cast<int>(__double2loint(fma(-p, q, v) + M));
 }
 
-// symmetric residue of a small integer |v| < 2^14 modulo an odd p: v / p is
-// never within 1/(2p) of a half-integer, and the float quotient's error is
-// below |v / p| 2^-23 < 2^-15
+// symmetric residue of a small integer |v| < 2^16 modulo an odd p: v / p is
+// never within 1/(2p) >= 2^-9 of a half-integer, and the float quotient's
+// error is below |v / p| 2^-23 < 2^-16
 __device__ __forceinline__ int sym_mod_small(int v, int p, float inv_p) {
   return v - p * __float2int_rn(__int2float_rn(v) * inv_p);
 }
@@ -181,7 +183,7 @@ __global__ void __launch_bounds__(128, 6) ozaki_residue_kernel(const double2* __
 #pragma unroll
       for (int j = 0; j < kOzResK; ++j) {
         const int rr = sym_mod_magic(xr[j], p, inv);
-        const int t = jm * sym_mod_magic(xi[j], p, inv);  // |t| <= 107 * 120
+        const int t = jm * sym_mod_magic(xi[j], p, inv);  // |t| <= 120 * 361
         u[j] = sym_mod_small(rr + t, oz_mod(i), invf);
         w[j] = sym_mod_small(rr - t, oz_mod(i), invf);
       }
@@ -568,77 +570,70 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
 }
 
 // ------------------------------------------------------------ 4. CRT
-// Explicit CRT in exact double limbs.  With M = prod p_i and residues
-// X = c_i r_i (mod p_i) for representatives r_i (|r_i| <= p_i - 1) and unit
-// constants c_i (1/2 for Re = (phi1 + phi2)/2, 1/(2 j_i) for
-// Im = (phi1 - phi2)/(2 j_i)), the weights y_i = (M/p_i) * ((c_i (M/p_i)^-1) mod p_i) give
-//     X = sum_i r_i y_i - k M,   k = rint(sum_i r_i (y_i / M)),
-// exact for |X| < M/4 (the host's choice of b keeps |X| <= M/4).
-// y_i and M are split into NL limbs of LB bits (3 x 33 for n_mod <= 13,
-// M < 2^99; 4 x 30 otherwise); every limb sum S_j = sum_i r_i y_ij (< 2^46)
-// and T_j = S_j - k M_j is an exact double, so X = sum_j T_j 2^(j LB) is
-// rounded once, at the end.  k only needs |error| < 1/4 (X/M is within 1/4 of
-// an integer): the quotient sum runs in int32 with 19-bit weights.
+// Explicit CRT as a fraction.  With M = prod p_i and residues X = c_i r_i
+// (mod p_i) for representatives |r_i| <= p_i - 1 and unit constants c_i (1/2
+// for Re = (phi1 + phi2)/2, 1/(2 j_i) for Im = (phi1 - phi2)/(2 j_i)),
+//     X / M = sum_i r_i u_i / p_i  (mod 1),   u_i = c_i (M/p_i)^-1 mod p_i,
+// and |X| <= M/4 (the host's choice of b), so X / M is the representative of
+// that sum in [-1/4, 1/4].  Each weight u_i / p_i is held as two 40-bit
+// fixed-point limbs w_i1 = c_i1 2^-40, w_i2 = c_i2 2^-80 (rounded at 2^-80):
+//     s1 = sum_i r_i w_i1   exact (every term a multiple of 2^-40, |s1| 2^40 <
+//                           20 * 240 * 2^40 < 2^53),
+//     s2 = sum_i r_i w_i2   (|s2| < 2^-27, rounded at 2^-106),
+//     f  = (s1 - rn(s1)) + s2,   X = f * M.
+// s1 - rn(s1) is exact, rn(s1) is the right integer because X / M is within
+// 1/4 + 2^-27 of it, and the truncated weights err by < 20 * 240 * 2^-80: f
+// carries X / M to ~2^-53 relative, so X = f * fl(M) is within ~2 ulp.  The
+// limb count does not grow with n_mod (the former integer-limb form needed
+// 4 limbs above 13 moduli) and no quotient sum is needed.
 struct OzCrtConst {
-  double y[2][kOzMaxMod][4];   // [Re, Im] limbs of y_i, least significant first
-  int32_t f[2][kOzMaxMod];     // rn(2^19 y_i / M): the quotient sum in int32
-  double m[4];                 // limbs of M
+  double w[2][kOzMaxMod][2];  // [Re, Im][modulus] fixed-point limbs of u_i / p_i
+  double m;                   // fl(M)
 };
-constexpr int kOzMinMod = 11;
-__constant__ OzCrtConst c_oz_crt[kOzMaxMod - kOzMinMod + 1];  // one table per n_mod = 11 .. 16
-__host__ __device__ constexpr int oz_crt_limbs(int nm) { return nm <= 13 ? 3 : 4; }
-__host__ __device__ constexpr int oz_crt_limb_bits(int nm) { return nm <= 13 ? 33 : 30; }
+__constant__ OzCrtConst c_oz_crt[kOzMaxMod - kOzMinMod + 1];  // one table per n_mod = 11 .. 20
 
-// exact int -> double / float through the mantissa (no I2F): a double with high
+// exact int -> double through the mantissa (no I2F): a double with high
 // word 0x43300000 and low word w is 2^52 + w
 __device__ __forceinline__ double i2d_exact(int v) {
   return __hiloint2double(0x43300000, static_cast<int>(static_cast<unsigned>(v) ^ 0x80000000u)) -
          4503601774854144.0;  // 2^52 + 2^31
 }
 
+// X / M for the 2 Re / 2j Im residue sums of one element (PART 0 / 1)
 template <int NM, int PART>
-__device__ __forceinline__ double crt_value(const int (&r)[NM]) {
-  constexpr int NL = oz_crt_limbs(NM);
+__device__ __forceinline__ double crt_frac(const int (&r)[NM]) {
   const OzCrtConst& C = c_oz_crt[NM - kOzMinMod];
-  int32_t fk = 0;
-  double s[NL];
-#pragma unroll
-  for (int j = 0; j < NL; ++j) s[j] = 0.0;
+  double s1 = 0.0, s2 = 0.0;
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
-    fk += r[i] * C.f[PART][i];
     const double ri = i2d_exact(r[i]);
-#pragma unroll
-    for (int j = 0; j < NL; ++j) s[j] = fma(ri, C.y[PART][i][j], s[j]);
+    s1 = fma(ri, C.w[PART][i][0], s1);
+    s2 = fma(ri, C.w[PART][i][1], s2);
   }
-  // k = rn(sum r_i y_i / M): |r_i| <= 240 and 2^19 y_i / M < 2^19 keep the sum in
-  // int32 (13 * 240 * 2^19 < 2^31); the rounded weights err by <= 13 * 240 *
-  // 2^-20 < 0.003, far inside the 1/4 margin of X / M from a half-integer
-  const double k = i2d_exact((fk + (1 << 18)) >> 19);
-  constexpr double kL = static_cast<double>(1ull << oz_crt_limb_bits(NM));
-  double x = fma(-k, C.m[NL - 1], s[NL - 1]);
-#pragma unroll
-  for (int j = NL - 2; j >= 0; --j) x = fma(x, kL, fma(-k, C.m[j], s[j]));
-  return x;
+  return (s1 - rint(s1)) + s2;
 }
 
 // 2^sh in two exact power-of-two factors (|sh| <= 2044)
 __device__ __forceinline__ double scale2(double x, int sh) { return (x * pow2i(sh / 2)) * pow2i(sh - sh / 2); }
 
-// Finish one element from its per-modulus phi1(C), phi2(C) residues (the
-// conjugation of L^H R is in the GEMM's choice of planes).
+// sign-extended byte e of w (one PRMT / SGXT)
+__device__ __forceinline__ int sbyte(uint32_t w, int e) { return static_cast<int8_t>(w >> (8 * e)); }
+
+// Finish one element from its per-modulus phi1(C), phi2(C) residues, byte e
+// of w1[i] / w2[i] (the conjugation of L^H R is in the GEMM's choice of planes).
 template <int NM>
-__device__ __forceinline__ double2 crt_finish(const OzCrtParams& p, const int (&F1)[NM], const int (&F2)[NM],
-                                              int m, int n) {
+__device__ __forceinline__ double2 crt_element(const OzCrtParams& p, const uint32_t (&w1)[NM],
+                                               const uint32_t (&w2)[NM], int e, int sh, int m, int n) {
   int re[NM], im[NM];
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
-    re[i] = F1[i] + F2[i];  // 2 Re C   (mod p_i)
-    im[i] = F1[i] - F2[i];  // 2 j Im C (mod p_i)
+    const int f1 = sbyte(w1[i], e), f2 = sbyte(w2[i], e);
+    re[i] = f1 + f2;  // 2 Re C   (mod p_i)
+    im[i] = f1 - f2;  // 2 j Im C (mod p_i)
   }
-  const int sh = p.el[m] + p.er[n] - 2 * p.b;
-  const double xr = scale2(crt_value<NM, 0>(re), sh);
-  const double xi = scale2(crt_value<NM, 1>(im), sh);
+  const double mm = c_oz_crt[NM - kOzMinMod].m;
+  const double xr = scale2(crt_frac<NM, 0>(re) * mm, sh);
+  const double xi = scale2(crt_frac<NM, 1>(im) * mm, sh);
   double vr = p.alpha_re * xr - p.alpha_im * xi;
   double vi = p.alpha_re * xi + p.alpha_im * xr;
   if (p.beta_re != 0.0 || p.beta_im != 0.0) {
@@ -650,68 +645,80 @@ __device__ __forceinline__ double2 crt_finish(const OzCrtParams& p, const int (&
   return make_double2(vr, vi);
 }
 
-// Lower-triangle elements (m >= n), 4 consecutive rows per thread (one 32-bit
-// load per modulus and product from the tile-packed residues), threads along
-// m: residue loads and the C[m, n] stores are coalesced; the mirror
-// C[n, m] = conj(C[m, n]) is a strided store (matcore.hermitian_mirror,
-// matcore.py:89-105).  Block row y handles the column pair (n0 + y,
-// n0 + ncols - 1 - y), whose row counts add up to about the same for every y,
-// so no block of the rectangular grid falls entirely above the diagonal.
-constexpr int kOzCrtRows = 4;
-#ifndef HSB_CRT_UNROLL
-#define HSB_CRT_UNROLL 1
-#endif
-constexpr int kOzCrtUnroll = HSB_CRT_UNROLL;  // rows unrolled per step (A/B builds)
+// destination of element (m, n): C, or the owner's receive slot (peer output)
+__device__ __forceinline__ double2* crt_dst(const OzCrtParams& p, int m, int n) {
+  if (p.peer) {
+    const int q = static_cast<int>(n / p.cpr);
+    return p.peer[q] + ((p.rank * p.cpr + (n - q * p.cpr)) * p.pld + m);
+  }
+  return reinterpret_cast<double2*>(p.c) + (m + static_cast<int64_t>(n) * p.ldc);
+}
+
+// Lower-triangle elements (m >= n).  A block owns 8 output columns (one per
+// warp) x 128 rows; lane l holds rows 4l .. 4l+3 of its warp's column: one
+// 32-bit load per modulus and product from the tile-packed residues (128
+// contiguous bytes per warp), and C[m, n] stored from registers (a warp's four
+// stores cover 2 KB contiguously).  The mirror C[n, m] = conj(C[m, n])
+// (matcore.hermitian_mirror, matcore.py:89-105) is transposed through shared
+// memory so that each warp store writes four full 128-byte lines (8
+// consecutive rows n of 4 columns m) instead of 16-byte strided pieces.
+// Block row y handles the column-block pair (y, ncb - 1 - y), whose row counts
+// add up to about the same for every y.
+constexpr int kCrtCols = 8;      // columns per block (= warps)
+constexpr int kCrtRows = 128;    // rows per block (= 32 lanes x 4)
 template <int NM>
-__global__ void __launch_bounds__(128) ozaki_crt_kernel(const OzCrtParams p, int ncols) {
-  const int na = p.n0 + static_cast<int>(blockIdx.y), nb = p.n0 + ncols - 1 - static_cast<int>(blockIdx.y);
-  const int gend = (p.n + kOzCrtRows - 1) / kOzCrtRows;
-  const int ga = na / kOzCrtRows, gb = nb / kOzCrtRows;
-  int g = static_cast<int>(blockIdx.x * blockDim.x + threadIdx.x), n;
-  if (g < gend - ga) {
-    n = na;
-    g += ga;
+__global__ void __launch_bounds__(256) ozaki_crt_kernel(const OzCrtParams p, int ncols) {
+  __shared__ double2 stage[kCrtCols][kCrtRows + 1];  // [n][position], +1: conflict-free transposed reads
+  const int ncb = (ncols + kCrtCols - 1) / kCrtCols;
+  const int cba = static_cast<int>(blockIdx.y), cbb = ncb - 1 - cba;
+  const int rsa = p.n0 + cba * kCrtCols, rsb = p.n0 + cbb * kCrtCols;  // first row = first column
+  const int cha = (p.n - rsa + kCrtRows - 1) / kCrtRows;
+  int chunk = static_cast<int>(blockIdx.x), rs;
+  if (chunk < cha) {
+    rs = rsa;
   } else {
-    g -= gend - ga;
-    if (nb == na || g >= gend - gb) return;
-    n = nb;
-    g += gb;
+    chunk -= cha;
+    if (cbb == cba || chunk >= (p.n - rsb + kCrtRows - 1) / kCrtRows) return;
+    rs = rsb;
   }
-  const int m0 = g * kOzCrtRows;
-  const int t = p.tile_index[(m0 >> 8) * p.T + (n >> 8)];
-  const uint8_t* r0 = reinterpret_cast<const uint8_t*>(p.res) + static_cast<int64_t>(t) * kOzTileBytes +
-                      (n & 255) * 256 + (m0 & 255);
-  uint32_t w1[NM], w2[NM];  // straight-line: all 2 x NM loads in flight together
-#pragma unroll
-  for (int i = 0; i < NM; ++i) {
-    w1[i] = __ldg(reinterpret_cast<const uint32_t*>(r0 + i * p.mod_stride));
-    w2[i] = __ldg(reinterpret_cast<const uint32_t*>(r0 + p.prod_stride + i * p.mod_stride));
-  }
-  double2* C = reinterpret_cast<double2*>(p.c);
-#pragma unroll kOzCrtUnroll
-  for (int e = 0; e < kOzCrtRows; ++e) {
-    const int m = m0 + e;
-    if (m < n || m >= p.n) continue;
-    int F1[NM], F2[NM];
+  const int nend = min(p.n0 + ncols, p.n);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = rs + warp;                     // this warp's column
+  const int r0 = rs + chunk * kCrtRows;        // first row of the block
+  const int m0 = r0 + 4 * lane;
+  const bool mirror = (p.flags & kMirror) != 0;
+  if (n < nend && m0 < p.n && m0 + 3 >= n) {
+    // rows m0 .. m0+3 lie in one 256-row tile; tile row >= tile column
+    const int t = p.tile_index[(m0 >> 8) * p.T + (n >> 8)];
+    const uint8_t* rp = reinterpret_cast<const uint8_t*>(p.res) + static_cast<int64_t>(t) * kOzTileBytes +
+                        (n & 255) * 256 + (m0 & 255);
+    uint32_t w1[NM], w2[NM];  // straight-line: all 2 x NM loads in flight together
 #pragma unroll
     for (int i = 0; i < NM; ++i) {
-      F1[i] = static_cast<int8_t>(w1[i] >> (8 * e));
-      F2[i] = static_cast<int8_t>(w2[i] >> (8 * e));
+      w1[i] = __ldg(reinterpret_cast<const uint32_t*>(rp + i * p.mod_stride));
+      w2[i] = __ldg(reinterpret_cast<const uint32_t*>(rp + p.prod_stride + i * p.mod_stride));
     }
-    const double2 v = crt_finish<NM>(p, F1, F2, m, n);
-    if (p.peer) {
-      // fused scatter: write straight into the owning rank's receive slot (NVLink
-      // peer memory); the owner only sums its slots afterwards
-      const int qn = static_cast<int>(n / p.cpr);
-      p.peer[qn][(p.rank * p.cpr + (n - qn * p.cpr)) * p.pld + m] = v;
-      if ((p.flags & kMirror) && m > n) {
-        const int qm = static_cast<int>(m / p.cpr);
-        p.peer[qm][(p.rank * p.cpr + (m - qm * p.cpr)) * p.pld + n] = make_double2(v.x, -v.y);
-      }
-      continue;
+    const int ern = __ldg(p.er + n) - 2 * p.b;
+#pragma unroll 1
+    for (int e = 0; e < 4; ++e) {
+      const int m = m0 + e;
+      if (m < n || m >= p.n) continue;
+      const double2 v = crt_element<NM>(p, w1, w2, e, __ldg(p.el + m) + ern, m, n);
+      *crt_dst(p, m, n) = v;
+      stage[warp][e * 32 + lane] = v;
     }
-    C[m + static_cast<int64_t>(n) * p.ldc] = v;
-    if ((p.flags & kMirror) && m > n) C[n + static_cast<int64_t>(m) * p.ldc] = make_double2(v.x, -v.y);
+  }
+  if (!mirror) return;
+  __syncthreads();
+  // transposed: thread (c = tid & 7, j = tid >> 3) writes C[rs + c, r0 + j + 32 q]
+  const int c = threadIdx.x & 7, nn = rs + c;
+  if (nn >= nend) return;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int jr = (threadIdx.x >> 3) + 32 * q, m = r0 + jr;  // row of the staged element
+    if (m <= nn || m >= p.n) continue;
+    const double2 v = stage[c][(jr & 3) * 32 + (jr >> 2)];
+    *crt_dst(p, nn, m) = make_double2(v.x, -v.y);
   }
 }
 
@@ -791,8 +798,9 @@ __global__ void __launch_bounds__(256) ozaki_vcrt_kernel(const OzVcrtParams p) {
         im[i] = F1[i] - F2[i];
       }
       const int sh = st + __ldg(p.el + g) - p.bsum;
-      const double xr = scale2(crt_value<NM, 0>(re), sh);
-      const double xi = scale2(crt_value<NM, 1>(im), sh);
+      const double mm = c_oz_crt[NM - kOzMinMod].m;
+      const double xr = scale2(crt_frac<NM, 0>(re) * mm, sh);
+      const double xi = scale2(crt_frac<NM, 1>(im) * mm, sh);
       dst[static_cast<int64_t>(g) * p.ldv] = make_double2(xr, xi);
       m = fabs(xr) + fabs(xi);
     }
@@ -812,23 +820,14 @@ __global__ void __launch_bounds__(256) ozaki_vcrt_kernel(const OzVcrtParams p) {
   }
 }
 
-// CRT tables for every n_mod, computed and uploaded once per process (the
-// tables are constant, so concurrent builds on several contexts never race)
+// CRT tables for every n_mod (ozaki_crt_kernel's fraction form): the weights
+// u_i / p_i as two 40-bit fixed-point limbs, rounded to nearest at 2^-80, from
+// exact integer arithmetic (u_i < 2^8, so u_i 2^80 fits 128 bits); fl(M) from
+// the exact product in 32-bit digits.
 static OzCrtConst oz_crt_table(int n_mod) {
   using u128 = unsigned __int128;
-  u128 M = 1;
-  for (int i = 0; i < n_mod; ++i) M *= static_cast<u128>(oz_mod(i));
   OzCrtConst c;
   std::memset(&c, 0, sizeof(c));
-  const int lb = oz_crt_limb_bits(n_mod), nl = oz_crt_limbs(n_mod);
-  auto limbs = [&](u128 v, double* out) {
-    const u128 mask = (static_cast<u128>(1) << lb) - 1;
-    for (int j = 0; j < 4; ++j) {
-      out[j] = j < nl ? static_cast<double>(static_cast<uint64_t>(v & mask)) : 0.0;
-      v >>= lb;
-    }
-  };
-  const double Md = static_cast<double>(M);
   auto inverse = [](int a, int p) {
     a = ((a % p) + p) % p;
     for (int x = 1; x < p; ++x)
@@ -837,31 +836,75 @@ static OzCrtConst oz_crt_table(int n_mod) {
   };
   for (int i = 0; i < n_mod; ++i) {
     const int pi = oz_mod(i);
-    const u128 Mi = M / static_cast<u128>(pi);
-    const int mi_inv = inverse(static_cast<int>(Mi % static_cast<u128>(pi)), pi);
+    int mi = 1;  // (M / p_i) mod p_i
+    for (int j = 0; j < n_mod; ++j)
+      if (j != i) mi = (mi * (oz_mod(j) % pi)) % pi;
+    const int mi_inv = inverse(mi, pi);
     // Re: c = 1/2 ; Im: c = 1/(2 j)
     const int cpart[2] = {inverse(2, pi), inverse(2 * oz_sqrtm1(i), pi)};
     for (int part = 0; part < 2; ++part) {
-      const u128 y = Mi * static_cast<u128>((cpart[part] * mi_inv) % pi);  // < M
-      limbs(y, c.y[part][i]);
-      c.f[part][i] = static_cast<int32_t>(std::llround(static_cast<double>(y) / Md * 524288.0));
+      const u128 u = static_cast<u128>((cpart[part] * mi_inv) % pi);
+      const u128 q = ((u << 80) + static_cast<u128>(pi / 2)) / static_cast<u128>(pi);  // rn(2^80 u / p)
+      const u128 mask = (static_cast<u128>(1) << 40) - 1;
+      c.w[part][i][0] = std::ldexp(static_cast<double>(static_cast<uint64_t>(q >> 40)), -40);
+      c.w[part][i][1] = std::ldexp(static_cast<double>(static_cast<uint64_t>(q & mask)), -80);
     }
   }
-  limbs(M, c.m);
+  // M in base-2^32 digits, then rounded once: the top 64 bits (exact in a u64)
+  // plus a sticky bit for the rest
+  uint32_t dg[8] = {1, 0, 0, 0, 0, 0, 0, 0};
+  for (int i = 0; i < n_mod; ++i) {
+    uint64_t carry = 0;
+    for (int j = 0; j < 8; ++j) {
+      const uint64_t v = static_cast<uint64_t>(dg[j]) * static_cast<uint64_t>(oz_mod(i)) + carry;
+      dg[j] = static_cast<uint32_t>(v);
+      carry = v >> 32;
+    }
+  }
+  // bit length, then the top 64 significant bits and a sticky bit
+  int nbits = 0;
+  for (int j = 7; j >= 0; --j)
+    if (dg[j]) {
+      nbits = 32 * j + 32 - __builtin_clz(dg[j]);
+      break;
+    }
+  auto bit = [&](int k) { return k >= 0 ? (dg[k >> 5] >> (k & 31)) & 1u : 0u; };
+  const int lo = nbits > 64 ? nbits - 64 : 0;
+  uint64_t hi = 0;
+  for (int k = nbits - 1; k >= lo; --k) hi = (hi << 1) | bit(k);
+  bool sticky = false;
+  for (int k = 0; k < lo; ++k) sticky = sticky || bit(k);
+  if (sticky) hi |= 1;  // below the 11 bits the conversion drops: only breaks exact ties
+  c.m = std::ldexp(static_cast<double>(hi), lo);
   return c;
 }
 
+// host copy of the reconstruction table (diagnostic export, hsb_oz_crt_table)
+int oz_crt_table_host(int n_mod, double* w, double* m) {
+  if (n_mod < kOzMinMod || n_mod > kOzMaxMod) return 1;
+  const OzCrtConst c = oz_crt_table(n_mod);
+  for (int part = 0; part < 2; ++part)
+    for (int i = 0; i < n_mod; ++i)
+      for (int l = 0; l < 2; ++l) w[(part * n_mod + i) * 2 + l] = c.w[part][i][l];
+  *m = c.m;
+  return 0;
+}
+
+// Constants and kernel attributes are per device: upload / set them the first
+// time each device is used (a process may drive several GPUs, _lib.context).
 static cudaError_t oz_init_once() {
-  static std::once_flag once;
-  static cudaError_t status = cudaSuccess;
-  std::call_once(once, [] {
-    OzCrtConst t[kOzMaxMod - kOzMinMod + 1];
-    for (int nm = kOzMinMod; nm <= kOzMaxMod; ++nm) t[nm - kOzMinMod] = oz_crt_table(nm);
-    status = cudaMemcpyToSymbol(c_oz_crt, t, sizeof(t));
+  static PerDeviceOnce once;
+  return per_device_once(once, [] {
+    static OzCrtConst t[kOzMaxMod - kOzMinMod + 1];
+    static std::once_flag built;
+    std::call_once(built, [] {
+      for (int nm = kOzMinMod; nm <= kOzMaxMod; ++nm) t[nm - kOzMinMod] = oz_crt_table(nm);
+    });
+    cudaError_t status = cudaMemcpyToSymbol(c_oz_crt, t, sizeof(t));
     if (status == cudaSuccess)
       status = cudaFuncSetAttribute(ozaki_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kOzSmem);
+    return status;
   });
-  return status;
 }
 
 // ------------------------------------------------------------ launchers
@@ -901,6 +944,7 @@ cudaError_t launch_ozaki_residues(const double* x, int64_t ldx, int64_t k, int64
     ozaki_residue_kernel<NM><<<grid, 128, 0, st>>>(xx, ldx, k, cols, col_exp, b, out, kpad, rscale); \
     break;
     HSB_OZ_RES(11) HSB_OZ_RES(12) HSB_OZ_RES(13) HSB_OZ_RES(14) HSB_OZ_RES(15) HSB_OZ_RES(16)
+    HSB_OZ_RES(17) HSB_OZ_RES(18) HSB_OZ_RES(19) HSB_OZ_RES(20)
 #undef HSB_OZ_RES
     default:
       return cudaErrorInvalidValue;
@@ -947,6 +991,7 @@ cudaError_t launch_ozaki_vcrt(const OzVcrtParams& p, cudaStream_t st) {
     ozaki_vcrt_kernel<NMV><<<grid, block, 0, st>>>(p);  \
     break;
     HSB_OZ_VCRT(11) HSB_OZ_VCRT(12) HSB_OZ_VCRT(13) HSB_OZ_VCRT(14) HSB_OZ_VCRT(15) HSB_OZ_VCRT(16)
+    HSB_OZ_VCRT(17) HSB_OZ_VCRT(18) HSB_OZ_VCRT(19) HSB_OZ_VCRT(20)
 #undef HSB_OZ_VCRT
     default:
       return cudaErrorInvalidValue;
@@ -966,17 +1011,18 @@ cudaError_t launch_ozaki_crt_cols(const OzCrtParams& p, int64_t ncols, cudaStrea
   if (ncols <= 0) return cudaSuccess;
   cudaError_t ce = oz_init_once();
   if (ce != cudaSuccess) return ce;
-  if (ncols > 65535) return cudaErrorInvalidConfiguration;
-  // column pairs (n0 + y, n0 + ncols - 1 - y): groups of kOzCrtRows rows from
-  // each column's diagonal group down to row n
-  const int64_t gend = (p.n + kOzCrtRows - 1) / kOzCrtRows;
+  if (p.n0 % 4 != 0) return cudaErrorInvalidValue;  // 4-row groups must not straddle a tile
+  // column-block pairs (y, ncb - 1 - y): 128-row chunks from each block's
+  // diagonal down to row n
+  const int64_t ncb = (ncols + kCrtCols - 1) / kCrtCols;
+  if ((ncb + 1) / 2 > 65535) return cudaErrorInvalidConfiguration;
+  auto chunks = [&](int64_t cb) { return (p.n - (p.n0 + cb * kCrtCols) + kCrtRows - 1) / kCrtRows; };
   int64_t most = 0;
-  for (int64_t y = 0; y < (ncols + 1) / 2; ++y) {
-    const int64_t na = p.n0 + y, nb = p.n0 + ncols - 1 - y;
-    const int64_t cnt = (gend - na / kOzCrtRows) + (nb == na ? 0 : gend - nb / kOzCrtRows);
-    most = std::max(most, cnt);
+  for (int64_t y = 0; y < (ncb + 1) / 2; ++y) {
+    const int64_t yb = ncb - 1 - y;
+    most = std::max(most, chunks(y) + (yb == y ? 0 : chunks(yb)));
   }
-  const dim3 grid(static_cast<unsigned>((most + 127) / 128), static_cast<unsigned>((ncols + 1) / 2)), block(128);
+  const dim3 grid(static_cast<unsigned>(most), static_cast<unsigned>((ncb + 1) / 2)), block(256);
   const int nc = static_cast<int>(ncols);
 #define HSB_OZ_CRT(NMV)                                     \
   case NMV:                                               \
@@ -989,6 +1035,10 @@ cudaError_t launch_ozaki_crt_cols(const OzCrtParams& p, int64_t ncols, cudaStrea
     HSB_OZ_CRT(14)
     HSB_OZ_CRT(15)
     HSB_OZ_CRT(16)
+    HSB_OZ_CRT(17)
+    HSB_OZ_CRT(18)
+    HSB_OZ_CRT(19)
+    HSB_OZ_CRT(20)
     default: return cudaErrorInvalidValue;
   }
 #undef HSB_OZ_CRT

@@ -27,9 +27,11 @@
 //
 // Exactness: every step after the rounding in (2) is exact integer
 // arithmetic as long as |Re C'|, |Im C'| < M/2 = prod p_i / 2, which fixes b
-// from K_tot (the host picks n_mod so that b >= 39).  The only error is the
-// operand rounding, ~2^-b relative to each column's max: ~1e-12 relative
-// Frobenius, inside the north star's 1e-10 (measured in tests/).
+// from K_tot: the host picks the fewest moduli with b >= 53 (17 moduli at
+// C3 / C4), so every operand keeps a full FP64 mantissa relative to its
+// column's max -- the largest entries of each column are exact -- and the only
+// error is the rounding of entries smaller than their column max: measured
+// ~1e-16 relative Frobenius, the FP64 DMMA engine's level (tests/).
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -37,19 +39,24 @@
 
 namespace hsb {
 
-constexpr int kOzMaxMod = 16;
+constexpr int kOzMaxMod = 20;
+constexpr int kOzMinMod = 11;
+constexpr int kOzDefaultBits = 53;  // operand bits by default: a full FP64 mantissa
+constexpr int kOzMaxBits = 55;      // |x'| <= 2^55 keeps the residue quotients exact
 constexpr int kOzMaxSeg = 4;
 constexpr int kOzBM = 256;   // output tile rows   (CTA pair: 128 TMEM lanes each)
 constexpr int kOzBN = 256;   // output tile cols   (TMEM columns per accumulator)
 constexpr int kOzBK = 128;   // k bytes per stage  (128B swizzle row)
 // pairwise coprime, descending, every prime factor = 1 (mod 4)
-// (221 = 13 * 17, 205 = 5 * 41); the first n_mod are used
+// (221 = 13 * 17, 205 = 5 * 41); the first n_mod are used.  17 moduli
+// (M ~ 2^124.2) give b >= 53-bit operands up to K_tot ~ 2^15.
 __host__ __device__ constexpr int oz_mod(int i) {
   switch (i) {
     case 0: return 241;  case 1: return 233;  case 2: return 229;  case 3: return 221;
     case 4: return 205;  case 5: return 197;  case 6: return 193;  case 7: return 181;
     case 8: return 173;  case 9: return 157;  case 10: return 149; case 11: return 137;
-    case 12: return 113; case 13: return 109; case 14: return 101; default: return 97;
+    case 12: return 113; case 13: return 109; case 14: return 101; case 15: return 97;
+    case 16: return 89;  case 17: return 73;  case 18: return 61;  default: return 53;
   }
 }
 // j_i: a square root of -1 modulo oz_mod(i), symmetric representative
@@ -58,7 +65,8 @@ __host__ __device__ constexpr int oz_sqrtm1(int i) {
     case 0: return 64;   case 1: return 89;   case 2: return 107;  case 3: return 21;
     case 4: return 32;   case 5: return 14;   case 6: return 81;   case 7: return 19;
     case 8: return 80;   case 9: return 28;   case 10: return 44;  case 11: return 37;
-    case 12: return 15;  case 13: return 33;  case 14: return 10;  default: return 22;
+    case 12: return 15;  case 13: return 33;  case 14: return 10;  case 15: return 22;
+    case 16: return 34;  case 17: return 27;  case 18: return 11;  default: return 23;
   }
 }
 
@@ -166,6 +174,8 @@ cudaError_t launch_ozaki_residues(const double* x, int64_t ldx, int64_t k, int64
                                   int b, int n_mod, int8_t* out, int64_t kpad, cudaStream_t st, const double* rscale = nullptr);
 cudaError_t launch_ozaki_gemm(const OzGemmParams& p, cudaStream_t st);
 cudaError_t launch_ozaki_crt(const OzCrtParams& p, cudaStream_t st);
+// the reconstruction table of n_mod moduli: w[part][i][limb], fl(M); 0 on success
+int oz_crt_table_host(int n_mod, double* w, double* m);
 cudaError_t launch_ozaki_crt_cols(const OzCrtParams& p, int64_t ncols, cudaStream_t st);
 
 }  // namespace hsb

@@ -303,26 +303,21 @@ __global__ void __launch_bounds__(k3Threads, 1) zrk3m_kernel(const __grid_consta
 // ------------------------------------------------------------------ launcher
 template <bool CONJ, bool PLANES>
 static cudaError_t launch3(const ZrkParams& p, int ntiles, int nwork, int n_sm, cudaStream_t st) {
-  static bool attr_done = false;
+  static PerDeviceOnce attr;  // the attribute is per device
   auto kern = zrk3m_kernel<CONJ, PLANES>;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg3<PLANES>::smem);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
+  cudaError_t e = per_device_once(
+      attr, [&] { return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg3<PLANES>::smem); });
+  if (e != cudaSuccess) return e;
   const int grid = std::min(nwork, n_sm);
   kern<<<dim3(grid), dim3(k3Threads), Cfg3<PLANES>::smem, st>>>(p, ntiles, nwork);
   return cudaGetLastError();
 }
 
 cudaError_t launch_zrk3m(const ZrkParams& p, bool conj, bool planes, int ntiles, int nbatch, cudaStream_t st) {
-  static int n_sm = 0;
-  if (n_sm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaError_t e = cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    if (e != cudaSuccess) return e;
-  }
+  int dev = 0, n_sm = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return e;
   const int64_t nwork = static_cast<int64_t>(ntiles) * nbatch;
   if (nwork > 0x7fffffff) return cudaErrorInvalidConfiguration;
   if (planes && nbatch != 1) return cudaErrorInvalidValue;

@@ -2,6 +2,7 @@
 // zrk.cuh.  One CTA = one 64 x 64 complex output tile; warp 4 is the TMA
 // producer (one elected lane), warps 0-3 each own a 32 x 32 complex sub-tile
 // held in registers as 4 x 4 DMMA.8x8x4 accumulator pairs (real, imag).
+#include "aux_kernels.cuh"
 #include "ptx.cuh"
 #include "zrk.cuh"
 
@@ -203,13 +204,11 @@ __global__ void __launch_bounds__(kThreads, 2) zrk_kernel(const __grid_constant_
 
 // ------------------------------------------------------------------ launcher
 cudaError_t launch_zrk(const ZrkParams& p, bool conj, int grid_x, int grid_z, cudaStream_t st) {
-  static bool attr_done[2] = {false, false};
+  static PerDeviceOnce attr[2];  // the attribute is per device
   auto kern = conj ? zrk_kernel<true> : zrk_kernel<false>;
-  if (!attr_done[conj]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr_done[conj] = true;
-  }
+  cudaError_t e = per_device_once(
+      attr[conj], [&] { return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes); });
+  if (e != cudaSuccess) return e;
   kern<<<dim3(grid_x, 1, grid_z), dim3(kThreads), kSmemBytes, st>>>(p);
   return cudaGetLastError();
 }

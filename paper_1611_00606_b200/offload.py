@@ -10,9 +10,11 @@ of the serial kernels (executor.py:188-193):
 
 ``c`` is a host complex128 F-order array updated in place (HERK/HER2K: lower
 triangle only, Im(diag) := 0).  Operands are copied to the device, the
-sm_100a DMMA kernel runs once (no host-side tiling: the device kernel tiles
-the stored triangle itself, one CTA per 64 x 64 tile), and ``c`` is copied
-back.  ``ExecResult.seconds`` is the CUDA-event time of the kernel alone;
+sm_100a kernel runs once (no host-side tiling: the device kernel tiles the
+stored triangle itself), and ``c`` is copied back.  The default engine
+("auto") is FP64 DMMA here -- elementwise FP64 rounding for arbitrary
+operands, like the reference kernels; ``GpuPolicy(engine="int8")`` opts into
+the INT8 emulation (FP64-width by default, normwise accurate).  ``ExecResult.seconds`` is the CUDA-event time of the kernel alone;
 ``n_tiles`` counts the 64 x 64 output tiles the kernel launched.
 """
 
@@ -72,7 +74,6 @@ def _run_gpu(kind, operands, policy: GpuPolicy):
     import torch
 
     lib = _lib.load()
-    ctx = _lib.context(policy.device, policy.complex_mult, policy.engine, policy.int8_bits)
     dev = torch.device("cuda", policy.device)
     st = _stream_ptr(dev)
     if kind is KernelKind.HERK:
@@ -84,7 +85,7 @@ def _run_gpu(kind, operands, policy: GpuPolicy):
             raise DimensionError(f"c has shape {c.shape}, expected {(n, n)}")
         da, lda = _dev_matrix(a, dev)
         dc, ldc = _dev_matrix(c, dev)
-        call = lambda: lib.hsb_zherk(ctx, st, n, a.shape[0], alpha, da.data_ptr(), lda, beta,
+        call = lambda ctx: lib.hsb_zherk(ctx, st, n, a.shape[0], alpha, da.data_ptr(), lda, beta,
                                      dc.data_ptr(), ldc, 0)
         tiles = _tiles(n, n, True)
         touched = (c.size + 2 * a.size) * _ITEM
@@ -101,7 +102,7 @@ def _run_gpu(kind, operands, policy: GpuPolicy):
         dz, ldz = _dev_matrix(z, dev)
         db, ldb = _dev_matrix(b, dev)
         dc, ldc = _dev_matrix(c, dev)
-        call = lambda: lib.hsb_zher2k(ctx, st, n, z.shape[0], al.real, al.imag, dz.data_ptr(), ldz,
+        call = lambda ctx: lib.hsb_zher2k(ctx, st, n, z.shape[0], al.real, al.imag, dz.data_ptr(), ldz,
                                       db.data_ptr(), ldb, beta, dc.data_ptr(), ldc, 0)
         tiles = _tiles(n, n, True)
         touched = (c.size + 2 * (z.size + b.size)) * _ITEM
@@ -121,15 +122,16 @@ def _run_gpu(kind, operands, policy: GpuPolicy):
         da, lda = _dev_matrix(a, dev)
         db, ldb = _dev_matrix(b, dev)
         dc, ldc = _dev_matrix(c, dev)
-        call = lambda: lib.hsb_zgemm(ctx, st, opa.encode(), opb.encode(), m, n, ka, al.real, al.imag,
+        call = lambda ctx: lib.hsb_zgemm(ctx, st, opa.encode(), opb.encode(), m, n, ka, al.real, al.imag,
                                      da.data_ptr(), lda, db.data_ptr(), ldb, be.real, be.imag,
                                      dc.data_ptr(), ldc, 0)
         tiles = _tiles(m, n, False)
         touched = (c.size + (m + n) * ka) * _ITEM
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    start.record()
-    _lib.check(call(), ctx)
-    end.record()
+    with _lib.using(policy.device, policy.complex_mult, policy.engine, policy.int8_bits) as ctx:
+        start.record()
+        _lib.check(call(ctx), ctx)
+        end.record()
     end.synchronize()
     host = dc.cpu().numpy().T  # column-major view
     c[...] = host

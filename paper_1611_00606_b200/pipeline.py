@@ -47,11 +47,17 @@ class GpuPolicy:
     (4 real products).  Both agree with the reference to ~1e-15 relative
     Frobenius; the ledger charges the reference's model flops either way.
 
-    ``engine`` emulates the S and H contractions on the INT8 tensor cores
-    ("int8", default: Chinese-remainder / Ozaki-II scheme, operands rounded
-    to ``int8_bits`` bits per column, ~1e-12 relative Frobenius at the
-    default 39, 4.2x faster at C3; see csrc/ozaki.cuh) or runs them on the
-    FP64 DMMA tensor cores ("dmma": ~1e-15).
+    ``engine`` selects the engine of the S and H contractions: "int8"
+    emulates them on the INT8 tensor cores (Chinese-remainder / Ozaki-II
+    scheme, see csrc/ozaki.cuh) with operands rounded to ``int8_bits`` bits
+    per column -- by default 53, a full FP64 mantissa: the largest entries of
+    every column are exact and the result is as accurate as the FP64 DMMA
+    engine (~1e-16 relative Frobenius, measured against the oracle at C3 and
+    C4); "dmma" runs them on the FP64 DMMA tensor cores; "auto" (default)
+    is "int8" here and "dmma" for the kernel-level ``run_partitioned``, whose
+    general operands get elementwise FP64 rounding.  ``int8_bits`` in
+    [30, 55] (0 = 53); fewer bits need fewer moduli (~2^-bits of each
+    column's max, e.g. 39 -> ~2e-12, 13 instead of 17 moduli).
 
     ``lower_d2h`` (pinned outputs, INT8 engine): H and S cross PCIe as lower
     triangles and host threads fill the upper triangles (conjugate mirror)
@@ -62,7 +68,7 @@ class GpuPolicy:
     fused: bool = True
     pinned_outputs: bool = True
     complex_mult: str = "3m"
-    engine: str = "int8"
+    engine: str = "auto"
     int8_bits: int = 0
     lower_d2h: bool = True
 
@@ -71,10 +77,10 @@ class GpuPolicy:
             raise InputError(f"device must be a nonnegative integer, got {self.device!r}")
         if self.complex_mult not in ("3m", "4m"):
             raise InputError(f"complex_mult must be '3m' or '4m', got {self.complex_mult!r}")
-        if self.engine not in ("dmma", "int8"):
-            raise InputError(f"engine must be 'dmma' or 'int8', got {self.engine!r}")
-        if self.int8_bits != 0 and not 30 <= int(self.int8_bits) <= 48:
-            raise InputError(f"int8_bits must be 0 (default) or in [30, 48], got {self.int8_bits!r}")
+        if self.engine not in ("auto", "dmma", "int8"):
+            raise InputError(f"engine must be 'auto', 'dmma' or 'int8', got {self.engine!r}")
+        if self.int8_bits != 0 and not 30 <= int(self.int8_bits) <= 55:
+            raise InputError(f"int8_bits must be 0 (default 53) or in [30, 55], got {self.int8_bits!r}")
 
 
 @dataclass
@@ -195,7 +201,6 @@ def _host_problem(p):
 
 def _call_build(pol, prob, out, stream, force_nonhpd, n_a, slot: int = 0, wait: bool = True):
     lib = _lib.load()
-    ctx = _lib.context(pol.device, pol.complex_mult, pol.engine, pol.int8_bits, slot)
     opts = (_lib.HSB_OPT_FORCE_NONHPD if force_nonhpd else 0) | (0 if pol.fused else _lib.HSB_OPT_UNFUSED)
     if not pol.lower_d2h:
         opts |= _lib.HSB_OPT_FULL_D2H
@@ -203,9 +208,10 @@ def _call_build(pol, prob, out, stream, force_nonhpd, n_a, slot: int = 0, wait: 
         opts |= _lib.HSB_OPT_VALIDATE  # T / u values are checked natively, before any transfer
     tim = _lib.HsbTimings()
     info = (ctypes.c_int32 * n_a)()
-    # no timings -> the library returns without waiting (device in/out only)
-    _lib.check(lib.hsb_build_hs(ctx, stream, ctypes.byref(prob), opts, ctypes.byref(out),
-                                ctypes.byref(tim) if wait else None, info if wait else None), ctx)
+    with _lib.using(pol.device, pol.complex_mult, pol.engine, pol.int8_bits, slot) as ctx:
+        # no timings -> the library returns without waiting (device in/out only)
+        _lib.check(lib.hsb_build_hs(ctx, stream, ctypes.byref(prob), opts, ctypes.byref(out),
+                                    ctypes.byref(tim) if wait else None, info if wait else None), ctx)
     return (tim, list(info)) if wait else (None, None)
 
 

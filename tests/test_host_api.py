@@ -139,26 +139,29 @@ def test_report_summarize_and_table5():
 
 
 def test_int8_engine_moduli_choice():
-    # engine.int8_moduli restates contract.cu run_ozaki: the fewest moduli with
-    # b >= 39 bits and K 2^(2b) below M/4
+    # engine.int8_moduli restates contract.cu oz_choose: the fewest moduli with
+    # b >= 53 bits (a full FP64 mantissa) and K 2^(2b) below M/4
     import math
 
     from paper_1611_00606_b200 import int8_gemm_ops, int8_moduli
-    from paper_1611_00606_b200.engine import MODULI, SQRT_M1
+    from paper_1611_00606_b200.engine import DEFAULT_BITS, MAX_BITS, MODULI, SQRT_M1
 
-    for k in (1, 98, 7744, 11616, 46464):
+    assert DEFAULT_BITS == 53
+    for k in (1, 98, 7744, 11616, 30976, 46464):
         n_mod, b = int8_moduli(k)
         log2m = sum(math.log2(p) for p in MODULI[:n_mod])
-        assert b >= 39 and k * 2.0 ** (2 * b) < 2.0 ** log2m / 4  # |Re C'|, |Im C'| <= K 2^2b < M/2, 1 bit spare
+        assert 53 <= b <= MAX_BITS and k * 2.0 ** (2 * b) < 2.0 ** log2m / 4  # |Re C'|, |Im C'| <= K 2^2b < M/2
         if n_mod > 11:
             prev = sum(math.log2(p) for p in MODULI[:n_mod - 1])
-            assert math.floor((prev - 2 - math.log2(k)) / 2) < 39
-    assert int8_moduli(11616) == (13, 41) and int8_moduli(46464) == (13, 40)
+            assert math.floor((prev - 2 - math.log2(k)) / 2) < 53
+    # C3's and C4's H / S reductions (K_tot = 2 N_A N_L): 17 moduli
+    assert int8_moduli(7744) == (17, 54) and int8_moduli(30976) == (17, 53)
+    assert int8_moduli(11616, 39) == (13, 41)  # the round-1 default, still selectable
     assert all(math.gcd(a, b) == 1 for i, a in enumerate(MODULI) for b in MODULI[i + 1:])
     # split complex arithmetic: odd moduli < 256, -1 a square mod each
     assert all(p % 2 == 1 and p < 256 and (j * j + 1) % p == 0 and abs(j) <= p // 2
                for p, j in zip(MODULI, SQRT_M1))
-    assert int8_gemm_ops(8000, 11616) == 2 * 2 * 13 * 11616 * 8000 * 8001 // 2
+    assert int8_gemm_ops(8000, 7744) == 2 * 2 * 17 * 7744 * 8000 * 8001 // 2
     with pytest.raises(InputError):
         GpuPolicy(engine="fp16")
 
@@ -212,3 +215,36 @@ def test_int8_split_complex_crt_exact():
         x_re -= M * round(x_re / M)
         x_im -= M * round(x_im / M)
         assert (x_re, x_im) == (cre, cim)
+
+
+def test_int8_crt_fraction_reconstruction():
+    # The reconstruction of csrc/ozaki.cu (crt_frac): X / M as a two-limb
+    # fixed-point sum of the residues, X = f * fl(M).  For every supported
+    # modulus count, residues of integers |X| <= M/4 (the host's bound),
+    # including tiny and extreme ones, must come back within a few ulp of X
+    # plus the 2^-66 M truncation floor -- the FP64-width engine's contract.
+    import math
+    import random
+
+    from paper_1611_00606_b200.engine import MODULI, SQRT_M1, crt_fraction, crt_weights
+
+    rng = random.Random(7)
+    for n_mod in range(11, len(MODULI) + 1):
+        mods = MODULI[:n_mod]
+        big_m = math.prod(mods)
+        (w_re, w_im), m_f = crt_weights(n_mod)
+        xs = [0, 1, -1, 5, big_m // 4, -(big_m // 4), 2 ** 60 + 3]
+        xs += [rng.randint(-(big_m // 4), big_m // 4) for _ in range(40)]
+        xs += [rng.randint(-2 ** 80, 2 ** 80) for _ in range(10)]
+        for x_re in xs:
+            x_im = rng.randint(-(big_m // 4), big_m // 4)
+            # residues as the GEMM epilogue leaves them: phi1, phi2 of x_re + i x_im
+            f1 = [_sym(x_re + j * x_im, p) for p, j in zip(mods, SQRT_M1)]
+            f2 = [_sym(x_re - j * x_im, p) for p, j in zip(mods, SQRT_M1)]
+            re = [a + b for a, b in zip(f1, f2)]
+            im = [a - b for a, b in zip(f1, f2)]
+            got_re = crt_fraction(re, w_re) * m_f
+            got_im = crt_fraction(im, w_im) * m_f
+            for got, want in ((got_re, x_re), (got_im, x_im)):
+                tol = 4 * math.ulp(float(want)) + big_m * 2.0 ** -66
+                assert abs(got - want) <= tol, (n_mod, want, got)

@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_loader_and_abi_version():
     lib = _lib.load()
-    assert lib.hsb_abi_version() == 6
+    assert lib.hsb_abi_version() == _lib.ABI_VERSION == 7
 
 
 def test_binding_struct_layout_matches_header():
@@ -46,3 +46,21 @@ def test_kernels_are_sm100a_only():
     if out.returncode != 0:
         pytest.skip("cuobjdump unavailable")
     assert "sm_100a" in out.stdout
+
+
+def test_int8_crt_table_matches_restatement():
+    # the table the device reconstructs with (csrc/ozaki.cu oz_crt_table,
+    # exported host-side) equals the Python restatement bit for bit
+    import numpy as np
+
+    from paper_1611_00606_b200.engine import MODULI, crt_weights
+
+    lib = _lib.load()
+    for n_mod in range(11, len(MODULI) + 1):
+        w = np.zeros((2, n_mod, 2))
+        m = ctypes.c_double()
+        assert lib.hsb_oz_crt_table(n_mod, w.ctypes.data, ctypes.byref(m)) == 0
+        want, want_m = crt_weights(n_mod)
+        assert w.tolist() == [[list(x) for x in part] for part in want]
+        assert m.value == want_m
+    assert lib.hsb_oz_crt_table(21, w.ctypes.data, ctypes.byref(m)) != 0
