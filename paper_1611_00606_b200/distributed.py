@@ -288,17 +288,26 @@ def build_hs_sharded_fused(dp, slots: "PeerSlots", policy=None, group=None):
     """Atom-sharded step with the fused reduce-scatter: this rank's partial H
     and S go straight from the reconstruction epilogue into the owners' slots
     (no NCCL collective on the data path); a barrier, then each owner sums
-    its slots.  Returns this rank's (cols, n_g) blocks of H and S."""
+    its slots, and a second barrier before the slots can be written again.
+    Returns this rank's (cols, n_g) blocks of H and S."""
     import torch
     import torch.distributed as dist
 
     from .pipeline import build_hs_device
 
+    stream = torch.cuda.current_stream(slots.h_recv.device)
     build_hs_device(dp, policy=policy, peer=slots, wait=False)
-    torch.cuda.current_stream(slots.h_recv.device).synchronize()
+    stream.synchronize()
     if dist.is_initialized():
+        dist.barrier(group=group)  # every rank's partial has landed in the owners' slots
+    hb, sb = slots.finish()
+    stream.synchronize()
+    if dist.is_initialized():
+        # the slots are reused: no rank may start its next build (whose epilogue
+        # writes into the owners' slots over NVLink) before every owner has
+        # finished summing this step's
         dist.barrier(group=group)
-    return slots.finish()
+    return hb, sb
 
 
 def kpoint_assignment(n_kpoints: int, world: int, rank: int) -> list[int]:

