@@ -20,16 +20,6 @@ __constant__ int32_t oz_mod_rt[kOzMaxMod] = {241, 233, 229, 221, 205, 197, 193, 
 // ------------------------------------------------------------ small helpers
 __device__ __forceinline__ int sym_lo(int p) { return -(p >> 1); }
 
-// symmetric residue of an exactly-integer double |v| < 2^46: r = v - p*floor(v/p + 1/2)
-// lies in [-(p-1)/2, (p-1)/2] (every modulus is odd) with no correction:
-// v/p is never within 1/(2p) >= 2^-9 of a half-integer while the product's
-// error is ~2^-15.
-// The integer is read from the mantissa (magic 1.5 * 2^52) instead of F2I.
-__device__ __forceinline__ int sym_mod_d(double v, double p, double inv_p) {
-  const double q = floor(fma(v, inv_p, 0.5));
-  const double r = fma(-p, q, v) + 6755399441055744.0;
-  return static_cast<int>(__double2loint(r));
-}
 // symmetric residue of an int32 v modulo an odd p < 256 in FP32:
 // t = (v >> 16) (2^16 mod p) + (v & 0xffff) = v (mod p), |t| < 2^22; the
 // quotient rn(t fl(1/p)) through the 1.5 * 2^23 magic constant is exact (its
@@ -119,29 +109,92 @@ __constant__ double oz_inv_rt[kOzMaxMod] = {
 // 2^e for |e| <= 1022 from the exponent bits
 __device__ __forceinline__ double pow2i(int e) { return __longlong_as_double(static_cast<long long>(e + 1023) << 52); }
 
-// residue of an exactly-integer double |v| <= 2^55 modulo p, as the low word of
-// r + 1.5 * 2^52 with r = v - p * q, q = rn(v * fl(1/p)) through the magic
-// constant: r = v - p q is exact (fma), and since the product's error
-// (|v| 2^-53 / p <= 2^2 / p) may exceed the 1/(2p) distance of v / p from a
-// half-integer once |v| > 2^46, r lies in [-(3p-1)/2, (3p-1)/2] rather than the
-// symmetric range: the callers only combine it into |rr + j ri| < 2^16 and
-// reduce that again with sym_mod_small.  No FRND, no division.
-__device__ __forceinline__ int sym_mod_magic(double v, double p, double inv_p) {
-  constexpr double M = 6755399441055744.0;  // 1.5 * 2^52
-  const double q = fma(v, inv_p, M) - M;
-  return static_cast<int>(__double2loint(fma(-p, q, v) + M));
+// ---- residues by byte dot products (IDP4A) --------------------------------
+// An operand integer x' (|x'| <= 2^55, exact in FP64) is split once per element
+// into two 32-bit words, x' = (hi - 2^31) 2^32 + lo with lo, hi unsigned, i.e.
+// eight unsigned bytes; then for every modulus
+//     x' mod p  =  sum_d byte_d (2^(8d) mod p)  -  (2^63 mod p)        (mod p)
+// is two dp4a.u32.s32 against packed symmetric weights, and the split-complex
+// planes phi1,2 = x' +- j y' fold j into y's weights: X + Y and X - Y with
+// |X|, |Y| <= 8 * 255 * 120 + 120 < 2^18.  Each is reduced to its symmetric
+// residue by an exact integer quotient (oz_sym_reduce).  Per element and
+// modulus ~11 integer instructions, no FP64 or conversion-pipe work (the
+// FP64 magic-quotient form issued ~32).
+__host__ __device__ constexpr int oz_pow2_mod(int e, int p) {
+  int r = 1 % p;
+  for (int i = 0; i < e; ++i) r = (2 * r) % p;
+  return r;
 }
+__host__ __device__ constexpr int oz_symrep(long long v, int p) {
+  long long r = v % p;
+  if (r < 0) r += p;
+  return static_cast<int>(r > p / 2 ? r - p : r);
+}
+// packed int8 weights of bytes d0 .. d0+3: (mult * 2^(8d)) mod p, symmetric
+__host__ __device__ constexpr uint32_t oz_wpack(int i, int mult, int d0) {
+  uint32_t w = 0;
+  for (int d = 0; d < 4; ++d)
+    w |= (static_cast<uint32_t>(oz_symrep(static_cast<long long>(mult) * oz_pow2_mod(8 * (d0 + d), oz_mod(i)),
+                                          oz_mod(i))) & 0xffu) << (8 * d);
+  return w;
+}
+// -(mult * 2^63) mod p, symmetric: the bias of hi
+__host__ __device__ constexpr int oz_bias(int i, int mult) {
+  return oz_symrep(-static_cast<long long>(mult) * oz_pow2_mod(63, oz_mod(i)), oz_mod(i));
+}
+// rn(2^32 / p): the quotient multiplier of oz_sym_reduce
+__host__ __device__ constexpr long long oz_qmul(int i) { return ((1ll << 32) + oz_mod(i) / 2) / oz_mod(i); }
 
-// symmetric residue of a small integer |v| < 2^16 modulo an odd p: v / p is
-// never within 1/(2p) >= 2^-9 of a half-integer, and the float quotient's
-// error is below |v / p| 2^-23 < 2^-16
-__device__ __forceinline__ int sym_mod_small(int v, int p, float inv_p) {
-  return v - p * __float2int_rn(__int2float_rn(v) * inv_p);
+__device__ __forceinline__ int dp4a_us(uint32_t a, uint32_t b, int c) {
+  int d;
+  asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+// symmetric residue of |v| < 2^19 modulo p: q = floor((v m + 2^31) / 2^32) =
+// rn(v / p) exactly (m = rn(2^32 / p) errs by <= 1/2, so v m / 2^32 is within
+// |v| 2^-33 <= 2^-14 of v / p, which is >= 1/(2p) > 2^-9 from any half-integer)
+template <int I>
+__device__ __forceinline__ int oz_sym_reduce(int v) {
+  const int q = static_cast<int>((static_cast<long long>(v) * oz_qmul(I) + (1ll << 31)) >> 32);
+  return v - oz_mod(I) * q;
+}
+// exact x' = (hi - 2^31) 2^32 + lo of an exactly-integer double |x| <= 2^55:
+// h = floor(x 2^-32) by a round-down add of the 1.5 * 2^52 magic constant (x 2^-32
+// is exact), l = x - h 2^32 in [0, 2^32) exactly, both read from the low
+// mantissa word.  (Round-to-nearest would give l = +2^31 on ties, which does
+// not fit the word.)
+__device__ __forceinline__ void oz_split(double x, uint32_t& lo, uint32_t& hi) {
+  constexpr double M = 6755399441055744.0;  // 1.5 * 2^52
+  const double hm = __dadd_rd(x * 2.3283064365386963e-10, M);  // M + floor(x 2^-32)
+  lo = static_cast<uint32_t>(__double2loint(fma(-(hm - M), 4294967296.0, x) + M));
+  hi = static_cast<uint32_t>(__double2loint(hm)) + 0x80000000u;
+}
+template <int I>
+__device__ __forceinline__ void oz_planes(uint32_t xl, uint32_t xh, uint32_t yl, uint32_t yh, int& u, int& w) {
+  const int X = dp4a_us(xh, oz_wpack(I, 1, 4), dp4a_us(xl, oz_wpack(I, 1, 0), oz_bias(I, 1)));
+  const int Y = dp4a_us(yh, oz_wpack(I, oz_sqrtm1(I), 4), dp4a_us(yl, oz_wpack(I, oz_sqrtm1(I), 0), oz_bias(I, oz_sqrtm1(I))));
+  u = oz_sym_reduce<I>(X + Y);  // phi1 = x' + j y'
+  w = oz_sym_reduce<I>(X - Y);  // phi2 = x' - j y'
+}
+template <int NM, int I = 0>
+__device__ __forceinline__ void oz_residue_planes(const uint32_t (&xl)[4], const uint32_t (&xh)[4],
+                                                  const uint32_t (&yl)[4], const uint32_t (&yh)[4], int8_t* o0,
+                                                  int8_t* o1, int64_t mod_stride) {
+  if constexpr (I < NM) {
+    int u[4], w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) oz_planes<I>(xl[j], xh[j], yl[j], yh[j], u[j], w[j]);
+    const auto pack = [](const int* v) {
+      return __byte_perm(__byte_perm(v[0], v[1], 0x40), __byte_perm(v[2], v[3], 0x40), 0x5410);
+    };
+    *reinterpret_cast<uint32_t*>(o0) = pack(u);
+    *reinterpret_cast<uint32_t*>(o1) = pack(w);
+    oz_residue_planes<NM, I + 1>(xl, xh, yl, yh, o0 + mod_stride, o1 + mod_stride, mod_stride);
+  }
 }
 
 // thread = 4 consecutive k of one column; writes 4 bytes into each of the
-// 2 planes x NM moduli (4 k per thread at 6 CTAs/SM measured 12 % faster than
-// 8 k at 3 CTAs/SM, probes/residue_bench.cu): out[((plane * NM + i) * cols + col) * kpad + k],
+// 2 planes x NM moduli: out[((plane * NM + i) * cols + col) * kpad + k],
 // plane 0 = phi1(z') = x' + j y', plane 1 = phi2(z') = x' - j y' (mod p_i)
 constexpr int kOzResK = 4;
 template <int NM>
@@ -172,29 +225,14 @@ __global__ void __launch_bounds__(128, 6) ozaki_residue_kernel(const double2* __
         xr[j] = xi[j] = 0.0;
       }
     }
-    int8_t* o0 = out + c * kpad + k0;
-    int8_t* o1 = o0 + plane_stride;
+    uint32_t xl[kOzResK], xh[kOzResK], yl[kOzResK], yh[kOzResK];
 #pragma unroll
-    for (int i = 0; i < NM; ++i) {
-      const double p = oz_mod(i), inv = oz_inv_rt[i];
-      const int jm = oz_sqrtm1(i);
-      const float invf = 1.0f / oz_mod(i);
-      int u[kOzResK], w[kOzResK];
-#pragma unroll
-      for (int j = 0; j < kOzResK; ++j) {
-        const int rr = sym_mod_magic(xr[j], p, inv);
-        const int t = jm * sym_mod_magic(xi[j], p, inv);  // |t| <= 120 * 361
-        u[j] = sym_mod_small(rr + t, oz_mod(i), invf);
-        w[j] = sym_mod_small(rr - t, oz_mod(i), invf);
-      }
-      const auto pack = [](const int* v) {
-        return __byte_perm(__byte_perm(v[0], v[1], 0x40), __byte_perm(v[2], v[3], 0x40), 0x5410);
-      };
-      *reinterpret_cast<uint32_t*>(o0) = pack(u);
-      *reinterpret_cast<uint32_t*>(o1) = pack(w);
-      o0 += mod_stride;
-      o1 += mod_stride;
+    for (int j = 0; j < kOzResK; ++j) {
+      oz_split(xr[j], xl[j], xh[j]);
+      oz_split(xi[j], yl[j], yh[j]);
     }
+    int8_t* o0 = out + c * kpad + k0;
+    oz_residue_planes<NM>(xl, xh, yl, yh, o0, o0 + plane_stride, mod_stride);
   }
 }
 
@@ -599,6 +637,11 @@ __device__ __forceinline__ double i2d_exact(int v) {
          4503601774854144.0;  // 2^52 + 2^31
 }
 
+// v - 2^31 for a biased word v = x + 2^31 (|x| < 2^31), exactly
+__device__ __forceinline__ double i2d_biased(unsigned v) {
+  return __hiloint2double(0x43300000, static_cast<int>(v)) - 4503601774854144.0;  // 2^52 + 2^31
+}
+
 // X / M for the 2 Re / 2j Im residue sums of one element (PART 0 / 1)
 template <int NM, int PART>
 __device__ __forceinline__ double crt_frac(const int (&r)[NM]) {
@@ -619,21 +662,12 @@ __device__ __forceinline__ double scale2(double x, int sh) { return (x * pow2i(s
 // sign-extended byte e of w (one PRMT / SGXT)
 __device__ __forceinline__ int sbyte(uint32_t w, int e) { return static_cast<int8_t>(w >> (8 * e)); }
 
-// Finish one element from its per-modulus phi1(C), phi2(C) residues, byte e
-// of w1[i] / w2[i] (the conjugation of L^H R is in the GEMM's choice of planes).
-template <int NM>
-__device__ __forceinline__ double2 crt_element(const OzCrtParams& p, const uint32_t (&w1)[NM],
-                                               const uint32_t (&w2)[NM], int e, int sh, int m, int n) {
-  int re[NM], im[NM];
-#pragma unroll
-  for (int i = 0; i < NM; ++i) {
-    const int f1 = sbyte(w1[i], e), f2 = sbyte(w2[i], e);
-    re[i] = f1 + f2;  // 2 Re C   (mod p_i)
-    im[i] = f1 - f2;  // 2 j Im C (mod p_i)
-  }
-  const double mm = c_oz_crt[NM - kOzMinMod].m;
-  const double xr = scale2(crt_frac<NM, 0>(re) * mm, sh);
-  const double xi = scale2(crt_frac<NM, 1>(im) * mm, sh);
+// Finish one element from its X / M fractions (Re, Im): scale by
+// 2^(e_m + e_n - 2b), alpha / beta, Im(diag) = 0
+__device__ __forceinline__ double2 crt_finish(const OzCrtParams& p, double fr, double fi, double mm, int sh, int m,
+                                              int n) {
+  const double xr = scale2(fr * mm, sh);
+  const double xi = scale2(fi * mm, sh);
   double vr = p.alpha_re * xr - p.alpha_im * xi;
   double vi = p.alpha_re * xi + p.alpha_im * xr;
   if (p.beta_re != 0.0 || p.beta_im != 0.0) {
@@ -655,63 +689,110 @@ __device__ __forceinline__ double2* crt_dst(const OzCrtParams& p, int m, int n) 
 }
 
 // Lower-triangle elements (m >= n).  A block owns 8 output columns (one per
-// warp) x 128 rows; lane l holds rows 4l .. 4l+3 of its warp's column: one
-// 32-bit load per modulus and product from the tile-packed residues (128
-// contiguous bytes per warp), and C[m, n] stored from registers (a warp's four
-// stores cover 2 KB contiguously).  The mirror C[n, m] = conj(C[m, n])
-// (matcore.hermitian_mirror, matcore.py:89-105) is transposed through shared
-// memory so that each warp store writes four full 128-byte lines (8
-// consecutive rows n of 4 columns m) instead of 16-byte strided pieces.
-// Block row y handles the column-block pair (y, ncb - 1 - y), whose row counts
-// add up to about the same for every y.
+// warp) x one 128-row chunk (aligned to 128, so it lies in one 256 x 256
+// residue tile).  The block's residues -- 2 products x NM moduli x 8 columns x
+// 128 rows, 1 KB per (product, modulus) -- are fetched with 16-byte cp.async
+// into shared memory (no registers held, every byte in flight at once: the
+// register-load form was load-latency bound); lane l then reads rows
+// 4l .. 4l+3 of its warp's column (conflict-free 32-bit words) and C[m, n] is
+// stored from registers (a warp's four stores cover 2 KB contiguously).  The
+// mirror C[n, m] = conj(C[m, n]) (matcore.hermitian_mirror, matcore.py:89-105)
+// is transposed through the same shared memory so that each warp store writes
+// four full 128-byte lines (8 consecutive rows n of 4 columns m).  Block row y
+// handles the column-block pair (y, ncb - 1 - y), whose chunk counts add up to
+// about the same for every y.
 constexpr int kCrtCols = 8;      // columns per block (= warps)
 constexpr int kCrtRows = 128;    // rows per block (= 32 lanes x 4)
+__device__ __forceinline__ int crt_chunks(int n, int cs) { return (n - 1) / kCrtRows - cs / kCrtRows + 1; }
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
 template <int NM>
-__global__ void __launch_bounds__(256) ozaki_crt_kernel(const OzCrtParams p, int ncols) {
-  __shared__ double2 stage[kCrtCols][kCrtRows + 1];  // [n][position], +1: conflict-free transposed reads
+__global__ void __launch_bounds__(256, 3) ozaki_crt_kernel(const OzCrtParams p, int ncols) {
+  // residues [product][modulus][column][128 rows], then (reused) the mirror stage
+  constexpr int kResBytes = 2 * NM * kCrtCols * kCrtRows;
+  constexpr int kStageBytes = kCrtCols * (kCrtRows + 1) * 16;
+  __shared__ __align__(16) uint8_t smem[kResBytes > kStageBytes ? kResBytes : kStageBytes];
+  auto stage = reinterpret_cast<double2 (*)[kCrtRows + 1]>(smem);  // [n][position], +1: conflict-free reads
   const int ncb = (ncols + kCrtCols - 1) / kCrtCols;
   const int cba = static_cast<int>(blockIdx.y), cbb = ncb - 1 - cba;
-  const int rsa = p.n0 + cba * kCrtCols, rsb = p.n0 + cbb * kCrtCols;  // first row = first column
-  const int cha = (p.n - rsa + kCrtRows - 1) / kCrtRows;
-  int chunk = static_cast<int>(blockIdx.x), rs;
+  const int csa = p.n0 + cba * kCrtCols, csb = p.n0 + cbb * kCrtCols;  // first column = first useful row
+  int chunk = static_cast<int>(blockIdx.x), cs;
+  const int cha = crt_chunks(p.n, csa);
   if (chunk < cha) {
-    rs = rsa;
+    cs = csa;
   } else {
     chunk -= cha;
-    if (cbb == cba || chunk >= (p.n - rsb + kCrtRows - 1) / kCrtRows) return;
-    rs = rsb;
+    if (cbb == cba || chunk >= crt_chunks(p.n, csb)) return;
+    cs = csb;
   }
+  const int r0 = (cs / kCrtRows + chunk) * kCrtRows;  // first row of the block
   const int nend = min(p.n0 + ncols, p.n);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n = rs + warp;                     // this warp's column
-  const int r0 = rs + chunk * kCrtRows;        // first row of the block
+  const int n = cs + warp;                            // this warp's column
   const int m0 = r0 + 4 * lane;
   const bool mirror = (p.flags & kMirror) != 0;
-  if (n < nend && m0 < p.n && m0 + 3 >= n) {
-    // rows m0 .. m0+3 lie in one 256-row tile; tile row >= tile column
-    const int t = p.tile_index[(m0 >> 8) * p.T + (n >> 8)];
-    const uint8_t* rp = reinterpret_cast<const uint8_t*>(p.res) + static_cast<int64_t>(t) * kOzTileBytes +
-                        (n & 255) * 256 + (m0 & 255);
-    uint32_t w1[NM], w2[NM];  // straight-line: all 2 x NM loads in flight together
+
+  // 1. every residue byte of the block in flight at once
+  {
+    const int t = p.tile_index[(r0 >> 8) * p.T + (cs >> 8)];
+    const uint8_t* base = reinterpret_cast<const uint8_t*>(p.res) + static_cast<int64_t>(t) * kOzTileBytes +
+                          (cs & 255) * 256 + (r0 & 255);
+    const uint32_t sbase = smem_u32(smem);
+    for (int c = threadIdx.x; c < 2 * NM * 64; c += blockDim.x) {
+      const int q = c >> 6, col = (c >> 3) & 7, part = c & 7;  // plane (product, modulus), column, 16 B piece
+      const int prod = q / NM, mod = q - prod * NM;
+      cp_async16(sbase + q * 1024 + col * 128 + part * 16,
+                 base + prod * p.prod_stride + mod * p.mod_stride + col * 256 + part * 16);
+    }
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+  }
+  __syncthreads();
+  const bool active = n < nend && m0 < p.n && m0 + 3 >= n;
+  uint32_t w1[NM], w2[NM];
+#pragma unroll
+  for (int i = 0; i < NM; ++i) {
+    w1[i] = *reinterpret_cast<const uint32_t*>(smem + i * 1024 + warp * 128 + 4 * lane);
+    w2[i] = *reinterpret_cast<const uint32_t*>(smem + (NM + i) * 1024 + warp * 128 + 4 * lane);
+  }
+  __syncthreads();  // the residue area becomes the mirror stage
+  if (active) {
+    // the four rows' limb sums: modulus outer, so each weight (uniform, from
+    // the constant bank) serves four elements
+    const OzCrtConst& C = c_oz_crt[NM - kOzMinMod];
+    double r1[4], r2[4], i1[4], i2[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) r1[e] = r2[e] = i1[e] = i2[e] = 0.0;
 #pragma unroll
     for (int i = 0; i < NM; ++i) {
-      w1[i] = __ldg(reinterpret_cast<const uint32_t*>(rp + i * p.mod_stride));
-      w2[i] = __ldg(reinterpret_cast<const uint32_t*>(rp + p.prod_stride + i * p.mod_stride));
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        // f1 + f2 = 2 Re C, f1 - f2 = 2 j Im C (mod p_i), read through the mantissa
+        const int f1 = sbyte(w1[i], e), f2 = sbyte(w2[i], e);
+        const double re = i2d_biased(static_cast<unsigned>(f1 + f2) + 0x80000000u);
+        const double im = i2d_biased(static_cast<unsigned>(f1 - f2) + 0x80000000u);
+        r1[e] = fma(re, C.w[0][i][0], r1[e]);
+        r2[e] = fma(re, C.w[0][i][1], r2[e]);
+        i1[e] = fma(im, C.w[1][i][0], i1[e]);
+        i2[e] = fma(im, C.w[1][i][1], i2[e]);
+      }
     }
+    const double mm = C.m;
     const int ern = __ldg(p.er + n) - 2 * p.b;
-#pragma unroll 1
+#pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int m = m0 + e;
       if (m < n || m >= p.n) continue;
-      const double2 v = crt_element<NM>(p, w1, w2, e, __ldg(p.el + m) + ern, m, n);
+      const double fr = (r1[e] - rint(r1[e])) + r2[e], fi = (i1[e] - rint(i1[e])) + i2[e];
+      const double2 v = crt_finish(p, fr, fi, mm, __ldg(p.el + m) + ern, m, n);
       *crt_dst(p, m, n) = v;
       stage[warp][e * 32 + lane] = v;
     }
   }
   if (!mirror) return;
   __syncthreads();
-  // transposed: thread (c = tid & 7, j = tid >> 3) writes C[rs + c, r0 + j + 32 q]
-  const int c = threadIdx.x & 7, nn = rs + c;
+  // transposed: thread (c = tid & 7, j = tid >> 3) writes C[cs + c, r0 + j + 32 q]
+  const int c = threadIdx.x & 7, nn = cs + c;
   if (nn >= nend) return;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -1011,12 +1092,15 @@ cudaError_t launch_ozaki_crt_cols(const OzCrtParams& p, int64_t ncols, cudaStrea
   if (ncols <= 0) return cudaSuccess;
   cudaError_t ce = oz_init_once();
   if (ce != cudaSuccess) return ce;
-  if (p.n0 % 4 != 0) return cudaErrorInvalidValue;  // 4-row groups must not straddle a tile
-  // column-block pairs (y, ncb - 1 - y): 128-row chunks from each block's
-  // diagonal down to row n
+  if (p.n0 % kCrtCols != 0) return cudaErrorInvalidValue;  // column blocks stay inside a tile
+  // column-block pairs (y, ncb - 1 - y): 128-aligned row chunks from each
+  // block's diagonal down to row n
   const int64_t ncb = (ncols + kCrtCols - 1) / kCrtCols;
   if ((ncb + 1) / 2 > 65535) return cudaErrorInvalidConfiguration;
-  auto chunks = [&](int64_t cb) { return (p.n - (p.n0 + cb * kCrtCols) + kCrtRows - 1) / kCrtRows; };
+  auto chunks = [&](int64_t cb) {
+    const int64_t cs = p.n0 + cb * kCrtCols;
+    return (p.n - 1) / kCrtRows - cs / kCrtRows + 1;
+  };
   int64_t most = 0;
   for (int64_t y = 0; y < (ncb + 1) / 2; ++y) {
     const int64_t yb = ncb - 1 - y;

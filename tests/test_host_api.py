@@ -248,3 +248,48 @@ def test_int8_crt_fraction_reconstruction():
             for got, want in ((got_re, x_re), (got_im, x_im)):
                 tol = 4 * math.ulp(float(want)) + big_m * 2.0 ** -66
                 assert abs(got - want) <= tol, (n_mod, want, got)
+
+
+def test_int8_residue_dp4a_arithmetic():
+    # CPU restatement of csrc/ozaki.cu's residue planes: x' (|x'| <= 2^55, an
+    # exact double) split into lo + (hi - 2^31) 2^32 by a round-down magic add,
+    # eight unsigned bytes dotted with the packed weights (mult 2^(8d) mod p) by
+    # dp4a, phi1,2 = X +- Y reduced by the exact integer quotient
+    # floor((v m + 2^31) / 2^32), m = rn(2^32 / p).  Includes the tie inputs
+    # (x' = 2^31 mod 2^32) that a round-to-nearest split would break.
+    import math
+    import random
+    import struct
+
+    from paper_1611_00606_b200.engine import MODULI, SQRT_M1
+
+    magic = 6755399441055744.0
+
+    def lo32(d):
+        return struct.unpack("<Q", struct.pack("<d", d))[0] & 0xFFFFFFFF
+
+    def split(x):
+        hm = math.floor(x * 2.0 ** -32) + magic
+        return lo32((x - (hm - magic) * 4294967296.0) + magic), (lo32(hm) + 0x80000000) & 0xFFFFFFFF
+
+    def dp4a(a, mult, d0, p, c):
+        return c + sum(((a >> (8 * d)) & 0xFF) * _sym(mult * pow(2, 8 * (d0 + d), p), p) for d in range(4))
+
+    def reduce(v, p):
+        return v - p * ((v * (((1 << 32) + p // 2) // p) + (1 << 31)) >> 32)
+
+    rng = random.Random(3)
+    xs = [0.0, 1.0, -1.0, float(2 ** 55), float(-2 ** 55), float(2 ** 31), float(3 * 2 ** 31), float(-(2 ** 31)),
+          9763880150499328.0]
+    xs += [float(rng.randint(-2 ** 55, 2 ** 55) & ~((1 << rng.randint(0, 40)) - 1)) for _ in range(3000)]
+    for x in xs:
+        y = xs[rng.randrange(len(xs))]
+        xl, xh = split(x)
+        yl, yh = split(y)
+        assert ((xh - 2 ** 31) << 32) + xl == int(x)
+        for p, j in zip(MODULI, SQRT_M1):
+            big_x = dp4a(xh, 1, 4, p, dp4a(xl, 1, 0, p, _sym(-pow(2, 63, p), p)))
+            big_y = dp4a(yh, j, 4, p, dp4a(yl, j, 0, p, _sym(-j * pow(2, 63, p), p)))
+            assert abs(big_x) + abs(big_y) < 2 ** 19
+            assert reduce(big_x + big_y, p) == _sym(int(x) + j * int(y), p)
+            assert reduce(big_x - big_y, p) == _sym(int(x) - j * int(y), p)
