@@ -1,12 +1,20 @@
 """Benchmark: H+S build per k-point on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3|C4|C5] [--impl ours|reference]
 
 One step = one full H+S build (Algorithm 1: Loop 1, H1, S1, U norm, S2,
 Loop 2, H2/H3, mirror) for one k-point of the configured synthetic system.
 Under torchrun (N > 1) the atoms are sharded across ranks and each step ends
 with an NCCL reduce-scatter of H and S into 1-D block columns (strong
-scaling: total work fixed).
+scaling: total work fixed).  ``--config C5``: one step = the 16 k-points of
+the C3 system (physical inputs, matching coefficients on the device), dealt
+round robin to the ranks with no communication (strong scaling).
+
+Engine: the default ("auto") runs S and H on the INT8 tensor cores at FP64
+width (every operand rounded to >= 53 bits of its column's max -- a full FP64
+mantissa -- exact int8 residue products, CRT reconstruction; csrc/ozaki.cuh).
+Its error against the CPU oracle is measured in the same run (``accuracy``).
+``--engine dmma`` runs the FP64 DMMA tensor cores instead.
 
 Reported:
   value       model FP64 TFLOP/s of the device-resident path (inputs already
@@ -14,10 +22,13 @@ Reported:
   e2e         same metric through the public drop-in API with host numpy
               inputs and outputs (H2D of every input and D2H of H and S inside
               the timed region)
-  roofline    the dominant kernel (fused H contraction) against the measured
-              FP64 DMMA peak (profiles/fp64_peak_r01.jsonl)
-  cpu_baseline  the oracle's scipy/OpenBLAS restatement of Algorithm 1 on a
-              bounded sample, timed on this host (rank 0, N = 1 only)
+  roofline    the dominant kernel (the fused H contraction's INT8 GEMM, or
+              the DMMA kernel) against its measured tensor peak
+  roofline_coeff  the matching-coefficient kernel against measured HBM bandwidth
+  accuracy    relative Frobenius error of this run's H and S against the CPU
+              oracle (Algorithm 1 on OpenBLAS) and against the DMMA engine
+  cpu_baseline  the oracle's scipy/OpenBLAS restatement of Algorithm 1 on the
+              same instance (full config), timed on this host (rank 0, N = 1)
 
 Model flops = sum of report.section_flops (/root/reference/pkg/src/hsgen/
 report.py:79-105), the reference's closed form.
@@ -46,7 +57,9 @@ CONFIG_DESC = {
     "C2": "NaCl-like cell: 8 atoms / 2 types, lmax=8 (N_L=81), NG=3000",
     "C3": "paper-scale test: 32 atoms / 4 types, lmax=10 (N_L=121), NG=8000",
     "C4": "large supercell: 128 atoms / 4 types, lmax=10 (N_L=121), NG=20000",
+    "C5": "k-point batch: 16 k-points of the 32-atom system (lmax=10, NG~8000 each), physical inputs",
 }
+C5_KPOINTS = 16
 NOMINAL_FP64_TFLOPS = 37.2  # 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz
 
 
@@ -58,15 +71,19 @@ def measured_peaks() -> dict:
 
 
 def int8_peak():
-    """Measured dense INT8 peak: cuBLASLt int8 GEMM burst (probes/int8_peak.py,
-    committed result); fallback 2 x the bf16 burst of MEASURED_PEAKS.json."""
+    """Dense INT8 tensor peak: 2 x the driver-measured dense bf16 burst of
+    MEASURED_PEAKS.json (INT8 runs at twice the bf16 rate on B200); the
+    cuBLASLt int8 GEMM we measured ourselves (probes/int8_peak.py) beside it."""
+    bf16 = measured_peaks().get("bf16_tflops")
+    own = None
     path = ROOT / "profiles" / "int8_peak_r01.json"
     try:
-        rec = json.loads(path.read_text())
-        return rec["int8_tops_burst"], (f"measured cuBLASLt int8 GEMM burst ({path.relative_to(ROOT)}; "
-                                        f"sustained {rec['int8_tops_sustained']:.0f} TOPS under the power cap)")
+        own = json.loads(path.read_text())["int8_tops_burst"]
     except (OSError, ValueError, KeyError):
-        return 2.0 * measured_peaks().get("bf16_tflops", 1644.4), "2 x bf16_tflops of MEASURED_PEAKS.json"
+        pass
+    if bf16:
+        return 2.0 * bf16, "2 x bf16_tflops of MEASURED_PEAKS.json (driver-measured dense bf16 burst)", own
+    return own or 3079.9, f"measured cuBLASLt int8 GEMM burst ({path.relative_to(ROOT)})", own
 
 
 def fp64_peak():
@@ -158,51 +175,254 @@ def shard(n_atoms: int, rank: int, world: int):
     return lo, lo + base + (1 if rank < extra else 0)
 
 
-def cpu_baseline_run(dims_full, sample_ng: int, seed: int, steps: int = 1):
-    """Time the oracle (scipy/OpenBLAS Algorithm 1) on a bounded sample."""
+def cpu_baseline_run(dims_full, sample_ng: int, seed: int, steps: int = 1, nonhpd_fraction: float = 0.0,
+                     instance=None):
+    """Time the oracle (scipy/OpenBLAS Algorithm 1) on the config's instance
+    (``sample_ng`` 0 = the full N_G; a smaller value cuts N_G).  Returns
+    (times, flops, threads, sample, output of the last step)."""
     from oracle import alg1
     from paper_1611_00606_b200 import Dims, ProblemSpec, generate, total_model_flops
 
-    ng = min(sample_ng, dims_full.n_g)
+    ng = dims_full.n_g if sample_ng <= 0 else min(sample_ng, dims_full.n_g)
     d = Dims(dims_full.n_atoms, dims_full.n_l, ng)
-    p = generate(ProblemSpec(d, seed=seed))
-    times = []
+    p = instance if instance is not None and ng == dims_full.n_g else \
+        generate(ProblemSpec(d, seed=seed, nonhpd_fraction=nonhpd_fraction))
+    times, out = [], None
     for _ in range(steps):
         t0 = time.perf_counter()
-        alg1.build_hs_cpu(p)
+        out = alg1.build_hs_cpu(p)
         times.append(time.perf_counter() - t0)
-    flops = total_model_flops(d, 0)
+    flops = total_model_flops(d, out["nonhpd"])
     try:
         from threadpoolctl import threadpool_info
         threads = max((i.get("num_threads", 1) for i in threadpool_info()), default=os.cpu_count())
     except Exception:  # noqa: BLE001
         threads = os.cpu_count()
-    sample = (f"{d.n_atoms} atoms x N_L={d.n_l} x NG={d.n_g} (the config's full atom/lm stack, "
-              f"NG cut to {d.n_g}); scipy-OpenBLAS ZHER2K/ZHERK Algorithm 1 (oracle/alg1.py)")
-    return times, flops, threads, sample
+    cut = "the config's full instance" if ng == dims_full.n_g else f"the config's full atom/lm stack, NG cut to {ng}"
+    sample = (f"{d.n_atoms} atoms x N_L={d.n_l} x NG={d.n_g} ({cut}, seed {seed}); scipy-OpenBLAS "
+              f"ZHER2K/ZHERK/ZGEMM Algorithm 1 (oracle/alg1.py), the same instance the GPU arm builds")
+    return times, flops, threads, sample, out
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the oracle port of the reference CPU path on this host."""
+    """--impl reference: the oracle port of the reference CPU path on this host,
+    on the same config as our arm (C5: the 16 k-points' instance shape, one
+    k-point per step is timed and the step covers 16 of them)."""
     if rank != 0:
         return
     from paper_1611_00606_b200 import CONFIGS
 
-    dims = CONFIGS[args.config]
-    times, flops, threads, sample = cpu_baseline_run(dims, args.cpu_sample_ng, args.seed,
-                                                     steps=args.warmup + args.steps)
+    cfg = "C3" if args.config == "C5" else args.config
+    dims = CONFIGS[cfg]
+    times, flops, threads, sample, _ = cpu_baseline_run(dims, args.cpu_sample_ng, args.seed,
+                                                        steps=args.warmup + args.steps,
+                                                        nonhpd_fraction=args.nonhpd_fraction)
     timed = times[args.warmup:] if len(times) > args.warmup else times
     t = sum(timed) / len(timed)
     value = flops / t / 1e12
+    ms = t * 1e3 * (C5_KPOINTS if args.config == "C5" else 1)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
-        "config": {"workload": args.config, "desc": CONFIG_DESC[args.config], "sample_ng": min(args.cpu_sample_ng, dims.n_g)},
+        "config": {"workload": args.config, "desc": CONFIG_DESC[args.config],
+                   "sample_ng": dims.n_g if args.cpu_sample_ng <= 0 else min(args.cpu_sample_ng, dims.n_g),
+                   "same_config": args.cpu_sample_ng <= 0},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def rel_err_dev(a, b) -> float:
+    """||a - b||_F / (1 + ||b||_F) of two device tensors (matcore.rel_frob_error)."""
+    import torch
+
+    return float(torch.linalg.norm(a - b) / (1.0 + torch.linalg.norm(b)))
+
+
+def coeff_roofline(system, kpt, gset, dev, reps: int = 10) -> dict:
+    """The matching-coefficient kernel alone (hsb_match_coeffs), CUDA events on
+    its stream: algorithmic bytes 2 K N_G 16 (A and B written once; the inputs
+    are KB) per launch against the measured HBM copy bandwidth."""
+    import torch
+
+    from paper_1611_00606_b200 import physics
+
+    n_g, k = int(gset.shape[0]), system.n_atoms * system.n_l
+    a = torch.empty((n_g, k), dtype=torch.complex128, device=dev)
+    b = torch.empty_like(a)
+    for _ in range(3):
+        physics.match_coeffs_device(system, kpt, gset, dev.index, out=(a, b))
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        physics.match_coeffs_device(system, kpt, gset, dev.index, out=(a, b))
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / reps
+    bytes_ = 2 * k * n_g * 16
+    peak = measured_peaks().get("hbm_gbs", 6546.9)
+    traffic = None
+    prof = ROOT / "profiles" / "roofline_traffic.json"
+    try:
+        rec = json.loads(prof.read_text()).get("C3/match")
+        traffic = rec["bytes"] if rec and n_g == rec.get("n_g") else None
+    except (OSError, ValueError):
+        pass
+    return {"bound": "hbm", "kernel": "match_coeffs_kernel (A, B from Y_lm, j_l, j_l', e^{iK.tau})",
+            "achieved": bytes_ / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+            "frac": bytes_ / (ms * 1e-3) / 1e9 / peak, "traffic": traffic,
+            "peak_source": "hbm_gbs of MEASURED_PEAKS.json (driver-measured copy bandwidth)",
+            "algorithmic_bytes_per_launch": bytes_, "avg_launch_ms": ms, "n_g": n_g, "k": k}
+
+
+def c5_kpoints():
+    """The 16 k-points of config C5: a 4 x 2 x 2 grid (fractional, centred
+    cells), SURVEY.md 8(d)."""
+    return [np.array([(i + 0.5) / 4 - 0.5, (j + 0.5) / 2 - 0.5, (l + 0.5) / 2 - 0.5])
+            for i in range(4) for j in range(2) for l in range(2)]
+
+
+def run_c5(args, world, rank, dev, dev_index):
+    """C5: 16 independent k-points of the C3 system from physical inputs
+    (matching coefficients on the device), dealt round robin to the ranks
+    (distributed.kpoint_assignment): no communication.  One step = all 16
+    k-points; value = their model flops / max-over-ranks step time."""
+    import torch
+
+    from paper_1611_00606_b200 import CONFIGS, Dims, GpuPolicy, physics, section_flops
+    from paper_1611_00606_b200 import distributed as hsdist
+    from paper_1611_00606_b200.pipeline import DeviceProblem, build_hs_device
+
+    c3 = CONFIGS["C3"]
+    lmax = int(round(c3.n_l ** 0.5)) - 1
+    system, _k0, kmax, _ = physics.synthetic_system(c3.n_atoms, 4, lmax, c3.n_g, seed=args.seed)
+    t_aa, t_ab, t_bb = physics.synthetic_t_matrices(system, seed=args.seed)
+    kpts = c5_kpoints()
+    gsets = [physics.gvector_set(system.lattice, k, kmax) for k in kpts]
+    flops = [float(sum(section_flops(Dims(c3.n_atoms, c3.n_l, int(g.shape[0])), 0).values())) for g in gsets]
+    mine = hsdist.kpoint_assignment(len(kpts), world, rank)
+    policy = GpuPolicy(device=dev_index, engine=args.engine)
+    int8 = args.engine != "dmma"
+    k_rows = system.n_atoms * system.n_l
+    n_max = max(int(g.shape[0]) for g in gsets)
+    abuf = torch.empty(n_max * k_rows, dtype=torch.complex128, device=dev)
+    bbuf = torch.empty_like(abuf)
+    hbuf = torch.empty(n_max * n_max, dtype=torch.complex128, device=dev)
+    sbuf = torch.empty_like(hbuf)
+    t_dev = physics._device_t(system, t_aa, t_ab, t_bb, dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def one(i):
+        n = int(gsets[i].shape[0])
+        a, b = abuf[: n * k_rows].view(n, k_rows), bbuf[: n * k_rows].view(n, k_rows)
+        physics.match_coeffs_device(system, kpts[i], gsets[i], dev_index, out=(a, b))
+        dp = DeviceProblem(Dims(system.n_atoms, system.n_l, n), a, b, *t_dev)
+        return build_hs_device(dp, hbuf[: n * n].view(n, n), sbuf[: n * n].view(n, n), policy)[3]
+
+    def step():
+        return [one(i) for i in mine]
+
+    for _ in range(args.warmup):
+        step()
+    hsdist.barrier(dev)
+    sampler = ClockSampler(dev_index)
+    sampler.start()
+    sampler.wait_first()
+    step()
+    hsdist.barrier(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler.begin()
+    e0.record(stream)
+    ts = [step() for _ in range(args.steps)]
+    e1.record(stream)
+    hsdist.barrier(dev)
+    sampler.end()
+    clocks = sampler.stop()
+    ms = hsdist.max_over_ranks(e0.elapsed_time(e1) / args.steps, dev)
+    value = sum(flops) / (ms * 1e-3) / 1e12
+    last = ts[-1][-1] if ts and ts[-1] else None
+    launches = sum(int(t["launches"]) for st in ts for t in st)
+
+    # end to end: this rank's k-points through the public physical entry point,
+    # H and S to pinned host memory, host wall time, max over ranks
+    e2e = None
+    if not args.no_e2e:
+        del abuf, bbuf, hbuf, sbuf
+        torch.cuda.empty_cache()
+        from paper_1611_00606_b200 import _lib as hsb_lib
+
+        hsb_lib.trim_all(dev_index)
+        depth = int(os.environ.get("HSB_PHYS_DEPTH", "3"))
+        mk, mg = [kpts[i] for i in mine], [gsets[i] for i in mine]
+        for o in physics.iter_hs_physical_kpoints(system, mk[: depth + 1], mg[: depth + 1], t_aa, t_ab, t_bb,
+                                                  policy, depth=depth):
+            del o  # warm contexts and the pinned cache
+        hsdist.barrier(dev)
+        t0 = time.perf_counter()
+        d2h = 0
+        for _ in range(args.steps):
+            for hh, sh, _, tp, _ in physics.iter_hs_physical_kpoints(system, mk, mg, t_aa, t_ab, t_bb, policy,
+                                                                     depth=depth):
+                _ = hh[-1, 0], sh[-1, 0]
+                d2h += int(tp["d2h_bytes"])
+                del hh, sh
+        wall_ms = (time.perf_counter() - t0) / args.steps * 1e3
+        e2e_ms = hsdist.max_over_ranks(wall_ms, dev)
+        t_bytes = sum(np.asarray(x).nbytes for m in (t_aa, t_ab, t_bb) for x in m) + 8 * k_rows
+        h2d = t_bytes + sum(g.nbytes for g in mg)
+        e2e = {"value": sum(flops) / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h / args.steps),
+               "api": f"physics.iter_hs_physical_kpoints(this rank's {len(mine)} k-points, depth={depth}) per step, "
+                      "host wall time, max over ranks; H and S to pinned host memory"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        times, fl, threads, sample, _ = cpu_baseline_run(CONFIGS["C3"], args.cpu_sample_ng, args.seed, steps=1)
+        cpu = {"value": fl / times[-1] / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "port",
+               "sample": "one C3-shaped k-point: " + sample, "seconds": times[-1]}
+
+    roof = None
+    if last is not None:
+        from paper_1611_00606_b200 import int8_gemm_ops, int8_moduli
+
+        n_g = int(gsets[mine[-1]].shape[0])
+        k_tot = 2 * k_rows
+        if int8:
+            peak_tops, peak_src, _own = int8_peak()
+            alg = int8_gemm_ops(n_g, k_tot)
+            roof = {"bound": "tensor", "kernel": "ozaki_gemm_kernel of the fused H (last k-point of the step)",
+                    "achieved": alg / last["h_core"] / 1e12, "peak": peak_tops, "unit": "TOPS (int8)",
+                    "frac": alg / last["h_core"] / 1e12 / peak_tops, "peak_source": peak_src,
+                    "moduli_bits": list(int8_moduli(k_tot)), "avg_launch_ms": last["h_core"] * 1e3, "traffic": None}
+        else:
+            peak, src = fp64_peak()
+            alg = 6 * k_tot * (n_g * (n_g + 1) // 2)
+            roof = {"bound": "tensor", "kernel": "zrk3m_kernel fused H (last k-point of the step)",
+                    "achieved": alg / last["h_core"] / 1e12, "peak": peak, "unit": "TFLOP/s",
+                    "frac": alg / last["h_core"] / 1e12 / peak, "peak_source": src,
+                    "avg_launch_ms": last["h_core"] * 1e3, "traffic": None}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": ("c128 in/out, FP64 width: S and H as exact int8 residue GEMMs of operands rounded to "
+                      ">= 53 bits of their column's max (CRT in f64)" if int8 else "c128 (f64 DMMA)"),
+            "data": "synthetic physical system (seeded lattice, atoms, radial data, T matrices); "
+                    "A and B from the device matching kernel",
+            "config": {"workload": "C5", "desc": CONFIG_DESC["C5"], "kpoints": len(kpts),
+                       "kpoint_grid": "4x2x2", "n_g_per_kpoint": [int(g.shape[0]) for g in gsets],
+                       "kpoints_per_rank": [len(hsdist.kpoint_assignment(len(kpts), world, r)) for r in range(world)],
+                       "parallelism": f"k-point replicas x{world} (no communication)",
+                       "engine": "int8 (FP64 width)" if int8 else "dmma",
+                       "model_tflop_per_step": sum(flops) / 1e12,
+                       "l2_note": "inputs larger than L2 (A/B stacks ~0.5 GB each per k-point)"},
+            "gpu_launches": launches, "roofline": roof, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
 
 
 def main():
@@ -217,7 +437,7 @@ def main():
     ap.add_argument("--unfused", action="store_true", help="one launch per reference section")
     ap.add_argument("--complex-mult", default="3m", choices=["3m", "4m"],
                     help="real-product form of the complex contractions (3 or 4 DMMA products)")
-    ap.add_argument("--engine", default="int8", choices=["int8", "dmma"],
+    ap.add_argument("--engine", default="auto", choices=["auto", "int8", "dmma"],
                     help="S/H contractions on the INT8 tensor cores (CRT emulation, ~1e-12) or FP64 DMMA")
     ap.add_argument("--no-compare", action="store_true", help="skip the second-engine measurement")
     ap.add_argument("--rs", default="nccl", choices=["nccl", "fused"],
@@ -225,7 +445,7 @@ def main():
                          "reconstruction epilogue into CUDA-IPC peer slots (INT8 engine)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-ng", type=int, default=4000)
+    ap.add_argument("--cpu-sample-ng", type=int, default=0, help="0: the full config (same instance)")
     ap.add_argument("--pageable-inputs", action="store_true",
                     help="e2e with ordinary numpy inputs instead of pinned host buffers")
     args = ap.parse_args()
@@ -236,6 +456,7 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    int8 = args.engine != "dmma"  # "auto": the INT8 engine at FP64 width
 
     import torch
     import torch.distributed as dist
@@ -255,6 +476,11 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
+    if args.config == "C5":
+        run_c5(args, world, rank, dev, dev_index)
+        if world > 1:
+            dist.destroy_process_group()
+        return
     dims = CONFIGS[args.config]
     lo, hi = shard(dims.n_atoms, rank, world)
     local = Dims(hi - lo, dims.n_l, dims.n_g)
@@ -277,7 +503,7 @@ def main():
     slots = hsdist.PeerSlots.group(n_g, dev) if world > 1 and args.rs == "fused" else None
 
     def step(pol=policy):
-        if world > 1 and slots is not None and pol.engine == "int8":
+        if world > 1 and slots is not None and pol.engine != "dmma":
             hsdist.build_hs_sharded_fused(dp, slots, pol)
             return None
         if world > 1:
@@ -322,25 +548,28 @@ def main():
     h_core = statistics.mean(t["h_core"] for t in ts)
     k_l = local.n_atoms * local.n_l
     k_tot_h = 2 * k_l  # H = A^H V1 + B^H V2 (V1 = T_AA A + T_AB B, V2 = T_AB^H A + T_BB B)
-    if args.engine == "int8":
+    peak64, peak64_src = fp64_peak()
+    if int8:
         from paper_1611_00606_b200 import int8_gemm_ops, int8_moduli
 
         n_mod, bits = int8_moduli(k_tot_h)
         alg = int8_gemm_ops(n_g, k_tot_h)
-        peak_tops, peak_src = int8_peak()
+        peak_tops, peak_src, own_peak = int8_peak()
         roof = {"bound": "tensor",
                 "kernel": "ozaki_gemm_kernel (tcgen05.mma.cta_group::2.kind::i8, TMA, TMEM) of the fused H "
-                          "= A^H V1 + B^H V2, INT8 CRT emulation",
+                          "= A^H V1 + B^H V2, INT8 engine at FP64 width",
                 "achieved": alg / h_core / 1e12, "peak": peak_tops, "unit": "TOPS (int8)",
                 "frac": alg / h_core / 1e12 / peak_tops,
                 "peak_source": peak_src,
+                "frac_vs_measured_cublaslt_int8": alg / h_core / 1e12 / own_peak if own_peak else None,
                 "algorithmic_ops_per_launch": alg,
                 "op_form": f"2 real products (split complex) x {n_mod} moduli x K_tot {k_tot_h} x N(N+1)/2, 2 ops per MAC "
-                           f"(operands rounded to {bits} bits)",
+                           f"(operands rounded to {bits} bits of their column's max)",
                 "model_flops_per_launch": h_flops, "model_tflops": h_flops / h_core / 1e12,
+                "model_tflops_vs_fp64_dmma_peak": h_flops / h_core / 1e12 / peak64,
+                "fp64_dmma_peak": peak64, "fp64_peak_source": peak64_src,
                 "avg_launch_ms": h_core * 1e3}
     else:
-        peak, peak_src = fp64_peak()
         # algorithmic flops of the form that runs: K_tot complex MACs per element of
         # the lower triangle; 3M spends 3 real MACs per complex MAC (6 flops), 4M 4 (8)
         alg = (6 if args.complex_mult == "3m" else 8) * k_tot_h * (n_g * (n_g + 1) // 2)
@@ -348,8 +577,8 @@ def main():
         roof = {"bound": "tensor",
                 "kernel": ("zrk3m_kernel<conj,planes>" if args.complex_mult == "3m" else "zrk_kernel<conj>")
                 + " fused H = A^H V1 + B^H V2",
-                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "peak_source": peak_src,
+                "achieved": achieved, "peak": peak64, "unit": "TFLOP/s", "frac": achieved / peak64,
+                "peak_source": peak64_src,
                 "algorithmic_flops_per_launch": alg,
                 "flop_form": (f"3M: 6 real flops per complex MAC x K_tot {k_tot_h} x N(N+1)/2"
                               if args.complex_mult == "3m" else f"4M: 8 flops per complex MAC x K_tot {k_tot_h} x N(N+1)/2"),
@@ -360,16 +589,20 @@ def main():
     prof = ROOT / "profiles" / "roofline_traffic.json"
     if prof.exists():
         try:
-            key = f"{args.config}/int8" if args.engine == "int8" else f"{args.config}/{args.complex_mult}"
+            key = f"{args.config}/int8" if int8 else f"{args.config}/{args.complex_mult}"
             rec = json.loads(prof.read_text()).get(key)
             traffic = rec["bytes"] if rec else None
         except ValueError:
             traffic = None
 
     # ---------------------------------------------- the other engine, same run
+    # (and the two engines' results compared: the headline's H, S are kept)
     other = None
+    accuracy = {}
+    if world == 1:
+        h_main, s_main = h[:n_g].clone(), s[:n_g].clone()
     if not args.no_compare:
-        alt = "dmma" if args.engine == "int8" else "int8"
+        alt = "dmma" if int8 else "int8"
         pol2 = GpuPolicy(device=dev_index, fused=not args.unfused, complex_mult=args.complex_mult, engine=alt)
         for _ in range(args.warmup):
             step(pol2)
@@ -382,6 +615,12 @@ def main():
         barrier()
         ms2 = hsdist.max_over_ranks(e0.elapsed_time(e1) / args.steps, dev)
         other = {"engine": alt, "ms_per_step": ms2, "value": flops_full / (ms2 * 1e-3) / 1e12, "unit": "TFLOP/s"}
+        if world == 1:
+            accuracy[f"vs_{alt}_engine"] = {"h": rel_err_dev(h_main, h[:n_g]), "s": rel_err_dev(s_main, s[:n_g])}
+    if world == 1:
+        h_host = np.asfortranarray(h_main.cpu().numpy().T)  # column-major matrices
+        s_host = np.asfortranarray(s_main.cpu().numpy().T)
+        del h_main, s_main
 
     # ------------------------------------------------------------ end to end
     e2e = None
@@ -457,7 +696,7 @@ def main():
     # coefficients on the device, H and S out in pinned host memory: K distinct
     # k-points of the config's system (ragged G sets, ~N_G each; config C5's
     # shape) through physics.iter_hs_physical_kpoints
-    e2e_phys = None
+    e2e_phys = coeff = None
     if world == 1 and not args.no_e2e:
         from paper_1611_00606_b200 import physics
 
@@ -470,6 +709,7 @@ def main():
         gsets = [physics.gvector_set(system.lattice, k, kmax) for k in kpts]
         flops_p = sum(float(sum(section_flops(Dims(dims.n_atoms, dims.n_l, int(g.shape[0])), 0).values()))
                       for g in gsets)
+        coeff = coeff_roofline(system, kpts[0], gsets[0], dev)
         depth_p = int(os.environ.get("HSB_PHYS_DEPTH", "3"))
         try:
             # warm contexts and the pinned cache at the largest G set of the batch
@@ -503,30 +743,42 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        times, flops, threads, sample = cpu_baseline_run(dims, args.cpu_sample_ng, args.seed, steps=1)
+        from paper_1611_00606_b200 import rel_frob_error
+
+        times, flops, threads, sample, ref = cpu_baseline_run(dims, args.cpu_sample_ng, args.seed, steps=1,
+                                                              nonhpd_fraction=args.nonhpd_fraction, instance=p)
         cpu = {"value": flops / times[-1] / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "port",
                "sample": sample, "seconds": times[-1]}
+        if ref["h"].shape == h_host.shape:  # the same instance: parity in the same run
+            accuracy["vs_cpu_oracle"] = {"h": rel_frob_error(h_host, ref["h"]), "s": rel_frob_error(s_host, ref["s"]),
+                                         "metric": "||X - X_oracle||_F / (1 + ||X_oracle||_F) (matcore.rel_frob_error)",
+                                         "oracle": "oracle/alg1.py (Algorithm 1 on scipy/OpenBLAS, complex128)"}
+        del ref
+    if world == 1:
+        del h_host, s_host
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None,
-            "dtype": ("c128 in/out; S/H products as exact int8 residue GEMMs (CRT), f64 reconstruction"
-                      if args.engine == "int8" else "c128 (f64 DMMA)"),
+            "dtype": ("c128 in/out, FP64 width: S and H as exact int8 residue GEMMs of operands rounded to "
+                      ">= 53 bits of their column's max (17 moduli, CRT in f64)" if int8 else "c128 (f64 DMMA)"),
             "data": "synthetic (seeded hsgen-compatible generator)",
             "config": {"workload": args.config, "desc": CONFIG_DESC[args.config], "n_atoms": dims.n_atoms,
                        "n_l": dims.n_l, "n_g": dims.n_g, "nonhpd_fraction": args.nonhpd_fraction,
                        "parallelism": f"atom-shard x{world}" + ((" + fused peer scatter" if args.rs == "fused" else
                                                                       " + NCCL reduce-scatter") if world > 1 else ""),
-                       "fused": not args.unfused, "engine": args.engine, "complex_mult": args.complex_mult, "model_tflop_per_step": flops_full / 1e12,
+                       "fused": not args.unfused, "engine": ("int8 (FP64 width)" if int8 else "dmma"),
+                       "complex_mult": args.complex_mult, "model_tflop_per_step": flops_full / 1e12,
                        "l2_note": "inputs larger than L2 (A/B stacks 496 MB each at C3)"},
             "gpu_launches": launches,
             "roofline": dict(roof, traffic=traffic, h_section_ms=h_sec * 1e3,
                              s_section_model_tflops=(sect["S1"] + sect["S2"]) / s_sec / 1e12),
             "sections_ms": {k: statistics.mean(t[k] for t in ts) * 1e3
                             for k in ("loop1", "h1", "s1", "unorm", "s2", "loop2", "h2", "h3", "total")},
-            "e2e": e2e, "e2e_physical": e2e_phys, "cpu_baseline": cpu, "clocks": clocks, "other_engine": other,
+            "e2e": e2e, "e2e_physical": e2e_phys, "roofline_coeff": coeff, "accuracy": accuracy or None,
+            "cpu_baseline": cpu, "clocks": clocks, "other_engine": other,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
