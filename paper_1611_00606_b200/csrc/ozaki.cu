@@ -2,6 +2,8 @@
 // (scheme in ozaki.cuh): column exponents, split-complex residue planes, the
 // tcgen05 kind::i8 modular GEMM over lower-triangle tiles, and the CRT
 // reconstruction with the Hermitian mirror.
+#include <cudaTypedefs.h>
+
 #include <climits>
 #include <cmath>
 #include <cstring>
@@ -176,10 +178,11 @@ __device__ __forceinline__ void oz_planes(uint32_t xl, uint32_t xh, uint32_t yl,
   u = oz_sym_reduce<I>(X + Y);  // phi1 = x' + j y'
   w = oz_sym_reduce<I>(X - Y);  // phi2 = x' - j y'
 }
+// the planes of modulus I .. NM-1 for this thread's 4 elements, as 32-bit
+// shared stores at compile-time offsets (plane q = (product, modulus), 1 KB each)
 template <int NM, int I = 0>
 __device__ __forceinline__ void oz_residue_planes(const uint32_t (&xl)[4], const uint32_t (&xh)[4],
-                                                  const uint32_t (&yl)[4], const uint32_t (&yh)[4], int8_t* o0,
-                                                  int8_t* o1, int64_t mod_stride) {
+                                                  const uint32_t (&yl)[4], const uint32_t (&yh)[4], uint32_t* s0) {
   if constexpr (I < NM) {
     int u[4], w[4];
 #pragma unroll
@@ -187,52 +190,65 @@ __device__ __forceinline__ void oz_residue_planes(const uint32_t (&xl)[4], const
     const auto pack = [](const int* v) {
       return __byte_perm(__byte_perm(v[0], v[1], 0x40), __byte_perm(v[2], v[3], 0x40), 0x5410);
     };
-    *reinterpret_cast<uint32_t*>(o0) = pack(u);
-    *reinterpret_cast<uint32_t*>(o1) = pack(w);
-    oz_residue_planes<NM, I + 1>(xl, xh, yl, yh, o0 + mod_stride, o1 + mod_stride, mod_stride);
+    s0[I * 256] = pack(u);
+    s0[(NM + I) * 256] = pack(w);
+    oz_residue_planes<NM, I + 1>(xl, xh, yl, yh, s0);
   }
 }
 
-// thread = 4 consecutive k of one column; writes 4 bytes into each of the
-// 2 planes x NM moduli: out[((plane * NM + i) * cols + col) * kpad + k],
+// Block = 8 columns (one per warp) x 128 k; lane l owns k = 4l .. 4l+3 of its
+// warp's column (coalesced 16-byte loads).  The planes are assembled in
+// shared memory as [plane][modulus][column][128 k] -- 32-bit stores at
+// compile-time offsets -- and written by one TMA bulk tensor store of the box
+// {128 k, 8 columns, NM moduli, 2 planes} into the [plane][modulus][col][kpad]
+// buffer (out-of-range k / columns clipped by the TMA unit): no per-store
+// 64-bit address arithmetic, full-line DRAM writes.
 // plane 0 = phi1(z') = x' + j y', plane 1 = phi2(z') = x' - j y' (mod p_i)
 constexpr int kOzResK = 4;
+constexpr int kOzResCols = 8;
+constexpr int kOzResKBlk = 128;
 template <int NM>
-__global__ void __launch_bounds__(128, 6) ozaki_residue_kernel(const double2* __restrict__ x, int64_t ldx, int64_t k,
+__global__ void __launch_bounds__(256, 3) ozaki_residue_kernel(const __grid_constant__ CUtensorMap out_map,
+                                                            const double2* __restrict__ x, int64_t ldx, int64_t k,
                                                             int64_t cols, const int32_t* __restrict__ col_exp, int b,
-                                                            int8_t* __restrict__ out, int64_t kpad,
                                                             const double* __restrict__ rscale) {
-  const int64_t k0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kOzResK;
-  if (k0 >= kpad) return;
-  const int64_t mod_stride = cols * kpad;
-  const int64_t plane_stride = NM * mod_stride;
-  for (int64_t c = blockIdx.y; c < cols; c += gridDim.y) {
+  __shared__ __align__(128) uint32_t tile[2 * NM * kOzResCols * kOzResKBlk / 4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * kOzResKBlk + kOzResK * lane;
+  const int64_t c = static_cast<int64_t>(blockIdx.y) * kOzResCols + warp;
+  uint32_t xl[kOzResK] = {}, xh[kOzResK] = {}, yl[kOzResK] = {}, yh[kOzResK] = {};
+  if (c < cols) {
     // x * 2^(b - e) in two exact power-of-two steps (each factor stays finite)
     const int sh = b - __ldg(col_exp + c);
     const double s1 = pow2i(sh / 2), s2 = pow2i(sh - sh / 2);
-    double xr[kOzResK], xi[kOzResK];
 #pragma unroll
     for (int j = 0; j < kOzResK; ++j) {
+      double xr = 0.0, xi = 0.0;
       if (k0 + j < k) {
         double2 v = x[c * ldx + k0 + j];
         if (rscale) {  // fl(u x), as diag_scale_kernel rounds it
           const double u = __ldg(rscale + k0 + j);
           v = make_double2(u * v.x, u * v.y);
         }
-        xr[j] = rint((v.x * s1) * s2);
-        xi[j] = rint((v.y * s1) * s2);
-      } else {
-        xr[j] = xi[j] = 0.0;
+        xr = rint((v.x * s1) * s2);
+        xi = rint((v.y * s1) * s2);
       }
+      oz_split(xr, xl[j], xh[j]);
+      oz_split(xi, yl[j], yh[j]);
     }
-    uint32_t xl[kOzResK], xh[kOzResK], yl[kOzResK], yh[kOzResK];
-#pragma unroll
-    for (int j = 0; j < kOzResK; ++j) {
-      oz_split(xr[j], xl[j], xh[j]);
-      oz_split(xi[j], yl[j], yh[j]);
-    }
-    int8_t* o0 = out + c * kpad + k0;
-    oz_residue_planes<NM>(xl, xh, yl, yh, o0, o0 + plane_stride, mod_stride);
+  }
+  // (columns past the end store zeros; the TMA store clips them anyway)
+  oz_residue_planes<NM>(xl, xh, yl, yh, tile + (warp * kOzResKBlk) / 4 + lane);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> TMA reads
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];\n\t"
+        "cp.async.bulk.commit_group;\n\t"
+        "cp.async.bulk.wait_group.read 0;" ::"l"(reinterpret_cast<uint64_t>(&out_map)),
+        "r"(static_cast<int>(blockIdx.x) * kOzResKBlk), "r"(static_cast<int>(blockIdx.y) * kOzResCols), "r"(0),
+        "r"(0), "r"(smem_u32(tile))
+        : "memory");
   }
 }
 
@@ -1013,16 +1029,43 @@ cudaError_t launch_ozaki_colexp_ab(const double* a, const double* b, int64_t ld,
   return cudaGetLastError();
 }
 
+// the driver's cuTensorMapEncodeTiled (through the runtime: no -lcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 oz_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &f, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
 cudaError_t launch_ozaki_residues(const double* x, int64_t ldx, int64_t k, int64_t cols, const int32_t* col_exp,
                                   int b, int n_mod, int8_t* out, int64_t kpad, cudaStream_t st, const double* rscale) {
   if (cols <= 0 || kpad <= 0) return cudaSuccess;
-  const int64_t threads_k = kpad / kOzResK;
-  dim3 grid(static_cast<unsigned>((threads_k + 127) / 128), static_cast<unsigned>(cols < 65535 ? cols : 65535));
+  if (kpad % 16 != 0 || (cols + kOzResCols - 1) / kOzResCols > 65535) return cudaErrorInvalidValue;
+  const PFN_cuTensorMapEncodeTiled_v12000 encode = oz_encode_fn();
+  if (!encode) return cudaErrorNotSupported;
+  // out[plane][modulus][col][kpad] as a 4-D uint8 tensor; box = one block's tile
+  CUtensorMap map;
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(kpad), static_cast<cuuint64_t>(cols),
+                              static_cast<cuuint64_t>(n_mod), 2};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(kpad), static_cast<cuuint64_t>(kpad * cols),
+                                 static_cast<cuuint64_t>(kpad * cols * n_mod)};
+  const cuuint32_t box[4] = {kOzResKBlk, kOzResCols, static_cast<cuuint32_t>(n_mod), 2}, es[4] = {1, 1, 1, 1};
+  if (encode(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, out, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+      CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  const dim3 grid(static_cast<unsigned>((kpad + kOzResKBlk - 1) / kOzResKBlk),
+                  static_cast<unsigned>((cols + kOzResCols - 1) / kOzResCols));
   const double2* xx = reinterpret_cast<const double2*>(x);
   switch (n_mod) {
 #define HSB_OZ_RES(NM) \
   case NM:             \
-    ozaki_residue_kernel<NM><<<grid, 128, 0, st>>>(xx, ldx, k, cols, col_exp, b, out, kpad, rscale); \
+    ozaki_residue_kernel<NM><<<grid, 256, 0, st>>>(map, xx, ldx, k, cols, col_exp, b, rscale); \
     break;
     HSB_OZ_RES(11) HSB_OZ_RES(12) HSB_OZ_RES(13) HSB_OZ_RES(14) HSB_OZ_RES(15) HSB_OZ_RES(16)
     HSB_OZ_RES(17) HSB_OZ_RES(18) HSB_OZ_RES(19) HSB_OZ_RES(20)
