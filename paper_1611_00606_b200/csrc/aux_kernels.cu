@@ -127,6 +127,22 @@ __global__ void conj_transpose_kernel(const double2* __restrict__ t, double2* __
   }
 }
 
+// out_a[k, r] = t_a[k, r] / u[a n + r]: per-atom n x n blocks with column r
+// divided by the atom's u_r (correctly rounded), so that L^H R yields rows
+// scaled by 1/u (the INT8 engine's H = A^H V1 + (UB)^H (U^-1 V2) regrouping)
+__global__ void scale_cols_inv_kernel(const double2* __restrict__ t, double2* __restrict__ out,
+                                      const double* __restrict__ u, int n, int64_t count) {
+  const int64_t nn = static_cast<int64_t>(n) * n;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < count * nn;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t a = idx / nn;
+    const int r = static_cast<int>((idx - a * nn) / n);
+    const double d = u[a * n + r];
+    const double2 w = t[idx];
+    out[idx] = make_double2(w.x / d, w.y / d);
+  }
+}
+
 // dst[r, g] = u[r] * src[r, g]   (kernels.diag_scale, kernels.py:328-339)
 __global__ void diag_scale_kernel(const double2* __restrict__ src, int64_t lds,
                                   double2* __restrict__ dst, int64_t ldd,
@@ -291,6 +307,15 @@ cudaError_t launch_conj_transpose(const double* t, double* out, int n, int64_t c
   if (total <= 0) return cudaSuccess;
   conj_transpose_kernel<<<grid_for(total, 256, 148 * 16), 256, 0, st>>>(reinterpret_cast<const double2*>(t),
                                                                          reinterpret_cast<double2*>(out), n, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scale_cols_inv(const double* t, double* out, const double* u, int n, int64_t count,
+                                  cudaStream_t st) {
+  const int64_t total = count * static_cast<int64_t>(n) * n;
+  if (total <= 0) return cudaSuccess;
+  scale_cols_inv_kernel<<<grid_for(total, 256, 148 * 16), 256, 0, st>>>(
+      reinterpret_cast<const double2*>(t), reinterpret_cast<double2*>(out), u, n, count);
   return cudaGetLastError();
 }
 

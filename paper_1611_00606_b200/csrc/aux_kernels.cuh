@@ -44,6 +44,9 @@ cudaError_t launch_half_mirror(const double* t, double* out, int n, int64_t coun
                                cudaStream_t st);
 // out_a = T_a^H for count consecutive n x n complex matrices
 cudaError_t launch_conj_transpose(const double* t, double* out, int n, int64_t count, cudaStream_t st);
+// out_a = t_a diag(1 / u_a) for per-atom n x n blocks (u: count * n entries)
+cudaError_t launch_scale_cols_inv(const double* t, double* out, const double* u, int n, int64_t count,
+                                  cudaStream_t st);
 cudaError_t launch_diag_scale(const double* src, int64_t lds, double* dst, int64_t ldd, const double* u,
                               int64_t rows, int64_t cols, cudaStream_t st);
 cudaError_t launch_mirror(double* c, int64_t ldc, int n, cudaStream_t st);

@@ -761,6 +761,14 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   const bool int8_v = int8_v_env && !unfused && ctx->engine == HSB_ENGINE_INT8 && 2 * nl <= 256;
   // INT8 engine, fused paths: shared left exponent / A residues (oz_left below)
   const bool oz_share = !unfused && ctx->engine == HSB_ENGINE_INT8 && !int8_v;
+  // ... and H regrouped as A^H V1 + (UB)^H W2 with W2 = U^-1 V2 (the rows of V2
+  // divided by u: B^H V2 = B^H U U^-1 V2), so H's left operands are exactly S's
+  // (A and UB, one shared exponent): their residue planes serve both
+  // contractions and B's own residue pass disappears.  W2 comes out of the V
+  // products directly: the columns of V2's left blocks (T_AB, T_BB) are divided
+  // by u first (per-atom 121 x 121 blocks; one correctly rounded division each).
+  static const bool no_h_ub = std::getenv("HSB_NO_H_UB") != nullptr;  // A/B experiments
+  const bool h_via_ub = oz_share && u_fused && !no_h_ub;
   int32_t* oz_er_v = nullptr;  // H's right exponents from the V products' epilogue
   auto vloop = [&]() -> hsb_status {
     if (int8_v) return HSB_OK;
@@ -771,6 +779,19 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     CK(launch_half_mirror(TBB, static_cast<double*>(pbb), static_cast<int>(nl), na, 1.0, st));
     CK(launch_conj_transpose(TAB, static_cast<double*>(tab_h), static_cast<int>(nl), na, st));
     launches += 3;
+    const double* v2_l0 = TAB;                              // (T_AB^H)^H
+    const double* v2_l1 = static_cast<const double*>(pbb);  // T_BB^H = T_BB
+    if (h_via_ub) {  // W2 = U^-1 V2: V2's left blocks with their columns divided by u
+      void *tab_s, *tbb_s;
+      CKS(ws(ctx, "tab_u", tblk_bytes * na, &tab_s));
+      CKS(ws(ctx, "tbb_u", tblk_bytes * na, &tbb_s));
+      CK(launch_scale_cols_inv(TAB, static_cast<double*>(tab_s), U, static_cast<int>(nl), na, st));
+      CK(launch_scale_cols_inv(static_cast<const double*>(pbb), static_cast<double*>(tbb_s), U,
+                               static_cast<int>(nl), na, st));
+      launches += 2;
+      v2_l0 = static_cast<const double*>(tab_s);
+      v2_l1 = static_cast<const double*>(tbb_s);
+    }
     // INT8 engine: the V products' epilogue also yields H's right column
     // exponents (max over V1 and V2), so no separate exponent pass reads them
     static const bool no_vexp = std::getenv("HSB_NO_VEXP") != nullptr;  // A/B experiments
@@ -784,8 +805,8 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     for (int half = 0; half < 2; ++half) {  // zrk form: sum_s L_s^H R_s
       ZrkCall z;
       z.col_exp = oz_er_v;
-      const double* l0 = half == 0 ? static_cast<const double*>(taa_full) : TAB;              // T_AA | (T_AB^H)^H
-      const double* l1 = half == 0 ? static_cast<const double*>(tab_h) : static_cast<const double*>(pbb);  // (T_AB)^H^H | T_BB
+      const double* l0 = half == 0 ? static_cast<const double*>(taa_full) : v2_l0;  // T_AA | (T_AB^H)^H
+      const double* l1 = half == 0 ? static_cast<const double*>(tab_h) : v2_l1;     // (T_AB)^H^H | T_BB
       z.segs.push_back({atom_mats(l0, na, nl), atom_rows(A, na, nl, ng, K)});
       z.segs.push_back({atom_mats(l1, na, nl), atom_rows(B, na, nl, ng, K)});
       z.m = nl;
@@ -815,10 +836,11 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     return HSB_OK;
   };
 
-  // INT8 engine, fused paths: one left exponent per column over A, B and UB
-  // (ozaki_colexp_ab, one pass over A and B) shared by S = A^H A + (UB)^H (UB)
-  // and the left side of H = A^H V1 + B^H V2, so A's residue planes are computed
-  // once for both contractions; H's right side (V1, V2) gets its own exponents.
+  // INT8 engine, fused paths: one left exponent per column over A and UB (and B
+  // when H's left side is B) (ozaki_colexp_ab, one pass over A and B) shared by
+  // S = A^H A + (UB)^H (UB) and the left side of H = A^H V1 + (UB)^H W2, so the
+  // residue planes of A and UB are computed once for both contractions; H's
+  // right side (V1, W2) gets its own exponents.
   // The planes are sized for the 2K reduction (oz_ktot) of both calls.
   int32_t* oz_el = nullptr;
   int8_t* oz_res_a = nullptr;
@@ -834,7 +856,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     CKS(ws(ctx, "oz_res_a", pbytes, &rb));
     oz_el = static_cast<int32_t*>(eb);
     oz_res_a = static_cast<int8_t*>(rb);
-    CK(hsb::launch_ozaki_colexp_ab(A, B, K, K, ng, U, oz_el, s_));
+    CK(hsb::launch_ozaki_colexp_ab(A, B, K, K, ng, U, oz_el, s_, !h_via_ub));
     CK(hsb::launch_ozaki_residues(A, K, K, ng, oz_el, bits, n_mod, oz_res_a, kpad, s_));
     launches += 2;
     if (with_ub) {
@@ -853,7 +875,7 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     z.oz_el = oz_el;
     z.oz_er = er ? er : oz_el;
     z.oz_pre.push_back({A, 0, oz_res_a});
-    if (oz_res_ub && !er) z.oz_pre.push_back({B, 0, oz_res_ub, U});  // S only
+    if (oz_res_ub && (!er || h_via_ub)) z.oz_pre.push_back({B, 0, oz_res_ub, U});  // S (and H via UB)
     z.oz_ktot = 2 * K;
   };
 
@@ -1008,7 +1030,10 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   } else {
     ZrkCall h = tri_call(H, ldo, ng, kLowerOnly | kMirror, 0.0);
     h.segs.push_back({plain(A, K, ng, K), plain(Z, K, ng, K)});  // A^H V1
-    h.segs.push_back({plain(B, K, ng, K), plain(R, K, ng, K)});  // B^H V2
+    if (h_via_ub)
+      h.segs.push_back({ub_view(), plain(R, K, ng, K)});  // (UB)^H W2
+    else
+      h.segs.push_back({plain(B, K, ng, K), plain(R, K, ng, K)});  // B^H V2
     h.tl = &tl, h.sect = "h", h.core = "h_core";
     h.peer = peer;
     h.peer_is_h = true;

@@ -79,7 +79,7 @@ __global__ void ozaki_colexp_kernel(const double2* __restrict__ x, int64_t ldx, 
 // residue planes serve both contractions
 __global__ void ozaki_colexp_ab_kernel(const double2* __restrict__ a, const double2* __restrict__ b, int64_t ld,
                                        int64_t k, int64_t cols, const double* __restrict__ u,
-                                       int32_t* __restrict__ e) {
+                                       int32_t* __restrict__ e, int with_b) {
   const int warps = blockDim.x >> 5;
   for (int64_t c = static_cast<int64_t>(blockIdx.x) * warps + (threadIdx.x >> 5); c < cols;
        c += static_cast<int64_t>(gridDim.x) * warps) {
@@ -89,7 +89,8 @@ __global__ void ozaki_colexp_ab_kernel(const double2* __restrict__ a, const doub
     for (int64_t r = threadIdx.x & 31; r < k; r += 32) {
       const double2 va = ca[r], vb = cb[r];
       const double uk = __ldg(u + r);
-      m = fmax(m, fmax(fabs(va.x) + fabs(va.y), fabs(vb.x) + fabs(vb.y)));
+      m = fmax(m, fabs(va.x) + fabs(va.y));
+      if (with_b) m = fmax(m, fabs(vb.x) + fabs(vb.y));
       m = fmax(m, fabs(uk * vb.x) + fabs(uk * vb.y));
     }
 #pragma unroll
@@ -1022,10 +1023,11 @@ cudaError_t launch_ozaki_colexp(const double* x, int64_t ldx, int64_t k, int64_t
 }
 
 cudaError_t launch_ozaki_colexp_ab(const double* a, const double* b, int64_t ld, int64_t k, int64_t cols,
-                                   const double* u, int32_t* exp_out, cudaStream_t st) {
+                                   const double* u, int32_t* exp_out, cudaStream_t st, bool with_b) {
   if (cols <= 0 || k <= 0) return cudaSuccess;
   ozaki_colexp_ab_kernel<<<grid_cap((cols + 7) / 8, 148 * 16), 256, 0, st>>>(
-      reinterpret_cast<const double2*>(a), reinterpret_cast<const double2*>(b), ld, k, cols, u, exp_out);
+      reinterpret_cast<const double2*>(a), reinterpret_cast<const double2*>(b), ld, k, cols, u, exp_out,
+      with_b ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -167,9 +167,9 @@ cudaError_t launch_ozaki_vcrt(const OzVcrtParams& p, cudaStream_t st);
 cudaError_t launch_ozaki_colexp(const double* x, int64_t ldx, int64_t k, int64_t cols, int32_t* exp_out,
                                 cudaStream_t st, const double* rscale = nullptr);
 cudaError_t launch_ozaki_init_exp(int32_t* e, int64_t n, cudaStream_t st);
-// e[c] = exponent of the column max over a, b and diag(u) b (written, not max-ed)
+// e[c] = exponent of the column max over a, diag(u) b and (with_b) b (written, not max-ed)
 cudaError_t launch_ozaki_colexp_ab(const double* a, const double* b, int64_t ld, int64_t k, int64_t cols,
-                                   const double* u, int32_t* exp_out, cudaStream_t st);
+                                   const double* u, int32_t* exp_out, cudaStream_t st, bool with_b);
 cudaError_t launch_ozaki_residues(const double* x, int64_t ldx, int64_t k, int64_t cols, const int32_t* col_exp,
                                   int b, int n_mod, int8_t* out, int64_t kpad, cudaStream_t st, const double* rscale = nullptr);
 cudaError_t launch_ozaki_gemm(const OzGemmParams& p, cudaStream_t st);
