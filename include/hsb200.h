@@ -305,6 +305,18 @@ typedef struct {
 HSB_API hsb_status hsb_match_coeffs(hsb_ctx* ctx, void* stream, const hsb_phys* phys,
                                     double* a_stack, double* b_stack, int64_t ld);
 
+/* North-star entry point in one call: the matching coefficients of `ph` into
+ * the device stacks p->a_stack / p->b_stack (ld = n_atoms * N_L), then the
+ * H/S build of hsb_build_hs on them (p: device location, T blocks and u on
+ * the device; same opts / out / timings / atom_info).  With the INT8 engine
+ * on the fused path the matching kernel also writes S's and H's left operands
+ * -- the column exponents and the residue planes of A and of diag(u) B -- as
+ * it generates each G column, so the build skips those
+ * passes over the stacks.  Replaces the pair match_coeffs + build_hs. */
+HSB_API hsb_status hsb_build_hs_physical(hsb_ctx* ctx, void* stream, const hsb_phys* ph, const hsb_problem* p,
+                                         uint32_t opts, const hsb_output* out, hsb_timings* tm,
+                                         int32_t* atom_info);
+
 #ifdef __cplusplus
 }
 #endif

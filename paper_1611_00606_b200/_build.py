@@ -20,7 +20,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libhsb200.so"
 SOURCES = ["zrk_kernel.cu", "zrk3m_kernel.cu", "aux_kernels.cu", "staging.cu", "match_kernel.cu", "ozaki.cu", "contract.cu", "hsb_api.cu"]
-HEADERS = ["zrk.cuh", "ptx.cuh", "ozaki.cuh", "host_ctx.cuh", "aux_kernels.cuh", "staging.cuh", "match.cuh"]
+HEADERS = ["zrk.cuh", "ptx.cuh", "ozaki.cuh", "ozaki_res.cuh", "host_ctx.cuh", "aux_kernels.cuh", "staging.cuh", "match.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -118,6 +118,9 @@ def load():
                                 _P, i64, u32]),
             "hsb_hermitian_mirror": (i32, [_P, _P, i64, _P, i64]),
             "hsb_match_coeffs": (i32, [_P, _P, ctypes.POINTER(HsbPhys), _P, _P, i64]),
+            "hsb_build_hs_physical": (i32, [_P, _P, ctypes.POINTER(HsbPhys), ctypes.POINTER(HsbProblem), u32,
+                                            ctypes.POINTER(HsbOutput), ctypes.POINTER(HsbTimings),
+                                            ctypes.POINTER(ctypes.c_int32)]),
             "hsb_build_hs": (i32, [_P, _P, ctypes.POINTER(HsbProblem), u32, ctypes.POINTER(HsbOutput),
                                    ctypes.POINTER(HsbTimings), ctypes.POINTER(ctypes.c_int32)]),
         }

@@ -56,6 +56,14 @@ struct hsb_ctx {
   std::vector<int2> oz_tiles_host;
   std::vector<int32_t> oz_tile_index_host;
   int32_t cplx = HSB_CPLX_3M;          // complex product form of the zrk kernels
+  // INT8 engine: left operands of S and H prepared by the matching kernel for
+  // the build hsb_build_hs_physical runs (A stack, shape, moduli, bits); the
+  // buffers are the workspace entries oz_exp_l, oz_res_a, oz_res2
+  struct OzPrepared {
+    const double* a = nullptr;
+    int64_t k = 0, ng = 0;
+    int32_t n_mod = 0, bits = 0;
+  } oz_prepared;
 };
 
 // Entry-point guard: serialises calls on one context (its workspace map, copy

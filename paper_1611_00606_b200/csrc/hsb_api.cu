@@ -476,10 +476,19 @@ static hsb_status validate_small_inputs(hsb_ctx* ctx, const hsb_problem* p) {
   return HSB_OK;
 }
 
+static hsb_status build_hs_core(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32_t opts,
+                                const hsb_output* out, hsb_timings* tm, int32_t* atom_info);
+
 hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32_t opts, const hsb_output* out,
                         hsb_timings* tm, int32_t* atom_info) {
   if (!ctx) return fail(nullptr, HSB_ERR_INPUT, "ctx is NULL");
   CtxCall call_guard(ctx, true);
+  ctx->oz_prepared = {};
+  return build_hs_core(ctx, stream, p, opts, out, tm, atom_info);
+}
+
+static hsb_status build_hs_core(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32_t opts,
+                                const hsb_output* out, hsb_timings* tm, int32_t* atom_info) {
   if (!p || !out) return fail(ctx, HSB_ERR_INPUT, "problem/output is NULL");
   const int64_t na = p->n_atoms, nl = p->n_l, ng = p->n_g;
   if (na < 1 || nl < 1 || ng < 1) return fail(ctx, HSB_ERR_INPUT, "dimensions must be positive");
@@ -851,6 +860,18 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
     CKS(oz_choose(ctx, 2 * K, &n_mod, &bits));
     const int64_t kpad = (K + 15) / 16 * 16;
     const size_t pbytes = static_cast<size_t>(hsb::kOzPlanes) * n_mod * ng * kpad;
+    const hsb_ctx::OzPrepared& pre = ctx->oz_prepared;
+    if (h_via_ub && pre.a == A && pre.k == K && pre.ng == ng && pre.n_mod == n_mod && pre.bits == bits) {
+      // the matching kernel already wrote the exponents and the A / UB planes
+      void *eb, *rb, *ubb;
+      CKS(ws(ctx, "oz_exp_l", static_cast<size_t>(ng) * 4, &eb));
+      CKS(ws(ctx, "oz_res_a", pbytes, &rb));
+      CKS(ws(ctx, "oz_res2", pbytes, &ubb));
+      oz_el = static_cast<int32_t*>(eb);
+      oz_res_a = static_cast<int8_t*>(rb);
+      oz_res_ub = static_cast<int8_t*>(ubb);
+      return HSB_OK;
+    }
     void *eb, *rb;
     CKS(ws(ctx, "oz_exp_l", static_cast<size_t>(ng) * 4, &eb));
     CKS(ws(ctx, "oz_res_a", pbytes, &rb));
@@ -1215,11 +1236,10 @@ hsb_status hsb_build_hs(hsb_ctx* ctx, void* stream, const hsb_problem* p, uint32
   return HSB_OK;
 }
 
-hsb_status hsb_match_coeffs(hsb_ctx* ctx, void* stream, const hsb_phys* ph, double* a_stack, double* b_stack,
-                            int64_t ld) {
-  if (!ctx) return fail(nullptr, HSB_ERR_INPUT, "ctx is NULL");
-  CtxCall call_guard(ctx, false);
-  if (!ph || !a_stack || !b_stack) return fail(ctx, HSB_ERR_INPUT, "NULL argument");
+// validate the physical inputs and upload them into the context's workspace;
+// the caller's host arrays may be reused once this returns
+static hsb_status match_setup(hsb_ctx* ctx, cudaStream_t st, const hsb_phys* ph, int64_t ld, MatchParams* mp_out) {
+  if (!ph) return fail(ctx, HSB_ERR_INPUT, "NULL argument");
   if (ph->n_atoms < 1 || ph->n_g < 1 || ph->n_types < 1 || ph->lmax < 0)
     return fail(ctx, HSB_ERR_INPUT, "dimensions must be positive");
   if (ph->lmax > kMaxL) return fail(ctx, HSB_ERR_UNSUPPORTED, "lmax above 31");
@@ -1231,8 +1251,6 @@ hsb_status hsb_match_coeffs(hsb_ctx* ctx, void* stream, const hsb_phys* ph, doub
     return fail(ctx, HSB_ERR_INPUT, "NULL input array");
   for (int64_t a = 0; a < ph->n_atoms; ++a)
     if (ph->type_of[a] < 0 || ph->type_of[a] >= ph->n_types) return fail(ctx, HSB_ERR_INPUT, "type index out of range");
-  cudaSetDevice(ctx->device);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t gb = ph->n_g * 3 * 4, tb = ph->n_atoms * 3 * 8, yb = ph->n_atoms * 4, rb = ph->n_types * 8,
                db = ph->n_types * (ph->lmax + 1) * 4 * 8;
   void *g, *t, *y, *r, *d;
@@ -1262,10 +1280,71 @@ hsb_status hsb_match_coeffs(hsb_ctx* ctx, void* stream, const hsb_phys* ph, doub
   mp.n_types = ph->n_types;
   mp.lmax = ph->lmax;
   if (match_smem_bytes(mp) > 200 * 1024) return fail(ctx, HSB_ERR_UNSUPPORTED, "too many atoms for one column CTA");
-  CK(launch_match_coeffs(mp, a_stack, b_stack, st));
-  // the small uploads above come from caller memory: finish them before returning
+  // the small uploads come from caller memory: land them before returning
   CK(cudaStreamSynchronize(st));
+  *mp_out = mp;
   return HSB_OK;
+}
+
+hsb_status hsb_match_coeffs(hsb_ctx* ctx, void* stream, const hsb_phys* ph, double* a_stack, double* b_stack,
+                            int64_t ld) {
+  if (!ctx) return fail(nullptr, HSB_ERR_INPUT, "ctx is NULL");
+  CtxCall call_guard(ctx, false);
+  if (!ph || !a_stack || !b_stack) return fail(ctx, HSB_ERR_INPUT, "NULL argument");
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  MatchParams mp;
+  CKS(match_setup(ctx, st, ph, ld, &mp));
+  CK(launch_match_coeffs(mp, a_stack, b_stack, st));
+  return HSB_OK;
+}
+
+hsb_status hsb_build_hs_physical(hsb_ctx* ctx, void* stream, const hsb_phys* ph, const hsb_problem* p,
+                                 uint32_t opts, const hsb_output* out, hsb_timings* tm, int32_t* atom_info) {
+  if (!ctx) return fail(nullptr, HSB_ERR_INPUT, "ctx is NULL");
+  CtxCall call_guard(ctx, true);
+  ctx->oz_prepared = {};
+  if (!ph || !p || !out) return fail(ctx, HSB_ERR_INPUT, "NULL argument");
+  if (p->location != HSB_LOC_DEVICE || !p->a_stack || !p->b_stack || !p->u_dev)
+    return fail(ctx, HSB_ERR_INPUT, "the physical build needs device stacks (outputs of the matching kernel) and u");
+  const int64_t nlm = static_cast<int64_t>(ph->lmax + 1) * (ph->lmax + 1);
+  if (p->n_atoms != ph->n_atoms || p->n_l != nlm || p->n_g != ph->n_g)
+    return fail(ctx, HSB_ERR_DIMENSION, "problem dimensions disagree with the physical inputs");
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t K = p->n_atoms * p->n_l, ng = p->n_g;
+  double* A = const_cast<double*>(static_cast<const double*>(p->a_stack));
+  double* B = const_cast<double*>(static_cast<const double*>(p->b_stack));
+  MatchParams mp;
+  CKS(match_setup(ctx, st, ph, K, &mp));
+  // INT8 engine, fused path: the matching kernel also emits S's and H's left
+  // operands (exponents, A and UB residue planes)
+  static const bool no_res = std::getenv("HSB_NO_MATCH_RES") != nullptr;  // A/B experiments
+  if (ctx->engine == HSB_ENGINE_INT8 && !(opts & HSB_OPT_UNFUSED) && !no_res) {
+    int n_mod = 0, bits = 0;
+    CKS(oz_choose(ctx, 2 * K, &n_mod, &bits));
+    const int64_t kpad = (K + 15) / 16 * 16;
+    const size_t pbytes = static_cast<size_t>(hsb::kOzPlanes) * n_mod * ng * kpad;
+    void *eb, *rb, *ubb;
+    CKS(ws(ctx, "oz_exp_l", static_cast<size_t>(ng) * 4, &eb));
+    CKS(ws(ctx, "oz_res_a", pbytes, &rb));
+    CKS(ws(ctx, "oz_res2", pbytes, &ubb));
+    MatchRes r;
+    r.u = static_cast<const double*>(p->u_dev);
+    r.col_exp = static_cast<int32_t*>(eb);
+    r.res_a = static_cast<int8_t*>(rb);
+    r.res_ub = static_cast<int8_t*>(ubb);
+    r.kpad = kpad;
+    r.b = bits;
+    r.n_mod = n_mod;
+    CK(launch_match_coeffs_res(mp, A, B, r, st));
+    ctx->oz_prepared = {A, K, ng, n_mod, bits};
+  } else {
+    CK(launch_match_coeffs(mp, A, B, st));
+  }
+  const hsb_status s = build_hs_core(ctx, stream, p, opts, out, tm, atom_info);
+  ctx->oz_prepared = {};
+  return s;
 }
 
 }  // extern "C"

@@ -23,6 +23,22 @@ struct MatchParams {
 };
 
 cudaError_t launch_match_coeffs(const MatchParams& p, double* A, double* B, cudaStream_t st);
+
+// Matching coefficients plus the INT8 engine's left operands of S and H in one
+// pass: each CTA owns whole G columns, so it also takes the
+// column's exponent e = max over A and fl(u B) (|Re| + |Im|) and writes the
+// residue planes of A and of UB = diag(u) B at b bits, n_mod moduli
+// ([plane][modulus][col][kpad] int8), exactly as ozaki_colexp_ab +
+// ozaki_residue_kernel would from the stored stacks.
+struct MatchRes {
+  const double* u;   // device, n_atoms * N_L row norms
+  int32_t* col_exp;  // device, n_g: the shared left exponent
+  int8_t* res_a;     // planes of A
+  int8_t* res_ub;    // planes of UB
+  int64_t kpad;
+  int32_t b, n_mod;
+};
+cudaError_t launch_match_coeffs_res(const MatchParams& p, double* A, double* B, const MatchRes& r, cudaStream_t st);
 size_t match_smem_bytes(const MatchParams& p);
 
 }  // namespace hsb

@@ -21,6 +21,7 @@
 #include <stdint.h>
 
 #include "match.cuh"
+#include "ozaki_res.cuh"
 
 namespace hsb {
 
@@ -98,8 +99,10 @@ __device__ void spherical_bessel(double x, int nmax, double* j) {
 constexpr int kMatchCols = 8;
 constexpr int kMatchThreads = 256;
 
+// NM = 0: A and B only; NM > 0: also the residue planes of A and UB (MatchRes)
+template <int NM>
 __global__ void __launch_bounds__(kMatchThreads) match_coeffs_kernel(MatchParams p, double2* __restrict__ A,
-                                                                      double2* __restrict__ B) {
+                                                                      double2* __restrict__ B, MatchRes res) {
   extern __shared__ double smem_d[];
   const int lmax = p.lmax, nlm = (lmax + 1) * (lmax + 1), nl1 = lmax + 1;
   double2* ys = reinterpret_cast<double2*>(smem_d);                     // [col][nlm]: pre i^l conj(Y_lm)
@@ -205,6 +208,7 @@ __global__ void __launch_bounds__(kMatchThreads) match_coeffs_kernel(MatchParams
 
   // ---- stream the columns: rows (atom, L), 16-byte coalesced stores
   const int64_t K = static_cast<int64_t>(p.n_atoms) * nlm;
+  __shared__ double red[kMatchThreads / 32];
   for (int c = 0; c < ncols; ++c) {
     double2* colA = A + (g0 + c) * p.ld;
     double2* colB = B + (g0 + c) * p.ld;
@@ -212,13 +216,64 @@ __global__ void __launch_bounds__(kMatchThreads) match_coeffs_kernel(MatchParams
     const double2* ph = phase + c * p.n_atoms;
     const double* fac = fa + c * p.n_types * nl1;
     const double* fbc = fb + c * p.n_types * nl1;
-    for (int64_t r = tid; r < K; r += kMatchThreads) {
+    auto coeffs = [&](int64_t r, double2& va, double2& vb) {
       const int a = static_cast<int>(r / nlm), L = static_cast<int>(r - static_cast<int64_t>(a) * nlm);
       const int t = p.type_of[a], l = lidx[L];
       const double2 base = cmul(yc[L], ph[a]);
       const double ca = fac[t * nl1 + l], cb = fbc[t * nl1 + l];
-      colA[r] = make_double2(base.x * ca, base.y * ca);
-      colB[r] = make_double2(base.x * cb, base.y * cb);
+      va = make_double2(base.x * ca, base.y * ca);
+      vb = make_double2(base.x * cb, base.y * cb);
+    };
+    double mx = 0.0;
+    for (int64_t r = tid; r < K; r += kMatchThreads) {
+      double2 va, vb;
+      coeffs(r, va, vb);
+      colA[r] = va;
+      colB[r] = vb;
+      if constexpr (NM > 0) {  // fl(u b), as diag_scale_kernel rounds it
+        const double u = __ldg(res.u + r);
+        mx = fmax(mx, fmax(fabs(va.x) + fabs(va.y), fabs(u * vb.x) + fabs(u * vb.y)));
+      }
+    }
+    if constexpr (NM > 0) {
+      // the column's exponent (frexp of the max: max < 2^e), then its residues
+#pragma unroll
+      for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (lane == 0) red[warp] = mx;
+      __syncthreads();
+      double m = red[0];
+#pragma unroll
+      for (int w = 1; w < kMatchThreads / 32; ++w) m = fmax(m, red[w]);
+      int e = 0;
+      frexp(m, &e);
+      if (tid == 0) res.col_exp[g0 + c] = e;
+      const int sh = res.b - e;
+      const double s1 = pow2i(sh / 2), s2 = pow2i(sh - sh / 2);
+      const int64_t mod_stride = p.n_g * res.kpad, plane_stride = NM * mod_stride;
+      for (int64_t r0 = 4 * tid; r0 < res.kpad; r0 += 4 * kMatchThreads) {
+        uint32_t al[4], ah[4], bl[4], bh[4], ul[4], uh[4], vl[4], vh[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          double ar = 0.0, ai = 0.0, ur = 0.0, ui = 0.0;
+          if (r0 + j < K) {
+            double2 va, vb;
+            coeffs(r0 + j, va, vb);
+            const double u = __ldg(res.u + r0 + j);
+            ar = rint((va.x * s1) * s2);
+            ai = rint((va.y * s1) * s2);
+            ur = rint(((u * vb.x) * s1) * s2);
+            ui = rint(((u * vb.y) * s1) * s2);
+          }
+          oz_split(ar, al[j], ah[j]);
+          oz_split(ai, bl[j], bh[j]);
+          oz_split(ur, ul[j], uh[j]);
+          oz_split(ui, vl[j], vh[j]);
+        }
+        const int64_t off = (g0 + c) * res.kpad + r0;
+        oz_residue_planes_global<NM>(al, ah, bl, bh, res.res_a + off, plane_stride, mod_stride);
+        oz_residue_planes_global<NM>(ul, uh, vl, vh, res.res_ub + off, plane_stride, mod_stride);
+      }
+      __syncthreads();  // red[] is rewritten by the next column
     }
   }
 }
@@ -230,18 +285,37 @@ size_t match_smem_bytes(const MatchParams& p) {
          nlm + 16;
 }
 
-cudaError_t launch_match_coeffs(const MatchParams& p, double* A, double* B, cudaStream_t st) {
+template <int NM>
+static cudaError_t launch_match(const MatchParams& p, double* A, double* B, const MatchRes& r, cudaStream_t st) {
   const size_t smem = match_smem_bytes(p);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(match_coeffs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(match_coeffs_kernel<NM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
   const int64_t blocks = (p.n_g + kMatchCols - 1) / kMatchCols;
   if (blocks <= 0) return cudaSuccess;
-  match_coeffs_kernel<<<static_cast<unsigned>(blocks), kMatchThreads, smem, st>>>(
-      p, reinterpret_cast<double2*>(A), reinterpret_cast<double2*>(B));
+  match_coeffs_kernel<NM><<<static_cast<unsigned>(blocks), kMatchThreads, smem, st>>>(
+      p, reinterpret_cast<double2*>(A), reinterpret_cast<double2*>(B), r);
   return cudaGetLastError();
+}
+
+cudaError_t launch_match_coeffs(const MatchParams& p, double* A, double* B, cudaStream_t st) {
+  return launch_match<0>(p, A, B, MatchRes{}, st);
+}
+
+cudaError_t launch_match_coeffs_res(const MatchParams& p, double* A, double* B, const MatchRes& r, cudaStream_t st) {
+  if (r.kpad % 16 != 0 || r.kpad < static_cast<int64_t>(p.n_atoms) * (p.lmax + 1) * (p.lmax + 1))
+    return cudaErrorInvalidValue;
+  switch (r.n_mod) {
+#define HSB_MATCH_RES(NM) \
+  case NM:                \
+    return launch_match<NM>(p, A, B, r, st);
+    HSB_MATCH_RES(15) HSB_MATCH_RES(16) HSB_MATCH_RES(17) HSB_MATCH_RES(18) HSB_MATCH_RES(19) HSB_MATCH_RES(20)
+#undef HSB_MATCH_RES
+    default:
+      return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace hsb

@@ -278,8 +278,11 @@ def build_hs_physical(system: PhysicalSystem, kpt, gset, t_aa, t_ab, t_bb, polic
     or column-major numpy arrays with ``host_outputs``).
 
     Matching coefficients are generated on the device and consumed in place
-    by the H/S pipeline (no host round trip).  Returns
-    (H, S, SplitCounts, timings, atom_info) like ``build_hs_device``.
+    by the H/S pipeline (no host round trip), in one library call
+    (hsb_build_hs_physical): with the INT8 engine the matching kernel also
+    writes the exponents and residue planes of A and diag(u) B that S and H
+    start from.  Returns (H, S, SplitCounts, timings,
+    atom_info) like ``build_hs_device``.
     """
     import torch
 
@@ -287,10 +290,12 @@ def build_hs_physical(system: PhysicalSystem, kpt, gset, t_aa, t_ab, t_bb, polic
 
     pol = policy if isinstance(policy, GpuPolicy) else GpuPolicy()
     dev = torch.device("cuda", pol.device)
-    a, b = match_coeffs_device(system, kpt, gset, pol.device)
     dims = Dims(system.n_atoms, system.n_l, int(gset.shape[0]))
+    a = torch.empty((dims.n_g, dims.k), dtype=torch.complex128, device=dev)
+    b = torch.empty_like(a)
     dp = DeviceProblem(dims, a, b, *_device_t(system, t_aa, t_ab, t_bb, dev))
-    return build_hs_device(dp, policy=pol, force_nonhpd=force_nonhpd, host_outputs=host_outputs)
+    phys, _keep = _phys_struct(system, kpt, gset)
+    return build_hs_device(dp, policy=pol, force_nonhpd=force_nonhpd, host_outputs=host_outputs, phys=phys)
 
 
 def iter_hs_physical_kpoints(system: PhysicalSystem, kpts, gsets, t_aa, t_ab, t_bb, policy=None,
@@ -332,10 +337,10 @@ def iter_hs_physical_kpoints(system: PhysicalSystem, kpts, gsets, t_aa, t_ab, t_
     def run(i, slot, stream, order):
         n_g = int(gsets[i].shape[0])
         a, b = bufs[slot][0][:n_g], bufs[slot][1][:n_g]
-        match_coeffs_device(system, kpts[i], gsets[i], pol.device, stream=stream, slot=slot, out=(a, b))
         dp = DeviceProblem(Dims(system.n_atoms, system.n_l, n_g), a, b, *tdev)
+        phys, _keep = _phys_struct(system, kpts[i], gsets[i])
         return build_hs_device(dp, policy=pol, force_nonhpd=force_nonhpd, stream=stream, host_outputs=True,
-                               slot=slot, order=order)
+                               slot=slot, order=order, phys=phys)
 
     if depth == 1:
         st = torch.cuda.current_stream(dev)

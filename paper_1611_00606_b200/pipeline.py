@@ -199,7 +199,7 @@ def _host_problem(p):
     return prob, (blocks, arrays)
 
 
-def _call_build(pol, prob, out, stream, force_nonhpd, n_a, slot: int = 0, wait: bool = True):
+def _call_build(pol, prob, out, stream, force_nonhpd, n_a, slot: int = 0, wait: bool = True, phys=None):
     lib = _lib.load()
     opts = (_lib.HSB_OPT_FORCE_NONHPD if force_nonhpd else 0) | (0 if pol.fused else _lib.HSB_OPT_UNFUSED)
     if not pol.lower_d2h:
@@ -210,8 +210,13 @@ def _call_build(pol, prob, out, stream, force_nonhpd, n_a, slot: int = 0, wait: 
     info = (ctypes.c_int32 * n_a)()
     with _lib.using(pol.device, pol.complex_mult, pol.engine, pol.int8_bits, slot) as ctx:
         # no timings -> the library returns without waiting (device in/out only)
-        _lib.check(lib.hsb_build_hs(ctx, stream, ctypes.byref(prob), opts, ctypes.byref(out),
-                                    ctypes.byref(tim) if wait else None, info if wait else None), ctx)
+        if phys is not None:  # matching coefficients into prob's stacks, then the build (one call)
+            _lib.check(lib.hsb_build_hs_physical(ctx, stream, ctypes.byref(phys), ctypes.byref(prob), opts,
+                                                 ctypes.byref(out), ctypes.byref(tim) if wait else None,
+                                                 info if wait else None), ctx)
+        else:
+            _lib.check(lib.hsb_build_hs(ctx, stream, ctypes.byref(prob), opts, ctypes.byref(out),
+                                        ctypes.byref(tim) if wait else None, info if wait else None), ctx)
     return (tim, list(info)) if wait else (None, None)
 
 
@@ -469,7 +474,7 @@ class DeviceProblem:
 
 def build_hs_device(dp: DeviceProblem, h=None, s=None, policy=None, force_nonhpd: bool = False,
                     stream=None, s_ready=None, wait: bool = True, peer=None, host_outputs: bool = False,
-                    slot: int = 0, order=None):
+                    slot: int = 0, order=None, phys=None):
     """Device-resident build: returns (H, S, SplitCounts, timings, atom_info).
 
     H and S are torch complex128 (n_g, n_g) tensors holding the column-major
@@ -484,7 +489,9 @@ def build_hs_device(dp: DeviceProblem, h=None, s=None, policy=None, force_nonhpd
     (see ``_lane_pipeline``).  ``host_outputs``
     returns H and S as column-major numpy arrays in (pinned) host memory
     instead, downloaded while the contractions run (the drop-in path's output
-    streaming, lower triangles completed by the host mirror).
+    streaming, lower triangles completed by the host mirror).  ``phys`` (an
+    ``_lib.HsbPhys``, see physics.py) makes the call generate the matching
+    coefficients into ``dp``'s A and B stacks first (hsb_build_hs_physical).
     """
     import torch
 
@@ -538,7 +545,7 @@ def build_hs_device(dp: DeviceProblem, h=None, s=None, policy=None, force_nonhpd
     if stream is None:
         stream = torch.cuda.current_stream(dev)
     tim, info = _call_build(pol, prob, out, ctypes.c_void_p(stream.cuda_stream), force_nonhpd, n_a, slot=slot,
-                            wait=wait)
+                            wait=wait, phys=phys)
     if not wait:
         return h, s, None, None, None
     if host_outputs:

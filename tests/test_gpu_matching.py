@@ -130,3 +130,27 @@ def test_physical_kpoint_pipeline_rejects_mismatched_lists():
     t = synthetic_t_matrices(system, seed=1)
     with pytest.raises(InputError):
         list(iter_hs_physical_kpoints(system, [k, k], [g], *t))
+
+
+@pytest.mark.parametrize("lmax,ng,nonhpd", [(8, 1500, 0.25), (10, 3000, 0.0)])
+def test_physical_build_fused_residues_match_the_standalone_passes(lmax, ng, nonhpd):
+    # hsb_build_hs_physical: the matching kernel writes the INT8 engine's left
+    # operands (column exponents, A and diag(u) B residue planes) as it
+    # generates each G column; the build must equal, bit for bit, the
+    # standalone path (coefficients to HBM, then the exponent and residue
+    # passes over the stored stacks)
+    from paper_1611_00606_b200 import DeviceProblem, GpuPolicy, build_hs_device
+    from paper_1611_00606_b200.physics import _device_t
+
+    system, k, kmax, g = synthetic_system(6, 3, lmax, ng, seed=lmax, kpt_frac=(0.2, -0.1, 0.3))
+    t_aa, t_ab, t_bb = synthetic_t_matrices(system, seed=4, nonhpd_fraction=nonhpd)
+    pol = GpuPolicy()
+    h1, s1, sp1, t1, _ = build_hs_physical(system, k, g, t_aa, t_ab, t_bb, policy=pol)
+    a, b = match_coeffs_device(system, k, g)
+    dp = DeviceProblem(Dims(system.n_atoms, system.n_l, len(g)), a, b,
+                       *_device_t(system, t_aa, t_ab, t_bb, a.device))
+    h2, s2, sp2, t2, _ = build_hs_device(dp, policy=pol)
+    torch.cuda.synchronize()
+    assert (sp1.hpd, sp1.nonhpd) == (sp2.hpd, sp2.nonhpd)
+    assert torch.equal(h1, h2) and torch.equal(s1, s2)
+    assert t1["launches"] < t2["launches"]  # the exponent and A / UB residue passes are gone
