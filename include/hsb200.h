@@ -193,6 +193,12 @@ typedef struct {
                                       triangles + host-side conjugate mirror
                                       (the default on the streamed INT8 path;
                                       same bytes in the result) */
+#define HSB_OPT_LOWER_ONLY   0x10u /* device outputs, fused path: write H and
+                                      S as lower triangles with a real
+                                      diagonal and no mirror (the strict upper
+                                      triangles are left untouched) -- the
+                                      partial sums of the triangle-packed
+                                      reduce-scatter (distributed.py) */
 
 /* Receive slots of an atom-sharded build across n_ranks GPUs (north star (3);
  * SURVEY 8f row 2).  Rank q owns columns [q * cols_per_rank, (q + 1) *

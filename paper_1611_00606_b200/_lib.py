@@ -28,6 +28,7 @@ HSB_OPT_FORCE_NONHPD = 0x1
 HSB_OPT_UNFUSED = 0x2
 HSB_OPT_VALIDATE = 0x4
 HSB_OPT_FULL_D2H = 0x8
+HSB_OPT_LOWER_ONLY = 0x10
 HSB_CPLX_4M = 0
 HSB_CPLX_3M = 1
 COMPLEX_MULT = {"4m": HSB_CPLX_4M, "3m": HSB_CPLX_3M}

@@ -503,6 +503,10 @@ static hsb_status build_hs_core(hsb_ctx* ctx, void* stream, const hsb_problem* p
     if (!p->t_aa || !p->t_ab || !p->t_bb || !p->u_norms) return fail(ctx, HSB_ERR_INPUT, "host block arrays are NULL");
     CKS(validate_small_inputs(ctx, p));
   }
+  if ((opts & HSB_OPT_LOWER_ONLY) && (out->location != HSB_LOC_DEVICE || out->peer))
+    return fail(ctx, HSB_ERR_INPUT, "HSB_OPT_LOWER_ONLY needs device outputs");
+  // fused paths: the final H / S epilogues mirror (FULL) unless lower triangles were asked for
+  const uint32_t out_mirror = (opts & HSB_OPT_LOWER_ONLY) ? kZeroImagDiag : kMirror;
   cudaSetDevice(ctx->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (!ctx->copy_stream) CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
@@ -921,7 +925,7 @@ static hsb_status build_hs_core(hsb_ctx* ctx, void* stream, const hsb_problem* p
     CK(cudaEventRecord(ev_a, cs));
     CK(cudaStreamWaitEvent(st, ev_a, 0));
     CK(tl.mark(st, "h2d"));
-    ZrkCall s1 = tri_call(S, ldo, ng, kLowerOnly | kMirror, 1.0);
+    ZrkCall s1 = tri_call(S, ldo, ng, kLowerOnly | out_mirror, 1.0);
     s1.segs.push_back({plain(A, K, ng, K), plain(A, K, ng, K)});
     s1.tl = &tl, s1.sect = "s1", s1.core = "s1_core";
     if (chunk_s) s1.chunk_events = &s_chunks;
@@ -945,8 +949,10 @@ static hsb_status build_hs_core(hsb_ctx* ctx, void* stream, const hsb_problem* p
     ZrkCall s2 = tri_call(S, ldo, ng, kLowerOnly | kZeroImagDiag, 1.0);
     s2.segs.push_back({plain(UB, K, ng, K), plain(UB, K, ng, K)});
     CKS(run_zrk(ctx, st, s2, &launches));
-    CK(launch_mirror(S, ldo, static_cast<int>(ng), st));
-    ++launches;
+    if (!(opts & HSB_OPT_LOWER_ONLY)) {
+      CK(launch_mirror(S, ldo, static_cast<int>(ng), st));
+      ++launches;
+    }
     CK(tl.mark(st, "s2"));
   } else {
     // INT8 engine: S's operand preparation (exponents, A and UB residues) does
@@ -971,7 +977,7 @@ static hsb_status build_hs_core(hsb_ctx* ctx, void* stream, const hsb_problem* p
       CK(cudaStreamWaitEvent(st, ev_prep_out, 0));
     }
     CKS(unorm());
-    ZrkCall s = tri_call(S, ldo, ng, kLowerOnly | kMirror, 0.0);
+    ZrkCall s = tri_call(S, ldo, ng, kLowerOnly | out_mirror, 0.0);
     s.segs.push_back({plain(A, K, ng, K), plain(A, K, ng, K)});
     s.segs.push_back({ub_view(), ub_view()});
     s.tl = &tl, s.sect = "s", s.core = "s_core";
@@ -1045,11 +1051,13 @@ static hsb_status build_hs_core(hsb_ctx* ctx, void* stream, const hsb_problem* p
       h3.segs.push_back({plain(Y, k_hpd, ng, K), plain(Y, k_hpd, ng, K)});
       CKS(run_zrk(ctx, st, h3, &launches));
     }
-    CK(launch_mirror(H, ldo, static_cast<int>(ng), st));
-    ++launches;
+    if (!(opts & HSB_OPT_LOWER_ONLY)) {
+      CK(launch_mirror(H, ldo, static_cast<int>(ng), st));
+      ++launches;
+    }
     CK(tl.mark(st, "h3"));
   } else {
-    ZrkCall h = tri_call(H, ldo, ng, kLowerOnly | kMirror, 0.0);
+    ZrkCall h = tri_call(H, ldo, ng, kLowerOnly | out_mirror, 0.0);
     h.segs.push_back({plain(A, K, ng, K), plain(Z, K, ng, K)});  // A^H V1
     if (h_via_ub)
       h.segs.push_back({ub_view(), plain(R, K, ng, K)});  // (UB)^H W2

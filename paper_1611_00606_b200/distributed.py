@@ -175,6 +175,203 @@ def build_hs_sharded_device(dp, h, s, hb, sb, policy=None, group=None, comm_stre
     return hb, sb
 
 
+class TrianglePlan:
+    """Index maps of the triangle-packed exchange ("triangle-packed
+    reduce-scatter halves the bytes").
+
+    Columns are distributed 1-D block-cyclically -- blocks of ``nb`` columns,
+    block j owned by rank j mod P, the layout ScaLAPACK-style eigensolvers
+    consume -- which balances the lower triangle across owners.  Each rank's
+    partial H / S is built as a lower triangle only (HSB_OPT_LOWER_ONLY: the
+    epilogue writes no mirror), and then
+
+    1. reduce-scatter: every owner receives the summed lower trapezoid of each
+       of its blocks (rows from the block's first column down), packed in
+       owner order and padded to the largest owner's share;
+    2. all-to-all: the strict upper part of an owner's columns is the
+       conjugate transpose of lower-trapezoid rows held by the owners of
+       earlier blocks: each sends the nb x nb tiles its owners need;
+    3. the upper halves of the diagonal blocks are mirrored locally.
+
+    Bytes per rank: (P-1)/P * N^2/2 (reduce-scatter, half the full-matrix
+    form) + about N^2 / (2P) * (P-1)/P (tiles), complex128.
+
+    Index tensors are built once per (n_g, P, nb) on ``device``; element (r, c)
+    of a partial buffer (a row-major (>= n_g + 1, n_g) tensor whose row n_g is
+    zero, the padding target) is at c * n_g + r; of the local result (a
+    row-major (len(cols), n_g) tensor) at lc * n_g + r, lc the local column.
+    """
+
+    def __init__(self, n_g: int, world: int, nb: int = 64, device="cpu"):
+        import torch
+
+        self.n_g, self.world, self.nb = n_g, world, nb
+        nblk = -(-n_g // nb)
+        self.blocks = [list(range(q, nblk, world)) for q in range(world)]
+        rng = lambda j: (j * nb, min((j + 1) * nb, n_g))  # noqa: E731
+        self.cols = [torch.cat([torch.arange(*rng(j)) for j in bl]) if bl else torch.zeros(0, dtype=torch.long)
+                     for bl in self.blocks]
+        local_of = torch.empty(n_g, dtype=torch.long)  # local column of a global column on its owner
+        for q in range(world):
+            local_of[self.cols[q]] = torch.arange(len(self.cols[q]))
+
+        def trapezoid(j):  # (r, c) of block j's lower trapezoid, column by column
+            c0, c1 = rng(j)
+            c = torch.arange(c0, c1).repeat_interleave(n_g - c0)
+            r = torch.arange(c0, n_g).repeat(c1 - c0)
+            return r, c
+
+        send, recv, lens = [], [], []
+        for q in range(world):
+            rs, cs = zip(*[trapezoid(j) for j in self.blocks[q]]) if self.blocks[q] else ((), ())
+            r = torch.cat(rs) if rs else torch.zeros(0, dtype=torch.long)
+            c = torch.cat(cs) if cs else torch.zeros(0, dtype=torch.long)
+            send.append(c * n_g + r)
+            recv.append(local_of[c] * n_g + r)
+            lens.append(len(r))
+        self.chunk = max(lens) if lens else 0
+        pad = n_g * n_g  # row n_g of the partial buffer (zeros)
+        self.send_idx = torch.cat([torch.cat([x, torch.full((self.chunk - len(x),), pad, dtype=torch.long)])
+                                   for x in send]).to(device)
+        self.recv_pos = [x.to(device) for x in recv]
+        # tiles: owner q2 of block j2 sends rows of block j (j > j2, owned by q) of its
+        # block j2's columns; q writes their conjugates at (column r, row c)
+        self.tile_send, self.tile_split_out = [], []
+        self.tile_recv, self.tile_split_in = [], []
+        for me in range(world):
+            out_idx, out_split = [], []
+            for q in range(world):
+                idx = []
+                for j2 in self.blocks[me]:
+                    c0, c1 = rng(j2)
+                    for j in self.blocks[q]:
+                        if j <= j2:
+                            continue
+                        r0, r1 = rng(j)
+                        c = torch.arange(c0, c1).repeat_interleave(r1 - r0)
+                        r = torch.arange(r0, r1).repeat(c1 - c0)
+                        idx.append(local_of[c] * n_g + r)
+                flat = torch.cat(idx) if idx else torch.zeros(0, dtype=torch.long)
+                out_idx.append(flat)
+                out_split.append(len(flat))
+            self.tile_send.append(torch.cat(out_idx).to(device))
+            self.tile_split_out.append(out_split)
+        for me in range(world):
+            in_pos, in_split = [], []
+            for q2 in range(world):
+                pos = []
+                for j2 in self.blocks[q2]:
+                    c0, c1 = rng(j2)
+                    for j in self.blocks[me]:
+                        if j <= j2:
+                            continue
+                        r0, r1 = rng(j)
+                        c = torch.arange(c0, c1).repeat_interleave(r1 - r0)
+                        r = torch.arange(r0, r1).repeat(c1 - c0)
+                        pos.append(local_of[r] * n_g + c)  # element (c, r) of column r
+                flat = torch.cat(pos) if pos else torch.zeros(0, dtype=torch.long)
+                in_pos.append(flat)
+                in_split.append(len(flat))
+            self.tile_recv.append(torch.cat(in_pos).to(device))
+            self.tile_split_in.append(in_split)
+        # diagonal blocks: (r < c) of column c = conj of (c, r), both local
+        self.diag_dst, self.diag_src = [], []
+        for q in range(world):
+            dst, src = [], []
+            for j in self.blocks[q]:
+                c0, c1 = rng(j)
+                c, r = torch.meshgrid(torch.arange(c0, c1), torch.arange(c0, c1), indexing="ij")
+                m = r < c
+                dst.append(local_of[c[m]] * n_g + r[m])
+                src.append(local_of[r[m]] * n_g + c[m])
+            self.diag_dst.append((torch.cat(dst) if dst else torch.zeros(0, dtype=torch.long)).to(device))
+            self.diag_src.append((torch.cat(src) if src else torch.zeros(0, dtype=torch.long)).to(device))
+
+    def bytes_per_rank(self, rank: int) -> int:
+        """complex128 bytes that reach this rank over the links: its
+        reduce-scatter share plus the tiles received from other ranks."""
+        tiles = sum(x for q, x in enumerate(self.tile_split_in[rank]) if q != rank)
+        return 16 * ((self.world - 1) * self.chunk + tiles)
+
+
+def triangle_reduce_scatter(partial, plan: TrianglePlan, group=None, upper: bool = True):
+    """This rank's columns (plan.cols[rank], block-cyclic) of sum_ranks(partial),
+    FULL Hermitian, as a row-major (len(cols), n_g) complex128 tensor
+    (``upper=False``: the lower trapezoids only -- all an uplo='L' Hermitian
+    eigensolver reads -- skipping the tile exchange: half a full reduce-scatter's bytes).
+
+    ``partial`` is a row-major (>= n_g + 1, n_g) complex128 tensor holding this
+    rank's partial matrix as a lower triangle (rows >= column of each column;
+    the upper triangle is never read) and zeros in row n_g."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    n_g = plan.n_g
+    flat = partial.reshape(-1)
+    send = flat[plan.send_idx.to(flat.device)]
+    stage = partial.is_cuda and dist.get_backend(group) == "gloo"  # ranks sharing a GPU in tests
+    if stage:
+        send = send.cpu()
+    recv = torch.empty(plan.chunk, dtype=send.dtype, device=send.device)
+    dist.reduce_scatter_tensor(torch.view_as_real(recv), torch.view_as_real(send), op=dist.ReduceOp.SUM, group=group)
+    dev = partial.device
+    local = torch.zeros((len(plan.cols[rank]), n_g), dtype=partial.dtype, device=dev)
+    lf = local.view(-1)
+    pos = plan.recv_pos[rank].to(dev)
+    lf[pos] = recv[: len(pos)].to(dev)
+    if not upper:
+        return local
+    tsend = lf[plan.tile_send[rank].to(dev)]
+    if stage:
+        tsend = tsend.cpu()
+    trecv = torch.empty(sum(plan.tile_split_in[rank]), dtype=local.dtype, device=tsend.device)
+    dist.all_to_all_single(torch.view_as_real(trecv), torch.view_as_real(tsend),
+                           output_split_sizes=plan.tile_split_in[rank], input_split_sizes=plan.tile_split_out[rank],
+                           group=group)
+    lf[plan.tile_recv[rank].to(dev)] = trecv.to(dev).conj()
+    lf[plan.diag_dst[rank].to(dev)] = lf[plan.diag_src[rank].to(dev)].conj()
+    return local
+
+
+def build_hs_sharded_tri(p, policy=None, group=None, partial=None, nb: int = 64, plan=None):
+    """Atom-sharded H/S build with the triangle-packed exchange: this rank's
+    block-cyclic columns (``plan.cols[rank]``) of H and S.  ``partial(shard,
+    h, s)`` fills lower-triangle partial sums (default: the GPU pipeline with
+    HSB_OPT_LOWER_ONLY).  Returns (ShardedResult-like tuple) h_cols, s_cols,
+    global column indices, split counts summed over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    n_g = int(p.dims.n_g)
+    lo, hi = atom_ranges(int(p.dims.n_atoms), world)[rank]
+    if partial is None:
+        from .pipeline import build_hs_into
+
+        dev = torch.device("cuda", torch.cuda.current_device())
+
+        def partial(shard, h, s):
+            split, t, _ = build_hs_into(shard, h, s, policy, lower_only=True)
+            return split, t
+    else:
+        dev = torch.device("cpu")
+    if plan is None:
+        plan = TrianglePlan(n_g, world, nb, device=dev)
+    h = torch.zeros((n_g + 1, n_g), dtype=torch.complex128, device=dev)
+    s = torch.zeros_like(h)
+    counts = [0, 0]
+    if hi > lo:
+        split, _t = partial(shard_instance(p, range(lo, hi)), h, s)
+        counts = [split.hpd, split.nonhpd]
+    hc = triangle_reduce_scatter(h, plan, group)
+    sc = triangle_reduce_scatter(s, plan, group)
+    c = torch.tensor(counts, dtype=torch.int64,
+                     device=dev if dist.get_backend(group) == "nccl" else torch.device("cpu"))
+    dist.all_reduce(c, group=group)
+    return hc, sc, plan.cols[rank], int(c[0]), int(c[1])
+
+
 class PeerSlots:
     """Receive slots for the fused reduce-scatter (hsb_peer_out).
 

@@ -199,11 +199,14 @@ def _host_problem(p):
     return prob, (blocks, arrays)
 
 
-def _call_build(pol, prob, out, stream, force_nonhpd, n_a, slot: int = 0, wait: bool = True, phys=None):
+def _call_build(pol, prob, out, stream, force_nonhpd, n_a, slot: int = 0, wait: bool = True, phys=None,
+                lower_only: bool = False):
     lib = _lib.load()
     opts = (_lib.HSB_OPT_FORCE_NONHPD if force_nonhpd else 0) | (0 if pol.fused else _lib.HSB_OPT_UNFUSED)
     if not pol.lower_d2h:
         opts |= _lib.HSB_OPT_FULL_D2H
+    if lower_only:
+        opts |= _lib.HSB_OPT_LOWER_ONLY
     if prob.location == _lib.HSB_LOC_HOST:
         opts |= _lib.HSB_OPT_VALIDATE  # T / u values are checked natively, before any transfer
     tim = _lib.HsbTimings()
@@ -408,10 +411,12 @@ def build_hs_kpoints(instances, policy=None, force_nonhpd: bool = False, depth: 
     return list(iter_hs_kpoints(instances, policy, force_nonhpd, depth))
 
 
-def build_hs_into(p, h, s, policy=None, force_nonhpd: bool = False, stream=None):
+def build_hs_into(p, h, s, policy=None, force_nonhpd: bool = False, stream=None, lower_only: bool = False):
     """Host per-atom blocks in, device H/S out (torch tensors, row-major
     (>= n_g, n_g) holding the column-major matrices).  Used by the sharded
-    multi-GPU path, whose partial H/S go straight into a reduce-scatter."""
+    multi-GPU path, whose partial H/S go straight into a reduce-scatter.
+    ``lower_only``: lower triangles only, no mirror (HSB_OPT_LOWER_ONLY; the
+    triangle-packed exchange reads nothing else)."""
     import torch
 
     _validate_shapes(p)
@@ -429,7 +434,7 @@ def build_hs_into(p, h, s, policy=None, force_nonhpd: bool = False, stream=None)
     if stream is None:
         stream = torch.cuda.current_stream(h.device)
     tim, info = _call_build(pol, prob, out, ctypes.c_void_p(stream.cuda_stream), force_nonhpd,
-                            int(p.dims.n_atoms))
+                            int(p.dims.n_atoms), lower_only=lower_only)
     return SplitCounts(tim.n_hpd, tim.n_nonhpd), _timings_dict(tim), info
 
 

@@ -85,3 +85,72 @@ def test_partition_helpers():
     p = generate(ProblemSpec(Dims(4, 3, 5), seed=1))
     q = shard_instance(p, [1, 3])
     assert q.dims.n_atoms == 2 and q.a_blocks[1] is p.a_blocks[3]
+
+
+def _cpu_partial_lower(shard, h, s):
+    from oracle import alg1
+
+    out = alg1.build_hs_cpu(shard)
+    n = shard.dims.n_g
+    # lower triangles only (the HSB_OPT_LOWER_ONLY contract); garbage above
+    # the diagonal must not leak into the result
+    junk = np.triu(np.full((n, n), 7.0 + 3.0j), 1)
+    h[:n] = torch.from_numpy(np.ascontiguousarray((np.tril(out["h"]) + junk).T))
+    s[:n] = torch.from_numpy(np.ascontiguousarray((np.tril(out["s"]) + junk).T))
+    return SplitCounts(out["hpd"], out["nonhpd"]), {}
+
+
+def _worker_tri(rank, world, port, dims, nb, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_1611_00606_b200.distributed import build_hs_sharded_tri
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    p = generate(ProblemSpec(Dims(*dims), seed=4, nonhpd_fraction=0.3))
+    hc, sc, cols, hpd, nonhpd = build_hs_sharded_tri(p, partial=_cpu_partial_lower, nb=nb)
+    q.put((rank, hc.numpy(), sc.numpy(), cols.numpy(), hpd, nonhpd))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,dims,nb", [(2, (5, 6, 37), 4), (3, (4, 5, 50), 8), (4, (3, 4, 23), 16)])
+def test_triangle_packed_exchange_matches_single_process(world, dims, nb):
+    from oracle import alg1
+    from paper_1611_00606_b200.distributed import TrianglePlan
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_tri, args=(r, world, port, dims, nb, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    got = [q.get(timeout=120) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    p = generate(ProblemSpec(Dims(*dims), seed=4, nonhpd_fraction=0.4 - 0.1))
+    full = alg1.build_hs_cpu(p)
+    seen = []
+    for rank, hc, sc, cols, hpd, nonhpd in got:
+        assert hpd + nonhpd == dims[0]
+        # row-major (local column, row) -> columns cols of the matrices
+        assert rel_frob_error(hc.T, full["h"][:, cols]) < 1e-13
+        assert rel_frob_error(sc.T, full["s"][:, cols]) < 1e-13
+        seen += cols.tolist()
+    assert sorted(seen) == list(range(dims[2]))
+
+
+@pytest.mark.parametrize("n_g,world,nb", [(2000, 4, 32), (1500, 8, 16), (1200, 2, 64)])
+def test_triangle_plan_moves_about_half_the_bytes(n_g, world, nb):
+    # per-rank bytes of the triangle-packed exchange against a full-matrix
+    # reduce-scatter ((P-1)/P N^2 complex128): (P-1)/(2P) N^2 + the tiles
+    from paper_1611_00606_b200.distributed import TrianglePlan
+
+    plan = TrianglePlan(n_g, world, nb)
+    full = (world - 1) / world * n_g * n_g * 16
+    worst = max(plan.bytes_per_rank(r) for r in range(world))
+    model = full / 2 * (1 + 1 / world)  # RS of the triangle + upper tiles from the other ranks
+    assert worst < 1.15 * model and worst < 0.85 * full
+    # lower-only columns (what uplo='L' eigensolvers read): the reduce-scatter alone
+    assert (world - 1) * plan.chunk * 16 < 0.6 * full
+    assert sorted(torch.cat(plan.cols).tolist()) == list(range(n_g))

@@ -7,6 +7,9 @@ another's).  Each rank builds the partial H/S of its atom shard on the GPU
 
 * ``nccl`` path: ``build_hs_sharded`` -- partial into padded (ncols, N_G)
   buffers, ``reduce_scatter_block_columns`` (gloo here, NCCL on a box);
+* ``tri`` path: ``build_hs_sharded_tri`` -- lower-triangle partials
+  (HSB_OPT_LOWER_ONLY), the triangle-packed reduce-scatter and the tile
+  all-to-all into block-cyclic columns;
 * ``fused`` path: ``build_hs_sharded_fused`` -- the INT8 engine's CRT epilogue
   stores every element into its owner's receive slot (CUDA-IPC peer memory),
   owners sum their slots; run for 2 steps so the slot reuse is exercised;
@@ -55,6 +58,10 @@ def _worker(rank, world, port, mode, q):
         if mode == "nccl":
             res = hd.build_hs_sharded(p, pol)
             blocks = (res.col0, res.columns("h"), res.columns("s"), res.hpd, res.nonhpd)
+        elif mode == "tri":  # lower-triangle partials, triangle-packed exchange, block-cyclic columns
+            hc, sc, cols, hpd, nonhpd = hd.build_hs_sharded_tri(p, pol, nb=64)
+            blocks = (cols.cpu().numpy(), np.asfortranarray(hc.cpu().numpy().T),
+                      np.asfortranarray(sc.cpu().numpy().T), hpd, nonhpd)
         else:
             slots = hd.PeerSlots.group(p.dims.n_g, dev)
             lo, hi = hd.atom_ranges(p.dims.n_atoms, world)[rank]
@@ -77,7 +84,7 @@ def _worker(rank, world, port, mode, q):
         raise
 
 
-@pytest.mark.parametrize("mode", ["nccl", "fused"])
+@pytest.mark.parametrize("mode", ["nccl", "fused", "tri"])
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_gpu_ranks_match_oracle(world, mode):
     import torch.multiprocessing as mp
@@ -102,8 +109,11 @@ def test_sharded_gpu_ranks_match_oracle(world, mode):
     h_cols = np.concatenate([g[2] for g in got], axis=1)
     s_cols = np.concatenate([g[3] for g in got], axis=1)
     assert h_cols.shape == (DIMS[2], DIMS[2])
+    if mode == "tri":  # block-cyclic ownership: put the columns back in order
+        order = np.argsort(np.concatenate([g[1] for g in got]))
+        h_cols, s_cols = h_cols[:, order], s_cols[:, order]
     eh, es = rel_frob_error(h_cols, full["h"]), rel_frob_error(s_cols, full["s"])
     print(f"world {world} {mode}: rel err H {eh:.2e} S {es:.2e}")
     assert eh < 1e-14 and es < 1e-14
-    if mode == "nccl":
+    if mode in ("nccl", "tri"):
         assert all(g[4] == full["hpd"] and g[4] + g[5] == DIMS[0] for g in got)
