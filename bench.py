@@ -440,7 +440,7 @@ def main():
     ap.add_argument("--engine", default="auto", choices=["auto", "int8", "dmma"],
                     help="S/H contractions on the INT8 tensor cores (CRT emulation, ~1e-12) or FP64 DMMA")
     ap.add_argument("--no-compare", action="store_true", help="skip the second-engine measurement")
-    ap.add_argument("--rs", default="nccl", choices=["nccl", "fused"],
+    ap.add_argument("--rs", default="nccl", choices=["nccl", "fused", "tri"],
                     help="N > 1: NCCL reduce-scatter (S overlapped with H) or the fused scatter from the "
                          "reconstruction epilogue into CUDA-IPC peer slots (INT8 engine)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -501,10 +501,19 @@ def main():
 
     comm_stream = torch.cuda.Stream(device=dev) if world > 1 else None
     slots = hsdist.PeerSlots.group(n_g, dev) if world > 1 and args.rs == "fused" else None
+    tri_plan = hsdist.TrianglePlan(n_g, world, 64, device=dev) if world > 1 and args.rs == "tri" else None
+    if tri_plan is not None:  # lower-triangle partials with a zero row n_g (the packing's padding target)
+        h_t = torch.zeros((n_g + 1, n_g), dtype=torch.complex128, device=dev)
+        s_t = torch.zeros_like(h_t)
 
     def step(pol=policy):
         if world > 1 and slots is not None and pol.engine != "dmma":
             hsdist.build_hs_sharded_fused(dp, slots, pol)
+            return None
+        if tri_plan is not None:
+            build_hs_device(dp, h_t, s_t, pol, wait=False, lower_only=True)
+            hsdist.triangle_reduce_scatter(s_t, tri_plan)
+            hsdist.triangle_reduce_scatter(h_t, tri_plan)
             return None
         if world > 1:
             # S's reduce-scatter overlaps the H contraction (s_ready event)
@@ -767,8 +776,10 @@ def main():
             "data": "synthetic (seeded hsgen-compatible generator)",
             "config": {"workload": args.config, "desc": CONFIG_DESC[args.config], "n_atoms": dims.n_atoms,
                        "n_l": dims.n_l, "n_g": dims.n_g, "nonhpd_fraction": args.nonhpd_fraction,
-                       "parallelism": f"atom-shard x{world}" + ((" + fused peer scatter" if args.rs == "fused" else
-                                                                      " + NCCL reduce-scatter") if world > 1 else ""),
+                       "parallelism": f"atom-shard x{world}" + ({"fused": " + fused peer scatter",
+                                                                 "tri": " + triangle-packed NCCL reduce-scatter",
+                                                                 "nccl": " + NCCL reduce-scatter"}[args.rs]
+                                                                if world > 1 else ""),
                        "fused": not args.unfused, "engine": ("int8 (FP64 width)" if int8 else "dmma"),
                        "complex_mult": args.complex_mult, "model_tflop_per_step": flops_full / 1e12,
                        "l2_note": "inputs larger than L2 (A/B stacks 496 MB each at C3)"},

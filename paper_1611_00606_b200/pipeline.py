@@ -479,7 +479,7 @@ class DeviceProblem:
 
 def build_hs_device(dp: DeviceProblem, h=None, s=None, policy=None, force_nonhpd: bool = False,
                     stream=None, s_ready=None, wait: bool = True, peer=None, host_outputs: bool = False,
-                    slot: int = 0, order=None, phys=None):
+                    slot: int = 0, order=None, phys=None, lower_only: bool = False):
     """Device-resident build: returns (H, S, SplitCounts, timings, atom_info).
 
     H and S are torch complex128 (n_g, n_g) tensors holding the column-major
@@ -497,6 +497,7 @@ def build_hs_device(dp: DeviceProblem, h=None, s=None, policy=None, force_nonhpd
     streaming, lower triangles completed by the host mirror).  ``phys`` (an
     ``_lib.HsbPhys``, see physics.py) makes the call generate the matching
     coefficients into ``dp``'s A and B stacks first (hsb_build_hs_physical).
+    ``lower_only``: H and S as lower triangles, no mirror (HSB_OPT_LOWER_ONLY).
     """
     import torch
 
@@ -550,7 +551,7 @@ def build_hs_device(dp: DeviceProblem, h=None, s=None, policy=None, force_nonhpd
     if stream is None:
         stream = torch.cuda.current_stream(dev)
     tim, info = _call_build(pol, prob, out, ctypes.c_void_p(stream.cuda_stream), force_nonhpd, n_a, slot=slot,
-                            wait=wait, phys=phys)
+                            wait=wait, phys=phys, lower_only=lower_only)
     if not wait:
         return h, s, None, None, None
     if host_outputs:

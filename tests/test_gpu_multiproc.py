@@ -100,7 +100,7 @@ def test_sharded_gpu_ranks_match_oracle(world, mode):
     got = [q.get(timeout=600) for _ in range(world)]
     for pr in procs:
         pr.join(timeout=120)
-    errors = [g for g in got if g[1] == "error"]
+    errors = [g for g in got if isinstance(g[1], str) and g[1] == "error"]
     assert not errors, errors
     assert all(pr.exitcode == 0 for pr in procs)
     p = generate(ProblemSpec(Dims(*DIMS), seed=9, nonhpd_fraction=0.3))
