@@ -268,7 +268,8 @@ def coeff_roofline(system, kpt, gset, dev, reps: int = 10) -> dict:
     prof = ROOT / "profiles" / "roofline_traffic.json"
     try:
         rec = json.loads(prof.read_text()).get("C3/match")
-        traffic = rec["bytes"] if rec and n_g == rec.get("n_g") else None
+        # per-column DRAM bytes of the C3 capture, scaled to this G set (same rows)
+        traffic = int(rec["bytes"] / rec["n_g"] * n_g) if rec and k == 3872 else None
     except (OSError, ValueError):
         pass
     return {"bound": "hbm", "kernel": "match_coeffs_kernel (A, B from Y_lm, j_l, j_l', e^{iK.tau})",

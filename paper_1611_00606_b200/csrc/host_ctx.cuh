@@ -42,6 +42,9 @@ struct hsb_ctx {
   std::map<std::string, DevBuf> bufs;
   void* pinned = nullptr;  // small pinned host scratch (routing info / offsets)
   size_t pinned_bytes = 0;
+  void* m_stage = nullptr;  // pinned staging of the matching kernel's small inputs
+  size_t m_stage_bytes = 0;
+  cudaEvent_t m_stage_done = nullptr;  // its last uploads consumed (reuse after this)
   hsb::Stager stager;                 // pinned-slot host<->device transfers
   int* done_cnt = nullptr;            // mapped pinned per-column-block tile counters
   size_t done_cnt_len = 0;

@@ -73,6 +73,8 @@ void hsb_ctx_destroy(hsb_ctx* ctx) {
   for (auto& kv : ctx->bufs)
     if (kv.second.ptr) cudaFree(kv.second.ptr);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->m_stage) cudaFreeHost(ctx->m_stage);
+  if (ctx->m_stage_done) cudaEventDestroy(ctx->m_stage_done);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->done_cnt) cudaFreeHost(ctx->done_cnt);
   delete ctx;
@@ -1267,11 +1269,31 @@ static hsb_status match_setup(hsb_ctx* ctx, cudaStream_t st, const hsb_phys* ph,
   CKS(ws(ctx, "m_type", yb, &y));
   CKS(ws(ctx, "m_rmt", rb, &r));
   CKS(ws(ctx, "m_radial", db, &d));
-  CK(cudaMemcpyAsync(g, ph->gvec, gb, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(t, ph->tau, tb, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(y, ph->type_of, yb, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(r, ph->rmt, rb, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(d, ph->radial, db, cudaMemcpyHostToDevice, st));
+  // the small inputs go through a pinned staging buffer: the copies are truly
+  // asynchronous (no host stall between back-to-back calls); the buffer is
+  // reused once the previous call's copies have run (event)
+  const size_t sizes[5] = {gb, tb, yb, rb, db};
+  const void* srcs[5] = {ph->gvec, ph->tau, ph->type_of, ph->rmt, ph->radial};
+  void* dsts[5] = {g, t, y, r, d};
+  size_t total = 0, offs[5];
+  for (int i = 0; i < 5; ++i) {
+    offs[i] = total;
+    total += (sizes[i] + 255) / 256 * 256;
+  }
+  if (ctx->m_stage_done) CK(cudaEventSynchronize(ctx->m_stage_done));
+  else CK(cudaEventCreateWithFlags(&ctx->m_stage_done, cudaEventDisableTiming));
+  if (ctx->m_stage_bytes < total) {
+    if (ctx->m_stage) cudaFreeHost(ctx->m_stage);
+    ctx->m_stage = nullptr;
+    ctx->m_stage_bytes = 0;
+    CK(cudaHostAlloc(&ctx->m_stage, total, cudaHostAllocDefault));
+    ctx->m_stage_bytes = total;
+  }
+  for (int i = 0; i < 5; ++i) {
+    std::memcpy(static_cast<char*>(ctx->m_stage) + offs[i], srcs[i], sizes[i]);
+    CK(cudaMemcpyAsync(dsts[i], static_cast<char*>(ctx->m_stage) + offs[i], sizes[i], cudaMemcpyHostToDevice, st));
+  }
+  CK(cudaEventRecord(ctx->m_stage_done, st));
   MatchParams mp;
   std::memset(&mp, 0, sizeof(mp));
   mp.gvec = static_cast<int32_t*>(g);
@@ -1288,8 +1310,6 @@ static hsb_status match_setup(hsb_ctx* ctx, cudaStream_t st, const hsb_phys* ph,
   mp.n_types = ph->n_types;
   mp.lmax = ph->lmax;
   if (match_smem_bytes(mp) > 200 * 1024) return fail(ctx, HSB_ERR_UNSUPPORTED, "too many atoms for one column CTA");
-  // the small uploads come from caller memory: land them before returning
-  CK(cudaStreamSynchronize(st));
   *mp_out = mp;
   return HSB_OK;
 }

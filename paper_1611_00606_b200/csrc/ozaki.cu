@@ -612,10 +612,12 @@ __device__ __forceinline__ int sbyte(uint32_t w, int e) { return static_cast<int
 
 // Finish one element from its X / M fractions (Re, Im): scale by
 // 2^(e_m + e_n - 2b), alpha / beta, Im(diag) = 0
+template <bool PLAIN>
 __device__ __forceinline__ double2 crt_finish(const OzCrtParams& p, double fr, double fi, double mm, int sh, int m,
                                               int n) {
   const double xr = scale2(fr * mm, sh);
   const double xi = scale2(fi * mm, sh);
+  if (PLAIN) return make_double2(xr, (m == n && (p.flags & (kMirror | kZeroImagDiag))) ? 0.0 : xi);
   double vr = p.alpha_re * xr - p.alpha_im * xi;
   double vi = p.alpha_re * xi + p.alpha_im * xr;
   if (p.beta_re != 0.0 || p.beta_im != 0.0) {
@@ -655,7 +657,8 @@ __device__ __forceinline__ int crt_chunks(int n, int cs) { return (n - 1) / kCrt
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
-template <int NM>
+// PLAIN: alpha = 1, beta = 0 (every build call): no scaling, no read of C
+template <int NM, bool PLAIN>
 __global__ void __launch_bounds__(256, 3) ozaki_crt_kernel(const OzCrtParams p, int ncols) {
   // residues [product][modulus][column][128 rows], then (reused) the mirror stage
   constexpr int kResBytes = 2 * NM * kCrtCols * kCrtRows;
@@ -686,13 +689,12 @@ __global__ void __launch_bounds__(256, 3) ozaki_crt_kernel(const OzCrtParams p, 
     const int t = p.tile_index[(r0 >> 8) * p.T + (cs >> 8)];
     const uint8_t* base = reinterpret_cast<const uint8_t*>(p.res) + static_cast<int64_t>(t) * kOzTileBytes +
                           (cs & 255) * 256 + (r0 & 255);
-    const uint32_t sbase = smem_u32(smem);
-    for (int c = threadIdx.x; c < 2 * NM * 64; c += blockDim.x) {
-      const int q = c >> 6, col = (c >> 3) & 7, part = c & 7;  // plane (product, modulus), column, 16 B piece
-      const int prod = q / NM, mod = q - prod * NM;
-      cp_async16(sbase + q * 1024 + col * 128 + part * 16,
-                 base + prod * p.prod_stride + mod * p.mod_stride + col * 256 + part * 16);
-    }
+    // plane q = (product, modulus) sits q * mod_stride further (prod_stride =
+    // n_mod * mod_stride); thread = (16-byte piece, column, first plane)
+    const int part = threadIdx.x & 7, col = (threadIdx.x >> 3) & 7, q0 = threadIdx.x >> 6;
+    const uint8_t* src = base + q0 * p.mod_stride + col * 256 + part * 16;
+    uint32_t dst = smem_u32(smem) + q0 * 1024 + col * 128 + part * 16;
+    for (int q = q0; q < 2 * NM; q += 4, src += 4 * p.mod_stride, dst += 4096) cp_async16(dst, src);
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
   }
   __syncthreads();
@@ -732,7 +734,7 @@ __global__ void __launch_bounds__(256, 3) ozaki_crt_kernel(const OzCrtParams p, 
       const int m = m0 + e;
       if (m < n || m >= p.n) continue;
       const double fr = (r1[e] - rint(r1[e])) + r2[e], fi = (i1[e] - rint(i1[e])) + i2[e];
-      const double2 v = crt_finish(p, fr, fi, mm, __ldg(p.el + m) + ern, m, n);
+      const double2 v = crt_finish<PLAIN>(p, fr, fi, mm, __ldg(p.el + m) + ern, m, n);
       *crt_dst(p, m, n) = v;
       stage[warp][e * 32 + lane] = v;
     }
@@ -1069,6 +1071,7 @@ cudaError_t launch_ozaki_crt_cols(const OzCrtParams& p, int64_t ncols, cudaStrea
   cudaError_t ce = oz_init_once();
   if (ce != cudaSuccess) return ce;
   if (p.n0 % kCrtCols != 0) return cudaErrorInvalidValue;  // column blocks stay inside a tile
+  if (p.prod_stride != p.mod_stride * p.n_mod) return cudaErrorInvalidValue;  // planes evenly spaced
   // column-block pairs (y, ncb - 1 - y): 128-aligned row chunks from each
   // block's diagonal down to row n
   const int64_t ncb = (ncols + kCrtCols - 1) / kCrtCols;
@@ -1084,9 +1087,13 @@ cudaError_t launch_ozaki_crt_cols(const OzCrtParams& p, int64_t ncols, cudaStrea
   }
   const dim3 grid(static_cast<unsigned>(most), static_cast<unsigned>((ncb + 1) / 2)), block(256);
   const int nc = static_cast<int>(ncols);
-#define HSB_OZ_CRT(NMV)                                     \
-  case NMV:                                               \
-    ozaki_crt_kernel<NMV><<<grid, block, 0, st>>>(p, nc); \
+  const bool plain = p.alpha_re == 1.0 && p.alpha_im == 0.0 && p.beta_re == 0.0 && p.beta_im == 0.0;
+#define HSB_OZ_CRT(NMV)                                                \
+  case NMV:                                                          \
+    if (plain)                                                       \
+      ozaki_crt_kernel<NMV, true><<<grid, block, 0, st>>>(p, nc);    \
+    else                                                             \
+      ozaki_crt_kernel<NMV, false><<<grid, block, 0, st>>>(p, nc);   \
     break;
   switch (p.n_mod) {
     HSB_OZ_CRT(11)
