@@ -174,6 +174,22 @@ __global__ void sum_planes_kernel(const double2* __restrict__ x, int64_t ldx, in
   }
 }
 
+__global__ void sum_planes_batched_kernel(const double2* __restrict__ x, int n, int64_t bstride, int64_t count,
+                                          int minus, double* __restrict__ out, int kp) {
+  const int64_t total = count * n * kp;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(idx % kp);
+    const int64_t bc = idx / kp, b = bc / n, c = bc - b * n;
+    double v = 0.0;
+    if (k < n) {
+      const double2 w = x[b * bstride + c * static_cast<int64_t>(n) + k];
+      v = minus ? w.x - w.y : w.x + w.y;
+    }
+    out[idx] = v;
+  }
+}
+
 // In-place Hermitian mirror (matcore.hermitian_mirror, matcore.py:89-105):
 // 32 x 32 tile pairs staged through shared memory so both the lower-tile read
 // and the upper-tile write are coalesced.
@@ -331,6 +347,15 @@ cudaError_t launch_sum_planes(const double* x, int64_t ldx, int64_t rows, int64_
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   sum_planes_kernel<<<grid_for(rows * cols, 256, 148 * 32), 256, 0, st>>>(reinterpret_cast<const double2*>(x), ldx,
                                                                           rows, cols, minus, plus, ldp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sum_planes_batched(const double* x, int n, int64_t bstride, int64_t count, bool minus,
+                                     double* out, int kp, cudaStream_t st) {
+  const int64_t total = count * n * kp;
+  if (total <= 0) return cudaSuccess;
+  sum_planes_batched_kernel<<<grid_for(total, 256, 148 * 16), 256, 0, st>>>(
+      reinterpret_cast<const double2*>(x), n, bstride, count, minus ? 1 : 0, out, kp);
   return cudaGetLastError();
 }
 

@@ -37,7 +37,12 @@ constexpr size_t kPotrfSmemMax = 200 * 1024;  // packed lower triangle up to n =
 
 cudaError_t launch_zrk(const ZrkParams& p, bool conj, int grid_x, int grid_z, cudaStream_t st);
 // 3M (Gauss) variant, persistent: ntiles tiles per batch x nbatch batches
-cudaError_t launch_zrk3m(const ZrkParams& p, bool conj, bool planes, int ntiles, int nbatch, cudaStream_t st);
+cudaError_t launch_zrk3m(const ZrkParams& p, bool conj, int pmode, int ntiles, int nbatch, cudaStream_t st);
+// per-atom planes of count n x n column-major complex blocks (atom stride bstride
+// complex): out[(b * n + c) * kp + k] = Re x -/+ Im x (minus: Re - Im), zero for
+// k in [n, kp)
+cudaError_t launch_sum_planes_batched(const double* x, int n, int64_t bstride, int64_t count, bool minus,
+                                     double* out, int kp, cudaStream_t st);
 cudaError_t launch_potrf_route(const double* t_aa, double* q, int32_t* info, int n_atoms, int n,
                                bool force_nonhpd, double* gscratch, cudaStream_t st);
 cudaError_t launch_half_mirror(const double* t, double* out, int n, int64_t count, double scale,

@@ -59,7 +59,9 @@ struct ZrkParams {
   CUtensorMap lmap[kMaxSeg];  // 3-D maps over the real view, box {16, 64|1, 1|64}
   CUtensorMap rmap[kMaxSeg];
   CUtensorMap lsum[kMaxSeg];  // 3M with planes: 2-D maps over Re-Im of L / Re+Im of R,
-  CUtensorMap rsum[kMaxSeg];  // box {8 complex k, 64 cols}, no swizzle (zrk3m_kernel.cu)
+  CUtensorMap rsum[kMaxSeg];  // box {8 complex k, 64 cols}, no swizzle (zrk3m_kernel.cu);
+                              // batched left operands (lplane3d): 3-D {kp, cols, batch}, box {8, 64, 1}
+  int32_t lplane3d;           // 1: lsum maps are 3-D per-atom planes (batch coordinate last)
   SegDesc seg[kMaxSeg];
   int32_t nseg;
   int32_t total_chunks;

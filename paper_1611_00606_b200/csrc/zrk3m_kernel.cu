@@ -27,12 +27,15 @@
 //     chunks: conflict-free LDS.128;
 //   * 12 pipeline stages x 16 KB.
 //
-// PLANES: the host precomputes Re-Im of every left operand and Re+Im of every
-// right operand (sum_planes_kernel), loaded by TMA beside the complex tiles
-// (+8 KB per stage, 8 stages), so the main loop is LDS + DMMA only.  Without
-// planes (batched per-atom views, whose odd row strides TMA cannot address
-// as real planes) the sums are formed in registers with DADD, which shares
-// the FP64 pipe with DMMA (ncu: 90 % vs 96 % DMMA-active on the H launch).
+// PMODE (plane mode): 2 -- the host precomputes Re-Im of every left operand and
+// Re+Im of every right operand (sum_planes_kernel), loaded by TMA beside the
+// complex tiles (+8 KB per stage, 8 stages), so the main loop is LDS + DMMA
+// only; 1 -- left planes only: the batched per-atom products (V products),
+// whose left operands are the small T blocks, get them as per-atom planes
+// padded to an even k (so the 3-D TMA view's atom stride is 16-byte aligned;
+// +4 KB per stage, 9 stages), and form only the right operand's sum in
+// registers (2 of the 6 DADD per k step); 0 -- both sums in registers (DADD
+// shares the FP64 pipe with DMMA: ncu 90 % vs 96 % DMMA-active on the H launch).
 #include <algorithm>
 
 #include "aux_kernels.cuh"
@@ -44,10 +47,10 @@ namespace hsb {
 constexpr int k3ConsumerWarps = 8;  // 2 (rows) x 4 (cols) warps of 32 x 16
 constexpr int k3Threads = (k3ConsumerWarps + 1) * 32;
 constexpr int kPlaneTileBytes = kBM * 8 * 8;  // 64 rows x 8 complex k, one double each
-template <bool PLANES>
+template <int PMODE>
 struct Cfg3 {
-  static constexpr int stage_bytes = kStageBytes + (PLANES ? 2 * kPlaneTileBytes : 0);
-  static constexpr int stages = PLANES ? 8 : 12;
+  static constexpr int stage_bytes = kStageBytes + PMODE * kPlaneTileBytes;
+  static constexpr int stages = PMODE == 2 ? 8 : PMODE == 1 ? 9 : 12;  // PMODE 1: 180 KB, room for a residue block beside it
   static constexpr int smem = stages * stage_bytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
@@ -80,14 +83,15 @@ __device__ __forceinline__ void work_tile(const ZrkParams& p, int w, int ntiles,
   }
 }
 
-template <bool CONJ, bool PLANES>
+template <bool CONJ, int PMODE>
 __global__ void __launch_bounds__(k3Threads, 1) zrk3m_kernel(const __grid_constant__ ZrkParams p, int ntiles,
                                                               int nwork) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;  // 128B swizzle atom = 1024 B
   const double2* tiles = reinterpret_cast<const double2*>(smem_raw + (base - raw));
-  using C3 = Cfg3<PLANES>;
+  using C3 = Cfg3<PMODE>;
+  constexpr bool LPLANE = PMODE >= 1, RPLANE = PMODE == 2;
   constexpr int kSt = C3::stages;
   constexpr int kSB = C3::stage_bytes;
   const uint32_t bar_base = base + kSt * kSB;  // full[s] then empty[s]
@@ -112,10 +116,8 @@ __global__ void __launch_bounds__(k3Threads, 1) zrk3m_kernel(const __grid_consta
       for (int s = 0; s < p.nseg; ++s) {
         prefetch_tmap(&p.lmap[s]);
         prefetch_tmap(&p.rmap[s]);
-        if (PLANES) {
-          prefetch_tmap(&p.lsum[s]);
-          prefetch_tmap(&p.rsum[s]);
-        }
+        if (LPLANE) prefetch_tmap(&p.lsum[s]);
+        if (RPLANE) prefetch_tmap(&p.rsum[s]);
       }
       int stage = 0;
       uint32_t phase = 1;  // fresh empty barriers read as "released"
@@ -139,10 +141,14 @@ __global__ void __launch_bounds__(k3Threads, 1) zrk3m_kernel(const __grid_consta
               tma_load_3d(dst + kTileBytes, &p.rmap[s], k0, z, col0, fb);
             else
               tma_load_3d(dst + kTileBytes, &p.rmap[s], k0, col0, z, fb);
-            if (PLANES) {  // plain operands only (z == 0): 2-D planes, k in complex units
-              tma_load_2d(dst + kStageBytes, &p.lsum[s], kc * 8, row0, fb);
-              tma_load_2d(dst + kStageBytes + kPlaneTileBytes, &p.rsum[s], kc * 8, col0, fb);
+            if (LPLANE) {  // k in complex units
+              if (p.lplane3d)
+                tma_load_3d(dst + kStageBytes, &p.lsum[s], kc * 8, row0, z, fb);
+              else
+                tma_load_2d(dst + kStageBytes, &p.lsum[s], kc * 8, row0, fb);
             }
+            if (RPLANE)  // plain operands only (z == 0): 2-D planes
+              tma_load_2d(dst + kStageBytes + kPlaneTileBytes, &p.rsum[s], kc * 8, col0, fb);
             if (++stage == kSt) {
               stage = 0;
               phase ^= 1u;
@@ -191,11 +197,13 @@ __global__ void __launch_bounds__(k3Threads, 1) zrk3m_kernel(const __grid_consta
       const double2* Bs = As + kTile2;
       // plane tiles: 64 rows x 4 double2 (complex k = 2t, 2t+1 of this lane)
       double2 sa[4], sb[2];
-      if (PLANES) {
+      if (LPLANE) {
         const double2* Ps = Bs + kTile2;
-        const double2* Qs = Ps + kPlaneTileBytes / 16;
 #pragma unroll
         for (int i = 0; i < 4; ++i) sa[i] = Ps[(wm * 32 + i * 8 + g) * 4 + t];
+      }
+      if (RPLANE) {
+        const double2* Qs = Bs + kTile2 + kPlaneTileBytes / 16;
 #pragma unroll
         for (int j = 0; j < 2; ++j) sb[j] = Qs[(wn * 16 + j * 8 + g) * 4 + t];
       }
@@ -209,14 +217,17 @@ __global__ void __launch_bounds__(k3Threads, 1) zrk3m_kernel(const __grid_consta
         for (int i = 0; i < 4; ++i) a[i] = As[oa + i * 64];
 #pragma unroll
         for (int j = 0; j < 2; ++j) b[j] = Bs[ob + j * 64];
-        if (PLANES) {
+        if (LPLANE) {
 #pragma unroll
           for (int i = 0; i < 4; ++i) as[i] = s ? sa[i].y : sa[i].x;
-#pragma unroll
-          for (int j = 0; j < 2; ++j) bs[j] = s ? sb[j].y : sb[j].x;
         } else {
 #pragma unroll
           for (int i = 0; i < 4; ++i) as[i] = CONJ ? a[i].x - a[i].y : a[i].x + a[i].y;
+        }
+        if (RPLANE) {
+#pragma unroll
+          for (int j = 0; j < 2; ++j) bs[j] = s ? sb[j].y : sb[j].x;
+        } else {
 #pragma unroll
           for (int j = 0; j < 2; ++j) bs[j] = b[j].x + b[j].y;
         }
@@ -301,29 +312,36 @@ __global__ void __launch_bounds__(k3Threads, 1) zrk3m_kernel(const __grid_consta
 }
 
 // ------------------------------------------------------------------ launcher
-template <bool CONJ, bool PLANES>
+template <bool CONJ, int PMODE>
 static cudaError_t launch3(const ZrkParams& p, int ntiles, int nwork, int n_sm, cudaStream_t st) {
   static PerDeviceOnce attr;  // the attribute is per device
-  auto kern = zrk3m_kernel<CONJ, PLANES>;
+  auto kern = zrk3m_kernel<CONJ, PMODE>;
   cudaError_t e = per_device_once(
-      attr, [&] { return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg3<PLANES>::smem); });
+      attr, [&] { return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg3<PMODE>::smem); });
   if (e != cudaSuccess) return e;
   const int grid = std::min(nwork, n_sm);
-  kern<<<dim3(grid), dim3(k3Threads), Cfg3<PLANES>::smem, st>>>(p, ntiles, nwork);
+  kern<<<dim3(grid), dim3(k3Threads), Cfg3<PMODE>::smem, st>>>(p, ntiles, nwork);
   return cudaGetLastError();
 }
 
-cudaError_t launch_zrk3m(const ZrkParams& p, bool conj, bool planes, int ntiles, int nbatch, cudaStream_t st) {
+cudaError_t launch_zrk3m(const ZrkParams& p, bool conj, int pmode, int ntiles, int nbatch, cudaStream_t st) {
   int dev = 0, n_sm = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return e;
   const int64_t nwork = static_cast<int64_t>(ntiles) * nbatch;
   if (nwork > 0x7fffffff) return cudaErrorInvalidConfiguration;
-  if (planes && nbatch != 1) return cudaErrorInvalidValue;
+  if (pmode == 2 && nbatch != 1) return cudaErrorInvalidValue;
   const int nw = static_cast<int>(nwork);
-  if (conj) return planes ? launch3<true, true>(p, ntiles, nw, n_sm, st) : launch3<true, false>(p, ntiles, nw, n_sm, st);
-  return planes ? launch3<false, true>(p, ntiles, nw, n_sm, st) : launch3<false, false>(p, ntiles, nw, n_sm, st);
+  switch (pmode * 2 + (conj ? 1 : 0)) {
+    case 0: return launch3<false, 0>(p, ntiles, nw, n_sm, st);
+    case 1: return launch3<true, 0>(p, ntiles, nw, n_sm, st);
+    case 2: return launch3<false, 1>(p, ntiles, nw, n_sm, st);
+    case 3: return launch3<true, 1>(p, ntiles, nw, n_sm, st);
+    case 4: return launch3<false, 2>(p, ntiles, nw, n_sm, st);
+    case 5: return launch3<true, 2>(p, ntiles, nw, n_sm, st);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace hsb
