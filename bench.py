@@ -358,9 +358,9 @@ def run_c5(args, world, rank, dev, dev_index):
         hsb_lib.trim_all(dev_index)
         depth = int(os.environ.get("HSB_PHYS_DEPTH", "3"))
         mk, mg = [kpts[i] for i in mine], [gsets[i] for i in mine]
-        for o in physics.iter_hs_physical_kpoints(system, mk[: depth + 1], mg[: depth + 1], t_aa, t_ab, t_bb,
-                                                  policy, depth=depth):
-            del o  # warm contexts and the pinned cache
+        for _ in range(max(1, min(args.warmup, 2))):  # warm contexts, lanes and the pinned cache (whole steps)
+            for o in physics.iter_hs_physical_kpoints(system, mk, mg, t_aa, t_ab, t_bb, policy, depth=depth):
+                del o
         hsdist.barrier(dev)
         t0 = time.perf_counter()
         d2h = 0
