@@ -23,16 +23,15 @@ __constant__ int32_t oz_mod_rt[kOzMaxMod] = {241, 233, 229, 221, 205, 197, 193, 
 // ------------------------------------------------------------ small helpers
 __device__ __forceinline__ int sym_lo(int p) { return -(p >> 1); }
 
-// symmetric residue of an int32 v modulo an odd p < 256 in FP32:
-// t = (v >> 16) (2^16 mod p) + (v & 0xffff) = v (mod p), |t| < 2^22; the
-// quotient rn(t fl(1/p)) through the 1.5 * 2^23 magic constant is exact (its
-// error, below 1/(4p), is under the 1/(2p) distance of t/p from a half-integer)
-__device__ __forceinline__ int sym_mod_i32(int v, float pf, float invf, int c16) {
-  constexpr float M = 12582912.0f;
+// symmetric residue of an int32 v (the GEMM accumulator) modulo an odd p < 256:
+// t = (v >> 16) (2^16 mod p) + (v & 0xffff) = v (mod p), |t| < 2^22, then
+// q = floor((t m + 2^31) / 2^32) = rn(t / p) with m = rn(2^32 / p): the error
+// |t| 2^-33 <= 2^-11 stays below the 1/(2p) >= 2^-9 distance of t / p from a
+// half-integer.  IMAD.WIDE + IMAD instead of five FP32 operations.
+__device__ __forceinline__ int sym_mod_i32q(int v, int p, int c16, long long m) {
   const int t = (v >> 16) * c16 + (v & 0xffff);
-  const float tf = __int_as_float(0x4B400000 + t) - M;
-  const float q = __fadd_rn(__fmaf_rn(tf, invf, M), -M);
-  return __float_as_int(__fadd_rn(__fmaf_rn(-pf, q, tf), M)) - 0x4B400000;
+  const int q = static_cast<int>((static_cast<long long>(t) * m + (1ll << 31)) >> 32);
+  return t - p * q;
 }
 __device__ __forceinline__ int sym_adj(int r, int p) {
   const int lo = sym_lo(p);
@@ -197,11 +196,12 @@ constexpr int kOzHalf = 128;                      // rows of A and of B per CTA
 constexpr int kOzABytes = kOzHalf * kOzBK;        // 16 KB
 constexpr int kOzStageBytes = 2 * kOzABytes;      // 32 KB
 constexpr int kOzSmem = kOzStages * kOzStageBytes + 1024 + 256;
-// warp 0 TMA, warp 1 MMA (leader) + TMEM owner, warps 2-9 epilogue: two warps per
-// TMEM lane quarter, each reducing half of the accumulator's columns, so short
-// reductions (few k chunks per tile: small configs, atom shards) are not
-// epilogue-bound
-constexpr int kOzEpiWarps = 8;
+// warp 0 TMA, warp 1 MMA (leader) + TMEM owner, warps 2-17 epilogue: four warps
+// per TMEM lane quarter, each reducing a quarter of the accumulator's columns,
+// so short reductions (few k chunks per tile: small configs, atom shards) are
+// not epilogue-bound
+constexpr int kOzEpiWarps = 16;
+constexpr int kOzEpiParts = kOzEpiWarps / 4;  // column parts per lane quarter
 constexpr int kOzThreads = (2 + kOzEpiWarps) * 32;
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;       // shared::cluster address of the leader's copy
 
@@ -474,7 +474,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
     // ------------------------------------------------------------ epilogue (both CTAs)
     // warp w owns TMEM lanes 32*(w%4) .. +31 = rows of this CTA's half; residue mod p, int8
     const int q = warp & 3;                        // TMEM lane quarter (warp id mod 4)
-    const int half = (warp - 2) / 4;               // columns [128 half, 128 half + 128)
+    const int part = (warp - 2) / 4;               // columns [part, part + 1) * kOzBN / kOzEpiParts
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int seq = 0;; ++seq) {
@@ -483,7 +483,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
       int prod, slab, mod, t, tm, tn;
       oz_work(p, w, prod, slab, mod, t, tm, tn);
       const int ip = oz_mod_rt[mod];
-      const float pf = static_cast<float>(ip), invf = 1.0f / pf;
+      const long long qm = ((1ll << 32) + ip / 2) / ip;  // rn(2^32 / p)
       const int c16 = ((65536 % ip) > ip / 2) ? (65536 % ip) - ip : (65536 % ip);
       mbar_wait(tfull(acc), acc_phase);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -501,7 +501,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
       }
       const int nrow = min(kOzBN, p.nrows - tm * 256);
       const bool col_ok = tn * 256 + cloc < p.n;
-      for (int c = half * (kOzBN / 64); c < (half + 1) * (kOzBN / 64); ++c) {
+      constexpr int kChunks = kOzBN / 32 / kOzEpiParts;  // 32-column TMEM loads per warp
+      for (int c = part * kChunks; c < (part + 1) * kChunks; ++c) {
         if (c * 32 >= nrow) break;  // warp-uniform
         uint32_t v[32];
         tmem_ld32(tmem + ((q * 32) << 16) + acc * kOzBN + c * 32, v);
@@ -511,7 +512,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
           for (int j = 0; j < 8; ++j) {
             int r4[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) r4[i] = sym_mod_i32(static_cast<int32_t>(v[4 * j + i]), pf, invf, c16);
+            for (int i = 0; i < 4; ++i) r4[i] = sym_mod_i32q(static_cast<int32_t>(v[4 * j + i]), ip, c16, qm);
             w[j] = __byte_perm(__byte_perm(r4[0], r4[1], 0x40), __byte_perm(r4[2], r4[3], 0x40), 0x5410);
           }
           uint4* o = reinterpret_cast<uint4*>(out + c * 32);

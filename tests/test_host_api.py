@@ -293,3 +293,24 @@ def test_int8_residue_dp4a_arithmetic():
             assert abs(big_x) + abs(big_y) < 2 ** 19
             assert reduce(big_x + big_y, p) == _sym(int(x) + j * int(y), p)
             assert reduce(big_x - big_y, p) == _sym(int(x) - j * int(y), p)
+
+
+def test_int8_gemm_epilogue_reduction_exact():
+    # csrc/ozaki.cu sym_mod_i32q: the GEMM epilogue's reduction of an int32
+    # accumulator v to its symmetric residue: t = (v >> 16) c16 + (v & 0xffff),
+    # q = floor((t m + 2^31) / 2^32), m = rn(2^32 / p); r = t - p q
+    import random
+
+    from paper_1611_00606_b200.engine import MODULI
+
+    rng = random.Random(11)
+    vs = [0, 1, -1, 2 ** 31 - 1, -2 ** 31, 65535, -65536] + [rng.randint(-2 ** 31, 2 ** 31 - 1) for _ in range(4000)]
+    for p in MODULI:
+        c16 = 65536 % p
+        c16 = c16 - p if c16 > p // 2 else c16
+        m = ((1 << 32) + p // 2) // p
+        for v in vs:
+            t = (v >> 16) * c16 + (v & 0xFFFF)
+            assert abs(t) < 2 ** 22
+            q = (t * m + (1 << 31)) >> 32
+            assert t - p * q == _sym(v, p)
