@@ -439,7 +439,8 @@ def main():
     ap.add_argument("--complex-mult", default="3m", choices=["3m", "4m"],
                     help="real-product form of the complex contractions (3 or 4 DMMA products)")
     ap.add_argument("--engine", default="auto", choices=["auto", "int8", "dmma"],
-                    help="S/H contractions on the INT8 tensor cores (CRT emulation, ~1e-12) or FP64 DMMA")
+                    help="S/H contractions: auto = the INT8 tensor cores at FP64 width (CRT emulation, >= 53-bit "
+                         "operands, the default), int8 (same), or FP64 DMMA")
     ap.add_argument("--no-compare", action="store_true", help="skip the second-engine measurement")
     ap.add_argument("--rs", default="nccl", choices=["nccl", "fused", "tri"],
                     help="N > 1: NCCL reduce-scatter (S overlapped with H) or the fused scatter from the "

@@ -57,7 +57,7 @@ class GpuPolicy:
     is "int8" here and "dmma" for the kernel-level ``run_partitioned``, whose
     general operands get elementwise FP64 rounding.  ``int8_bits`` in
     [30, 55] (0 = 53); fewer bits need fewer moduli (~2^-bits of each
-    column's max, e.g. 39 -> ~2e-12, 13 instead of 17 moduli).
+    column's max; e.g. 39 bits -> ~2e-12 with 13 instead of 17 moduli).
 
     ``lower_d2h`` (pinned outputs, INT8 engine): H and S cross PCIe as lower
     triangles and host threads fill the upper triangles (conjugate mirror)

@@ -13,7 +13,7 @@ from paper_1611_00606_b200 import (DimensionError, GpuPolicy, InputError, Kernel
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-12
-TOL_INT8 = 1e-10  # north star bound; the INT8 engine's operand rounding gives ~1e-12
+TOL_INT8 = 1e-13  # the INT8 engine at FP64 width (>= 53-bit operands); the north star asks for 1e-10
 
 
 def _tol(pol):
