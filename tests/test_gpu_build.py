@@ -298,3 +298,63 @@ def test_kpoint_pipeline_failure_mid_batch_does_not_hang():
     # the lanes were released: a new batch runs normally
     ps[2].a_blocks[1][3, 5] = 0.0
     assert len(list(iter_hs_kpoints(ps, _pol("int8"), depth=3))) == 6
+
+
+def test_concurrent_calls_on_one_context_keep_their_engines():
+    # two threads share process-wide context slot 0 with different engines:
+    # every call must run on its own engine (settings + call are atomic per
+    # context: _lib.using / CtxCall), so each result equals, bit for bit, the
+    # serial result of its engine (_lib.py context races)
+    import threading
+
+    p = generate(ProblemSpec(Dims(3, 16, 120), seed=31, nonhpd_fraction=0.3))
+    pols = {"int8": GpuPolicy(engine="int8"), "dmma": GpuPolicy(engine="dmma")}
+    want = {k: build_hs(p, pol) for k, pol in pols.items()}
+    assert not np.array_equal(want["int8"].h.matrix, want["dmma"].h.matrix)  # the engines are distinguishable
+    errors = []
+
+    def worker(k):
+        try:
+            for _ in range(12):
+                out = build_hs(p, pols[k])
+                if not (np.array_equal(out.h.matrix, want[k].h.matrix)
+                        and np.array_equal(out.s.matrix, want[k].s.matrix)):
+                    errors.append(k)
+        except Exception as exc:  # noqa: BLE001
+            errors.append(repr(exc))
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in ("int8", "dmma", "int8", "dmma")]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+
+
+@pytest.mark.parametrize("engine", ["auto", "dmma"])
+def test_lower_only_outputs_leave_the_upper_triangle_untouched(engine):
+    # HSB_OPT_LOWER_ONLY (the triangle-packed exchange's partials): the lower
+    # triangle equals the FULL build's, the diagonal is real, and not one byte
+    # of the strict upper triangle is written
+    import torch
+
+    from paper_1611_00606_b200 import DeviceProblem, build_hs_device
+
+    p = generate(ProblemSpec(Dims(4, 20, 300), seed=32, nonhpd_fraction=0.25))
+    dp = DeviceProblem.from_instance(p)
+    pol = GpuPolicy(engine=engine)
+    hf, sf, _, _, _ = build_hs_device(dp, policy=pol)
+    n = p.dims.n_g
+    sentinel = complex(123.0, -7.0)
+    h = torch.full((n, n), sentinel, dtype=torch.complex128, device=dp.a_stack.device)
+    s = torch.full_like(h, sentinel)
+    build_hs_device(dp, h, s, pol, lower_only=True)
+    torch.cuda.synchronize()
+    for got, full in ((h, hf), (s, sf)):
+        g = got.cpu().numpy().T  # column-major matrix
+        f = full.cpu().numpy().T
+        low = np.tril_indices(n)
+        up = np.triu_indices(n, 1)
+        assert np.array_equal(g[low], f[low])
+        assert np.all(g[up] == sentinel)
+        assert np.all(np.diagonal(g).imag == 0)
