@@ -275,7 +275,7 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
         *out = q;
         return HSB_OK;
       }
-    Src q{v.base, v.k, v.ld, nullptr, (v.k + 15) / 16 * 16, side, v.rscale};
+    Src q{v.base, v.k, v.ld, nullptr, oz_kpad(v.k), side, v.rscale};
     for (const ZrkCall::OzPre& pz : z.oz_pre)
       if (pz.base == v.base && pz.side == side && pz.rscale == v.rscale) q.planes = pz.planes;
     if (!q.planes) {
@@ -583,7 +583,7 @@ hsb_status run_ozaki_hv(hsb_ctx* ctx, cudaStream_t st, const HvCall& c, ZrkCall 
   CKS(oz_choose(ctx, 2 * K, &n_mod, &b));
   // left blocks: 256 k rows per atom (the atom's nl rows shifted by (nl a) mod 16,
   // matching the 16-byte aligned start of the right operand's TMA box)
-  const int64_t kpad = (K + 15) / 16 * 16, kpad_t = 256;
+  const int64_t kpad = oz_kpad(K), kpad_t = 256;
   const int64_t tcols = na * 256;
   void *el_b, *er_b, *et_b, *la, *lb, *t1, *t2, *rt1, *rt2;
   CKS(ws(ctx, "oz_exp_l", ng * sizeof(int32_t), &el_b));

@@ -864,7 +864,7 @@ static hsb_status build_hs_core(hsb_ctx* ctx, void* stream, const hsb_problem* p
     if (!oz_share || oz_el) return HSB_OK;
     int n_mod = 0, bits = 0;
     CKS(oz_choose(ctx, 2 * K, &n_mod, &bits));
-    const int64_t kpad = (K + 15) / 16 * 16;
+    const int64_t kpad = hsb::oz_kpad(K);
     const size_t pbytes = static_cast<size_t>(hsb::kOzPlanes) * n_mod * ng * kpad;
     const hsb_ctx::OzPrepared& pre = ctx->oz_prepared;
     if (h_via_ub && pre.a == A && pre.k == K && pre.ng == ng && pre.n_mod == n_mod && pre.bits == bits) {
@@ -1351,7 +1351,7 @@ hsb_status hsb_build_hs_physical(hsb_ctx* ctx, void* stream, const hsb_phys* ph,
   if (ctx->engine == HSB_ENGINE_INT8 && !(opts & HSB_OPT_UNFUSED) && !no_res) {
     int n_mod = 0, bits = 0;
     CKS(oz_choose(ctx, 2 * K, &n_mod, &bits));
-    const int64_t kpad = (K + 15) / 16 * 16;
+    const int64_t kpad = hsb::oz_kpad(K);
     const size_t pbytes = static_cast<size_t>(hsb::kOzPlanes) * n_mod * ng * kpad;
     void *eb, *rb, *ubb;
     CKS(ws(ctx, "oz_exp_l", static_cast<size_t>(ng) * 4, &eb));

@@ -5,6 +5,7 @@
 #include <cudaTypedefs.h>
 
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -963,6 +964,15 @@ cudaError_t launch_ozaki_colexp_ab(const double* a, const double* b, int64_t ld,
       reinterpret_cast<const double2*>(a), reinterpret_cast<const double2*>(b), ld, k, cols, u, exp_out,
       with_b ? 1 : 0);
   return cudaGetLastError();
+}
+
+int64_t oz_kpad(int64_t k) {
+  static const int64_t align = [] {
+    const char* e = std::getenv("HSB_OZ_KPAD");
+    const int64_t v = e ? std::atoll(e) : 128;
+    return v >= 16 && v % 16 == 0 ? v : int64_t{128};
+  }();
+  return (k + align - 1) / align * align;
 }
 
 // the driver's cuTensorMapEncodeTiled (through the runtime: no -lcuda)

@@ -70,6 +70,11 @@ __host__ __device__ constexpr int oz_sqrtm1(int i) {
   }
 }
 
+// k extent of a residue plane row (bytes): the reduction length rounded up to
+// kOzKpadAlign so every 128-byte TMA row segment of a GEMM operand box is one
+// L2 line (HSB_OZ_KPAD for experiments; TMA needs a multiple of 16)
+int64_t oz_kpad(int64_t k);
+
 // planes of a residue buffer: [plane][modulus][col][kpad] int8
 enum OzPlane { kOzPhi1 = 0, kOzPhi2 = 1 };
 constexpr int kOzPlanes = 2;
