@@ -726,12 +726,12 @@ static hsb_status build_hs_core(hsb_ctx* ctx, void* stream, const hsb_problem* p
   CK(order_wait(out->compute_after, 2, st));
 
   // ------------------------------------------- Loop 2, part 1: Cholesky routing
-  CK(launch_potrf_route(TAA, static_cast<double*>(q), static_cast<int32_t*>(info_d), static_cast<int>(na),
-                        static_cast<int>(nl), force_nonhpd, static_cast<double*>(potrf_scr), st));
-  ++launches;
-  CK(launch_route_atoms(static_cast<int32_t*>(info_d), static_cast<int>(na), static_cast<int>(nl),
-                        static_cast<int32_t*>(offs_d), hostbuf_dev, st));
-  ++launches;
+  // On the fused INT8 path with the side preparation (the default) nothing on
+  // the device waits for the routing -- H = A^H V1 + (UB)^H W2 covers HPD and
+  // non-HPD atoms alike; only the split counts need it -- so the 32-CTA,
+  // latency-bound potrf runs on the copy stream after S's operand preparation,
+  // beside the S contraction, instead of ahead of everything on the compute
+  // stream; the host collects the counts after enqueueing H.
   cudaEvent_t ev_info;
   CK(cudaEventCreateWithFlags(&ev_info, cudaEventDisableTiming));
   struct EvDel {
@@ -740,8 +740,22 @@ static hsb_status build_hs_core(hsb_ctx* ctx, void* stream, const hsb_problem* p
       if (e) cudaEventDestroy(e);
     }
   } ev_info_del{ev_info};
-  CK(cudaEventRecord(ev_info, st));
+  auto routing = [&](cudaStream_t s_) -> hsb_status {
+    CK(launch_potrf_route(TAA, static_cast<double*>(q), static_cast<int32_t*>(info_d), static_cast<int>(na),
+                          static_cast<int>(nl), force_nonhpd, static_cast<double*>(potrf_scr), s_));
+    ++launches;
+    CK(launch_route_atoms(static_cast<int32_t*>(info_d), static_cast<int>(na), static_cast<int>(nl),
+                          static_cast<int32_t*>(offs_d), hostbuf_dev, s_));
+    ++launches;
+    CK(cudaEventRecord(ev_info, s_));
+    return HSB_OK;
+  };
+  static const bool no_defer_routing = std::getenv("HSB_NO_DEFER_ROUTING") != nullptr;  // A/B experiments
+  const bool defer_routing = !unfused && !overlap_upload && ctx->engine == HSB_ENGINE_INT8 && !no_defer_routing &&
+                             !(std::getenv("HSB_INT8_V") != nullptr) && !(std::getenv("HSB_NO_SIDE_PREP") != nullptr);
+  if (!defer_routing) CKS(routing(st));
   CK(tl.mark(st, "loop2"));
+  bool side_prep_used = false;  // set by the fused branch below
 
   auto loop1 = [&]() -> hsb_status {  // Z_a = T_AB^H A_a + (1/2 T_BB)^H B_a (builder.py:73-88)
     CK(launch_half_mirror(TBB, static_cast<double*>(pbb), static_cast<int>(nl), na, 0.5, st));
@@ -962,6 +976,7 @@ static hsb_status build_hs_core(hsb_ctx* ctx, void* stream, const hsb_problem* p
     // DMMA V products (they leave registers and shared memory for it on every SM)
     static const bool no_side = std::getenv("HSB_NO_SIDE_PREP") != nullptr;  // A/B experiments
     const bool side_prep = oz_share && u_fused && !int8_v && !no_side;
+    side_prep_used = side_prep;
     cudaEvent_t ev_prep_in = nullptr, ev_prep_out = nullptr;
     if (side_prep) {
       CK(cudaEventCreateWithFlags(&ev_prep_in, cudaEventDisableTiming));
@@ -976,6 +991,7 @@ static hsb_status build_hs_core(hsb_ctx* ctx, void* stream, const hsb_problem* p
     if (side_prep) {
       CKS(oz_left(cs, true));
       CK(cudaEventRecord(ev_prep_out, cs));
+      if (defer_routing) CKS(routing(cs));  // after the event: S does not wait for it
       CK(cudaStreamWaitEvent(st, ev_prep_out, 0));
     }
     CKS(unorm());
@@ -999,12 +1015,18 @@ static hsb_status build_hs_core(hsb_ctx* ctx, void* stream, const hsb_problem* p
 
   // ------------------------------------------- routing (host, overlaps S)
   hc.mark("enqueue to S");
-  CK(cudaEventSynchronize(ev_info));
-  hc.mark("routing wait");
+  if (defer_routing && !side_prep_used) CKS(routing(st));  // (no side preparation ran: on the compute stream)
   int64_t n_hpd = 0, n_nh = 0;
-  std::atomic_thread_fence(std::memory_order_acquire);
-  for (int64_t i = 0; i < na; ++i) (info_h[i] == 0 ? n_hpd : n_nh)++;
-  if (atom_info) std::memcpy(atom_info, info_h, na * 4);
+  auto await_routing = [&]() -> hsb_status {
+    CK(cudaEventSynchronize(ev_info));
+    hc.mark("routing wait");
+    n_hpd = n_nh = 0;
+    std::atomic_thread_fence(std::memory_order_acquire);
+    for (int64_t i = 0; i < na; ++i) (info_h[i] == 0 ? n_hpd : n_nh)++;
+    if (atom_info) std::memcpy(atom_info, info_h, na * 4);
+    return HSB_OK;
+  };
+  if (!defer_routing) CKS(await_routing());
   const int32_t* offs_dev = static_cast<int32_t*>(offs_d);
 
   // ------------------------------------------- Loop 2, part 2 (builder.py:162-185)
@@ -1117,6 +1139,7 @@ static hsb_status build_hs_core(hsb_ctx* ctx, void* stream, const hsb_problem* p
     }
     CK(tl.mark(st, "h"));
     tr.mark(st, "h_done");
+    if (defer_routing) CKS(await_routing());
   }
   CK(order_done(out->compute_done, 2, st));
 
@@ -1223,8 +1246,9 @@ static hsb_status build_hs_core(hsb_ctx* ctx, void* stream, const hsb_problem* p
     tm->loop2 = tl.total("loop2");
     tm->unorm = tl.total("unorm");
     const double fS = 4.0 * K * double(ng) * ng;
-    const double fH1 = 8.0 * K * double(ng) * ng, fH2 = 8.0 * k_nh * double(ng) * ng,
-                 fH3 = 4.0 * k_hpd * double(ng) * ng;
+    // (the routing may have been collected after H was enqueued: recount)
+    const double fH1 = 8.0 * K * double(ng) * ng, fH2 = 8.0 * n_nh * nl * double(ng) * ng,
+                 fH3 = 4.0 * n_hpd * nl * double(ng) * ng;
     const double ts = tl.total("s") + tl.total("s_core");  // fused S: split S1/S2 by model flops (equal)
     tm->s1 = tl.total("s1") + tl.total("s1_core") + ts * 0.5;
     tm->s2 = tl.total("s2") + tl.total("s2_core") + ts * 0.5;

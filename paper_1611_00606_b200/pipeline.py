@@ -389,8 +389,9 @@ def _lane_pipeline(count: int, depth: int, pol, n_max: int, run):
     try:
         for i in range(count):
             ready[i].wait()
-            if failure:
+            if results[i] is None:  # released by a lane's failure, not built: stop here
                 raise failure[0]
+            # (a result that completed before another item failed is still yielded, in order)
             r, results[i] = results[i], None
             with window:
                 consumed[0] = i + 1
