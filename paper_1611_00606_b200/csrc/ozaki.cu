@@ -660,8 +660,9 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
 // PLAIN: alpha = 1, beta = 0 (every build call): no scaling, no read of C
+// 4 blocks per SM (64 registers) up to 18 moduli; 19-20 would spill at 64, so keep 3
 template <int NM, bool PLAIN>
-__global__ void __launch_bounds__(256, 3) ozaki_crt_kernel(const OzCrtParams p, int ncols) {
+__global__ void __launch_bounds__(256, NM <= 18 ? 4 : 3) ozaki_crt_kernel(const OzCrtParams p, int ncols) {
   // residues [product][modulus][column][128 rows], then (reused) the mirror stage
   constexpr int kResBytes = 2 * NM * kCrtCols * kCrtRows;
   constexpr int kStageBytes = kCrtCols * (kCrtRows + 1) * 16;
@@ -1077,6 +1078,20 @@ cudaError_t launch_ozaki_crt(const OzCrtParams& p, cudaStream_t st) {
   return launch_ozaki_crt_cols(p, ncols, st);
 }
 
+// 4 blocks of 35 KB per SM need the largest shared-memory carveout (the
+// default the driver picks for this kernel holds 3)
+template <int NM, bool PLAIN>
+static cudaError_t crt_launch(dim3 grid, dim3 block, cudaStream_t st, const OzCrtParams& p, int nc) {
+  static PerDeviceOnce attr;
+  const cudaError_t e = per_device_once(attr, [] {
+    return cudaFuncSetAttribute(ozaki_crt_kernel<NM, PLAIN>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                cudaSharedmemCarveoutMaxShared);
+  });
+  if (e != cudaSuccess) return e;
+  ozaki_crt_kernel<NM, PLAIN><<<grid, block, 0, st>>>(p, nc);
+  return cudaSuccess;
+}
+
 cudaError_t launch_ozaki_crt_cols(const OzCrtParams& p, int64_t ncols, cudaStream_t st) {
   if (ncols <= 0) return cudaSuccess;
   cudaError_t ce = oz_init_once();
@@ -1099,13 +1114,13 @@ cudaError_t launch_ozaki_crt_cols(const OzCrtParams& p, int64_t ncols, cudaStrea
   const dim3 grid(static_cast<unsigned>(most), static_cast<unsigned>((ncb + 1) / 2)), block(256);
   const int nc = static_cast<int>(ncols);
   const bool plain = p.alpha_re == 1.0 && p.alpha_im == 0.0 && p.beta_re == 0.0 && p.beta_im == 0.0;
-#define HSB_OZ_CRT(NMV)                                                \
-  case NMV:                                                          \
-    if (plain)                                                       \
-      ozaki_crt_kernel<NMV, true><<<grid, block, 0, st>>>(p, nc);    \
-    else                                                             \
-      ozaki_crt_kernel<NMV, false><<<grid, block, 0, st>>>(p, nc);   \
-    break;
+#define HSB_OZ_CRT(NMV)                                                   \
+  case NMV: {                                                           \
+    const cudaError_t e = plain ? crt_launch<NMV, true>(grid, block, st, p, nc) \
+                                : crt_launch<NMV, false>(grid, block, st, p, nc); \
+    if (e != cudaSuccess) return e;                                     \
+    break;                                                              \
+  }
   switch (p.n_mod) {
     HSB_OZ_CRT(11)
     HSB_OZ_CRT(12)
