@@ -267,6 +267,7 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
     const double* rscale;
   };
   std::vector<Src> srcs;
+  std::vector<OzResSrc> pending;  // planes still to compute: one batched launch
   int computed = 0;
   auto planes_of = [&](const OperandView& v, int side, Src* out) -> hsb_status {
     if (!pre || el == er) side = 0;  // one exponent array: both sides share residues
@@ -283,7 +284,7 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
       void* buf;
       CKS(ws(ctx, name.c_str(), static_cast<size_t>(kOzPlanes) * n_mod * n * q.kpad, &buf));
       q.planes = static_cast<int8_t*>(buf);
-      CK(launch_ozaki_residues(v.base, v.ld, v.k, n, side ? er : el, b, n_mod, q.planes, q.kpad, st, v.rscale));
+      pending.push_back({v.base, v.ld, v.k, side ? er : el, v.rscale, q.planes, q.kpad});
     }
     srcs.push_back(q);
     *out = q;
@@ -294,10 +295,17 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
   // products phi1(C), phi2(C) (ozaki.cuh): conjugation swaps the left planes
   const int lp[kOzProds] = {z.conj ? kOzPhi2 : kOzPhi1, z.conj ? kOzPhi1 : kOzPhi2};
   const int rp[kOzProds] = {kOzPhi1, kOzPhi2};
+  std::vector<Src> seg_l(segs.size()), seg_r(segs.size());
   for (size_t si = 0; si < segs.size(); ++si) {
-    Src L, R;
-    CKS(planes_of(segs[si].l, 0, &L));
-    CKS(planes_of(segs[si].r, 1, &R));
+    CKS(planes_of(segs[si].l, 0, &seg_l[si]));
+    CKS(planes_of(segs[si].r, 1, &seg_r[si]));
+  }
+  for (size_t i = 0; i < pending.size(); i += kOzResMaxSrc)
+    CK(launch_ozaki_residues_batch(pending.data() + i, static_cast<int>(std::min<size_t>(kOzResMaxSrc, pending.size() - i)),
+                                   n, b, n_mod, st));
+  for (size_t si = 0; si < segs.size(); ++si) {
+    const Src& L = seg_l[si];
+    const Src& R = seg_r[si];
     const int64_t pl = static_cast<int64_t>(n_mod) * n * L.kpad, pr = static_cast<int64_t>(n_mod) * n * R.kpad;
     for (int pi = 0; pi < kOzProds; ++pi) {  // MMA A operand: the right factor (output columns)
       CKS(oz_encode(ctx, &gp.map[pi][si][0], R.planes + rp[pi] * pr, R.k, n, R.kpad, n_mod, 128));
@@ -408,7 +416,7 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
     }
     t0 = t1;
   }
-  if (launches) *launches += 3 + (pre ? 0 : 2 * static_cast<int>(segs.size())) + computed;
+  if (launches) *launches += 3 + (pre ? 0 : 2 * static_cast<int>(segs.size())) + (computed + kOzResMaxSrc - 1) / kOzResMaxSrc;
   return HSB_OK;
 }
 

@@ -898,17 +898,17 @@ static hsb_status build_hs_core(hsb_ctx* ctx, void* stream, const hsb_problem* p
     oz_el = static_cast<int32_t*>(eb);
     oz_res_a = static_cast<int8_t*>(rb);
     CK(hsb::launch_ozaki_colexp_ab(A, B, K, K, ng, U, oz_el, s_, !h_via_ub));
-    CK(hsb::launch_ozaki_residues(A, K, K, ng, oz_el, bits, n_mod, oz_res_a, kpad, s_));
-    launches += 2;
+    hsb::OzResSrc rs[2] = {{A, K, K, oz_el, nullptr, oz_res_a, kpad}, {}};
     if (with_ub) {
       // the buffer H's contraction uses for its third operand (V2) afterwards,
       // in stream order behind S: no extra workspace
       void* ubb;
       CKS(ws(ctx, "oz_res2", pbytes, &ubb));
       oz_res_ub = static_cast<int8_t*>(ubb);
-      CK(hsb::launch_ozaki_residues(B, K, K, ng, oz_el, bits, n_mod, oz_res_ub, kpad, s_, U));
-      ++launches;
+      rs[1] = {B, K, K, oz_el, U, oz_res_ub, kpad};
     }
+    CK(hsb::launch_ozaki_residues_batch(rs, with_ub ? 2 : 1, ng, bits, n_mod, s_));  // A and UB: one launch
+    launches += 2;
     return HSB_OK;
   };
   auto oz_use_left = [&](ZrkCall& z, const int32_t* er) {

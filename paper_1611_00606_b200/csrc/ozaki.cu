@@ -4,6 +4,7 @@
 // reconstruction with the Hermitian mirror.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 #include <cmath>
@@ -139,19 +140,31 @@ __device__ __forceinline__ void oz_residue_planes(const uint32_t (&xl)[4], const
 constexpr int kOzResK = 4;
 constexpr int kOzResCols = 8;
 constexpr int kOzResKBlk = 128;
+// blockIdx.z selects one of up to kOzResMaxSrc operands of one launch (same
+// exponent width b, moduli and column count; each with its own map / kpad)
+struct OzResBatch {
+  CUtensorMap map[kOzResMaxSrc];
+  OzResSrc src[kOzResMaxSrc];
+  int64_t kpad[kOzResMaxSrc];
+  int64_t cols;
+  int b;
+};
 template <int NM>
-__global__ void __launch_bounds__(256, 3) ozaki_residue_kernel(const __grid_constant__ CUtensorMap out_map,
-                                                            const double2* __restrict__ x, int64_t ldx, int64_t k,
-                                                            int64_t cols, const int32_t* __restrict__ col_exp, int b,
-                                                            const double* __restrict__ rscale) {
+__global__ void __launch_bounds__(256, 3) ozaki_residue_kernel(const __grid_constant__ OzResBatch p) {
   __shared__ __align__(128) uint32_t tile[2 * NM * kOzResCols * kOzResKBlk / 4];
+  const OzResSrc& sr = p.src[blockIdx.z];
+  if (static_cast<int64_t>(blockIdx.x) * kOzResKBlk >= p.kpad[blockIdx.z]) return;  // shorter operand of the batch
+  const double2* __restrict__ x = reinterpret_cast<const double2*>(sr.x);
+  const double* __restrict__ rscale = sr.rscale;
+  const int64_t ldx = sr.ldx, k = sr.k, cols = p.cols;
+  const int b = p.b;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t k0 = static_cast<int64_t>(blockIdx.x) * kOzResKBlk + kOzResK * lane;
   const int64_t c = static_cast<int64_t>(blockIdx.y) * kOzResCols + warp;
   uint32_t xl[kOzResK] = {}, xh[kOzResK] = {}, yl[kOzResK] = {}, yh[kOzResK] = {};
   if (c < cols) {
     // x * 2^(b - e) in two exact power-of-two steps (each factor stays finite)
-    const int sh = b - __ldg(col_exp + c);
+    const int sh = b - __ldg(sr.col_exp + c);
     const double s1 = pow2i(sh / 2), s2 = pow2i(sh - sh / 2);
 #pragma unroll
     for (int j = 0; j < kOzResK; ++j) {
@@ -177,7 +190,7 @@ __global__ void __launch_bounds__(256, 3) ozaki_residue_kernel(const __grid_cons
     asm volatile(
         "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];\n\t"
         "cp.async.bulk.commit_group;\n\t"
-        "cp.async.bulk.wait_group.read 0;" ::"l"(reinterpret_cast<uint64_t>(&out_map)),
+        "cp.async.bulk.wait_group.read 0;" ::"l"(reinterpret_cast<uint64_t>(&p.map[blockIdx.z])),
         "r"(static_cast<int>(blockIdx.x) * kOzResKBlk), "r"(static_cast<int>(blockIdx.y) * kOzResCols), "r"(0),
         "r"(0), "r"(smem_u32(tile))
         : "memory");
@@ -989,30 +1002,40 @@ static PFN_cuTensorMapEncodeTiled_v12000 oz_encode_fn() {
   return fn;
 }
 
-cudaError_t launch_ozaki_residues(const double* x, int64_t ldx, int64_t k, int64_t cols, const int32_t* col_exp,
-                                  int b, int n_mod, int8_t* out, int64_t kpad, cudaStream_t st, const double* rscale) {
-  if (cols <= 0 || kpad <= 0) return cudaSuccess;
-  if (kpad % 16 != 0 || (cols + kOzResCols - 1) / kOzResCols > 65535) return cudaErrorInvalidValue;
+cudaError_t launch_ozaki_residues_batch(const OzResSrc* srcs, int nsrc, int64_t cols, int b, int n_mod,
+                                        cudaStream_t st) {
+  if (nsrc <= 0 || cols <= 0) return cudaSuccess;
+  if (nsrc > kOzResMaxSrc || (cols + kOzResCols - 1) / kOzResCols > 65535) return cudaErrorInvalidValue;
   const PFN_cuTensorMapEncodeTiled_v12000 encode = oz_encode_fn();
   if (!encode) return cudaErrorNotSupported;
-  // out[plane][modulus][col][kpad] as a 4-D uint8 tensor; box = one block's tile
-  CUtensorMap map;
-  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(kpad), static_cast<cuuint64_t>(cols),
-                              static_cast<cuuint64_t>(n_mod), 2};
-  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(kpad), static_cast<cuuint64_t>(kpad * cols),
-                                 static_cast<cuuint64_t>(kpad * cols * n_mod)};
-  const cuuint32_t box[4] = {kOzResKBlk, kOzResCols, static_cast<cuuint32_t>(n_mod), 2}, es[4] = {1, 1, 1, 1};
-  if (encode(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, out, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
-      CUDA_SUCCESS)
-    return cudaErrorInvalidValue;
-  const dim3 grid(static_cast<unsigned>((kpad + kOzResKBlk - 1) / kOzResKBlk),
-                  static_cast<unsigned>((cols + kOzResCols - 1) / kOzResCols));
-  const double2* xx = reinterpret_cast<const double2*>(x);
+  OzResBatch p;
+  std::memset(&p, 0, sizeof(p));
+  p.cols = cols;
+  p.b = b;
+  int64_t kmax = 0;
+  for (int i = 0; i < nsrc; ++i) {
+    const int64_t kpad = srcs[i].kpad;
+    if (kpad <= 0 || kpad % 16 != 0) return cudaErrorInvalidValue;
+    // out[plane][modulus][col][kpad] as a 4-D uint8 tensor; box = one block's tile
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(kpad), static_cast<cuuint64_t>(cols),
+                                static_cast<cuuint64_t>(n_mod), 2};
+    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(kpad), static_cast<cuuint64_t>(kpad * cols),
+                                   static_cast<cuuint64_t>(kpad * cols * n_mod)};
+    const cuuint32_t box[4] = {kOzResKBlk, kOzResCols, static_cast<cuuint32_t>(n_mod), 2}, es[4] = {1, 1, 1, 1};
+    if (encode(&p.map[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, srcs[i].out, dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+    p.src[i] = srcs[i];
+    p.kpad[i] = kpad;
+    kmax = std::max(kmax, kpad);
+  }
+  const dim3 grid(static_cast<unsigned>((kmax + kOzResKBlk - 1) / kOzResKBlk),
+                  static_cast<unsigned>((cols + kOzResCols - 1) / kOzResCols), static_cast<unsigned>(nsrc));
   switch (n_mod) {
 #define HSB_OZ_RES(NM) \
   case NM:             \
-    ozaki_residue_kernel<NM><<<grid, 256, 0, st>>>(map, xx, ldx, k, cols, col_exp, b, rscale); \
+    ozaki_residue_kernel<NM><<<grid, 256, 0, st>>>(p); \
     break;
     HSB_OZ_RES(11) HSB_OZ_RES(12) HSB_OZ_RES(13) HSB_OZ_RES(14) HSB_OZ_RES(15) HSB_OZ_RES(16)
     HSB_OZ_RES(17) HSB_OZ_RES(18) HSB_OZ_RES(19) HSB_OZ_RES(20)
@@ -1021,6 +1044,13 @@ cudaError_t launch_ozaki_residues(const double* x, int64_t ldx, int64_t k, int64
       return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_ozaki_residues(const double* x, int64_t ldx, int64_t k, int64_t cols, const int32_t* col_exp,
+                                  int b, int n_mod, int8_t* out, int64_t kpad, cudaStream_t st, const double* rscale) {
+  if (cols <= 0 || kpad <= 0) return cudaSuccess;
+  const OzResSrc src{x, ldx, k, col_exp, rscale, out, kpad};
+  return launch_ozaki_residues_batch(&src, 1, cols, b, n_mod, st);
 }
 
 cudaError_t launch_ozaki_gemm(const OzGemmParams& p, cudaStream_t st) {

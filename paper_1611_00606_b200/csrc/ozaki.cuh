@@ -175,6 +175,20 @@ cudaError_t launch_ozaki_init_exp(int32_t* e, int64_t n, cudaStream_t st);
 // e[c] = exponent of the column max over a, diag(u) b and (with_b) b (written, not max-ed)
 cudaError_t launch_ozaki_colexp_ab(const double* a, const double* b, int64_t ld, int64_t k, int64_t cols,
                                    const double* u, int32_t* exp_out, cudaStream_t st, bool with_b);
+// one residue-plane source: x (ldx, k rows of complex) scaled per column by
+// 2^(b - col_exp), optionally by rscale per row, into out[plane][mod][col][kpad]
+constexpr int kOzResMaxSrc = 4;
+struct OzResSrc {
+  const double* x;
+  int64_t ldx, k;
+  const int32_t* col_exp;
+  const double* rscale;
+  int8_t* out;
+  int64_t kpad;
+};
+// up to kOzResMaxSrc sources of the same column count in one launch
+cudaError_t launch_ozaki_residues_batch(const OzResSrc* srcs, int nsrc, int64_t cols, int b, int n_mod,
+                                        cudaStream_t st);
 cudaError_t launch_ozaki_residues(const double* x, int64_t ldx, int64_t k, int64_t cols, const int32_t* col_exp,
                                   int b, int n_mod, int8_t* out, int64_t kpad, cudaStream_t st, const double* rscale = nullptr);
 cudaError_t launch_ozaki_gemm(const OzGemmParams& p, cudaStream_t st);
