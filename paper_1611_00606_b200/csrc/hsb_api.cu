@@ -318,11 +318,31 @@ ZrkCall tri_call(double* c, int64_t ldc, int64_t n, uint32_t flags, double beta)
 // never written by a later download (it starts at its own c0 >= c1), so the
 // host threads and the DMA engine touch disjoint bytes.  Halves the D2H bytes
 // (the e2e bound of the pinned-host path) for ~1 GB/s-per-core host work.
+// Split of the upper triangles between PCIe and the host mirror: column c
+// (in its 64-column download block) crosses PCIe from row d2h_row0(c) on, and
+// the host threads fill rows < d2h_row0(c).  frac = 0: lower triangles only.
+// Host DRAM carries the DMA writes plus the mirror's reads and writes, PCIe
+// the DMA: moving part of the upper triangles to the DMA engine balances the
+// two (the pinned-host e2e path is bound by their sum).
+constexpr double kD2hUpperHostIn = 0.0, kD2hUpperDevIn = 0.2;  // measured: profiles/d2h_split_r02.txt
+static int64_t d2h_row0(int64_t c, double frac) {
+  const int64_t a = c & ~int64_t{63};
+  return static_cast<int64_t>((1.0 - frac) * static_cast<double>(a)) & ~int64_t{7};
+}
+static double d2h_upper_frac(bool host_in) {
+  const char* e = std::getenv("HSB_D2H_UPPER");  // experiments / tests: a fraction in [0, 1]
+  if (e && *e) return std::min(std::max(std::atof(e), 0.0), 1.0);
+  // host inputs also read host DRAM (the A / B uploads): more of the upper
+  // triangles over PCIe
+  return host_in ? kD2hUpperHostIn : kD2hUpperDevIn;
+}
+
 struct HostMirror {
   struct Job {
     cudaEvent_t ev;
     double* m;
     int64_t ld, n, c0, c1;
+    double frac;
   };
   // a worker thread waits for each range's event and mirrors it, so the
   // caller keeps issuing downloads meanwhile
@@ -345,7 +365,7 @@ struct HostMirror {
     return n;
   }
   ~HostMirror() { finish(); }
-  cudaError_t push(cudaStream_t cs, double* m, int64_t ld, int64_t n, int64_t c0, int64_t c1) {
+  cudaError_t push(cudaStream_t cs, double* m, int64_t ld, int64_t n, int64_t c0, int64_t c1, double frac) {
     if (c1 >= n) return cudaSuccess;  // nothing above the diagonal blocks
     cudaEvent_t e;
     cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
@@ -360,7 +380,7 @@ struct HostMirror {
       worker = std::thread([this] { loop(); });
     }
     std::lock_guard<std::mutex> lk(mu);
-    q.push_back({e, m, ld, n, c0, c1});
+    q.push_back({e, m, ld, n, c0, c1, frac});
     cv.notify_one();
     return cudaSuccess;
   }
@@ -397,7 +417,7 @@ struct HostMirror {
       // (r, c) upper  <-  conj (c, r) lower; destination runs are contiguous
       // in r and written with non-temporal stores (no read-for-ownership)
       for (int64_t c = j0; c < j1; ++c)
-        for (int64_t r = i0; r < i1; ++r) {
+        for (int64_t r = i0, r1 = std::min(i1, d2h_row0(c, j.frac)); r < r1; ++r) {  // rows >= r1: DMA'd
 #if defined(__SSE2__)
           const __m128d sign = _mm_set_pd(-0.0, 0.0);
           _mm_stream_pd(m + 2 * (r + c * ld), _mm_xor_pd(_mm_load_pd(m + 2 * (c + r * ld)), sign));
@@ -1149,23 +1169,25 @@ static hsb_status build_hs_core(hsb_ctx* ctx, void* stream, const hsb_problem* p
     // with the H contraction; H follows on the compute stream.
     const size_t row = static_cast<size_t>(ng) * 16;
     // columns [c0, c1) of a final matrix to the host, on the copy stream.
-    // lower_d2h: one copy per 256-column block [a, b) of rows >= a, and a host
-    // mirror job for rows [a, b) of the columns >= b once it has landed
+    // lower_d2h: one copy per 64-column block [a, b) of rows >= d2h_row0(a), and a
+    // host mirror job for rows [a, b) of the columns >= b (below their d2h_row0)
+    // once it has landed
     // HSB_LOWER_D2H (experiments): which matrices cross as lower triangles ("hs", "s", "h", "-")
     static const std::string lower_which = [] {
       const char* e = std::getenv("HSB_LOWER_D2H");
       return std::string(e ? e : "hs");
     }();
+    const double upper_frac = d2h_upper_frac(host_in);
     auto download = [&](double* dst, const double* src, int64_t c0, int64_t c1) -> hsb_status {
       const bool lower = lower_d2h && lower_which.find(dst == out->h ? 'h' : 's') != std::string::npos;
-      const int64_t step = lower ? 256 : c1 - c0;
+      const int64_t step = lower ? 64 : c1 - c0;  // (c0 is a multiple of 64: d2h_row0's blocks)
       for (int64_t a = c0; a < c1; a += step) {
-        const int64_t b = std::min(c1, a + step), r0 = lower ? a : 0;
+        const int64_t b = std::min(c1, a + step), r0 = lower ? d2h_row0(a, upper_frac) : 0;
         CK(cudaMemcpy2DAsync(reinterpret_cast<char*>(dst) + (a * out->ld + r0) * 16, out->ld * 16,
                              reinterpret_cast<const char*>(src) + (a * ldo + r0) * 16, ldo * 16, (ng - r0) * 16,
                              b - a, cudaMemcpyDeviceToHost, cs));
         d2h_bytes += 16.0 * (ng - r0) * (b - a);
-        if (lower) CK(mirror.push(cs, dst, out->ld, ng, a, b));
+        if (lower) CK(mirror.push(cs, dst, out->ld, ng, a, b, upper_frac));
       }
       return HSB_OK;
     };

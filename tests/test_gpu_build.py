@@ -200,10 +200,14 @@ def test_nonfinite_stack_values_raise_invariant_error(field):
     assert rel_frob_error(out.s.matrix, brute.s_brute(q)) < TOL
 
 
+@pytest.mark.parametrize("upper", ["", "0", "0.5", "1"])
 @pytest.mark.parametrize("dims", [Dims(3, 17, 700), Dims(6, 25, 1283)])
-def test_lower_triangle_download_matches_full_download(dims):
-    # default pinned INT8 path: H / S cross PCIe as lower triangles and the
-    # host fills the upper triangles; bitwise the same as full downloads
+def test_lower_triangle_download_matches_full_download(dims, upper, monkeypatch):
+    # default pinned INT8 path: H / S cross PCIe as lower triangles plus a
+    # fraction of the upper ones (HSB_D2H_UPPER; "" = the default split) and
+    # host threads fill the rest of the upper triangles; bitwise the same as
+    # full downloads
+    monkeypatch.setenv("HSB_D2H_UPPER", upper)
     p = generate(ProblemSpec(dims, seed=31, nonhpd_fraction=0.3))
     a = build_hs(p, GpuPolicy(lower_d2h=True))
     b = build_hs(p, GpuPolicy(lower_d2h=False))
