@@ -176,9 +176,10 @@ def shard(n_atoms: int, rank: int, world: int):
 
 
 def cpu_baseline_run(dims_full, sample_ng: int, seed: int, steps: int = 1, nonhpd_fraction: float = 0.0,
-                     instance=None):
+                     instance=None, budget_s: float = float("inf")):
     """Time the oracle (scipy/OpenBLAS Algorithm 1) on the config's instance
-    (``sample_ng`` 0 = the full N_G; a smaller value cuts N_G).  Returns
+    (``sample_ng`` 0 = the full N_G; a smaller value cuts N_G), ``steps`` times
+    or until ``budget_s`` seconds have been spent (at least one step).  Returns
     (times, flops, threads, sample, output of the last step)."""
     from oracle import alg1
     from paper_1611_00606_b200 import Dims, ProblemSpec, generate, total_model_flops
@@ -192,6 +193,8 @@ def cpu_baseline_run(dims_full, sample_ng: int, seed: int, steps: int = 1, nonhp
         t0 = time.perf_counter()
         out = alg1.build_hs_cpu(p)
         times.append(time.perf_counter() - t0)
+        if sum(times) >= budget_s:
+            break
     flops = total_model_flops(d, out["nonhpd"])
     try:
         from threadpoolctl import threadpool_info
@@ -204,6 +207,9 @@ def cpu_baseline_run(dims_full, sample_ng: int, seed: int, steps: int = 1, nonhp
     return times, flops, threads, sample, out
 
 
+REFERENCE_BUDGET_S = 150.0
+
+
 def run_reference(args, rank, world):
     """--impl reference: the oracle port of the reference CPU path on this host,
     on the same config as our arm (C5: the 16 k-points' instance shape, one
@@ -214,17 +220,22 @@ def run_reference(args, rank, world):
 
     cfg = "C3" if args.config == "C5" else args.config
     dims = CONFIGS[cfg]
+    # the host needs no warm-up beyond the first build (page faults, thread
+    # pools): at most one untimed step, and the timed steps stop after
+    # REFERENCE_BUDGET_S so that any --steps finishes within a few minutes
+    warm = min(args.warmup, 1)
     times, flops, threads, sample, _ = cpu_baseline_run(dims, args.cpu_sample_ng, args.seed,
-                                                        steps=args.warmup + args.steps,
-                                                        nonhpd_fraction=args.nonhpd_fraction)
-    timed = times[args.warmup:] if len(times) > args.warmup else times
+                                                        steps=warm + args.steps,
+                                                        nonhpd_fraction=args.nonhpd_fraction,
+                                                        budget_s=REFERENCE_BUDGET_S)
+    timed = times[warm:] if len(times) > warm else times
     t = sum(timed) / len(timed)
     value = flops / t / 1e12
     ms = t * 1e3 * (C5_KPOINTS if args.config == "C5" else 1)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
+        "steps": args.steps, "warmup": args.warmup, "steps_timed": len(timed), "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
         "config": {"workload": args.config, "desc": CONFIG_DESC[args.config],
                    "sample_ng": dims.n_g if args.cpu_sample_ng <= 0 else min(args.cpu_sample_ng, dims.n_g),
                    "same_config": args.cpu_sample_ng <= 0},
