@@ -216,6 +216,15 @@ typedef struct hsb_peer_out {
   double* const* s_slots;
 } hsb_peer_out;
 
+/* The owner's reduction of the fused scatter: out[i] = sum over the n_slots
+ * receive slots (slot r at slots + 2 * r * slot_stride doubles) of slot_r[i],
+ * i < count complex128 elements, summed in rank order (deterministic).  Replaces
+ * the reduction inside ncclReduceScatter of the north star's atom-sharded
+ * build (the reference has no multi-GPU code).  Device pointers;
+ * asynchronous on `stream`. (ABI 8) */
+HSB_API hsb_status hsb_sum_slots(hsb_ctx* ctx, void* stream, const double* slots, int32_t n_slots,
+                                 int64_t slot_stride, int64_t count, double* out);
+
 /* CUDA IPC for the receive slots: a 64-byte handle of a device allocation,
  * and its mapping in another process (cudaIpcGetMemHandle / OpenMemHandle). */
 HSB_API hsb_status hsb_ipc_handle(hsb_ctx* ctx, void* dev_ptr, uint8_t handle[64]);

@@ -36,7 +36,7 @@ HSB_ENGINE_DMMA = 0
 HSB_ENGINE_INT8 = 1
 HSB_ENGINE_AUTO = 2
 ENGINES = {"dmma": HSB_ENGINE_DMMA, "int8": HSB_ENGINE_INT8, "auto": HSB_ENGINE_AUTO}
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 _P = ctypes.c_void_p
 _DPP = ctypes.POINTER(ctypes.c_void_p)
@@ -118,6 +118,7 @@ def load():
             "hsb_zgemm": (i32, [_P, _P, ch, ch, i64, i64, i64, dbl, dbl, _P, i64, _P, i64, dbl, dbl,
                                 _P, i64, u32]),
             "hsb_hermitian_mirror": (i32, [_P, _P, i64, _P, i64]),
+            "hsb_sum_slots": (i32, [_P, _P, _P, i32, i64, i64, _P]),
             "hsb_match_coeffs": (i32, [_P, _P, ctypes.POINTER(HsbPhys), _P, _P, i64]),
             "hsb_build_hs_physical": (i32, [_P, _P, ctypes.POINTER(HsbPhys), ctypes.POINTER(HsbProblem), u32,
                                             ctypes.POINTER(HsbOutput), ctypes.POINTER(HsbTimings),

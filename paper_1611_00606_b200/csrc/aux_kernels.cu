@@ -359,6 +359,32 @@ cudaError_t launch_sum_planes_batched(const double* x, int n, int64_t bstride, i
   return cudaGetLastError();
 }
 
+// out[i] = sum_r slots[r * stride + i] (complex): the owner's half of the fused
+// multi-GPU scatter (hsb_peer_out).  16-byte loads of every slot in flight,
+// summed in rank order (deterministic).  HBM-bound: (n_slots + 1) * 16 B per
+// element.
+__global__ void sum_slots_kernel(const double2* __restrict__ slots, int n_slots, int64_t stride, int64_t count,
+                                 double2* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double2 acc = __ldg(slots + i);
+    for (int r = 1; r < n_slots; ++r) {
+      const double2 v = __ldg(slots + r * stride + i);
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+    out[i] = acc;
+  }
+}
+
+cudaError_t launch_sum_slots(const double* slots, int n_slots, int64_t stride, int64_t count, double* out,
+                             cudaStream_t st) {
+  if (count <= 0 || n_slots <= 0) return cudaSuccess;
+  sum_slots_kernel<<<grid_for(count, 256, 148 * 16), 256, 0, st>>>(reinterpret_cast<const double2*>(slots), n_slots,
+                                                                   stride, count, reinterpret_cast<double2*>(out));
+  return cudaGetLastError();
+}
+
 __global__ void fill_i32_kernel(int32_t* p, int64_t n, int32_t v) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)

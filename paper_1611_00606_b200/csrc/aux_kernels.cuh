@@ -55,6 +55,9 @@ cudaError_t launch_scale_cols_inv(const double* t, double* out, const double* u,
 cudaError_t launch_diag_scale(const double* src, int64_t lds, double* dst, int64_t ldd, const double* u,
                               int64_t rows, int64_t cols, cudaStream_t st);
 cudaError_t launch_mirror(double* c, int64_t ldc, int n, cudaStream_t st);
+// out[i] = sum over n_slots slots (stride complex elements apart) of slot[i], complex
+cudaError_t launch_sum_slots(const double* slots, int n_slots, int64_t stride, int64_t count, double* out,
+                             cudaStream_t st);
 cudaError_t launch_fill_i32(int32_t* p, int64_t n, int32_t v, cudaStream_t st);
 // device-side Loop 2 routing (offsets of R / gather lists) + info export to mapped host memory
 cudaError_t launch_route_atoms(const int32_t* info, int na, int nl, int32_t* offs, int32_t* info_host,

@@ -33,7 +33,7 @@ using namespace hsb_host;
 // =============================================================================
 extern "C" {
 
-int32_t hsb_abi_version(void) { return 7; }
+int32_t hsb_abi_version(void) { return 8; }
 
 hsb_status hsb_ctx_create(int32_t device, hsb_ctx** out) {
   hsb_ctx* ctx = nullptr;
@@ -287,6 +287,18 @@ hsb_status hsb_hermitian_mirror(hsb_ctx* ctx, void* stream, int64_t n, double* c
   if (n == 0) return HSB_OK;
   cudaSetDevice(ctx->device);
   CK(launch_mirror(c, ldc, static_cast<int>(n), static_cast<cudaStream_t>(stream)));
+  return HSB_OK;
+}
+
+hsb_status hsb_sum_slots(hsb_ctx* ctx, void* stream, const double* slots, int32_t n_slots, int64_t slot_stride,
+                         int64_t count, double* out) {
+  if (!ctx) return fail(nullptr, HSB_ERR_INPUT, "ctx is NULL");
+  CtxCall call_guard(ctx, false);
+  if (n_slots < 1 || count < 0 || slot_stride < count) return fail(ctx, HSB_ERR_DIMENSION, "bad slot dimensions");
+  if (count == 0) return HSB_OK;
+  if (!slots || !out) return fail(ctx, HSB_ERR_INPUT, "slot/output pointers are NULL");
+  cudaSetDevice(ctx->device);
+  CK(launch_sum_slots(slots, n_slots, slot_stride, count, out, static_cast<cudaStream_t>(stream)));
   return HSB_OK;
 }
 

@@ -459,13 +459,29 @@ class PeerSlots:
         return st
 
     def finish(self, hb=None, sb=None):
-        """This rank's column blocks (cols, n_g) = sums of its receive slots.
-        Call once every rank's build has completed (e.g. after a barrier)."""
+        """This rank's column blocks (cols, n_g) = sums of its receive slots
+        (``hsb_sum_slots``, on the current stream).  Call once every rank's
+        build has completed (e.g. after a barrier)."""
+        import ctypes
+
         import torch
 
-        hb = torch.sum(self.h_recv, dim=0) if hb is None else torch.sum(self.h_recv, dim=0, out=hb)
-        sb = torch.sum(self.s_recv, dim=0) if sb is None else torch.sum(self.s_recv, dim=0, out=sb)
-        return hb, sb
+        from . import _lib
+
+        lib = _lib.load()
+        dev = self.h_recv.device
+        ctx = _lib.context(dev.index or 0)
+        stream = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+        out = []
+        for recv, o in ((self.h_recv, hb), (self.s_recv, sb)):
+            if o is None:
+                o = torch.empty(recv.shape[1:], dtype=recv.dtype, device=dev)
+            assert recv.is_contiguous() and o.is_contiguous() and o.shape == recv.shape[1:]
+            per_slot = recv[0].numel()
+            _lib.check(lib.hsb_sum_slots(ctx, stream, ctypes.c_void_p(recv.data_ptr()), recv.shape[0], per_slot,
+                                         per_slot, ctypes.c_void_p(o.data_ptr())), ctx)
+            out.append(o)
+        return out[0], out[1]
 
     def close(self):
         import ctypes

@@ -50,3 +50,18 @@ def test_peer_output_needs_the_int8_engine():
     slots = hd.PeerSlots.emulated(2, 77, dp.a_stack.device)
     with pytest.raises(RuntimeError, match="INT8"):
         build_hs_device(dp, policy=GpuPolicy(engine="dmma"), peer=slots[0])
+
+
+@pytest.mark.parametrize("n_slots,cols,n_g", [(1, 5, 33), (3, 17, 257), (8, 64, 1000)])
+def test_sum_slots_kernel_is_rank_ordered_sum(n_slots, cols, n_g):
+    # hsb_sum_slots (the owner's reduction of the fused scatter) against the
+    # same rank-ordered sum in torch: bitwise
+    g = torch.Generator(device="cuda").manual_seed(n_slots * 1000 + cols)
+    recv = torch.randn((n_slots, cols, n_g), dtype=torch.complex128, device="cuda", generator=g)
+    slots = hd.PeerSlots(n_slots, 0, cols, n_g, recv, recv.clone(), [], [])
+    hb, sb = slots.finish()
+    want = recv[0].clone()
+    for r in range(1, n_slots):
+        want += recv[r]
+    torch.cuda.synchronize()
+    assert torch.equal(hb, want) and torch.equal(sb, want)

@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_loader_and_abi_version():
     lib = _lib.load()
-    assert lib.hsb_abi_version() == _lib.ABI_VERSION == 7
+    assert lib.hsb_abi_version() == _lib.ABI_VERSION == 8
 
 
 def test_binding_struct_layout_matches_header():
