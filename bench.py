@@ -732,14 +732,30 @@ def main():
         flops_p = sum(float(sum(section_flops(Dims(dims.n_atoms, dims.n_l, int(g.shape[0])), 0).values()))
                       for g in gsets)
         coeff = coeff_roofline(system, kpts[0], gsets[0], dev)
+        from paper_1611_00606_b200 import _lib as hsb_lib
+
+        # the instance-path lanes' workspaces are not needed any more (C4: they
+        # would leave no room for a third physical lane)
+        hsb_lib.trim_all(dev_index)
+        torch.cuda.empty_cache()
         depth_p = int(os.environ.get("HSB_PHYS_DEPTH", "3"))
         try:
-            # warm contexts and the pinned cache at the largest G set of the batch
+            # warm contexts and the pinned cache at the largest G set of the
+            # batch; as deep as the lanes' workspaces fit (C4: 2)
             imax = int(np.argmax([g.shape[0] for g in gsets]))
-            warm_k = [kpts[imax]] * (depth_p + 2)
-            for o in physics.iter_hs_physical_kpoints(system, warm_k, [gsets[imax]] * len(warm_k), t_aa, t_ab, t_bb,
-                                                      policy, depth=depth_p):
-                del o
+            while True:
+                try:
+                    warm_k = [kpts[imax]] * (depth_p + 2)
+                    for o in physics.iter_hs_physical_kpoints(system, warm_k, [gsets[imax]] * len(warm_k), t_aa, t_ab,
+                                                              t_bb, policy, depth=depth_p):
+                        del o
+                    break
+                except (torch.OutOfMemoryError, RuntimeError) as exc:
+                    if depth_p == 1 or "memory" not in str(exc).lower():
+                        raise
+                    depth_p -= 1
+                    hsb_lib.trim_all(dev_index)
+                    torch.cuda.empty_cache()
             t0 = time.perf_counter()
             d2h_p = 0
             for hh, sh, _, tp, _ in physics.iter_hs_physical_kpoints(system, kpts, gsets, t_aa, t_ab, t_bb, policy,
