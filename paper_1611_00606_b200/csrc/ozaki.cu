@@ -266,6 +266,14 @@ __device__ __forceinline__ bool elect_one() {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+// Arrive on a (possibly remote) barrier that hands over no generic-proxy data:
+// "TMEM buffer drained" (after tcgen05.fence::before_thread_sync) and "work
+// slot read".  Release at CTA scope: the cluster-scope release above waits for
+// every outstanding global store of the arriving warp (the epilogue's residue
+// stores) -- ncu showed it as the top stall (membar) of short-K GEMMs.
+__device__ __forceinline__ void mbar_arrive_remote_cta(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -356,7 +364,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
     mbar_wait_cluster(wfull(j), static_cast<uint32_t>((seq / kOzQ) & 1));
     const int w = static_cast<int>(ld_shared_u32(wslot(j)));
     __syncwarp();
-    if (lane == 0) mbar_arrive_cluster(wempty(j) & kPeerMask);  // the leader's copy
+    if (lane == 0) mbar_arrive_remote_cta(wempty(j) & kPeerMask);  // the leader's copy
     return w;
   };
 
@@ -555,7 +563,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty(acc) & kPeerMask);
+      if (lane == 0) mbar_arrive_remote_cta(tempty(acc) & kPeerMask);
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1u;
