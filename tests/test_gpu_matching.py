@@ -84,7 +84,11 @@ def test_physical_build_host_outputs_match_device(engine):
     torch.cuda.synchronize()
     assert isinstance(hh, np.ndarray) and hh.shape == (len(g), len(g))
     assert (split.hpd, split.nonhpd) == (split_h.hpd, split_h.nonhpd)
-    assert np.array_equal(hh, h.cpu().numpy().T) and np.array_equal(sh, s.cpu().numpy().T)
+    for name, a, b in (("H", hh, h.cpu().numpy().T), ("S", sh, s.cpu().numpy().T)):
+        bad = np.argwhere(a != b)
+        assert len(bad) == 0, (f"{name}: {len(bad)} entries differ ({int(np.sum(bad[:, 0] < bad[:, 1]))} above the "
+                               f"diagonal), rows {bad[:, 0].min()}..{bad[:, 0].max()}, cols {bad[:, 1].min()}.."
+                               f"{bad[:, 1].max()}, max |diff| {np.max(np.abs(a - b)):.3e}, first {bad[:4].tolist()}")
     assert t["d2h_bytes"] > 0
 
 
