@@ -154,3 +154,46 @@ def test_triangle_plan_moves_about_half_the_bytes(n_g, world, nb):
     # lower-only columns (what uplo='L' eigensolvers read): the reduce-scatter alone
     assert (world - 1) * plan.chunk * 16 < 0.6 * full
     assert sorted(torch.cat(plan.cols).tolist()) == list(range(n_g))
+
+
+def _kpoint_worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import alg1
+    from paper_1611_00606_b200.distributed import build_kpoints
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    kpts = [generate(ProblemSpec(Dims(2, 4, 15 + 3 * i), seed=100 + i)) for i in range(7)]  # ragged N_G
+    mine = build_kpoints(kpts, builder=lambda p, _pol: alg1.build_hs_cpu(p))
+    gathered = [None] * world
+    dist.all_gather_object(gathered, sorted(mine))
+    q.put((rank, {k: (v["h"], v["s"]) for k, v in mine.items()}, gathered))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_kpoint_replicas_cover_every_kpoint_once(world):
+    # config C5's distribution: round-robin k-points, no
+    # communication on the data path; every k-point built exactly once and
+    # equal to the serial build
+    from oracle import alg1
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_kpoint_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    got = [q.get(timeout=120) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+    assert all(pr.exitcode == 0 for pr in procs)
+    owned = sorted(k for _, res, _ in got for k in res)
+    assert owned == list(range(7))
+    for rank, res, gathered in got:
+        assert sorted(res) == kpoint_assignment(7, world, rank)
+        assert sorted(k for g in gathered for k in g) == list(range(7))
+        for k, (h, s) in res.items():
+            ref = alg1.build_hs_cpu(generate(ProblemSpec(Dims(2, 4, 15 + 3 * k), seed=100 + k)))
+            assert np.array_equal(h, ref["h"]) and np.array_equal(s, ref["s"])

@@ -84,6 +84,57 @@ def _worker(rank, world, port, mode, q):
         raise
 
 
+def _kpoint_worker(rank, world, port, q):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+
+    from paper_1611_00606_b200 import GpuPolicy
+    from paper_1611_00606_b200 import distributed as hd
+
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        kpts = [generate(ProblemSpec(Dims(3, 25, 300 + 37 * i), seed=40 + i, nonhpd_fraction=0.3)) for i in range(5)]
+        mine = hd.build_kpoints(kpts, GpuPolicy())
+        q.put((rank, {k: (o.h.matrix, o.s.matrix) for k, o in mine.items()}))
+        dist.barrier()
+        dist.destroy_process_group()
+    except BaseException as exc:  # noqa: BLE001 -- report to the parent
+        q.put((rank, "error", repr(exc)))
+        raise
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_kpoint_replicas_on_gpu_match_oracle(world):
+    # config C5's k-point replicas: each rank builds its round-robin share on
+    # the GPU, no communication; every k-point once, each against the oracle
+    import torch.multiprocessing as mp
+
+    from oracle import alg1
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_kpoint_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    got = [q.get(timeout=600) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=120)
+    errors = [g for g in got if isinstance(g[1], str) and g[1] == "error"]
+    assert not errors, errors
+    assert all(pr.exitcode == 0 for pr in procs)
+    assert sorted(k for _, res in got for k in res) == list(range(5))
+    for _, res in got:
+        for k, (h, s) in res.items():
+            ref = alg1.build_hs_cpu(generate(ProblemSpec(Dims(3, 25, 300 + 37 * k), seed=40 + k, nonhpd_fraction=0.3)))
+            assert rel_frob_error(h, ref["h"]) < 1e-14 and rel_frob_error(s, ref["s"]) < 1e-14
+
+
 @pytest.mark.parametrize("mode", ["nccl", "fused", "tri"])
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_gpu_ranks_match_oracle(world, mode):
