@@ -438,7 +438,8 @@ hsb_status run_zrk(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launche
   // 3M on plain (unbatched) operands: Re-Im / Re+Im planes of each distinct
   // operand, computed once here and fed to the kernel by TMA
   const bool g3 = ctx->cplx == HSB_CPLX_3M;
-  bool planes = g3 && z.batch == 1;
+  static const bool no_zplanes = std::getenv("HSB_NO_ZPLANES") != nullptr;  // experiments
+  bool planes = g3 && z.batch == 1 && !no_zplanes;
   for (const Seg& s : z.segs)
     if (s.l.batch != 1 || s.r.batch != 1) planes = false;
   struct PlaneSrc {
@@ -556,7 +557,9 @@ hsb_status run_zrk(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launche
   int64_t grid_x = z.triangle ? static_cast<int64_t>(p.tiles_m) * (p.tiles_m + 1) / 2
                               : static_cast<int64_t>(p.tiles_m) * p.tiles_n;
   if (grid_x > 0x7fffffff || z.batch > 65535) return fail(ctx, HSB_ERR_UNSUPPORTED, "grid too large");
-  if (g3 && z.triangle && z.batch == 1 && p.tiles_m > kTileGroup) CKS(tile_order(ctx, p.tiles_m, st, &p.tile_list));
+  static const bool no_tile_order = std::getenv("HSB_NO_TILE_ORDER") != nullptr;  // experiments
+  if (g3 && z.triangle && z.batch == 1 && p.tiles_m > kTileGroup && !no_tile_order)
+    CKS(tile_order(ctx, p.tiles_m, st, &p.tile_list));
   if (z.tl) CK(timeline_mark(z.tl, st, z.sect));
   if (g3) {
     if (grid_x * z.batch > 0x7fffffff) return fail(ctx, HSB_ERR_UNSUPPORTED, "grid too large");

@@ -363,6 +363,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
     const int j = seq & (kOzQ - 1);
     mbar_wait_cluster(wfull(j), static_cast<uint32_t>((seq / kOzQ) & 1));
     const int w = static_cast<int>(ld_shared_u32(wslot(j)));
+    // the slot is rewritten once every role has arrived, and an arrive does not
+    // wait for a load still in flight: branch on the value first (never taken)
+    // so the arrive cannot be scheduled ahead of the load's completion
+    if (w < 0) __trap();
     __syncwarp();
     if (lane == 0) mbar_arrive_remote_cta(wempty(j) & kPeerMask);  // the leader's copy
     return w;

@@ -49,7 +49,8 @@ constexpr int k3Threads = (k3ConsumerWarps + 1) * 32;
 constexpr int kPlaneTileBytes = kBM * 8 * 8;  // 64 rows x 8 complex k, one double each
 template <int PMODE>
 struct Cfg3 {
-  static constexpr int stage_bytes = kStageBytes + PMODE * kPlaneTileBytes;
+  static constexpr int load_bytes = kStageBytes + PMODE * kPlaneTileBytes;  // TMA bytes per stage
+  static constexpr int stage_bytes = load_bytes;
   static constexpr int stages = PMODE == 2 ? 8 : PMODE == 1 ? 9 : 12;  // PMODE 1: 180 KB, room for a residue block beside it
   static constexpr int smem = stages * stage_bytes + 1024 /*align*/ + 256 /*barriers*/;
 };
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(k3Threads, 1) zrk3m_kernel(const __grid_consta
           for (int kc = 0; kc < sd.kchunks; ++kc) {
             mbar_wait(empty_bar(stage), phase);
             const uint32_t fb = full_bar(stage);
-            mbar_expect_tx(fb, kSB);
+            mbar_expect_tx(fb, C3::load_bytes);
             const uint32_t dst = base + stage * kSB;
             const int k0 = kc * kBK;
             if (sd.lbpos == 1)
@@ -240,6 +241,14 @@ __global__ void __launch_bounds__(k3Threads, 1) zrk3m_kernel(const __grid_consta
             dmma_nv(cw[i][j][0], cw[i][j][1], as[i], bs[j]);
           }
       }
+      // Release the stage only once this warp's reads of it are complete: the
+      // scheduler sinks DMMAs (and so the waits on their LDS operands) below
+      // the arrive, and the arrive does not wait for LDS in flight, so the
+      // producer's next TMA could overwrite rows not yet read (rare wrong A
+      // rows in one warp's sub-tile, probes/stress_dmma_phys.py).  The proxy
+      // fence orders this thread's generic-proxy reads before the async-proxy
+      // (TMA) writes that follow the release.
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(empty_bar(stage));
       if (++stage == kSt) {
@@ -299,8 +308,13 @@ __global__ void __launch_bounds__(k3Threads, 1) zrk3m_kernel(const __grid_consta
         }
     }
     if (p.done_cnt) {
-      // all consumer stores of this tile precede the count (named barrier over
-      // the consumer warps; the system-scope fence publishes them to the host)
+      // all consumer stores of this tile precede the count: EVERY storing
+      // thread fences (its stores performed at device scope, where the copy
+      // engine reads them) before the named barrier over the consumer warps;
+      // a barrier alone orders issue, not completion -- with only thread 0
+      // fencing, a host download of a "final" column block occasionally read
+      // stores still in flight (probes/stress_host_outputs.py)
+      __threadfence();
       asm volatile("bar.sync 1, %0;" ::"n"(k3ConsumerWarps * 32) : "memory");
       if (threadIdx.x == 0) {
         __threadfence_system();

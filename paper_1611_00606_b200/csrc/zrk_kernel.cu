@@ -148,6 +148,9 @@ __global__ void __launch_bounds__(kThreads, 2) zrk_kernel(const __grid_constant_
           }
       }
     }
+    // this warp's shared-memory reads complete before the stage is released to
+    // the TMA producer (see zrk3m_kernel.cu: the arrive does not wait for LDS)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive(empty_bar(stage));
     if (++stage == kStages) {

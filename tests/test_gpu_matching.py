@@ -158,3 +158,29 @@ def test_physical_build_fused_residues_match_the_standalone_passes(lmax, ng, non
     assert (sp1.hpd, sp1.nonhpd) == (sp2.hpd, sp2.nonhpd)
     assert torch.equal(h1, h2) and torch.equal(s1, s2)
     assert t1["launches"] < t2["launches"]  # the exponent and A / UB residue passes are gone
+
+
+def test_dmma_physical_builds_are_bitwise_repeatable():
+    # regression: the DMMA kernels released a pipeline stage before their last
+    # shared-memory loads had completed (the arrive does not wait for LDS in
+    # flight), so the first builds of a new shape occasionally had a few wrong
+    # rows in one warp's sub-tile (probes/stress_dmma_phys.py).  Device,
+    # streamed-host and staged-host builds of one input must agree bit for bit.
+    from paper_1611_00606_b200 import GpuPolicy
+
+    system, k, kmax, g = synthetic_system(4, 2, 10, 2100, seed=3)
+    t = synthetic_t_matrices(system, seed=3, nonhpd_fraction=0.2)
+    pol, pol_staged = GpuPolicy(engine="dmma"), GpuPolicy(engine="dmma", pinned_outputs=False)
+    ref = None
+    for _ in range(3):
+        for kind in ("device", "host", "staged"):
+            if kind == "device":
+                h, s, *_ = build_hs_physical(system, k, g, *t, policy=pol)
+                torch.cuda.synchronize()
+                h, s = h.cpu().numpy().T, s.cpu().numpy().T
+            else:
+                h, s, *_ = build_hs_physical(system, k, g, *t, policy=pol if kind == "host" else pol_staged,
+                                             host_outputs=True)
+            if ref is None:
+                ref = (h.copy(), s.copy())
+            assert np.array_equal(h, ref[0]) and np.array_equal(s, ref[1]), kind
