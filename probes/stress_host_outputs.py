@@ -23,7 +23,7 @@ t_end = time.time() + seconds
 while time.time() < t_end:
     engine = rng.choice(["int8", "dmma"])
     pol = GpuPolicy(engine=engine)
-    kind = rng.choice(["phys", "phys", "inst", "kpts"])
+    kind = rng.choice(["phys", "phys", "inst", "kpts", "kphys", "lower"])
     if kind == "phys":
         key = rng.choice([(5, 2, 8, 1300, 5), (3, 2, 6, 700, 9), (4, 2, 10, 2100, 3)])
         if key not in systems:
@@ -43,6 +43,37 @@ while time.time() < t_end:
         a = build_hs(p, pol)
         b = build_hs(p, GpuPolicy(engine=engine, pinned_outputs=False))
         pairs = (("H", a.h.matrix, b.h.matrix), ("S", a.s.matrix, b.s.matrix))
+    elif kind == "kphys":
+        from paper_1611_00606_b200.physics import gvector_set, iter_hs_physical_kpoints
+        key = (3, 2, 6, 700, 9)
+        if key not in systems:
+            sysm, k, _, g = synthetic_system(*key[:4], seed=key[4])
+            systems[key] = (sysm, k, g, synthetic_t_matrices(sysm, seed=key[4], nonhpd_fraction=0.2))
+        sysm, k0, g0, t = systems[key]
+        kpts = [np.array(x) for x in [(0.0, 0.0, 0.0), (0.5, 0.25, 0.0), (0.125, -0.375, 0.25)]]
+        gsets = [g0] * len(kpts)
+        got = list(iter_hs_physical_kpoints(sysm, kpts, gsets, *t, policy=pol, depth=rng.choice([2, 3])))
+        pairs = []
+        for i, (hh, sh, *_r) in enumerate(got):
+            h, s, *_ = build_hs_physical(sysm, kpts[i], gsets[i], *t, policy=pol)
+            torch.cuda.synchronize()
+            pairs += [(f"kph{i}H", hh, h.cpu().numpy().T), (f"kph{i}S", sh, s.cpu().numpy().T)]
+    elif kind == "lower":
+        from paper_1611_00606_b200 import DeviceProblem, build_hs_device
+        dims = rng.choice([Dims(4, 25, 900), Dims(3, 49, 1300)])
+        p = generate(ProblemSpec(dims, seed=rng.randrange(1000), nonhpd_fraction=0.3))
+        dp = DeviceProblem.from_instance(p)
+        hf, sf, *_ = build_hs_device(dp, policy=pol)
+        hl = torch.zeros((dims.n_g + 1, dims.n_g), dtype=torch.complex128, device="cuda")
+        sl = torch.zeros_like(hl)
+        build_hs_device(dp, hl, sl, policy=pol, lower_only=True)
+        torch.cuda.synchronize()
+        n_ = dims.n_g
+        mask = np.tril(np.ones((n_, n_), dtype=bool))
+        a1, b1 = hf.cpu().numpy().T, hl[:n_].cpu().numpy().T
+        a2, b2 = sf.cpu().numpy().T, sl[:n_].cpu().numpy().T
+        pairs = (("lowH", np.where(mask, a1, 0), np.where(mask, b1, 0)),
+                 ("lowS", np.where(mask, a2, 0), np.where(mask, b2, 0)))
     else:
         dims = rng.choice([Dims(3, 25, 700), Dims(2, 36, 1000)])
         ps = [generate(ProblemSpec(dims, seed=rng.randrange(1000))) for _ in range(4)]
