@@ -304,7 +304,8 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
 }
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+// tcgen05.ld without the wait: several loads in flight, one tcgen05.wait::ld
+__device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
       "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -314,7 +315,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
         "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
 __device__ __forceinline__ void oz_work(const OzGemmParams& p, int w, int& prod, int& slab, int& mod, int& t,
@@ -528,10 +528,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
       const int nrow = min(kOzBN, p.nrows - tm * 256);
       const bool col_ok = tn * 256 + cloc < p.n;
       constexpr int kChunks = kOzBN / 32 / kOzEpiParts;  // 32-column TMEM loads per warp
-      for (int c = part * kChunks; c < (part + 1) * kChunks; ++c) {
+      // drain this warp's accumulator columns first and hand the TMEM buffer
+      // back to the MMA issuer before the reduction and the stores: with short
+      // reductions (a few k chunks per item) the MMA otherwise waits for the
+      // whole epilogue of the item two back
+      uint32_t vv[kChunks][32];
+#pragma unroll
+      for (int cc = 0; cc < kChunks; ++cc)
+        if ((part * kChunks + cc) * 32 < nrow)  // warp-uniform
+          tmem_ld32_issue(tmem + ((q * 32) << 16) + acc * kOzBN + (part * kChunks + cc) * 32, vv[cc]);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote_cta(tempty(acc) & kPeerMask);
+#pragma unroll
+      for (int cc = 0; cc < kChunks; ++cc) {
+        const int c = part * kChunks + cc;
         if (c * 32 >= nrow) break;  // warp-uniform
-        uint32_t v[32];
-        tmem_ld32(tmem + ((q * 32) << 16) + acc * kOzBN + c * 32, v);
+        const uint32_t (&v)[32] = vv[cc];
         if (col_ok) {
           uint32_t w[8];
 #pragma unroll
@@ -568,9 +582,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
         __syncwarp();
         if (lane == 0) atomicAdd(cnt, 1);
       }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive_remote_cta(tempty(acc) & kPeerMask);
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1u;
