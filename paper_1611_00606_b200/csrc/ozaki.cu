@@ -226,11 +226,13 @@ constexpr int kOzHalf = 128;                      // rows of A and of B per CTA
 constexpr int kOzABytes = kOzHalf * kOzBK;        // 16 KB
 constexpr int kOzStageBytes = 2 * kOzABytes;      // 32 KB
 constexpr int kOzSmem = kOzStages * kOzStageBytes + 1024 + 256;
-// warp 0 TMA, warp 1 MMA (leader) + TMEM owner, warps 2-17 epilogue: four warps
-// per TMEM lane quarter, each reducing a quarter of the accumulator's columns,
-// so short reductions (few k chunks per tile: small configs, atom shards) are
-// not epilogue-bound
-constexpr int kOzEpiWarps = 16;
+// warp 0 TMA, warp 1 MMA (leader) + TMEM owner, warps 2-9 epilogue: two warps
+// per TMEM lane quarter, each draining half of the accumulator's columns into
+// registers and releasing the TMEM buffer before it reduces and stores them
+// (with the early release, 16 epilogue warps -- round 2's first answer to
+// short reductions -- were no faster than 8: 8-way C3 shard GEMMs 4.35 vs
+// 4.15 ms, C3 unchanged, and 8 need no register spills of note)
+constexpr int kOzEpiWarps = 8;
 constexpr int kOzEpiParts = kOzEpiWarps / 4;  // column parts per lane quarter
 constexpr int kOzThreads = (2 + kOzEpiWarps) * 32;
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;       // shared::cluster address of the leader's copy
