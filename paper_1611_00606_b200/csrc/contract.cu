@@ -319,7 +319,11 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
   gp.nseg = static_cast<int32_t>(segs.size());
   // slabs of ~16 KB of k (see ozaki.cuh), balanced
   const int32_t total_chunks = gp.seg_chunk0[gp.nseg];
-  constexpr int32_t kSlabChunks = 16384 / kOzBK;
+  static const int32_t kSlabChunks = [] {  // HSB_OZ_SLAB_KB: slab k extent for experiments (default 16)
+    const char* e = std::getenv("HSB_OZ_SLAB_KB");
+    const int v = e ? std::atoi(e) : 0;
+    return static_cast<int32_t>((v > 0 ? v : 16) * 1024 / kOzBK);
+  }();
   gp.nslab = std::max(1, std::min<int32_t>(kOzMaxSlab, (total_chunks + kSlabChunks - 1) / kSlabChunks));
   for (int sl = 0; sl <= gp.nslab; ++sl)
     gp.slab_chunk0[sl] = static_cast<int32_t>(static_cast<int64_t>(total_chunks) * sl / gp.nslab);
