@@ -362,3 +362,26 @@ def test_lower_only_outputs_leave_the_upper_triangle_untouched(engine):
         assert np.array_equal(g[low], f[low])
         assert np.all(g[up] == sentinel)
         assert np.all(np.diagonal(g).imag == 0)
+
+
+@pytest.mark.parametrize("cm", ["3m", "int8"])
+def test_zero_columns_atoms_and_tiny_entries(cm):
+    # degenerate data the per-column scaling of the INT8 engine must survive:
+    # all-zero G columns of A and B (column maximum 0), an atom whose blocks
+    # are all zero, and a column whose entries are 1e-200 (exponent far below
+    # the others); both engines against the oracle
+    p = generate(ProblemSpec(Dims(4, 25, 700), seed=77, nonhpd_fraction=0.25))
+    for blocks in (p.a_blocks, p.b_blocks):
+        for blk in blocks:
+            blk[:, [0, 5, 699]] = 0.0
+            blk[:, 17] *= 1e-200
+    p.a_blocks[2][:] = 0.0
+    p.b_blocks[2][:] = 0.0
+    out = build_hs(p, _pol(cm))
+    ref = alg1.build_hs_cpu(p)
+    assert rel_frob_error(out.h.matrix, ref["h"]) < 1e-14
+    assert rel_frob_error(out.s.matrix, ref["s"]) < 1e-14
+    for c in (0, 5, 699):
+        assert not np.any(out.h.matrix[:, c]) and not np.any(out.s.matrix[:, c])
+    # the tiny column keeps its relative accuracy (per-column scaling)
+    assert np.linalg.norm(out.s.matrix[:, 17] - ref["s"][:, 17]) <= 1e-13 * np.linalg.norm(ref["s"][:, 17])
