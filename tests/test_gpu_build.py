@@ -385,3 +385,17 @@ def test_zero_columns_atoms_and_tiny_entries(cm):
         assert not np.any(out.h.matrix[:, c]) and not np.any(out.s.matrix[:, c])
     # the tiny column keeps its relative accuracy (per-column scaling)
     assert np.linalg.norm(out.s.matrix[:, 17] - ref["s"][:, 17]) <= 1e-13 * np.linalg.norm(ref["s"][:, 17])
+
+
+@pytest.mark.parametrize("cm", ["3m", "int8"])
+@pytest.mark.parametrize("dims", [Dims(1, 64, 256), Dims(2, 64, 512), Dims(2, 64, 257), Dims(3, 43, 255),
+                                  Dims(2, 225, 300), Dims(1, 1, 1)])
+def test_tile_boundaries(dims, cm):
+    # N_G and K exactly on / one past the 256-wide INT8 tiles and 128-byte k
+    # chunks, N_L above the 128-row V-product tiles, and the 1 x 1 x 1 corner
+    p = generate(ProblemSpec(dims, seed=dims.n_g + dims.n_l, nonhpd_fraction=0.5))
+    out = build_hs(p, _pol(cm))
+    ref = alg1.build_hs_cpu(p)
+    assert rel_frob_error(out.h.matrix, ref["h"]) < 1e-14
+    assert rel_frob_error(out.s.matrix, ref["s"]) < 1e-14
+    assert (out.split.hpd, out.split.nonhpd) == (ref["hpd"], ref["nonhpd"])
