@@ -65,3 +65,17 @@ def test_sum_slots_kernel_is_rank_ordered_sum(n_slots, cols, n_g):
         want += recv[r]
     torch.cuda.synchronize()
     assert torch.equal(hb, want) and torch.equal(sb, want)
+
+
+def test_sum_slots_rejects_bad_dimensions():
+    import ctypes
+
+    from paper_1611_00606_b200 import DimensionError, _lib
+
+    lib = _lib.load()
+    ctx = _lib.context(0)
+    buf = torch.zeros(8, dtype=torch.complex128, device="cuda")
+    for n_slots, stride, count in ((0, 4, 4), (2, 3, 4), (2, 4, -1)):
+        with pytest.raises(DimensionError):
+            _lib.check(lib.hsb_sum_slots(ctx, None, ctypes.c_void_p(buf.data_ptr()), n_slots, stride, count,
+                                         ctypes.c_void_p(buf.data_ptr())), ctx)
