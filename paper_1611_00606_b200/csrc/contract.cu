@@ -393,14 +393,36 @@ hsb_status run_ozaki(hsb_ctx* ctx, cudaStream_t st, const ZrkCall& z, int* launc
   const std::vector<int2>& tl_host = ctx->oz_tiles_host;
   // (the tile list is ordered in bands of kOzTileGroup columns, see oz_tiles)
   const int64_t group = (z.done_cnt || z.chunk_events) ? oz_tile_group() : T;
+  // wide work items (HSB_OZ_WIDE, experiments): consecutive row tiles of one
+  // column paired, one launch over the whole triangle
+  static const bool wide_env = std::getenv("HSB_OZ_WIDE") != nullptr;
+  const bool wide = wide_env && group == T && gp.nseg > 0;
+  gp.wide_list = nullptr;
+  int nwide = 0;
+  if (wide) {
+    std::vector<int4>& wl = ctx->oz_wide_host;
+    wl.clear();
+    for (int t = 0; t < total_tiles;) {
+      const int2 a = tl_host[static_cast<size_t>(t)];
+      const bool pair = t + 1 < total_tiles && tl_host[static_cast<size_t>(t) + 1].y == a.y &&
+                        tl_host[static_cast<size_t>(t) + 1].x == a.x + 1;
+      wl.push_back(make_int4(a.x, a.y, t, pair ? t + 1 : -1));
+      t += pair ? 2 : 1;
+    }
+    nwide = static_cast<int>(wl.size());
+    void* wbuf;
+    CKS(ws(ctx, "oz_wide", wl.size() * sizeof(int4), &wbuf));
+    CK(cudaMemcpyAsync(wbuf, wl.data(), wl.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
+    gp.wide_list = static_cast<const int4*>(wbuf);
+  }
   int t0 = 0;
   for (int64_t j0 = 0; j0 < T; j0 += group) {
     const int64_t j1 = std::min<int64_t>(j0 + group, T);
     int t1 = t0;
     while (t1 < total_tiles && tl_host[static_cast<size_t>(t1)].y < j1) ++t1;
     if (gp.nseg > 0 && t1 > t0) {
-      gp.tile0 = t0;
-      gp.ntiles = t1 - t0;
+      gp.tile0 = wide ? 0 : t0;
+      gp.ntiles = wide ? nwide : t1 - t0;
       if (z.tl) CK(timeline_mark(z.tl, st, z.sect));
       CK(launch_ozaki_gemm(gp, st));
       if (z.tl) CK(timeline_mark(z.tl, st, z.core));

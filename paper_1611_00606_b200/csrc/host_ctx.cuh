@@ -55,6 +55,7 @@ struct hsb_ctx {
   int32_t engine = HSB_ENGINE_DMMA;    // resolved per call (CtxCall): FP64 DMMA or INT8 CRT emulation
   std::mutex call_mu;                  // one entry point at a time per context (workspace, streams, settings)
   int32_t oz_min_bits = kOzDefaultBits; // INT8 engine: operand integer bits (accuracy ~2^-bits)
+  std::vector<int4> oz_wide_host;      // wide INT8 GEMM work items (contract.cu, HSB_OZ_WIDE)
   int64_t oz_tiles_n = 0;              // cached INT8-engine tile list (n of the output)
   std::vector<int2> oz_tiles_host;
   std::vector<int32_t> oz_tile_index_host;

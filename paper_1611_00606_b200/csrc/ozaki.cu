@@ -221,11 +221,20 @@ __global__ void __launch_bounds__(256, 3) ozaki_residue_kernel(const __grid_cons
 // its 128 rows x 256 int32 columns.  Per SM and 128-byte k chunk that is
 // 32 KB of TMA traffic for 4M MACs (half of a 1-CTA 128 x 256 tile's), so six
 // 32 KB stages fit in shared memory.
-constexpr int kOzStages = 7;
 constexpr int kOzHalf = 128;                      // rows of A and of B per CTA
 constexpr int kOzABytes = kOzHalf * kOzBK;        // 16 KB
-constexpr int kOzStageBytes = 2 * kOzABytes;      // 32 KB
-constexpr int kOzSmem = kOzStages * kOzStageBytes + 1024 + 256;
+// WIDE (long reductions): each stage holds the column panel's half and two row
+// panels' halves; the pair runs two MMAs per k step into its two TMEM
+// accumulators (no accumulator double buffering: the epilogue of an item is
+// short next to its ~240 k chunks), so a wave of pairs covers twice the tiles
+// with a third fewer operand panels streamed and a quarter less L2 -> SM traffic
+template <bool WIDE>
+struct OzG {
+  static constexpr int stages = WIDE ? 4 : 7;
+  static constexpr int nb = WIDE ? 2 : 1;                       // row-panel halves per stage
+  static constexpr int stage_bytes = (1 + nb) * kOzABytes;      // 32 or 48 KB
+  static constexpr int smem = stages * stage_bytes + 1024 + 256;
+};
 // warp 0 TMA, warp 1 MMA (leader) + TMEM owner, warps 2-9 epilogue: two warps
 // per TMEM lane quarter, each draining half of the accumulator's columns into
 // registers and releasing the TMEM buffer before it reduces and stores them
@@ -353,8 +362,12 @@ __device__ __forceinline__ void oz_work(const OzGemmParams& p, int w, int& prod,
   tn = tt.y;
 }
 
+template <bool WIDE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
     ozaki_gemm_kernel(const __grid_constant__ OzGemmParams p) {
+  using G = OzG<WIDE>;
+  constexpr int kOzStages = G::stages;
+  constexpr int kOzStageBytes = G::stage_bytes;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -441,6 +454,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
       if (w >= nwork) break;
       int prod, slab, mod, t, tm, tn;
       oz_work(p, w, prod, slab, mod, t, tm, tn);
+      if (WIDE) {
+        const int4 wt = p.wide_list[t];
+        tm = wt.x;
+        tn = wt.y;
+      }
       // MMA A operand (TMEM lanes, the epilogue threads) = tile column tn,
       // B operand (TMEM columns) = tile row tm: each thread then holds 32
       // consecutive rows of one output column, stored as 32 contiguous bytes
@@ -458,6 +476,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
           const uint32_t fb = full(stage) & kPeerMask;
           tma_load_3d_pair(dst, &p.map[prod][seg][0], kc * kOzBK + a_kofs, a0, mod, fb);
           tma_load_3d_pair(dst + kOzABytes, &p.map[prod][seg][1], kc * kOzBK, b0, mod, fb);
+          if (WIDE)  // the second row tile (rows past the matrix read as zeros)
+            tma_load_3d_pair(dst + 2 * kOzABytes, &p.map[prod][seg][1], kc * kOzBK, b0 + 256, mod, fb);
         }
         __syncwarp();
         if (++stage == kOzStages) {
@@ -474,13 +494,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 1;
       // descriptors of stage 0; a stage is kOzStageBytes further, a 32-byte k step +2
-      const uint64_t da0 = sw128_desc(base), db0 = sw128_desc(base + kOzABytes);
+      const uint64_t da0 = sw128_desc(base), db0 = sw128_desc(base + kOzABytes),
+                     db1 = sw128_desc(base + 2 * kOzABytes);
       for (int seq = 0;; ++seq) {
         const int w = take(seq);
         if (w >= nwork) break;
         mbar_wait(tempty(acc), acc_phase);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t d = tmem + acc * kOzBN;
+        const uint32_t d = tmem + acc * kOzBN;  // WIDE: acc stays 0, the second accumulator is d + 256
         uint32_t accum = 0;
         const int slab = (w / p.ntiles / p.n_mod) % p.nslab;
         int seg = 0;
@@ -495,7 +516,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
             const uint64_t so = static_cast<uint64_t>((stage * kOzStageBytes) >> 4);
 #pragma unroll
             for (int kk = 0; kk < kOzBK / 32; ++kk) {
-              if (kk < ksteps) mma_i8_pair(d, da0 + so + 2 * kk, db0 + so + 2 * kk, accum | kk);
+              if (kk < ksteps) {
+                mma_i8_pair(d, da0 + so + 2 * kk, db0 + so + 2 * kk, accum | kk);
+                if (WIDE) mma_i8_pair(d + kOzBN, da0 + so + 2 * kk, db1 + so + 2 * kk, accum | kk);
+              }
             }
             mma_commit_pair(empty(stage));
           }
@@ -508,7 +532,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
         }
         if (elect_one()) mma_commit_pair(tfull(acc));
         __syncwarp();
-        if (++acc == 2) {
+        if (WIDE) {
+          acc_phase ^= 1u;
+        } else if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1u;
         }
@@ -526,6 +552,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
       if (w >= nwork) break;
       int prod, slab, mod, t, tm, tn;
       oz_work(p, w, prod, slab, mod, t, tm, tn);
+      int t0 = t, t1 = -1;
+      if (WIDE) {
+        const int4 wt = p.wide_list[t];
+        tm = wt.x;
+        tn = wt.y;
+        t0 = wt.z;
+        t1 = wt.w;
+      }
       const int ip = oz_mod_rt[mod];
       const long long qm = ((1ll << 32) + ip / 2) / ip;  // rn(2^32 / p)
       const int c16 = ((65536 % ip) > ip / 2) ? (65536 % ip) - ip : (65536 % ip);
@@ -533,74 +567,95 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       // thread = output column tn * 256 + cloc (TMEM lane); registers = rows
       const int cloc = static_cast<int>(rank) * kOzHalf + q * 32 + lane;
-      int8_t* out = p.res + prod * p.prod_stride + mod * p.mod_stride + static_cast<int64_t>(t) * kOzTileBytes +
-                    cloc * 256;
-      int32_t* cnt = p.nslab > 1 ? p.slab_cnt + (static_cast<int64_t>(prod) * p.n_mod + mod) * p.tiles_total + t
-                                 : nullptr;
-      if (slab > 0) {  // slab s-1 of this tile: all epilogue warps of both CTAs finished
-        if (lane == 0)
-          while (*reinterpret_cast<volatile int32_t*>(cnt) < 2 * kOzEpiWarps * slab) __nanosleep(256);
-        __syncwarp();
-        __threadfence();
-      }
-      const int nrow = min(kOzBN, p.nrows - tm * 256);
       const bool col_ok = tn * 256 + cloc < p.n;
       constexpr int kChunks = kOzBN / 32 / kOzEpiParts;  // 32-column TMEM loads per warp
-      // drain this warp's accumulator columns first and hand the TMEM buffer
-      // back to the MMA issuer before the reduction and the stores: with short
-      // reductions (a few k chunks per item) the MMA otherwise waits for the
-      // whole epilogue of the item two back
       uint32_t vv[kChunks][32];
+      // drain this warp's columns of one accumulator into registers
+      auto drain = [&](int acc_cols, int row_tile) {
+        const int nrow = min(kOzBN, p.nrows - row_tile * 256);
 #pragma unroll
-      for (int cc = 0; cc < kChunks; ++cc)
-        if ((part * kChunks + cc) * 32 < nrow)  // warp-uniform
-          tmem_ld32_issue(tmem + ((q * 32) << 16) + acc * kOzBN + (part * kChunks + cc) * 32, vv[cc]);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive_remote_cta(tempty(acc) & kPeerMask);
+        for (int cc = 0; cc < kChunks; ++cc)
+          if ((part * kChunks + cc) * 32 < nrow)  // warp-uniform
+            tmem_ld32_issue(tmem + ((q * 32) << 16) + acc_cols + (part * kChunks + cc) * 32, vv[cc]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      };
+      // hand the TMEM buffer back to the MMA issuer (before the reduction and
+      // the stores: with short reductions the MMA otherwise waits for the
+      // whole epilogue of the item two back)
+      auto release = [&]() {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote_cta(tempty(acc) & kPeerMask);
+      };
+      // residues mod p of the drained columns into residue tile `tile` (slab
+      // s > 0: added to slab s - 1's in place, once that slab's warps are done)
+      auto store = [&](int tile, int row_tile) {
+        const int nrow = min(kOzBN, p.nrows - row_tile * 256);
+        int8_t* out = p.res + prod * p.prod_stride + mod * p.mod_stride + static_cast<int64_t>(tile) * kOzTileBytes +
+                      cloc * 256;
+        int32_t* cnt = p.nslab > 1 ? p.slab_cnt + (static_cast<int64_t>(prod) * p.n_mod + mod) * p.tiles_total + tile
+                                   : nullptr;
+        if (slab > 0) {  // slab s-1 of this tile: all epilogue warps of both CTAs finished
+          if (lane == 0)
+            while (*reinterpret_cast<volatile int32_t*>(cnt) < 2 * kOzEpiWarps * slab) __nanosleep(256);
+          __syncwarp();
+          __threadfence();
+        }
 #pragma unroll
-      for (int cc = 0; cc < kChunks; ++cc) {
-        const int c = part * kChunks + cc;
-        if (c * 32 >= nrow) break;  // warp-uniform
-        const uint32_t (&v)[32] = vv[cc];
-        if (col_ok) {
-          uint32_t w[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            int r4[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) r4[i] = sym_mod_i32q(static_cast<int32_t>(v[4 * j + i]), ip, c16, qm);
-            w[j] = __byte_perm(__byte_perm(r4[0], r4[1], 0x40), __byte_perm(r4[2], r4[3], 0x40), 0x5410);
-          }
-          uint4* o = reinterpret_cast<uint4*>(out + c * 32);
-          if (slab > 0) {  // the residue of the sum of the slabs
-            const uint4 o0 = __ldcg(o), o1 = __ldcg(o + 1);
-            const uint32_t ow[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+        for (int cc = 0; cc < kChunks; ++cc) {
+          const int c = part * kChunks + cc;
+          if (c * 32 >= nrow) break;  // warp-uniform
+          const uint32_t (&v)[32] = vv[cc];
+          if (col_ok) {
+            uint32_t w8[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-              uint32_t x = 0;
+              int r4[4];
 #pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const int a = static_cast<int8_t>(w[j] >> (8 * i)), b = static_cast<int8_t>(ow[j] >> (8 * i));
-                x |= (static_cast<uint32_t>(sym_adj(a + b, ip)) & 0xffu) << (8 * i);
-              }
-              w[j] = x;
+              for (int i = 0; i < 4; ++i) r4[i] = sym_mod_i32q(static_cast<int32_t>(v[4 * j + i]), ip, c16, qm);
+              w8[j] = __byte_perm(__byte_perm(r4[0], r4[1], 0x40), __byte_perm(r4[2], r4[3], 0x40), 0x5410);
             }
+            uint4* o = reinterpret_cast<uint4*>(out + c * 32);
+            if (slab > 0) {  // the residue of the sum of the slabs
+              const uint4 o0 = __ldcg(o), o1 = __ldcg(o + 1);
+              const uint32_t ow[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                uint32_t x = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const int a = static_cast<int8_t>(w8[j] >> (8 * i)), b = static_cast<int8_t>(ow[j] >> (8 * i));
+                  x |= (static_cast<uint32_t>(sym_adj(a + b, ip)) & 0xffu) << (8 * i);
+                }
+                w8[j] = x;
+              }
+            }
+            // one 256-bit store: the thread's 32 rows are one full 32-byte sector
+            // (two 128-bit stores queued twice the requests, each half a sector)
+            asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(o), "r"(w8[0]),
+                         "r"(w8[1]), "r"(w8[2]), "r"(w8[3]), "r"(w8[4]), "r"(w8[5]), "r"(w8[6]), "r"(w8[7])
+                         : "memory");
           }
-          // one 256-bit store: the thread's 32 rows are one full 32-byte sector
-          // (two 128-bit stores queued twice the requests, each half a sector)
-          asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(o), "r"(w[0]), "r"(w[1]),
-                       "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
-                       : "memory");
         }
+        if (cnt) {
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) atomicAdd(cnt, 1);
+        }
+      };
+      drain(acc * kOzBN, tm);
+      if (!WIDE || t1 < 0) {
+        release();
+        store(t0, tm);
+      } else {  // the second accumulator (row tile tm + 1) after the first is stored
+        store(t0, tm);
+        drain(kOzBN, tm + 1);
+        release();
+        store(t1, tm + 1);
       }
-      if (cnt) {
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) atomicAdd(cnt, 1);
-      }
-      if (++acc == 2) {
+      if (WIDE) {
+        acc_phase ^= 1u;
+      } else if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1u;
       }
@@ -993,7 +1048,11 @@ static cudaError_t oz_init_once() {
     });
     cudaError_t status = cudaMemcpyToSymbol(c_oz_crt, t, sizeof(t));
     if (status == cudaSuccess)
-      status = cudaFuncSetAttribute(ozaki_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kOzSmem);
+      status = cudaFuncSetAttribute(ozaki_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    OzG<false>::smem);
+    if (status == cudaSuccess)
+      status = cudaFuncSetAttribute(ozaki_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    OzG<true>::smem);
     return status;
   });
 }
@@ -1111,7 +1170,10 @@ cudaError_t launch_ozaki_gemm(const OzGemmParams& p, cudaStream_t st) {
   const int grid = 2 * pairs;
   e = launch_fill_i32(p.counter, 1, 0, st);  // a kernel, not a copy-engine memset
   if (e != cudaSuccess) return e;
-  ozaki_gemm_kernel<<<grid, kOzThreads, kOzSmem, st>>>(p);
+  if (p.wide_list)
+    ozaki_gemm_kernel<true><<<grid, kOzThreads, OzG<true>::smem, st>>>(p);
+  else
+    ozaki_gemm_kernel<false><<<grid, kOzThreads, OzG<false>::smem, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -120,6 +120,11 @@ struct OzGemmParams {
   int32_t a_k_per_tm;
   int32_t nrows;
   int32_t rect_atom0, rect_gtiles;
+  // wide mode (long reductions): work item t = wide_list[t] = (tile row tm,
+  // tile col tn, tile index of (tm, tn), tile index of (tm + 1, tn) or -1): the
+  // pair computes both row tiles against one shared column panel, one TMEM
+  // accumulator each (ntiles = number of wide items)
+  const int4* wide_list;
 };
 
 struct OzCrtParams {
