@@ -399,3 +399,34 @@ def test_tile_boundaries(dims, cm):
     assert rel_frob_error(out.h.matrix, ref["h"]) < 1e-14
     assert rel_frob_error(out.s.matrix, ref["s"]) < 1e-14
     assert (out.split.hpd, out.split.nonhpd) == (ref["hpd"], ref["nonhpd"])
+
+
+def test_wide_gemm_work_items_match_oracle():
+    # the opt-in wide INT8 GEMM (HSB_OZ_WIDE: two row tiles per CTA pair, read
+    # once per process, hence a subprocess): odd tile counts, slabs, both
+    # contractions, against the oracle and bitwise against the default kernel
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "from oracle import alg1\n"
+        "from paper_1611_00606_b200 import Dims, GpuPolicy, ProblemSpec, build_hs, generate, rel_frob_error\n"
+        "for dims in (Dims(3, 49, 1301), Dims(9, 121, 700), Dims(70, 121, 300)):\n"
+        "    p = generate(ProblemSpec(dims, seed=5, nonhpd_fraction=0.3))\n"
+        "    o = build_hs(p, GpuPolicy(engine='int8'))\n"
+        "    r = alg1.build_hs_cpu(p)\n"
+        "    np.save('/tmp/wide_%%d_h.npy' %% dims.n_g, o.h.matrix)\n"
+        "    print(rel_frob_error(o.h.matrix, r['h']), rel_frob_error(o.s.matrix, r['s']))\n" % str(ROOT))
+    env = dict(os.environ, HSB_OZ_WIDE="1")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    errs = [float(x) for line in out.stdout.split("\n") if line.strip() for x in line.split()]
+    assert len(errs) == 6 and max(errs) < 1e-14, errs
+    # the default kernel gives the same bits (same residues, same reconstruction)
+    for dims in (Dims(3, 49, 1301), Dims(9, 121, 700), Dims(70, 121, 300)):
+        p = generate(ProblemSpec(dims, seed=5, nonhpd_fraction=0.3))
+        assert np.array_equal(build_hs(p, GpuPolicy(engine="int8")).h.matrix, np.load("/tmp/wide_%d_h.npy" % dims.n_g))
